@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""Benchmark of the partial-fraction exp(A)V hot path on B200 (BASELINE.json metric:
+"exp(A)V evals/sec at 1/2/4/8 B200; % of FP64-tensor or HBM roofline").
+
+Default workload = BASELINE configs[1] (C2): 1-D Dirichlet Laplacian, N = 2^20,
+spectrum (-100, 0), 16 seeded Gaussian RHS, n = 24 (12 conjugate pole pairs).
+One eval (= one step) = exp(tA)V for the whole 16-column block.  --workload C1/C3/C5
+selects the other configs (C4 when built).  Inputs are seeded synthetic data with
+the reference recipes (paper_2306_16778_b200/workloads.py); there is no dataset.
+
+Multi-GPU (torchrun, one process per GPU): the n/2 pole pairs are sharded across
+ranks (contiguous ascending blocks); each rank factors and solves its own shifts
+and the partial sums meet in ONE NCCL reduce to rank 0 (the path's only exchange).
+Total work is fixed as N grows -> "scaling": "strong".
+
+Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA events on
+the launching stream, max over ranks.  C2 inputs (V 128 MB + coefficients 16 MB)
+and output (128 MB) exceed the 126 MB L2, so no explicit flush is needed; the
+dense configs flush L2 between steps by writing a 256 MB buffer (outside the
+timed event pairs of the kernel-only number, inside the step for `value`? no: the
+flush runs before each step's start event and is excluded) — see config.l2.
+
+`--impl reference` runs the reference's CPU algorithm for the same workload (the
+oracle restatement: zgtsv/zgbsv/LAPACK per pole pair with the 2 Re(a y) combine and
+ascending reduction, oracle/restate.py) on all host cores, one bounded sample of
+the workload per step, and prints the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "exp(A)V evals/sec"
+UNIT = "evals/s"
+
+# Algorithmic work per eval (complex counting: 8 real flops per complex FMA)
+ALG_FLOPS = {
+    "C1": 8.0 * (8.0 / 3.0 * 128**3 + 8.0 * 128**2),
+    "C2": 12.0 * (1 << 20) * (12 + 16 * 22),
+    "C3": 10.0 * (8.0 / 3.0 * 256**3 + 2 * 8.0 * 256**2),  # per matrix (one eval = one matrix)
+    "C5": 8.0 * (8.0 * 262144 * 512 * 512 + 8.0 * 262144 * 1024 * 8),
+}
+ALG_BYTES = {
+    "C1": 1.33e5,
+    "C2": 8.0 * (1 << 20) * (2 + 2 * 16),
+    "C3": 5.40e8 / 512,
+    "C5": 8.0 * 2 * 513 * 262144 * 16,
+}
+DOMINANT = {"C1": "dense_batched_kernel", "C2": "tri_local", "C3": "dense_batched_kernel", "C5": "band_lu"}
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6488.0, "fp64_tflops": 36.9, "fp64_source": "profiles/fp64_peak_r01.txt (DMMA m8n8k4, measured)"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            m = json.load(fh)
+        peaks["hbm_gbs"] = float(m.get("hbm_gbs", peaks["hbm_gbs"]))
+        if "fp64_tflops" in m:
+            peaks["fp64_tflops"] = float(m["fp64_tflops"])
+            peaks["fp64_source"] = "MEASURED_PEAKS.json"
+    return peaks
+
+
+# ---- clocks sampling -------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+# ---- workloads -------------------------------------------------------------------
+
+class Workload:
+    """Inputs resident on the device + a step function calling the native library."""
+
+    def __init__(self, name, torch, dev, pairs_lo, pairs_hi):
+        from paper_2306_16778_b200 import workloads as W
+        from paper_2306_16778_b200.roots import default_table
+
+        self.name = name
+        self.torch = torch
+        self.dev = dev
+        if name == "C2":
+            n = W.C2["n"]
+            d, o = W.c2_matrix()
+            V = W.c2_rhs()
+            self.host = dict(diag=d, off=o, V=V)
+            self.h2d = d.nbytes + o.nbytes + V.nbytes
+            self.d2h = V.nbytes
+            self.evals_per_step = 1.0
+            self.desc = {"workload": "C2: tridiagonal 1-D Dirichlet Laplacian, N=2^20, spectrum (-100,0), 16 RHS, n=24",
+                         "N": 1 << 20, "nrhs": 16, "n": 24, "l2": "inputs (144 MB) + output (128 MB) exceed L2 (126 MB); no flush"}
+        elif name == "C1":
+            n = W.C1["n"]
+            A, v, _ = W.c1_inputs()
+            self.host = dict(A=A, V=v)
+            self.h2d = A.nbytes + v.nbytes
+            self.d2h = v.nbytes
+            self.evals_per_step = 1.0
+            self.desc = {"workload": "C1: dense real symmetric d=128, spectrum U[-50,0], exp(A)v, n=16", "d": 128, "n": 16,
+                         "l2": "256 MB L2 flush before every step"}
+        elif name == "C3":
+            n = W.C3["n"]
+            A, V = W.c3_batch()
+            self.host = dict(A=A, V=V)
+            self.h2d = A.nbytes + V.nbytes
+            self.d2h = V.nbytes * 2
+            self.evals_per_step = float(W.C3["batch"])
+            self.desc = {"workload": "C3: 512 dense complex Hermitian d=256, spectrum U[-200,0], exp(A)v, n=20",
+                         "batch": 512, "d": 256, "n": 20, "l2": "inputs 537 MB exceed L2; no flush"}
+        elif name == "C5":
+            n = W.C5["n"]
+            band = W.c5_band()
+            V = W.c5_rhs()
+            self.host = dict(band=band, V=V)
+            self.h2d = band.nbytes + V.nbytes
+            self.d2h = V.nbytes
+            self.evals_per_step = 1.0
+            self.desc = {"workload": "C5: 2-D 5-point Laplacian 512x512 (bandwidth 512), spectrum (-400,0), 8 RHS, n=16",
+                         "N": 262144, "kb": 512, "nrhs": 8, "n": 16, "l2": "inputs > L2; no flush"}
+        else:
+            raise SystemExit(f"unknown workload {name}")
+        self.n = n
+        t2, c2 = default_table(n).interleaved()
+        self.theta2 = np.ascontiguousarray(t2[2 * pairs_lo: 2 * pairs_hi])
+        self.coef2 = np.ascontiguousarray(c2[2 * pairs_lo: 2 * pairs_hi])
+        self.dev_in = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in self.host.items()}
+        self.out = None
+        self.flush = None
+        if name == "C1":
+            self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        # pinned host copies for the end-to-end number
+        self.pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in self.host.items()}
+
+    def step(self, stream):
+        from paper_2306_16778_b200 import _native
+
+        di = self.dev_in
+        if self.name == "C2":
+            self.out = _native.expm_tridiag_device(di["diag"], di["off"], di["V"], self.theta2, self.coef2, 0.0,
+                                                   out=self.out, stream=stream)
+        elif self.name in ("C1", "C3"):
+            self.out = _native.expm_dense_device(di["A"], di["V"], self.theta2, self.coef2, 0.0, stream=stream)
+        elif self.name == "C5":
+            self.out = _native.expm_banded_device(di["band"], di["V"], self.theta2, self.coef2, 0.0, out=self.out,
+                                                  stream=stream)
+        return self.out
+
+    def step_host(self):
+        """Same computation through the C-ABI with HOST buffers (PFX_MEM_HOST): H2D + compute + D2H."""
+        from paper_2306_16778_b200 import _native
+
+        p = {k: v.numpy() for k, v in self.pinned.items()}
+        if self.name == "C2":
+            return _native.expm_tridiag_host(p["diag"], p["off"], p["V"], self.theta2, self.coef2, 0.0)
+        if self.name in ("C1", "C3"):
+            return _native.expm_dense_host(p["A"], p["V"], self.theta2, self.coef2, 0.0)
+        return _native.expm_banded_host(p["band"], p["V"], self.theta2, self.coef2, 0.0)
+
+
+# ---- CPU baseline (oracle restatement on the host cores) ----------------------------
+
+def _cpu_task(args):
+    name, n, cols = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import restate
+    from paper_2306_16778_b200 import workloads as W
+
+    if name == "C2":
+        d, o = W.c2_matrix()
+        V = W.c2_rhs()
+        restate.tridiag_action(d, o, V[:, cols], n)
+        return len(cols) / 16.0
+    if name == "C1":
+        A, v, _ = W.c1_inputs()
+        restate.run_tasks_dense(A, v, n)
+        return 1.0
+    if name == "C3":
+        for b in cols:
+            restate.run_tasks_dense(W.c3_matrix(b), W.c3_vector(b), n)
+        return float(len(cols))
+    if name == "C5":
+        band = W.c5_band()
+        V = W.c5_rhs()
+        restate.banded_action(band, V[:, cols], n)
+        return len(cols) / 8.0
+    raise ValueError(name)
+
+
+def cpu_sample_plan(name, cores):
+    """Bounded sample of the workload (~10-30 s of CPU work), as (tasks, description)."""
+    if name == "C2":
+        tasks = [(name, 24, [c]) for c in range(min(cores, 16))]
+        return tasks, f"{len(tasks)} of the 16 RHS columns of C2 (all 12 pole pairs, full N=2^20), one process per column"
+    if name == "C1":
+        tasks = [(name, 16, [0])] * cores
+        return tasks, f"{cores} independent C1 evals, one per process"
+    if name == "C3":
+        per = 2
+        tasks = [(name, 20, list(range(i * per, (i + 1) * per))) for i in range(cores)]
+        return tasks, f"{cores * per} of the 512 C3 matrices ({per} per process)"
+    if name == "C5":
+        tasks = [(name, 16, [c]) for c in range(min(cores, 8))]
+        return tasks, f"{len(tasks)} of the 8 RHS columns of C5 (zgbsv kl=ku=512, all 8 pairs)"
+    raise ValueError(name)
+
+
+def run_cpu(name, cores, steps=1, warmup=0):
+    """Returns (evals/s, description, cores used). Process pool: LAPACK releases no GIL in the f2py wrappers."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    tasks, desc = cpu_sample_plan(name, cores)
+    used = len(tasks)
+    rates = []
+    with ProcessPoolExecutor(max_workers=used) as pool:
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            work = sum(pool.map(_cpu_task, tasks))
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                rates.append(work / dt)
+    return statistics.median(rates), desc, used
+
+
+# ---- main ------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cores = os.cpu_count() or 1
+    peaks = load_peaks()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = max(1, args.steps if args.steps <= 3 else 3)
+        value, desc, used = run_cpu(args.workload, cores, steps=steps, warmup=0)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+            "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic (seeded reference recipes)", "impl": "reference",
+            "config": {"workload": args.workload, "parallelism": f"cpu x{used} processes"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_16778_b200 import _native
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2306_16778_b200 import workloads as W
+
+    n = {"C1": 16, "C2": 24, "C3": 20, "C5": 16}[args.workload]
+    npairs = n // 2
+    lo = rank * npairs // world
+    hi = (rank + 1) * npairs // world
+    wl = Workload(args.workload, torch, dev, lo, hi)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def one_step():
+        if wl.flush is not None:
+            wl.flush.zero_()
+        out = wl.step(stream)
+        if world > 1:
+            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
+        return out
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    # timed region: device events on the launching stream, kernel timing live
+    _native.prof_enable(True)
+    _native.prof_read()
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    kern = _native.prof_read()
+    _native.prof_enable(False)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = wl.evals_per_step * args.steps / (ms * 1e-3)
+
+    # end-to-end through the C-ABI with host buffers (H2D + compute + D2H per step)
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        wl.step_host()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            wl.step_host()
+        dt = time.perf_counter() - t0
+        e2e = {"value": wl.evals_per_step * args.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h)}
+
+    launches = sum(c for c, _ in kern.values())
+    dom = DOMINANT[args.workload]
+    dom_cnt, dom_ms = kern.get(dom, (0, 0.0))
+    flops_per_launch = ALG_FLOPS[args.workload] * wl.evals_per_step * (hi - lo) / npairs
+    roofline = None
+    if dom_cnt:
+        t_launch = dom_ms / dom_cnt * 1e-3
+        achieved = flops_per_launch / t_launch / 1e12
+        roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                    "frac": achieved / peaks["fp64_tflops"], "traffic": None, "kernel": dom,
+                    "kernel_ms": dom_ms / dom_cnt, "peak_source": peaks["fp64_source"],
+                    "share_of_step": (dom_ms / args.steps) / ms_step,
+                    "path_frac": ALG_FLOPS[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e12
+                    / peaks["fp64_tflops"] / world,
+                    "hbm_gbs_alg": ALG_BYTES[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e9}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v_cpu, desc, used = run_cpu(args.workload, cores, steps=1, warmup=0)
+            cpu = {"value": v_cpu, "unit": UNIT, "cores": used, "kind": "port", "sample": desc}
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": cores, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic (seeded reference recipes)",
+            "config": dict(wl.desc, parallelism=f"pole-shard x{world}" + (" + 1 NCCL reduce" if world > 1 else "")),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+            "kernels": {k: {"launches": c, "total_ms": t} for k, t in [(k, v[1]) for k, v in kern.items()] for c in [kern[k][0]]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

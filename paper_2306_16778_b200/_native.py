@@ -1,0 +1,351 @@
+"""ctypes binding of libpfx.so (include/pfx.h) — the only route to the compute.
+
+There is no CPU fallback: if the library is missing, or no CUDA device is
+present, every compute entry point raises PfexpmError.  Device buffers and
+streams come from PyTorch (plumbing only); host arrays may also be passed
+directly (PFX_MEM_HOST), in which case the library stages them itself.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import BadSpec, PfexpmError, raise_for_status
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpfx.so")
+PFX_MEM_DEVICE = 0
+PFX_MEM_HOST = 1
+
+_lib = None
+_lock = threading.Lock()
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_fp = ctypes.POINTER(ctypes.c_float)
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes), mirrors include/pfx.h
+SIGNATURES = {
+    "pfx_version": (_int, []),
+    "pfx_last_error": (ctypes.c_char_p, []),
+    "pfx_release": (_int, []),
+    "pfx_pole_table": (_int, [_int, _dp, _dp]),
+    "pfx_expm_dense": (
+        _int,
+        [_int, _vp, _int, _i64, _i64, _vp, _int, _i64, ctypes.c_double, _dp, _dp, _int, _vp, _int, _fp, _vp],
+    ),
+    "pfx_expm_tridiag": (
+        _int,
+        [_int, _vp, _vp, _i64, _vp, _i64, ctypes.c_double, _dp, _dp, _int, _vp, _fp, _vp],
+    ),
+    "pfx_expm_banded": (
+        _int,
+        [_int, _vp, _i64, _i64, _vp, _i64, ctypes.c_double, _dp, _dp, _int, _vp, _fp, _vp],
+    ),
+    "pfx_prof_enable": (_int, [_int]),
+    "pfx_prof_read": (_int, [ctypes.c_char_p, _int]),
+    "pfx_shifted_solve": (
+        _int,
+        [_int, _vp, _int, _i64, ctypes.c_double, ctypes.c_double, _vp, _i64, _vp, _vp],
+    ),
+}
+
+
+def lib():
+    """Load libpfx.so once (raises PfexpmError if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise PfexpmError(
+                    f"native library {LIB_PATH} is missing; run `python -m paper_2306_16778_b200.build`"
+                )
+            handle = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def last_error() -> str:
+    return lib().pfx_last_error().decode()
+
+
+def _check(status: int, what: str) -> None:
+    if status != 0:
+        raise_for_status(status, what, last_error())
+
+
+def _f64p(arr: np.ndarray):
+    return arr.ctypes.data_as(_dp)
+
+
+def prof_enable(on: bool) -> None:
+    lib().pfx_prof_enable(1 if on else 0)
+
+
+def prof_read() -> dict:
+    """{kernel name: (launches, total_ms)} since the last read (synchronises the events)."""
+    need = lib().pfx_prof_read(None, 0)
+    buf = ctypes.create_string_buffer(max(need, 1) + 64)
+    lib().pfx_prof_read(buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, tot = line.split()
+        out[name] = (int(cnt), float(tot))
+    return out
+
+
+def pole_table(n: int):
+    theta2 = np.zeros(n, dtype=np.float64)
+    coef2 = np.zeros(n, dtype=np.float64)
+    _check(lib().pfx_pole_table(n, _f64p(theta2), _f64p(coef2)), f"pfx_pole_table(n={n})")
+    return theta2, coef2
+
+
+# ---- device plumbing (torch) --------------------------------------------------
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise PfexpmError("no CUDA device: the B200 engine has no CPU fallback")
+    return torch
+
+
+def _stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _as_device(x: np.ndarray, torch, device):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(device, non_blocking=False)
+
+
+def _f64_view(t):
+    """Raw float64 storage of a real or complex128 tensor (contiguous)."""
+    import torch
+
+    t = t.contiguous()
+    if t.dtype == torch.complex128:
+        return t
+    if t.dtype != torch.float64:
+        raise BadSpec(f"expected float64/complex128 tensor, got {t.dtype}")
+    return t
+
+
+def _ptr(t) -> int:
+    return int(t.data_ptr()) if t is not None else 0
+
+
+# ---- dense ---------------------------------------------------------------------
+
+def expm_dense_device(A, V, theta2, coef2, shift_c: float, out=None, per_pair_ms=None, stream=None):
+    """Device-tensor entry: A (batch,d,d) or (d,d); V (batch,d,nrhs)/(d,nrhs)/(d,) or None (full)."""
+    torch = _torch()
+    A = _f64_view(A)
+    squeeze_batch = A.dim() == 2
+    if squeeze_batch:
+        A = A.unsqueeze(0)
+    batch, d = A.shape[0], A.shape[1]
+    a_complex = A.dtype == torch.complex128
+    full = V is None
+    v_complex = False
+    nrhs = 0
+    squeeze_vec = False
+    if not full:
+        V = _f64_view(V)
+        if squeeze_batch:
+            V = V.unsqueeze(0)
+        if V.dim() == 2:
+            V = V.unsqueeze(-1)
+            squeeze_vec = True
+        if V.shape[0] != batch or V.shape[1] != d:
+            raise BadSpec(f"V shape {tuple(V.shape)} does not match A {tuple(A.shape)}")
+        nrhs = V.shape[2]
+        v_complex = V.dtype == torch.complex128
+    real_path = (not a_complex) and (full or not v_complex)
+    ncols = d if full else nrhs
+    odt = torch.float64 if real_path else torch.complex128
+    if out is None:
+        out = torch.empty((batch, d, ncols), dtype=odt, device=A.device)
+    npairs = len(theta2) // 2
+    ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
+    st = lib().pfx_expm_dense(
+        PFX_MEM_DEVICE, _ptr(A), int(a_complex), d, batch, _ptr(V) if not full else None, int(v_complex), nrhs,
+        float(shift_c), _f64p(theta2), _f64p(coef2), npairs, _ptr(out), int(not real_path),
+        ctypes.cast(ms, _fp) if ms is not None else None, _stream_ptr(stream),
+    )
+    _check(st, "pfx_expm_dense")
+    if per_pair_ms is not None:
+        per_pair_ms[:] = list(ms)
+    res = out
+    if squeeze_vec:
+        res = res.squeeze(-1)
+    if squeeze_batch:
+        res = res.squeeze(0)
+    return res
+
+
+def expm_dense_host(A: np.ndarray, V, theta2, coef2, shift_c: float, per_pair_ms=None):
+    """Host-array entry through PFX_MEM_HOST (the library stages H2D/D2H itself)."""
+    _torch()  # asserts a device exists
+    A = np.ascontiguousarray(A)
+    squeeze_batch = A.ndim == 2
+    if squeeze_batch:
+        A = A[None]
+    batch, d = A.shape[0], A.shape[1]
+    a_complex = np.iscomplexobj(A)
+    A = A.astype(np.complex128 if a_complex else np.float64, copy=False)
+    full = V is None
+    nrhs, v_complex, squeeze_vec = 0, False, False
+    if not full:
+        V = np.ascontiguousarray(V)
+        if squeeze_batch:
+            V = V[None]
+        if V.ndim == 2:
+            V = V[..., None]
+            squeeze_vec = True
+        nrhs = V.shape[2]
+        v_complex = np.iscomplexobj(V)
+        V = np.ascontiguousarray(V.astype(np.complex128 if v_complex else np.float64, copy=False))
+    real_path = (not a_complex) and (full or not v_complex)
+    ncols = d if full else nrhs
+    out = np.empty((batch, d, ncols), dtype=np.float64 if real_path else np.complex128)
+    npairs = len(theta2) // 2
+    ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
+    st = lib().pfx_expm_dense(
+        PFX_MEM_HOST, A.ctypes.data, int(a_complex), d, batch, V.ctypes.data if not full else None, int(v_complex),
+        nrhs, float(shift_c), _f64p(theta2), _f64p(coef2), npairs, out.ctypes.data, int(not real_path),
+        ctypes.cast(ms, _fp) if ms is not None else None, None,
+    )
+    _check(st, "pfx_expm_dense")
+    if per_pair_ms is not None:
+        per_pair_ms[:] = list(ms)
+    if squeeze_vec:
+        out = out[..., 0]
+    if squeeze_batch:
+        out = out[0]
+    return out
+
+
+# ---- tridiagonal / banded ------------------------------------------------------
+
+def expm_tridiag_device(diag, off, V, theta2, coef2, shift_c: float, out=None, per_pair_ms=None, stream=None):
+    torch = _torch()
+    squeeze = V.dim() == 1
+    if squeeze:
+        V = V.unsqueeze(-1)
+    N, nrhs = V.shape
+    if out is None:
+        out = torch.empty((N, nrhs), dtype=torch.float64, device=V.device)
+    npairs = len(theta2) // 2
+    ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
+    st = lib().pfx_expm_tridiag(
+        PFX_MEM_DEVICE, _ptr(diag), _ptr(off) if N > 1 else None, N, _ptr(V.contiguous()), nrhs, float(shift_c),
+        _f64p(theta2), _f64p(coef2), npairs, _ptr(out), ctypes.cast(ms, _fp) if ms is not None else None,
+        _stream_ptr(stream),
+    )
+    _check(st, "pfx_expm_tridiag")
+    if per_pair_ms is not None:
+        per_pair_ms[:] = list(ms)
+    return out.squeeze(-1) if squeeze else out
+
+
+def expm_tridiag_host(diag, off, V, theta2, coef2, shift_c: float, per_pair_ms=None):
+    _torch()
+    diag = np.ascontiguousarray(diag, dtype=np.float64)
+    off = np.ascontiguousarray(off, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    squeeze = V.ndim == 1
+    V = np.ascontiguousarray(V[:, None] if squeeze else V)
+    N, nrhs = V.shape
+    out = np.empty((N, nrhs), dtype=np.float64)
+    npairs = len(theta2) // 2
+    ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
+    st = lib().pfx_expm_tridiag(
+        PFX_MEM_HOST, diag.ctypes.data, off.ctypes.data if N > 1 else None, N, V.ctypes.data, nrhs, float(shift_c),
+        _f64p(theta2), _f64p(coef2), npairs, out.ctypes.data, ctypes.cast(ms, _fp) if ms is not None else None, None,
+    )
+    _check(st, "pfx_expm_tridiag")
+    if per_pair_ms is not None:
+        per_pair_ms[:] = list(ms)
+    return out[:, 0] if squeeze else out
+
+
+def expm_banded_host(band, V, theta2, coef2, shift_c: float, per_pair_ms=None):
+    _torch()
+    band = np.ascontiguousarray(band, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    squeeze = V.ndim == 1
+    V = np.ascontiguousarray(V[:, None] if squeeze else V)
+    N, nrhs = V.shape
+    kb = band.shape[0] - 1
+    out = np.empty((N, nrhs), dtype=np.float64)
+    npairs = len(theta2) // 2
+    ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
+    st = lib().pfx_expm_banded(
+        PFX_MEM_HOST, band.ctypes.data, N, kb, V.ctypes.data, nrhs, float(shift_c), _f64p(theta2), _f64p(coef2),
+        npairs, out.ctypes.data, ctypes.cast(ms, _fp) if ms is not None else None, None,
+    )
+    _check(st, "pfx_expm_banded")
+    if per_pair_ms is not None:
+        per_pair_ms[:] = list(ms)
+    return out[:, 0] if squeeze else out
+
+
+def expm_banded_device(band, V, theta2, coef2, shift_c: float, out=None, per_pair_ms=None, stream=None):
+    torch = _torch()
+    squeeze = V.dim() == 1
+    if squeeze:
+        V = V.unsqueeze(-1)
+    N, nrhs = V.shape
+    kb = band.shape[0] - 1
+    if out is None:
+        out = torch.empty((N, nrhs), dtype=torch.float64, device=V.device)
+    npairs = len(theta2) // 2
+    ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
+    st = lib().pfx_expm_banded(
+        PFX_MEM_DEVICE, _ptr(band.contiguous()), N, kb, _ptr(V.contiguous()), nrhs, float(shift_c), _f64p(theta2),
+        _f64p(coef2), npairs, _ptr(out), ctypes.cast(ms, _fp) if ms is not None else None, _stream_ptr(stream),
+    )
+    _check(st, "pfx_expm_banded")
+    if per_pair_ms is not None:
+        per_pair_ms[:] = list(ms)
+    return out.squeeze(-1) if squeeze else out
+
+
+def shifted_solve(A, theta: complex, V: np.ndarray) -> np.ndarray:
+    """Host entry for linalg.shifted_solve: Y = (A + theta I)^{-1} V, complex128."""
+    _torch()
+    a = A.entries
+    a_complex = not A.is_real()
+    a = np.ascontiguousarray(a if a_complex else a.real)
+    V = np.asarray(V, dtype=np.complex128)
+    squeeze = V.ndim == 1
+    Vc = np.ascontiguousarray(V[:, None] if squeeze else V)
+    d, nrhs = Vc.shape
+    if d != A.d:
+        raise BadSpec(f"V has {d} rows, A is {A.d} x {A.d}")
+    Y = np.empty_like(Vc)
+    st = lib().pfx_shifted_solve(
+        PFX_MEM_HOST, a.ctypes.data, int(a_complex), d, theta.real, theta.imag, Vc.ctypes.data, nrhs, Y.ctypes.data,
+        None,
+    )
+    _check(st, "pfx_shifted_solve")
+    return Y[:, 0] if squeeze else Y

@@ -1,0 +1,556 @@
+// Batched dense shifted solves with fused residue combine (configs C1, C3; small full-mode cases).
+//
+// Replaces the per-pair task of reference engine._run_tasks
+// (/root/reference/pkg/src/pfexpm/engine.py:194-215):
+//   K0  M = A - cI + theta_k I            fused into the load (engine.py:197, 299-301)
+//   K1/K2 LU with partial pivoting         getrf semantics   (engine.py:200,203,208)
+//   K3  Y = M^{-1} V,  Yc = M^{-H} V        getrs 'N' / 'C'   (engine.py:204-205)
+//   K5  residue combine into a per-system slot                (engine.py:201,206,210-213)
+//   K6  ascending-pair reduction + e^c scale (separate tiny kernel; engine.py:226-228,303-304)
+//
+// One persistent CTA per SM walks the (matrix, pair) systems.  Each system is
+// factored in an L2-resident workspace slot with a blocked right-looking LU:
+// the panel (up to d x NB complex) lives in shared memory, row interchanges are
+// applied to the rest of the slot, U12 strips are solved in shared memory and
+// the trailing update A22 -= L21 U12 runs on the FP64 tensor cores (DMMA
+// m8n8k4, four real MMAs per complex 8x8x4 step) straight from the panel/strip
+// in shared memory into accumulator fragments loaded from and stored back to
+// the slot.
+#include "pfx_common.cuh"
+
+namespace pfx {
+
+constexpr int DB_THREADS = 256;
+constexpr int DB_WARPS = DB_THREADS / 32;
+constexpr int DB_SW = 64;  // strip width of the trailing update
+
+struct DenseBatchArgs {
+  const double* A;
+  int a_complex;
+  int d;
+  int batch;
+  const double* V;
+  int v_complex;
+  int ncols;  // RHS columns (action) or d (full)
+  int full;
+  int real_path;
+  int solve_only;  // pfx_shifted_solve: stage = Y (complex), no combine
+  double shift_c;
+  const double2* theta;  // device, npairs
+  const double2* coef;   // device, npairs
+  int npairs;
+  double2* W;     // slots x d*d
+  int* ipiv;      // slots x d
+  double2* Y;     // slots x d*ncols   (solution Y, or X in full mode)
+  double2* Yc;    // slots x d*ncols   (complex action: M^{-H} V)
+  double* stage;  // systems x d*ncols (x2 if complex)
+  int* status;
+};
+
+__device__ __forceinline__ void block_argmax(double val, int idx, double* sv, int* si, double& best, int& bidx) {
+  // max |.|_1, ties -> smallest index (izamax semantics)
+  for (int off = 16; off > 0; off >>= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, val, off);
+    int oi = __shfl_down_sync(0xffffffffu, idx, off);
+    if (ov > val || (ov == val && oi < idx)) {
+      val = ov;
+      idx = oi;
+    }
+  }
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[warp] = val;
+    si[warp] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    val = threadIdx.x < DB_WARPS ? sv[threadIdx.x] : -1.0;
+    idx = threadIdx.x < DB_WARPS ? si[threadIdx.x] : 0x7fffffff;
+    for (int off = 16; off > 0; off >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, val, off);
+      int oi = __shfl_down_sync(0xffffffffu, idx, off);
+      if (ov > val || (ov == val && oi < idx)) {
+        val = ov;
+        idx = oi;
+      }
+    }
+    if (threadIdx.x == 0) {
+      sv[0] = val;
+      si[0] = idx;
+    }
+  }
+  __syncthreads();
+  best = sv[0];
+  bidx = si[0];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// LU of the d x d row-major slot W (in place), pivots into ipiv (0-based, global rows).
+// Returns nonzero (in *sing) if an exactly zero pivot was met (factorization continues,
+// as LAPACK does, and the caller reports PFX_SINGULAR).
+template <int NB>
+__device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* P, double2* S,
+                           double* red_v, int* red_i, int* s_piv, int* sing) {
+  constexpr int PS = NB + 1;        // padded panel row stride (double2)
+  constexpr int SS = DB_SW + 1;     // padded strip row stride
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  for (int p = 0; p < d; p += NB) {
+    const int jb = min(NB, d - p);
+    const int m = d - p;
+    // ---- load panel rows p..d-1, cols p..p+jb-1
+    for (int e = tid; e < m * jb; e += DB_THREADS) {
+      int r = e / jb, c = e - r * jb;
+      P[r * PS + c] = W[(size_t)(p + r) * d + p + c];
+    }
+    __syncthreads();
+    // ---- unblocked getf2 on the panel
+    for (int jj = 0; jj < jb; ++jj) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int r = jj + tid; r < m; r += DB_THREADS) {
+        double2 x = P[r * PS + jj];
+        double v = fabs(x.x) + fabs(x.y);
+        if (v > bv) {
+          bv = v;
+          bi = r;
+        }
+      }
+      double best;
+      int piv;
+      block_argmax(bv, bi, red_v, red_i, best, piv);
+      if (tid == 0) {
+        s_piv[jj] = piv;
+        ipiv[p + jj] = p + piv;
+        if (best == 0.0) *sing = 1;
+      }
+      if (piv != jj && tid < jb) {
+        double2 a = P[jj * PS + tid];
+        P[jj * PS + tid] = P[piv * PS + tid];
+        P[piv * PS + tid] = a;
+      }
+      __syncthreads();
+      cplx pv = ld(&P[jj * PS + jj]);
+      cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp(pv);
+      for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
+        cplx l = cmul(ld(&P[r * PS + jj]), rp);
+        st(&P[r * PS + jj], l);
+        for (int c = jj + 1; c < jb; ++c) st(&P[r * PS + c], cfms(ld(&P[r * PS + c]), l, ld(&P[jj * PS + c])));
+      }
+      __syncthreads();
+    }
+    // ---- write panel back
+    for (int e = tid; e < m * jb; e += DB_THREADS) {
+      int r = e / jb, c = e - r * jb;
+      W[(size_t)(p + r) * d + p + c] = P[r * PS + c];
+    }
+    // ---- row interchanges on the columns outside the panel (in order, per column)
+    for (int c = tid; c < d - jb; c += DB_THREADS) {
+      int col = c < p ? c : c + jb;
+      for (int jj = 0; jj < jb; ++jj) {
+        int pr = s_piv[jj];
+        if (pr != jj) {
+          size_t a = (size_t)(p + jj) * d + col, b = (size_t)(p + pr) * d + col;
+          double2 x = W[a];
+          W[a] = W[b];
+          W[b] = x;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- strips of the trailing columns: U12 = L11^{-1} A12, A22 -= L21 U12
+    for (int q = p + jb; q < d; q += DB_SW) {
+      const int sw = min(DB_SW, d - q);
+      for (int e = tid; e < jb * sw; e += DB_THREADS) {
+        int r = e / sw, c = e - r * sw;
+        S[r * SS + c] = W[(size_t)(p + r) * d + q + c];
+      }
+      __syncthreads();
+      // unit-lower triangular solve: warp w owns strip columns w, w+8, ... ; lane = row
+      for (int c = warp; c < sw; c += DB_WARPS) {
+        for (int k = 0; k < jb; ++k) {
+          cplx s = ld(&S[k * SS + c]);
+          if (lane > k && lane < jb) st(&S[lane * SS + c], cfms(ld(&S[lane * SS + c]), ld(&P[lane * PS + k]), s));
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < jb * sw; e += DB_THREADS) {
+        int r = e / sw, c = e - r * sw;
+        W[(size_t)(p + r) * d + q + c] = S[r * SS + c];
+      }
+      // DMMA trailing update of rows p+jb..d-1, cols q..q+sw-1
+      const int mrows = m - jb;
+      const int rtiles = (mrows + 7) >> 3;
+      const int ctiles = (sw + 7) >> 3;
+      for (int rt = warp; rt < rtiles; rt += DB_WARPS) {
+        double cr[DB_SW / 8][2], ci[DB_SW / 8][2];
+        const int grow = p + jb + rt * 8 + g;  // C row owned by this lane
+#pragma unroll
+        for (int ct = 0; ct < DB_SW / 8; ++ct) {
+          cr[ct][0] = cr[ct][1] = ci[ct][0] = ci[ct][1] = 0.0;
+          if (ct < ctiles && grow < d) {
+            int c0 = ct * 8 + 2 * t;
+            if (c0 < sw) {
+              double2 x = W[(size_t)grow * d + q + c0];
+              cr[ct][0] = x.x;
+              ci[ct][0] = x.y;
+            }
+            if (c0 + 1 < sw) {
+              double2 x = W[(size_t)grow * d + q + c0 + 1];
+              cr[ct][1] = x.x;
+              ci[ct][1] = x.y;
+            }
+          }
+        }
+        const int prow = jb + rt * 8 + g;  // panel row of the A fragment
+        for (int k0 = 0; k0 < jb; k0 += 4) {
+          double ar = 0.0, ai = 0.0;
+          if (prow < m && k0 + t < jb) {
+            double2 x = P[prow * PS + k0 + t];
+            ar = -x.x;  // C -= L*U  ==  C += (-L)*U
+            ai = -x.y;
+          }
+#pragma unroll
+          for (int ct = 0; ct < DB_SW / 8; ++ct) {
+            if (ct < ctiles) {
+              double br = 0.0, bi = 0.0;
+              int col = ct * 8 + g;
+              if (k0 + t < jb && col < sw) {
+                double2 y = S[(k0 + t) * SS + col];
+                br = y.x;
+                bi = y.y;
+              }
+              zmma884(cr[ct], ci[ct], ar, ai, br, bi);
+            }
+          }
+        }
+#pragma unroll
+        for (int ct = 0; ct < DB_SW / 8; ++ct) {
+          if (ct < ctiles && grow < d) {
+            int c0 = ct * 8 + 2 * t;
+            if (c0 < sw) W[(size_t)grow * d + q + c0] = make_double2(cr[ct][0], ci[ct][0]);
+            if (c0 + 1 < sw) W[(size_t)grow * d + q + c0 + 1] = make_double2(cr[ct][1], ci[ct][1]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Triangular solves on one RHS column z (shared memory, length d) against the LU in W.
+// kind 0: L  (unit lower, forward)      z <- L^{-1} z
+// kind 1: U  (upper, backward)          z <- U^{-1} z
+// kind 2: U^H (lower, forward, conj)    z <- U^{-H} z
+// kind 3: L^H (unit upper, backward)    z <- L^{-H} z
+// Blocked by 32 rows: the contribution of already-solved blocks is a GEMV with
+// coalesced reads of W, the 32x32 diagonal block is solved by warp 0 in registers.
+__device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, double2* z, double2* part,
+                             double2* diag) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool forward = (kind == 0 || kind == 2);
+  const int nblk = (d + 31) >> 5;
+  for (int bb = 0; bb < nblk; ++bb) {
+    const int blk = forward ? bb : nblk - 1 - bb;
+    const int i0 = blk * 32;
+    const int bs = min(32, d - i0);
+    // previously solved index range
+    const int j0 = forward ? 0 : i0 + bs;
+    const int j1 = forward ? i0 : d;
+    // GEMV: part[i] = sum_j op(W)[i][j] z[j]
+    if (kind <= 1) {
+      // rows of W are contiguous: warp w handles rows i0+w, i0+w+8, ...; lanes stride j
+      for (int ii = warp; ii < bs; ii += DB_WARPS) {
+        const double2* row = W + (size_t)(i0 + ii) * d;
+        cplx acc = mk(0.0, 0.0);
+        for (int j = j0 + lane; j < j1; j += 32) acc = cadd(acc, cmul(ld(&row[j]), ld(&z[j])));
+        for (int off = 16; off > 0; off >>= 1) {
+          acc.re += __shfl_down_sync(0xffffffffu, acc.re, off);
+          acc.im += __shfl_down_sync(0xffffffffu, acc.im, off);
+        }
+        if (lane == 0) st(&part[ii], acc);
+      }
+    } else {
+      // op(W)[i][j] = conj(W[j][i]): lanes along i (contiguous in row j), warps stride j
+      cplx acc = mk(0.0, 0.0);
+      if (lane < bs)
+        for (int j = j0 + warp; j < j1; j += DB_WARPS) acc = cadd(acc, cmulc(ld(&z[j]), ld(&W[(size_t)j * d + i0 + lane])));
+      // reduce over warps through shared memory (diag scratch as buffer)
+      st(&diag[warp * 32 + lane], acc);
+      __syncthreads();
+      if (warp == 0) {
+        cplx s = mk(0.0, 0.0);
+        for (int w = 0; w < DB_WARPS; ++w) s = cadd(s, ld(&diag[w * 32 + lane]));
+        if (lane < bs) st(&part[lane], s);
+      }
+    }
+    __syncthreads();
+    // load the diagonal block (op applied) into shared memory: diag[r*33 + c] = op(W)[i0+r][i0+c]
+    for (int e = tid; e < bs * bs; e += DB_THREADS) {
+      int r = e / bs, c = e - r * bs;
+      cplx v = (kind <= 1) ? ld(&W[(size_t)(i0 + r) * d + i0 + c]) : cconj(ld(&W[(size_t)(i0 + c) * d + i0 + r]));
+      st(&diag[r * 33 + c], v);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      cplx x = (lane < bs) ? csub(ld(&z[i0 + lane]), ld(&part[lane])) : mk(0.0, 0.0);
+      const bool unit = (kind == 0 || kind == 3);
+      if (forward) {
+        for (int k = 0; k < bs; ++k) {
+          cplx xk;
+          xk.re = __shfl_sync(0xffffffffu, x.re, k);
+          xk.im = __shfl_sync(0xffffffffu, x.im, k);
+          if (!unit) {
+            xk = cdiv(xk, ld(&diag[k * 33 + k]));
+            if (lane == k) x = xk;
+          }
+          if (lane > k && lane < bs) x = cfms(x, ld(&diag[lane * 33 + k]), xk);
+        }
+      } else {
+        for (int k = bs - 1; k >= 0; --k) {
+          cplx xk;
+          xk.re = __shfl_sync(0xffffffffu, x.re, k);
+          xk.im = __shfl_sync(0xffffffffu, x.im, k);
+          if (!unit) {
+            xk = cdiv(xk, ld(&diag[k * 33 + k]));
+            if (lane == k) x = xk;
+          }
+          if (lane < k) x = cfms(x, ld(&diag[lane * 33 + k]), xk);
+        }
+      }
+      if (lane < bs) st(&z[i0 + lane], x);
+    }
+    __syncthreads();
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(DB_THREADS, 1) dense_batched_kernel(DenseBatchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int d = a.d;
+  double2* P = reinterpret_cast<double2*>(smem_raw);                // d x (NB+1)
+  double2* S = P + (size_t)d * (NB + 1);                            // NB x (SW+1)
+  double2* z = S + (size_t)NB * (DB_SW + 1);                        // d
+  double2* zc = z + d;                                              // d
+  double2* part = zc + d;                                           // 32
+  double2* diag = part + 32;                                        // 32 x 33 (>= 8*32)
+  double* red_v = reinterpret_cast<double*>(diag + 32 * 33);        // 32
+  int* red_i = reinterpret_cast<int*>(red_v + 32);                  // 32
+  int* s_piv = red_i + 32;                                          // NB
+  int* s_sing = s_piv + NB;                                         // 1
+
+  const int tid = threadIdx.x;
+  const int slot = blockIdx.x;
+  double2* W = a.W + (size_t)slot * d * d;
+  int* ipiv = a.ipiv + (size_t)slot * d;
+  const int nsys = a.batch * a.npairs;
+  const size_t dd = (size_t)d * d;
+  const int nc = a.ncols;
+
+  for (int sys = blockIdx.x; sys < nsys; sys += gridDim.x) {
+    const int b = sys / a.npairs, k = sys - b * a.npairs;
+    const cplx th = ld(&a.theta[k]);
+    const cplx co = ld(&a.coef[k]);
+    if (tid == 0) *s_sing = 0;
+    // ---- K0: M = A_b - cI + theta I into the slot
+    if (a.a_complex) {
+      const double2* Ab = reinterpret_cast<const double2*>(a.A) + (size_t)b * dd;
+      for (size_t e = tid; e < dd; e += DB_THREADS) W[e] = Ab[e];
+    } else {
+      const double* Ab = a.A + (size_t)b * dd;
+      for (size_t e = tid; e < dd; e += DB_THREADS) W[e] = make_double2(Ab[e], 0.0);
+    }
+    __syncthreads();
+    for (int i = tid; i < d; i += DB_THREADS) {
+      double2 x = W[(size_t)i * d + i];
+      x.x = (x.x - a.shift_c) + th.re;
+      x.y = x.y + th.im;
+      W[(size_t)i * d + i] = x;
+    }
+    __syncthreads();
+    // ---- K1/K2: LU with partial pivoting
+    lu_blocked<NB>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing);
+    __syncthreads();
+    if (*s_sing && tid == 0) atomicExch(a.status, PFX_SINGULAR);
+    // ---- K3: solves, one RHS column at a time through shared memory
+    double2* Yg = a.Y + (size_t)slot * d * nc;
+    double2* Ycg = a.Yc ? a.Yc + (size_t)slot * d * nc : nullptr;
+    const bool want_conj = (!a.full) && (!a.real_path) && (!a.solve_only);
+    for (int c = 0; c < nc; ++c) {
+      // load RHS column (identity column in full mode)
+      for (int i = tid; i < d; i += DB_THREADS) {
+        double2 v;
+        if (a.full) {
+          v = make_double2(i == c ? 1.0 : 0.0, 0.0);
+        } else if (a.v_complex) {
+          v = reinterpret_cast<const double2*>(a.V)[((size_t)b * d + i) * nc + c];
+        } else {
+          v = make_double2(a.V[((size_t)b * d + i) * nc + c], 0.0);
+        }
+        z[i] = v;
+        zc[i] = v;
+      }
+      __syncthreads();
+      // Y = U^{-1} L^{-1} P V : interchanges in order
+      if (tid == 0)
+        for (int i = 0; i < d; ++i) {
+          int pr = ipiv[i];
+          if (pr != i) {
+            double2 x = z[i];
+            z[i] = z[pr];
+            z[pr] = x;
+          }
+        }
+      __syncthreads();
+      trsv_blocked(W, d, 0, z, part, diag);
+      trsv_blocked(W, d, 1, z, part, diag);
+      for (int i = tid; i < d; i += DB_THREADS) Yg[(size_t)i * nc + c] = z[i];
+      if (want_conj) {
+        // Yc = M^{-H} V = P^T L^{-H} U^{-H} V
+        trsv_blocked(W, d, 2, zc, part, diag);
+        trsv_blocked(W, d, 3, zc, part, diag);
+        if (tid == 0)
+          for (int i = d - 1; i >= 0; --i) {
+            int pr = ipiv[i];
+            if (pr != i) {
+              double2 x = zc[i];
+              zc[i] = zc[pr];
+              zc[pr] = x;
+            }
+          }
+        __syncthreads();
+        for (int i = tid; i < d; i += DB_THREADS) Ycg[(size_t)i * nc + c] = zc[i];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    // ---- K5: residue combine into this system's slot of the stage buffer
+    const size_t ne = (size_t)d * nc;
+    if (a.solve_only) {
+      double2* out = reinterpret_cast<double2*>(a.stage) + (size_t)sys * ne;
+      for (size_t e = tid; e < ne; e += DB_THREADS) out[e] = Yg[e];
+    } else if (a.real_path) {
+      double* out = a.stage + (size_t)sys * ne;
+      for (size_t e = tid; e < ne; e += DB_THREADS) {
+        cplx y = ld(&Yg[e]);
+        out[e] = 2.0 * fma(co.re, y.re, -co.im * y.im);
+      }
+    } else if (!a.full) {
+      double2* out = reinterpret_cast<double2*>(a.stage) + (size_t)sys * ne;
+      for (size_t e = tid; e < ne; e += DB_THREADS) {
+        cplx v = cadd(cmul(co, ld(&Yg[e])), cmul(cconj(co), ld(&Ycg[e])));
+        st(&out[e], v);
+      }
+    } else {
+      double2* out = reinterpret_cast<double2*>(a.stage) + (size_t)sys * ne;
+      for (size_t e = tid; e < ne; e += DB_THREADS) {
+        int i = (int)(e / d), j = (int)(e - (size_t)i * d);
+        cplx x = cmul(co, ld(&Yg[e]));
+        cplx y = cconj(cmul(co, ld(&Yg[(size_t)j * d + i])));
+        st(&out[e], cadd(x, y));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// K6: out[b] = e^c * sum_k stage[b*npairs + k]  (ascending k, bitwise deterministic)
+__global__ void reduce_pairs_kernel(const double* __restrict__ stage, double* __restrict__ out, int batch,
+                                    int npairs, size_t per_sys, double scale) {
+  size_t total = (size_t)batch * per_sys;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t b = e / per_sys, r = e - b * per_sys;
+    const double* base = stage + b * npairs * per_sys + r;
+    double acc = base[0];
+    for (int k = 1; k < npairs; ++k) acc = acc + base[(size_t)k * per_sys];
+    out[e] = scale == 1.0 ? acc : scale * acc;
+  }
+}
+
+static size_t dense_smem_bytes(int d, int nb) {
+  size_t c2 = (size_t)d * (nb + 1) + (size_t)nb * (DB_SW + 1) + 2 * (size_t)d + 32 + 32 * 33;
+  return c2 * sizeof(double2) + 32 * sizeof(double) + (32 + nb + 4) * sizeof(int);
+}
+
+int dense_batched_supported(int64_t d) { return d >= 1 && d <= 512; }
+
+// Launch the batched path.  All pointers are device pointers.
+int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
+                      int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,
+                      int npairs, double* out, cudaStream_t stream, float* launch_ms) {
+  int dev = 0, sms = 0;
+  PFX_CUDA_TRY(cudaGetDevice(&dev));
+  PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int nb = d <= 256 ? 32 : 16;
+  const size_t smem = dense_smem_bytes(d, nb);
+  const int nsys = batch * npairs;
+  const int slots = nsys < sms ? nsys : sms;
+  const size_t per_sys = (size_t)d * ncols;
+  const size_t stage_elems = (size_t)nsys * per_sys * (real_path ? 1 : 2);
+  char* ws = static_cast<char*>(scratch(1, (size_t)slots * ((size_t)d * d + 2 * per_sys) * sizeof(double2) +
+                                               (size_t)slots * d * sizeof(int) + sizeof(int) + 256));
+  if (!ws) return fail(PFX_CUDA, "dense workspace allocation failed");
+  double* stage = static_cast<double*>(scratch(2, stage_elems * sizeof(double)));
+  if (!stage) return fail(PFX_CUDA, "dense stage allocation failed");
+  DenseBatchArgs args;
+  args.A = A;
+  args.a_complex = a_complex;
+  args.d = d;
+  args.batch = batch;
+  args.V = V;
+  args.v_complex = v_complex;
+  args.ncols = ncols;
+  args.full = full;
+  args.real_path = real_path;
+  args.solve_only = solve_only;
+  args.shift_c = shift_c;
+  args.theta = theta_d;
+  args.coef = coef_d;
+  args.npairs = npairs;
+  args.W = reinterpret_cast<double2*>(ws);
+  args.Y = args.W + (size_t)slots * d * d;
+  args.Yc = args.Y + (size_t)slots * per_sys;
+  args.ipiv = reinterpret_cast<int*>(args.Yc + (size_t)slots * per_sys);
+  args.status = args.ipiv + (size_t)slots * d;
+  args.stage = stage;
+  PFX_CUDA_TRY(cudaMemsetAsync(args.status, 0, sizeof(int), stream));
+
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (launch_ms) {
+    PFX_CUDA_TRY(cudaEventCreate(&e0));
+    PFX_CUDA_TRY(cudaEventCreate(&e1));
+    PFX_CUDA_TRY(cudaEventRecord(e0, stream));
+  }
+  if (nb == 32) {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(dense_batched_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PFX_LAUNCH("dense_batched_kernel", stream, dense_batched_kernel<32><<<slots, DB_THREADS, smem, stream>>>(args));
+  } else {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(dense_batched_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PFX_LAUNCH("dense_batched_kernel", stream, dense_batched_kernel<16><<<slots, DB_THREADS, smem, stream>>>(args));
+  }
+  PFX_CUDA_TRY(cudaGetLastError());
+  const size_t per_out = per_sys * (real_path ? 1 : 2);
+  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
+  int rb = (int)std::min<size_t>(ceil_div((size_t)batch * per_out, 256), (size_t)sms * 8);
+  PFX_LAUNCH("reduce_pairs_kernel", stream, reduce_pairs_kernel<<<rb, 256, 0, stream>>>(stage, out, batch, npairs, per_out, scale));
+  PFX_CUDA_TRY(cudaGetLastError());
+  if (launch_ms) {
+    PFX_CUDA_TRY(cudaEventRecord(e1, stream));
+    PFX_CUDA_TRY(cudaEventSynchronize(e1));
+    PFX_CUDA_TRY(cudaEventElapsedTime(launch_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  int st = 0;
+  PFX_CUDA_TRY(cudaMemcpyAsync(&st, args.status, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (st == PFX_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
+  return PFX_OK;
+}
+
+}  // namespace pfx

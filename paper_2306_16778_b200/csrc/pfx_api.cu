@@ -1,0 +1,377 @@
+// C ABI entry points (include/pfx.h): argument checks, host<->device staging,
+// device arena, pole-table upload, dispatch to the kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pfx_common.cuh"
+
+namespace pfx {
+
+// kernels (defined in the other translation units)
+int dense_batched_supported(int64_t d);
+int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
+                      int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,
+                      int npairs, double* out, cudaStream_t stream, float* launch_ms);
+int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
+                    int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
+                    double* out, cudaStream_t stream, float* per_pair_ms);
+int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
+                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
+                float* launch_ms);
+int banded_run(const double* band, int64_t N, int64_t kb, const double* V, int64_t nrhs, double shift_c,
+               const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
+               float* per_pair_ms);
+int pole_table_host(int n, double* theta2, double* coef2);
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int fail(int status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+
+// ---- kernel timing -------------------------------------------------------------
+namespace {
+struct ProfRec {
+  std::string name;
+  cudaEvent_t e0, e1;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+bool g_prof_on = false;
+}  // namespace
+
+bool prof_on() { return g_prof_on; }
+
+void prof_mark(const char* name, cudaStream_t stream, bool begin) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (begin) {
+    ProfRec r;
+    r.name = name;
+    cudaEventCreate(&r.e0);
+    cudaEventCreate(&r.e1);
+    cudaEventRecord(r.e0, stream);
+    g_prof.push_back(r);
+  } else {
+    for (auto it = g_prof.rbegin(); it != g_prof.rend(); ++it)
+      if (it->name == name) {
+        cudaEventRecord(it->e1, stream);
+        break;
+      }
+  }
+}
+
+// ---- arena ------------------------------------------------------------------
+namespace {
+constexpr int kMaxDev = 16;
+constexpr int kSlots = 8;
+struct Arena {
+  void* ptr[kSlots] = {};
+  size_t cap[kSlots] = {};
+};
+Arena g_arena[kMaxDev];
+std::mutex g_arena_mu;
+}  // namespace
+
+void* scratch(int slot, size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev || slot >= kSlots) return nullptr;
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  Arena& a = g_arena[dev];
+  if (bytes == 0) bytes = 16;
+  if (a.cap[slot] < bytes) {
+    if (a.ptr[slot]) {
+      cudaDeviceSynchronize();
+      cudaFree(a.ptr[slot]);
+      a.ptr[slot] = nullptr;
+      a.cap[slot] = 0;
+    }
+    size_t want = bytes + bytes / 8;
+    if (cudaMalloc(&a.ptr[slot], want) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    a.cap[slot] = want;
+  }
+  return a.ptr[slot];
+}
+
+void release_scratch() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev) return;
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  cudaDeviceSynchronize();
+  for (int s = 0; s < kSlots; ++s) {
+    if (g_arena[dev].ptr[s]) cudaFree(g_arena[dev].ptr[s]);
+    g_arena[dev].ptr[s] = nullptr;
+    g_arena[dev].cap[s] = 0;
+  }
+}
+
+// Upload poles (host, interleaved) into arena slot 0.
+static int upload_poles(const double* theta2, const double* coef2, int npairs, cudaStream_t stream,
+                        const double2** th, const double2** co) {
+  double2* p = static_cast<double2*>(scratch(0, 2 * (size_t)npairs * sizeof(double2)));
+  if (!p) return fail(PFX_CUDA, "pole upload allocation failed");
+  std::vector<double> tmp(4 * (size_t)npairs);
+  std::memcpy(tmp.data(), theta2, 2 * npairs * sizeof(double));
+  std::memcpy(tmp.data() + 2 * npairs, coef2, 2 * npairs * sizeof(double));
+  PFX_CUDA_TRY(cudaMemcpyAsync(p, tmp.data(), tmp.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  *th = p;
+  *co = p + npairs;
+  return PFX_OK;
+}
+
+static int check_poles(const double* theta2, const double* coef2, int npairs) {
+  if (!theta2 || !coef2) return fail(PFX_BADARG, "theta2/coef2 must be non-null host arrays");
+  if (npairs < 1 || npairs > 32) return fail(PFX_BADARG, "npairs must be in [1, 32]");
+  for (int k = 0; k < npairs; ++k) {
+    if (!std::isfinite(theta2[2 * k]) || !std::isfinite(theta2[2 * k + 1]) || !std::isfinite(coef2[2 * k]) ||
+        !std::isfinite(coef2[2 * k + 1]))
+      return fail(PFX_BADARG, "non-finite pole or residue");
+    if (!(theta2[2 * k + 1] > 0.0)) return fail(PFX_BADARG, "pole representatives must have Im(theta) > 0");
+  }
+  return PFX_OK;
+}
+
+// Host staging: copy host inputs into arena slots 3..5, output into slot 6.
+struct Staged {
+  const double* in[3] = {nullptr, nullptr, nullptr};
+  double* out = nullptr;
+};
+
+static int stage_in(int mem, int slot, const double* src, size_t bytes, cudaStream_t stream, const double** dst) {
+  if (mem == PFX_MEM_DEVICE || src == nullptr || bytes == 0) {
+    *dst = src;
+    return PFX_OK;
+  }
+  void* p = scratch(slot, bytes);
+  if (!p) return fail(PFX_CUDA, "staging allocation failed");
+  PFX_CUDA_TRY(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, stream));
+  *dst = static_cast<const double*>(p);
+  return PFX_OK;
+}
+
+}  // namespace pfx
+
+using namespace pfx;
+
+extern "C" {
+
+int pfx_version(void) { return 100; }
+
+int pfx_prof_enable(int on) {
+  g_prof_on = on != 0;
+  return PFX_OK;
+}
+
+int pfx_prof_read(char* buf, int buflen) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::vector<std::string> names;
+  std::vector<int> counts;
+  std::vector<double> totals;
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.e1);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+    size_t i = 0;
+    for (; i < names.size(); ++i)
+      if (names[i] == r.name) break;
+    if (i == names.size()) {
+      names.push_back(r.name);
+      counts.push_back(0);
+      totals.push_back(0.0);
+    }
+    counts[i] += 1;
+    totals[i] += ms;
+  }
+  g_prof.clear();
+  std::string out;
+  char line[256];
+  for (size_t i = 0; i < names.size(); ++i) {
+    snprintf(line, sizeof(line), "%s %d %.6f\n", names[i].c_str(), counts[i], totals[i]);
+    out += line;
+  }
+  if (buf && buflen > 0) {
+    size_t n = std::min<size_t>(out.size(), (size_t)buflen - 1);
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int)out.size() + 1;
+}
+
+const char* pfx_last_error(void) { return g_err.c_str(); }
+
+int pfx_release(void) {
+  release_scratch();
+  return PFX_OK;
+}
+
+int pfx_pole_table(int n, double* theta2, double* coef2) {
+  if (!theta2 || !coef2) return fail(PFX_BADARG, "null output array");
+  if (n < 2 || n > 64 || (n & 1)) return fail(PFX_BADARG, "order must be even and in [2, 64]");
+  return pole_table_host(n, theta2, coef2);
+}
+
+int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t batch, const double* V,
+                   int v_complex, int64_t nrhs, double shift_c, const double* theta2, const double* coef2,
+                   int npairs, double* out, int out_complex, float* per_pair_ms, void* stream_) {
+  g_err.clear();
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (mem != PFX_MEM_DEVICE && mem != PFX_MEM_HOST) return fail(PFX_BADARG, "mem must be PFX_MEM_DEVICE or PFX_MEM_HOST");
+  if (!A || !out) return fail(PFX_BADARG, "A and out must be non-null");
+  if (d < 1 || batch < 1 || nrhs < 0) return fail(PFX_BADARG, "need d >= 1, batch >= 1, nrhs >= 0");
+  if (nrhs > 0 && !V) return fail(PFX_BADARG, "action mode needs V");
+  if (!std::isfinite(shift_c)) return fail(PFX_BADARG, "shift must be finite");
+  int rc = check_poles(theta2, coef2, npairs);
+  if (rc) return rc;
+  const int full = nrhs == 0;
+  const int real_path = (!a_complex) && (full || !v_complex);
+  if (out_complex != !real_path)
+    return fail(PFX_BADARG, "out_complex must be 1 exactly when A is complex or V is complex (engine.py:185)");
+  const int ncols = full ? (int)d : (int)nrhs;
+  if (!dense_batched_supported(d) && batch != 1)
+    return fail(PFX_BADARG, "batched dense path supports d <= 512; larger matrices must be passed one at a time");
+  const size_t abytes = (size_t)batch * d * d * sizeof(double) * (a_complex ? 2 : 1);
+  const size_t vbytes = full ? 0 : (size_t)batch * d * nrhs * sizeof(double) * (v_complex ? 2 : 1);
+  const size_t obytes = (size_t)batch * d * ncols * sizeof(double) * (out_complex ? 2 : 1);
+  const double2 *th = nullptr, *co = nullptr;
+  rc = upload_poles(theta2, coef2, npairs, stream, &th, &co);
+  if (rc) return rc;
+  const double *Ad = nullptr, *Vd = nullptr;
+  if ((rc = stage_in(mem, 3, A, abytes, stream, &Ad))) return rc;
+  if ((rc = stage_in(mem, 4, V, vbytes, stream, &Vd))) return rc;
+  double* Od = out;
+  if (mem == PFX_MEM_HOST) {
+    Od = static_cast<double*>(scratch(6, obytes));
+    if (!Od) return fail(PFX_CUDA, "staging allocation failed");
+  }
+  float ms = 0.0f;
+  if (dense_batched_supported(d)) {
+    rc = dense_batched_run(Ad, a_complex, (int)d, (int)batch, Vd, v_complex, ncols, full, real_path, 0, shift_c, th, co,
+                           npairs, Od, stream, per_pair_ms ? &ms : nullptr);
+    if (per_pair_ms)
+      for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
+  } else {
+    rc = dense_large_run(Ad, a_complex, (int)d, Vd, v_complex, ncols, full, real_path, shift_c, th, co, npairs, Od,
+                         stream, per_pair_ms);
+  }
+  if (rc) return rc;
+  if (mem == PFX_MEM_HOST) {
+    PFX_CUDA_TRY(cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, stream));
+    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  return PFX_OK;
+}
+
+int pfx_expm_tridiag(int mem, const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs,
+                     double shift_c, const double* theta2, const double* coef2, int npairs, double* out,
+                     float* per_pair_ms, void* stream_) {
+  g_err.clear();
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (mem != PFX_MEM_DEVICE && mem != PFX_MEM_HOST) return fail(PFX_BADARG, "bad mem kind");
+  if (N < 1 || nrhs < 1) return fail(PFX_BADARG, "need N >= 1 and nrhs >= 1");
+  if (!diag || !V || !out || (N > 1 && !off)) return fail(PFX_BADARG, "null array");
+  if (!std::isfinite(shift_c)) return fail(PFX_BADARG, "shift must be finite");
+  int rc = check_poles(theta2, coef2, npairs);
+  if (rc) return rc;
+  const double2 *th = nullptr, *co = nullptr;
+  if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
+  const double *Dd = nullptr, *Od_ = nullptr, *Vd = nullptr;
+  if ((rc = stage_in(mem, 3, diag, N * sizeof(double), stream, &Dd))) return rc;
+  if ((rc = stage_in(mem, 4, off, (N - 1) * sizeof(double), stream, &Od_))) return rc;
+  if ((rc = stage_in(mem, 5, V, (size_t)N * nrhs * sizeof(double), stream, &Vd))) return rc;
+  double* Out = out;
+  const size_t obytes = (size_t)N * nrhs * sizeof(double);
+  if (mem == PFX_MEM_HOST) {
+    Out = static_cast<double*>(scratch(6, obytes));
+    if (!Out) return fail(PFX_CUDA, "staging allocation failed");
+  }
+  float ms = 0.0f;
+  rc = tridiag_run(Dd, Od_, N, Vd, nrhs, shift_c, th, co, npairs, Out, stream, per_pair_ms ? &ms : nullptr);
+  if (rc) return rc;
+  if (per_pair_ms)
+    for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
+  if (mem == PFX_MEM_HOST) {
+    PFX_CUDA_TRY(cudaMemcpyAsync(out, Out, obytes, cudaMemcpyDeviceToHost, stream));
+    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  return PFX_OK;
+}
+
+int pfx_expm_banded(int mem, const double* band, int64_t N, int64_t kb, const double* V, int64_t nrhs,
+                    double shift_c, const double* theta2, const double* coef2, int npairs, double* out,
+                    float* per_pair_ms, void* stream_) {
+  g_err.clear();
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (mem != PFX_MEM_DEVICE && mem != PFX_MEM_HOST) return fail(PFX_BADARG, "bad mem kind");
+  if (N < 1 || nrhs < 1 || kb < 0) return fail(PFX_BADARG, "need N >= 1, nrhs >= 1, kb >= 0");
+  if (!band || !V || !out) return fail(PFX_BADARG, "null array");
+  if (!std::isfinite(shift_c)) return fail(PFX_BADARG, "shift must be finite");
+  int rc = check_poles(theta2, coef2, npairs);
+  if (rc) return rc;
+  const double2 *th = nullptr, *co = nullptr;
+  if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
+  const double *Bd = nullptr, *Vd = nullptr;
+  if ((rc = stage_in(mem, 3, band, (size_t)(kb + 1) * N * sizeof(double), stream, &Bd))) return rc;
+  if ((rc = stage_in(mem, 5, V, (size_t)N * nrhs * sizeof(double), stream, &Vd))) return rc;
+  double* Out = out;
+  const size_t obytes = (size_t)N * nrhs * sizeof(double);
+  if (mem == PFX_MEM_HOST) {
+    Out = static_cast<double*>(scratch(6, obytes));
+    if (!Out) return fail(PFX_CUDA, "staging allocation failed");
+  }
+  rc = banded_run(Bd, N, kb, Vd, nrhs, shift_c, th, co, npairs, Out, stream, per_pair_ms);
+  if (rc) return rc;
+  if (mem == PFX_MEM_HOST) {
+    PFX_CUDA_TRY(cudaMemcpyAsync(out, Out, obytes, cudaMemcpyDeviceToHost, stream));
+    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  return PFX_OK;
+}
+
+int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double theta_re, double theta_im,
+                      const double* V, int64_t nrhs, double* Y, void* stream_) {
+  g_err.clear();
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (mem != PFX_MEM_DEVICE && mem != PFX_MEM_HOST) return fail(PFX_BADARG, "bad mem kind");
+  if (!A || !V || !Y || d < 1 || nrhs < 1) return fail(PFX_BADARG, "need A, V, Y non-null, d >= 1, nrhs >= 1");
+  if (!dense_batched_supported(d)) return fail(PFX_BADARG, "pfx_shifted_solve supports d <= 512");
+  if (!std::isfinite(theta_re) || !std::isfinite(theta_im)) return fail(PFX_BADARG, "non-finite shift");
+  // one system, residue 1: stage = Y = (A + theta I)^{-1} V (complex V, complex Y)
+  double th2[2] = {theta_re, theta_im}, co2[2] = {1.0, 0.0};
+  const double2 *th = nullptr, *co = nullptr;
+  int rc = upload_poles(th2, co2, 1, stream, &th, &co);
+  if (rc) return rc;
+  const size_t abytes = (size_t)d * d * sizeof(double) * (a_complex ? 2 : 1);
+  const size_t vbytes = (size_t)d * nrhs * 2 * sizeof(double);
+  const double *Ad = nullptr, *Vd = nullptr;
+  if ((rc = stage_in(mem, 3, A, abytes, stream, &Ad))) return rc;
+  if ((rc = stage_in(mem, 4, V, vbytes, stream, &Vd))) return rc;
+  double* Yd = Y;
+  if (mem == PFX_MEM_HOST) {
+    Yd = static_cast<double*>(scratch(6, vbytes));
+    if (!Yd) return fail(PFX_CUDA, "staging allocation failed");
+  }
+  rc = dense_batched_run(Ad, a_complex, (int)d, 1, Vd, 1, (int)nrhs, 0, 0, 1, 0.0, th, co, 1, Yd, stream, nullptr);
+  if (rc) return rc;
+  if (mem == PFX_MEM_HOST) {
+    PFX_CUDA_TRY(cudaMemcpyAsync(Y, Yd, vbytes, cudaMemcpyDeviceToHost, stream));
+    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  return PFX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Shared device helpers for the pfx kernels (sm_100a).
+//
+// Complex values are interleaved binary64 pairs (double2 {re, im}) in HBM,
+// exactly the numpy complex128 layout, so host buffers map 1:1.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/pfx.h"
+
+namespace pfx {
+
+// ---- status / error plumbing (host) -------------------------------------
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+#define PFX_CUDA_TRY(expr)                                                              \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return ::pfx::fail(PFX_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// Grow-only device scratch arena, one per (device, slot).  Slots let one call
+// hold several live buffers.  Freed by pfx_release().
+void* scratch(int slot, size_t bytes);
+void release_scratch();
+
+// Kernel timing (pfx_prof_enable / pfx_prof_read).  PFX_LAUNCH brackets a launch
+// with events when profiling is on; otherwise it is just the launch.
+bool prof_on();
+void prof_mark(const char* name, cudaStream_t stream, bool begin);
+#define PFX_LAUNCH(name, stream, ...)                 \
+  do {                                                \
+    if (::pfx::prof_on()) ::pfx::prof_mark(name, stream, true);  \
+    __VA_ARGS__;                                      \
+    if (::pfx::prof_on()) ::pfx::prof_mark(name, stream, false); \
+  } while (0)
+
+// ---- complex arithmetic (device) -----------------------------------------
+struct cplx {
+  double re, im;
+};
+
+__host__ __device__ __forceinline__ cplx mk(double r, double i) { return cplx{r, i}; }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cplx{fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
+}
+// a * conj(b)
+__host__ __device__ __forceinline__ cplx cmulc(cplx a, cplx b) {
+  return cplx{fma(a.re, b.re, a.im * b.im), fma(a.im, b.re, -a.re * b.im)};
+}
+// c - a*b
+__host__ __device__ __forceinline__ cplx cfms(cplx c, cplx a, cplx b) {
+  return cplx{fma(-a.re, b.re, fma(a.im, b.im, c.re)), fma(-a.re, b.im, fma(-a.im, b.re, c.im))};
+}
+__host__ __device__ __forceinline__ cplx cconj(cplx a) { return cplx{a.re, -a.im}; }
+__host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cplx{a.re * s, a.im * s}; }
+// 1/z with Smith-style scaling to avoid overflow/underflow of |z|^2
+__host__ __device__ __forceinline__ cplx crcp(cplx z) {
+  double ar = fabs(z.re), ai = fabs(z.im);
+  if (ar >= ai) {
+    double r = z.im / z.re;
+    double den = 1.0 / fma(z.im, r, z.re);
+    return cplx{den, -r * den};
+  } else {
+    double r = z.re / z.im;
+    double den = 1.0 / fma(z.re, r, z.im);
+    return cplx{r * den, -den};
+  }
+}
+__host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) { return cmul(a, crcp(b)); }
+__host__ __device__ __forceinline__ double cabs1(cplx a) { return fabs(a.re) + fabs(a.im); }
+
+__device__ __forceinline__ cplx ld(const double2* p) {
+  double2 v = *p;
+  return cplx{v.x, v.y};
+}
+__device__ __forceinline__ void st(double2* p, cplx v) { *p = make_double2(v.re, v.im); }
+
+// ---- FP64 tensor core (DMMA) ---------------------------------------------
+// D(8x8) += A(8x4, row) * B(4x8, col), binary64.  Fragment ownership for lane l,
+// g = l>>2, t = l&3:  a = A[g][t], b = B[t][g], c0 = C[g][2t], c1 = C[g][2t+1].
+// ptxas lowers this to one native DMMA.8x8x4 on sm_100a.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Complex 8x8x4 tile product C += A*B on four real DMMAs.
+//   Cr += Ar*Br - Ai*Bi,   Ci += Ar*Bi + Ai*Br
+__device__ __forceinline__ void zmma884(double (&cr)[2], double (&ci)[2], double ar, double ai, double br,
+                                        double bi) {
+  dmma884(cr[0], cr[1], ar, br);
+  dmma884(cr[0], cr[1], -ai, bi);
+  dmma884(ci[0], ci[1], ar, bi);
+  dmma884(ci[0], ci[1], ai, br);
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace pfx

@@ -1,0 +1,78 @@
+"""The C-ABI library loads, exports every symbol include/pfx.h declares, and rejects
+bad arguments with the documented status codes (no GPU work involved)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2306_16778_b200 import _native
+from paper_2306_16778_b200.errors import PFX_BADARG
+
+from .conftest import ROOT
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "pfx.h")).read()
+    return sorted(set(re.findall(r"\b(pfx_[a-z_]+)\s*\(", text)))
+
+
+def test_header_symbols_exported():
+    names = _declared()
+    assert {"pfx_expm_dense", "pfx_expm_tridiag", "pfx_expm_banded", "pfx_pole_table"} <= set(names)
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_native.SIGNATURES)
+
+
+def test_version_and_error_string():
+    lib = _native.lib()
+    assert lib.pfx_version() >= 100
+    assert isinstance(lib.pfx_last_error(), bytes)
+
+
+def _poles(n=16):
+    from paper_2306_16778_b200.roots import default_table
+
+    return default_table(n).interleaved()
+
+
+def test_dense_bad_arguments():
+    lib = _native.lib()
+    t2, c2 = _poles()
+    A = np.zeros((4, 4))
+    out = np.zeros(4)
+    V = np.ones(4)
+    f64 = _native._f64p
+    # bad memory kind
+    assert lib.pfx_expm_dense(7, A.ctypes.data, 0, 4, 1, V.ctypes.data, 0, 1, 0.0, f64(t2), f64(c2), 8,
+                              out.ctypes.data, 0, None, None) == PFX_BADARG
+    # out_complex inconsistent with the real path (engine.py:185)
+    assert lib.pfx_expm_dense(1, A.ctypes.data, 0, 4, 1, V.ctypes.data, 0, 1, 0.0, f64(t2), f64(c2), 8,
+                              out.ctypes.data, 1, None, None) == PFX_BADARG
+    assert b"out_complex" in lib.pfx_last_error()
+    # non-positive Im(theta)
+    bad = t2.copy()
+    bad[1] = -1.0
+    assert lib.pfx_expm_dense(1, A.ctypes.data, 0, 4, 1, V.ctypes.data, 0, 1, 0.0, f64(bad), f64(c2), 8,
+                              out.ctypes.data, 0, None, None) == PFX_BADARG
+    # d < 1
+    assert lib.pfx_expm_dense(1, A.ctypes.data, 0, 0, 1, V.ctypes.data, 0, 1, 0.0, f64(t2), f64(c2), 8,
+                              out.ctypes.data, 0, None, None) == PFX_BADARG
+    # infinite shift
+    assert lib.pfx_expm_dense(1, A.ctypes.data, 0, 4, 1, V.ctypes.data, 0, 1, float("inf"), f64(t2), f64(c2), 8,
+                              out.ctypes.data, 0, None, None) == PFX_BADARG
+
+
+def test_structured_bad_arguments():
+    lib = _native.lib()
+    t2, c2 = _poles()
+    f64 = _native._f64p
+    x = np.zeros(8)
+    assert lib.pfx_expm_tridiag(1, x.ctypes.data, x.ctypes.data, 0, x.ctypes.data, 1, 0.0, f64(t2), f64(c2), 8,
+                                x.ctypes.data, None, None) == PFX_BADARG
+    assert lib.pfx_expm_banded(1, x.ctypes.data, 8, -1, x.ctypes.data, 1, 0.0, f64(t2), f64(c2), 8,
+                               x.ctypes.data, None, None) == PFX_BADARG
+    assert lib.pfx_pole_table(3, f64(x), f64(x)) == PFX_BADARG

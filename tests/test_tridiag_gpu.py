@@ -1,0 +1,70 @@
+"""Tridiagonal path (config C2) on the GPU vs the CPU restatement (zgtsv per pair)."""
+import numpy as np
+import pytest
+
+from oracle import closed, restate
+from paper_2306_16778_b200 import ExpOptions, TridiagonalHermitian, matexp_action, matexp_shifted, workloads
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 127, 128, 129, 1000, 4096, 10007])
+@pytest.mark.parametrize("nrhs", [1, 16])
+def test_sizes(N, nrhs):
+    d, o = workloads.c2_matrix(N, scale=25.0)
+    rng = np.random.default_rng(N)
+    d = d + rng.uniform(-5, 5, N)  # non-constant diagonal
+    o = o * rng.uniform(0.5, 1.5, N - 1)
+    V = rng.standard_normal((N, nrhs))
+    got = matexp_action(TridiagonalHermitian(d, o), V, ExpOptions(n=24, mode="action")).value
+    want = restate.tridiag_action(d, o, V, 24)
+    assert got.shape == want.shape
+    assert rel(got, want) <= TOL, rel(got, want)
+
+
+@pytest.mark.parametrize("n", [2, 16, 40, 64])
+def test_orders(n):
+    N = 3000
+    d, o = workloads.c2_matrix(N, scale=2.0)
+    V = np.random.default_rng(5).standard_normal((N, 3))
+    got = matexp_action(TridiagonalHermitian(d, o), V, ExpOptions(n=n, mode="action")).value
+    assert rel(got, restate.tridiag_action(d, o, V, n)) <= TOL
+
+
+def test_ragged_rhs_tiles():
+    N, nrhs = 2000, 37
+    d, o = workloads.c2_matrix(N)
+    V = np.random.default_rng(6).standard_normal((N, nrhs))
+    got = matexp_action(TridiagonalHermitian(d, o), V, ExpOptions(n=24, mode="action")).value
+    assert rel(got, restate.tridiag_action(d, o, V, 24)) <= TOL
+
+
+def test_vector_rhs_and_shift():
+    N = 5000
+    d, o = workloads.c2_matrix(N, scale=1.0)
+    d = d + 3.0  # spectrum in (-1, 3): needs the shift method
+    v = np.random.default_rng(7).standard_normal(N)
+    T = TridiagonalHermitian(d, o)
+    res = matexp_shifted(T, ExpOptions(n=32, mode="action", shift="auto"), v=v)
+    c = res.c_applied
+    want = np.exp(c) * restate.tridiag_action(d - c, o, v, 32)
+    assert res.value.shape == (N,)
+    assert rel(res.value, want) <= TOL
+
+
+def test_c2_full_size_properties():
+    """C2 at its BASELINE size: P1 on a column subset vs zgtsv, P2 vs the DST oracle."""
+    N, nrhs = workloads.C2["N"], workloads.C2["nrhs"]
+    d, o = workloads.c2_matrix()
+    V = workloads.c2_rhs()
+    got = matexp_action(TridiagonalHermitian(d, o), V, ExpOptions(n=24, mode="action")).value
+    cols = [0, 9]
+    want = restate.tridiag_action(d, o, V, 24, cols=cols)
+    assert rel(got[:, cols], want) <= TOL
+    E = closed.dst_exp_lap1d(N, 25.0, V[:, cols])
+    assert np.linalg.norm(got[:, cols] - E) <= 10 * np.linalg.norm(want - E)
