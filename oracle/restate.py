@@ -115,6 +115,8 @@ def tridiag_action(diag, off, V, n: int, threads: int = 1, cols=None):
     B = (V[:, None] if squeeze else V).astype(complex)
 
     def task(slot):
+        if diag.shape[0] == 1:  # zgtsv wrapper rejects empty off-diagonals
+            return 2.0 * (coef[slot] * (B / (diag[0] + theta[slot]))).real
         _, _, _, y, info = lapack.zgtsv(off, diag + theta[slot], off, B)
         if info != 0:
             raise np.linalg.LinAlgError(f"zgtsv info={info}")

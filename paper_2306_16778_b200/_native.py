@@ -99,8 +99,7 @@ def prof_enable(on: bool) -> None:
 
 def prof_read() -> dict:
     """{kernel name: (launches, total_ms)} since the last read (synchronises the events)."""
-    need = lib().pfx_prof_read(None, 0)
-    buf = ctypes.create_string_buffer(max(need, 1) + 64)
+    buf = ctypes.create_string_buffer(1 << 16)
     lib().pfx_prof_read(buf, len(buf))
     out = {}
     for line in buf.value.decode().splitlines():

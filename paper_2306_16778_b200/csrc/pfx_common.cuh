@@ -74,6 +74,25 @@ __host__ __device__ __forceinline__ cplx crcp(cplx z) {
   }
 }
 __host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) { return cmul(a, crcp(b)); }
+
+// Fast binary64 reciprocal: MUFU seed + two Newton steps (<= 1 ulp for normal x).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+// 1/z = conj(z)/|z|^2 with the fast reciprocal; falls back to the scaled form
+// when |z|^2 leaves the comfortable exponent range.
+__device__ __forceinline__ cplx crcp_fast(cplx z) {
+  double n = fma(z.re, z.re, z.im * z.im);
+  if (!(n > 1e-280 && n < 1e280)) return crcp(z);
+  double r = frcp(n);
+  return cplx{z.re * r, -z.im * r};
+}
+__device__ __forceinline__ cplx cdiv_fast(cplx a, cplx b) { return cmul(a, crcp_fast(b)); }
 __host__ __device__ __forceinline__ double cabs1(cplx a) { return fabs(a.re) + fabs(a.im); }
 
 __device__ __forceinline__ cplx ld(const double2* p) {
@@ -100,6 +119,21 @@ __device__ __forceinline__ void zmma884(double (&cr)[2], double (&ci)[2], double
   dmma884(cr[0], cr[1], -ai, bi);
   dmma884(ci[0], ci[1], ar, bi);
   dmma884(ci[0], ci[1], ai, br);
+}
+
+// ---- async copies (LDGSTS) ---------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

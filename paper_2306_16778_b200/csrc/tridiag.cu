@@ -39,7 +39,7 @@ namespace pfx {
 constexpr int TR_L = 128;     // rows per chunk
 constexpr int TR_RT = 16;     // RHS per tile (threads per shift)
 constexpr int TR_KG = 16;     // max shifts per pass
-constexpr int TR_WIN = 8;     // rows per combine window
+constexpr int TR_WIN = 4;     // rows per combine window
 constexpr int TR_SCAN_T = 512;
 
 struct TriArgs {
@@ -63,6 +63,9 @@ struct TriArgs {
   double2* LB;  // P x npairs          prod(-l') over the chunk
   double2* G;   // P x npairs x nrhs   true forward carry-in g_{s-1}
   double2* Gb;  // P x npairs x nrhs   true backward carry-in g'_{e}
+  double2* Lf;  // N x npairs  forward multipliers l_i
+  double2* Lb;  // N x npairs  backward multipliers l'_i
+  double2* Wt;  // N x npairs  twisted weights 2a/gamma_i
   double* out;  // N x nrhs
 };
 
@@ -211,166 +214,201 @@ __global__ void __launch_bounds__(TR_SCAN_T) tri_mobius_scan(TriArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Shared-memory factor data of one chunk for a group of shifts.
-struct TriSmem {
-  double dg[TR_L];            // diag - c
-  double of[TR_L + 1];        // of[i] = e_{s-1+i}  (coupling rows s-1+i, s+i), 0 outside
-  double2 l[TR_KG][TR_L];     // forward multipliers
-  double2 lb[TR_KG][TR_L];    // backward multipliers
-  double2 w[TR_KG][TR_L];     // 2 a / gamma (or w*Lambda in the correction kernel)
-  double2 wb[TR_KG][TR_L];    // correction kernel only: w*Lambda'
-  double cbuf[TR_KG][TR_WIN][TR_RT];
-  double F[TR_L][TR_RT];
-  double2 lam[TR_KG][2];      // chunk products / carries
-};
-
-// Pivot chains for shift slot kk (thread-level, serial in rows), writing l / lb,
-// and (want_lambda) the running products Lambda into w / wb.
-__device__ void tri_chain(TriSmem& S, const TriArgs& a, int64_t c, int k, int kk, int dir, int rows,
-                          bool want_lambda) {
-  const cplx th = ld(&a.theta[k]);
-  if (dir == 0) {
-    cplx rho = ld(&a.rho_in[c * a.npairs + k]);
-    cplx lam = mk(1, 0);
-    for (int i = 0; i < rows; ++i) {
-      cplx b = mk(S.dg[i] + th.re, th.im);
-      double e = S.of[i];
-      cplx l = cscale(rho, e);
-      cplx u = csub(b, cscale(l, e));
-      rho = crcp(u);
-      S.l[kk][i] = make_double2(l.re, l.im);
-      lam = cmul(lam, mk(-l.re, -l.im));
-      if (want_lambda) S.w[kk][i] = make_double2(lam.re, lam.im);
-    }
-    S.lam[kk][0] = make_double2(lam.re, lam.im);
-  } else {
-    cplx rho = ld(&a.rhob_in[c * a.npairs + k]);
-    cplx lam = mk(1, 0);
-    for (int i = rows - 1; i >= 0; --i) {
-      cplx b = mk(S.dg[i] + th.re, th.im);
-      double e = S.of[i + 1];
-      cplx l = cscale(rho, e);
-      cplx u = csub(b, cscale(l, e));
-      rho = crcp(u);
-      S.lb[kk][i] = make_double2(l.re, l.im);
-      lam = cmul(lam, mk(-l.re, -l.im));
-      if (want_lambda) S.wb[kk][i] = make_double2(lam.re, lam.im);
-    }
-    S.lam[kk][1] = make_double2(lam.re, lam.im);
-  }
+// K_T3 tri_factor: one thread per (chunk, shift).  Pivot chains in continuant form
+// (the only loop-carried dependency is the three-term recurrence; the ratio
+// rho = p_{i-2}/p_{i-1} and everything after it is off the critical path):
+//   backward: q_i = b_i q_{i+1} - e_i^2 q_{i+2},  l'_i = e_i q_{i+2}/q_{i+1}
+//   forward:  p_i = b_i p_{i-1} - e_{i-1}^2 p_{i-2}, l_i = e_{i-1} p_{i-2}/p_{i-1}
+//   gamma_i = b_i - e_{i-1} l_i - e_i l'_i,  w_i = 2 a / gamma_i
+// Outputs (row-major [row][shift], so a row's shifts are contiguous for the sweeps):
+//   Lf = l, Lb = l', Wt = w, and the chunk products LF = prod(-l), LB = prod(-l').
+__device__ __forceinline__ void rescale2(cplx& x, cplx& y) {
+  double mx = fmax(fmax(cabs1(x), cabs1(y)), 1e-300);
+  int ex;
+  frexp(mx, &ex);
+  double s = ldexp(1.0, -ex);
+  x = cscale(x, s);
+  y = cscale(y, s);
 }
 
-__device__ void tri_load_chunk(TriSmem& S, const TriArgs& a, int64_t s, int rows) {
-  for (int i = threadIdx.x; i < rows; i += blockDim.x) S.dg[i] = a.diag[s + i] - a.c;
-  for (int i = threadIdx.x; i <= rows; i += blockDim.x) {
-    int64_t gi = s - 1 + i;  // coupling (gi, gi+1)
-    S.of[i] = (gi >= 0 && gi < a.N - 1) ? a.off[gi] : 0.0;
-  }
-}
-
-// gamma / w for all (kk, i) of the chunk
-__device__ void tri_weights(TriSmem& S, const TriArgs& a, int k0, int kg, int rows, double2 (*dst)[TR_L]) {
-  for (int e = threadIdx.x; e < kg * rows; e += blockDim.x) {
-    int kk = e / rows, i = e - kk * rows;
-    const cplx th = ld(&a.theta[k0 + kk]);
-    cplx b = mk(S.dg[i] + th.re, th.im);
-    cplx l = ld(&S.l[kk][i]), lb = ld(&S.lb[kk][i]);
-    // gamma = b - e_{i-1} l_i - e_i l'_i
-    cplx gam = csub(csub(b, cscale(l, S.of[i])), cscale(lb, S.of[i + 1]));
-    cplx co = ld(&a.coef[k0 + kk]);
-    cplx w = cscale(cdiv(co, gam), 2.0);
-    dst[kk][i] = make_double2(w.re, w.im);
-  }
-}
-
-// K_T3 ------------------------------------------------------------------------
-__global__ void __launch_bounds__(TR_RT* TR_KG) tri_local(TriArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TriSmem& S = *reinterpret_cast<TriSmem*>(smem_raw);
-  const int64_t c = blockIdx.x;
-  const int r0 = blockIdx.y * TR_RT;
+__global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= (int64_t)a.P * a.npairs) return;
+  const int k = (int)(tid % a.npairs);
+  const int64_t c = tid / a.npairs;
   const int64_t s = c * TR_L;
   const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
-  const int t = threadIdx.x;
-  const int r = t % TR_RT;       // rhs lane
-  const int kk = t / TR_RT;      // shift slot
-  const int rg = r0 + r;
-  const bool rv = rg < a.nrhs;
-  tri_load_chunk(S, a, s, rows);
-  for (int i = t; i < rows * TR_RT; i += blockDim.x) (&S.F[0][0])[i] = 0.0;
-  __syncthreads();
-  for (int k0 = 0; k0 < a.npairs; k0 += TR_KG) {
-    const int kg = min(TR_KG, a.npairs - k0);
-    // pivot chains: threads [0,kg) forward, [kg, 2kg) backward
-    if (t < 2 * kg) tri_chain(S, a, c, k0 + (t % kg), t % kg, t / kg, rows, false);
-    __syncthreads();
-    tri_weights(S, a, k0, kg, rows, S.w);
-    __syncthreads();
-    const bool active = kk < kg;
-    const int k = k0 + kk;
-    // forward sweep: contributions 2 Re(w (g - f))
-    cplx g = mk(0, 0);
-    for (int i0 = 0; i0 < rows; i0 += TR_WIN) {
-      const int wn = min(TR_WIN, rows - i0);
-      if (active) {
-        for (int j = 0; j < wn; ++j) {
-          const int i = i0 + j;
-          double f = rv ? a.V[(s + i) * a.nrhs + rg] : 0.0;
-          cplx l = ld(&S.l[kk][i]);
-          g = cplx{fma(-l.re, g.re, fma(l.im, g.im, f)), fma(-l.re, g.im, -l.im * g.re)};
-          cplx w = ld(&S.w[kk][i]);
-          S.cbuf[kk][j][r] = fma(w.re, g.re - f, -w.im * g.im);
-        }
-      }
-      __syncthreads();
-      for (int e = t; e < wn * TR_RT; e += blockDim.x) {
-        int j = e / TR_RT, rr = e - j * TR_RT;
-        double acc = S.F[i0 + j][rr];
-        for (int q = 0; q < kg; ++q) acc += S.cbuf[q][j][rr];
-        S.F[i0 + j][rr] = acc;
-      }
-      __syncthreads();
+  const cplx th = ld(&a.theta[k]);
+  const int np = a.npairs;
+  auto offe = [&](int64_t gi) -> double { return (gi >= 0 && gi < a.N - 1) ? a.off[gi] : 0.0; };
+  // backward chain
+  {
+    cplx q1 = mk(1, 0), q2 = ld(&a.rhob_in[c * np + k]);
+    cplx lam = mk(1, 0);
+    double e = offe(s + rows - 1);
+    for (int i = rows - 1; i >= 0; --i) {
+      cplx rho = cmul(q2, crcp_fast(q1));
+      cplx lv = cscale(rho, e);
+      cplx b = mk(a.diag[s + i] - a.c + th.re, th.im);
+      double e2 = e * e;
+      cplx q0 = cplx{fma(b.re, q1.re, fma(-b.im, q1.im, -e2 * q2.re)), fma(b.re, q1.im, fma(b.im, q1.re, -e2 * q2.im))};
+      st(&a.Lb[(s + i) * np + k], lv);
+      lam = cmul(lam, mk(-lv.re, -lv.im));
+      q2 = q1;
+      q1 = q0;
+      if ((i & 3) == 0) rescale2(q1, q2);
+      e = offe(s + i - 1);
     }
-    if (active && rv) st(&a.gF[(c * a.npairs + k) * a.nrhs + rg], g);
-    // backward sweep: contributions 2 Re(w g')
-    cplx gb = mk(0, 0);
-    for (int i1 = rows; i1 > 0; i1 -= TR_WIN) {
-      const int wn = min(TR_WIN, i1);
-      const int i0 = i1 - wn;
-      if (active) {
-        for (int j = wn - 1; j >= 0; --j) {
-          const int i = i0 + j;
-          double f = rv ? a.V[(s + i) * a.nrhs + rg] : 0.0;
-          cplx l = ld(&S.lb[kk][i]);
-          gb = cplx{fma(-l.re, gb.re, fma(l.im, gb.im, f)), fma(-l.re, gb.im, -l.im * gb.re)};
-          cplx w = ld(&S.w[kk][i]);
-          S.cbuf[kk][j][r] = fma(w.re, gb.re, -w.im * gb.im);
-        }
-      }
-      __syncthreads();
-      for (int e = t; e < wn * TR_RT; e += blockDim.x) {
-        int j = e / TR_RT, rr = e - j * TR_RT;
-        double acc = S.F[i0 + j][rr];
-        for (int q = 0; q < kg; ++q) acc += S.cbuf[q][j][rr];
-        S.F[i0 + j][rr] = acc;
-      }
-      __syncthreads();
-    }
-    if (active && rv) st(&a.gB[(c * a.npairs + k) * a.nrhs + rg], gb);
-    if (t < kg && blockIdx.y == 0) {
-      a.LF[c * a.npairs + k0 + t] = S.lam[t][0];
-      a.LB[c * a.npairs + k0 + t] = S.lam[t][1];
-    }
-    __syncthreads();
+    st(&a.LB[c * np + k], lam);
   }
-  for (int e = t; e < rows * TR_RT; e += blockDim.x) {
-    int i = e / TR_RT, rr = e - i * TR_RT;
-    if (r0 + rr < a.nrhs) a.out[(s + i) * a.nrhs + r0 + rr] = S.F[i][rr];
+  // forward chain + twisted weights
+  {
+    const cplx co2 = cscale(ld(&a.coef[k]), 2.0);
+    cplx p1 = mk(1, 0), p2 = ld(&a.rho_in[c * np + k]);
+    cplx lam = mk(1, 0);
+    double e0 = offe(s - 1);
+    for (int i = 0; i < rows; ++i) {
+      double e1 = offe(s + i);
+      cplx rho = cmul(p2, crcp_fast(p1));
+      cplx lv = cscale(rho, e0);
+      cplx b = mk(a.diag[s + i] - a.c + th.re, th.im);
+      double e2 = e0 * e0;
+      cplx p0 = cplx{fma(b.re, p1.re, fma(-b.im, p1.im, -e2 * p2.re)), fma(b.re, p1.im, fma(b.im, p1.re, -e2 * p2.im))};
+      cplx lbv = ld(&a.Lb[(s + i) * np + k]);
+      cplx gam = csub(csub(b, cscale(lv, e0)), cscale(lbv, e1));
+      cplx w = cdiv_fast(co2, gam);
+      st(&a.Lf[(s + i) * np + k], lv);
+      st(&a.Wt[(s + i) * np + k], w);
+      lam = cmul(lam, mk(-lv.re, -lv.im));
+      p2 = p1;
+      p1 = p0;
+      if ((i & 3) == 3) rescale2(p1, p2);
+      e0 = e1;
+    }
+    st(&a.LF[c * np + k], lam);
+  }
+}
+
+// K_T4 tri_sweep: one thread per (chunk, rhs); the recurrences of all shifts run
+// interleaved in registers (ILP = npairs), the combine over shifts is a register sum
+// in ascending shift order (deterministic).  Zero RHS carry-in; chunk summaries out.
+// K_T4 tri_sweep / K_T5 tri_fix share one streaming skeleton.  Thread layout: a
+// half-warp = one (chunk, 16-RHS tile), lane r = one right-hand side; the
+// recurrences of all shifts of that RHS run interleaved in registers (ILP =
+// npairs) and are summed over shifts in ascending order (deterministic).  Each
+// half-warp stages its chunk's factor data (l or l', w) and RHS rows through
+// shared memory in TR_T-row tiles with cp.async double buffering, so the global
+// loads of tile t+1 overlap the FP64 work of tile t.
+constexpr int TR_T = 8;            // rows per staged tile
+constexpr int TR_SW_WARPS = 4;     // warps per block
+
+template <int KM>
+struct TriStage {
+  double2 l[2][TR_T][KM];
+  double2 w[2][TR_T][KM];
+  double f[2][TR_T][TR_RT];
+};
+
+// stage rows [r0, r0+cnt) (cnt <= TR_T) of L and Wt plus the RHS tile into buffer b
+template <int KM>
+__device__ __forceinline__ void stage_tile(TriStage<KM>& S, int b, const TriArgs& a, const double2* L, int64_t r0,
+                                           int cnt, int rt0, int lane16) {
+  const int np = a.npairs;
+  const int nel = cnt * np;  // complex elements per array
+  const double2* ls = L + r0 * np;
+  const double2* ws = a.Wt + r0 * np;
+  double2* ld_ = &S.l[b][0][0];
+  double2* wd = &S.w[b][0][0];
+  for (int e = lane16; e < nel; e += 16) {
+    int rr = e / np, k = e - rr * np;
+    cp_async16(&ld_[rr * KM + k], &ls[e]);
+    cp_async16(&wd[rr * KM + k], &ws[e]);
+  }
+  const int rg = rt0 + lane16;
+  if (rg < a.nrhs)
+    for (int rr = 0; rr < cnt; ++rr) cp_async8(&S.f[b][rr][lane16], &a.V[(r0 + rr) * a.nrhs + rg]);
+}
+
+// MODE 0: sweep (zero carry; out = or += contributions, summaries gF/gB)
+// MODE 1: fix   (true carries G/G' through Lambda products; out +=)
+template <int KM, int DIR, int MODE>
+__global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_stream(TriArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, lane16 = lane & 15;
+  TriStage<KM>& S = reinterpret_cast<TriStage<KM>*>(smem_raw)[warp * 2 + half];
+  const int ntile = (a.nrhs + TR_RT - 1) / TR_RT;
+  const int64_t unit = (blockIdx.x * (int64_t)TR_SW_WARPS + warp) * 2 + half;  // (chunk, rhs tile)
+  if (unit >= (int64_t)a.P * ntile) return;  // whole half-warps exit together
+  const int64_t c = unit / ntile;
+  const int rt0 = (int)(unit - c * ntile) * TR_RT;
+  const int r = rt0 + lane16;
+  const bool rv = r < a.nrhs;
+  const int64_t s = c * TR_L;
+  const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
+  const int np = a.npairs;
+  const double2* L = DIR == 0 ? a.Lf : a.Lb;
+  cplx g[KM], G[KM];
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    if (MODE == 0) {
+      g[k] = mk(0, 0);
+    } else {
+      g[k] = mk(1, 0);  // Lambda
+      const double2* Gs = DIR == 0 ? a.G : a.Gb;
+      G[k] = (k < np && rv) ? ld(&Gs[(c * np + k) * a.nrhs + r]) : mk(0, 0);
+    }
+  }
+  const int ntl = (rows + TR_T - 1) / TR_T;
+  // tile t covers local rows [t*TR_T, ...) ; backward sweeps walk tiles and rows in reverse
+  auto tile_first = [&](int t) { return DIR == 0 ? t * TR_T : max(rows - (t + 1) * TR_T, 0); };
+  auto tile_cnt = [&](int t) { return DIR == 0 ? min(TR_T, rows - t * TR_T) : rows - t * TR_T - max(rows - (t + 1) * TR_T, 0); };
+  stage_tile<KM>(S, 0, a, L, s + tile_first(0), tile_cnt(0), rt0, lane16);
+  cp_async_commit();
+  for (int t = 0; t < ntl; ++t) {
+    const int b = t & 1;
+    if (t + 1 < ntl) stage_tile<KM>(S, b ^ 1, a, L, s + tile_first(t + 1), tile_cnt(t + 1), rt0, lane16);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int first = tile_first(t), cnt = tile_cnt(t);
+    for (int jj = 0; jj < cnt; ++jj) {
+      const int j = DIR == 0 ? jj : cnt - 1 - jj;
+      const int64_t row = s + first + j;
+      const double f = S.f[b][j][lane16];
+      double acc = 0.0;
+      if (MODE == 1 || DIR == 1) acc = rv ? a.out[row * a.nrhs + r] : 0.0;
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        if (k < np) {
+          const cplx l = ld(&S.l[b][j][k]);
+          const cplx w = ld(&S.w[b][j][k]);
+          if (MODE == 0) {
+            g[k] = cplx{fma(-l.re, g[k].re, fma(l.im, g[k].im, f)), fma(-l.re, g[k].im, -l.im * g[k].re)};
+            const double gre = DIR == 0 ? g[k].re - f : g[k].re;
+            acc = fma(w.re, gre, fma(-w.im, g[k].im, acc));
+          } else {
+            g[k] = cmul(g[k], mk(-l.re, -l.im));
+            const cplx tt = cmul(g[k], G[k]);
+            acc = fma(w.re, tt.re, fma(-w.im, tt.im, acc));
+          }
+        }
+      }
+      if (rv) a.out[row * a.nrhs + r] = acc;
+    }
+    __syncwarp();
+  }
+  if (MODE == 0 && rv) {
+    double2* dst = DIR == 0 ? a.gF : a.gB;
+#pragma unroll
+    for (int k = 0; k < KM; ++k)
+      if (k < np) st(&dst[(c * np + k) * a.nrhs + r], g[k]);
   }
 }
 
 // K_T4 ------------------------------------------------------------------------
-// One warp per (shift, rhs, direction).  Affine maps x -> A x + B composed over chunks.
+// One warp per (shift, rhs, direction).  Affine maps x -> A x + B composed over chunks;
+// each lane owns a contiguous range of chunks, loads are issued 8 at a time.
 __global__ void tri_carry_scan(TriArgs a) {
   const int warp_global = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -381,19 +419,29 @@ __global__ void tri_carry_scan(TriArgs a) {
   const int k = kr / a.nrhs, rr = kr - k * a.nrhs;
   const int P = a.P;
   const int per = (P + 31) / 32;
-  // lane composite
+  const double2* Ls = dir == 0 ? a.LF : a.LB;
+  const double2* gs = dir == 0 ? a.gF : a.gB;
   cplx A = mk(1, 0), B = mk(0, 0);
-  for (int j = 0; j < per; ++j) {
-    int q = lane * per + j;
-    if (q >= P) break;
-    int cc = dir == 0 ? q : P - 1 - q;
-    cplx Lc = ld(&(dir == 0 ? a.LF : a.LB)[(int64_t)cc * a.npairs + k]);
-    cplx gc = ld(&(dir == 0 ? a.gF : a.gB)[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
-    // new = Lc * (A x + B) + gc
-    B = cadd(cmul(Lc, B), gc);
-    A = cmul(Lc, A);
+  for (int j0 = 0; j0 < per; j0 += 8) {
+    cplx Lc[8], gc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int q = lane * per + j0 + u;
+      if (j0 + u < per && q < P) {
+        int cc = dir == 0 ? q : P - 1 - q;
+        Lc[u] = ld(&Ls[(int64_t)cc * a.npairs + k]);
+        gc[u] = ld(&gs[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
+      } else {
+        Lc[u] = mk(1, 0);
+        gc[u] = mk(0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      B = cadd(cmul(Lc[u], B), gc[u]);
+      A = cmul(Lc[u], A);
+    }
   }
-  // inclusive warp scan (later lanes apply after earlier ones)
   for (int off = 1; off < 32; off <<= 1) {
     cplx pA, pB;
     pA.re = __shfl_up_sync(0xffffffffu, A.re, off);
@@ -401,81 +449,34 @@ __global__ void tri_carry_scan(TriArgs a) {
     pB.re = __shfl_up_sync(0xffffffffu, B.re, off);
     pB.im = __shfl_up_sync(0xffffffffu, B.im, off);
     if (lane >= off) {
-      // mine o prev : x -> A (pA x + pB) + B
       B = cadd(cmul(A, pB), B);
       A = cmul(A, pA);
     }
   }
-  cplx x;  // carry entering this lane's first chunk = exclusive prefix applied to 0
+  cplx x;
   x.re = __shfl_up_sync(0xffffffffu, B.re, 1);
   x.im = __shfl_up_sync(0xffffffffu, B.im, 1);
   if (lane == 0) x = mk(0, 0);
-  for (int j = 0; j < per; ++j) {
-    int q = lane * per + j;
-    if (q >= P) break;
-    int cc = dir == 0 ? q : P - 1 - q;
-    st(&(dir == 0 ? a.G : a.Gb)[((int64_t)cc * a.npairs + k) * a.nrhs + rr], x);
-    cplx Lc = ld(&(dir == 0 ? a.LF : a.LB)[(int64_t)cc * a.npairs + k]);
-    cplx gc = ld(&(dir == 0 ? a.gF : a.gB)[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
-    x = cadd(cmul(Lc, x), gc);
-  }
-}
-
-// K_T5 ------------------------------------------------------------------------
-__global__ void __launch_bounds__(TR_RT* TR_KG) tri_correct(TriArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TriSmem& S = *reinterpret_cast<TriSmem*>(smem_raw);
-  const int64_t c = blockIdx.x;
-  const int r0 = blockIdx.y * TR_RT;
-  const int64_t s = c * TR_L;
-  const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
-  const int t = threadIdx.x;
-  tri_load_chunk(S, a, s, rows);
-  for (int i = t; i < rows * TR_RT; i += blockDim.x) (&S.F[0][0])[i] = 0.0;
-  __syncthreads();
-  for (int k0 = 0; k0 < a.npairs; k0 += TR_KG) {
-    const int kg = min(TR_KG, a.npairs - k0);
-    if (t < 2 * kg) tri_chain(S, a, c, k0 + (t % kg), t % kg, t / kg, rows, true);
-    __syncthreads();
-    // w (into cbuf-free storage): multiply Lambda in place by w
-    for (int e = t; e < kg * rows; e += blockDim.x) {
-      int kk = e / rows, i = e - kk * rows;
-      const cplx th = ld(&a.theta[k0 + kk]);
-      cplx b = mk(S.dg[i] + th.re, th.im);
-      cplx l = ld(&S.l[kk][i]), lb = ld(&S.lb[kk][i]);
-      cplx gam = csub(csub(b, cscale(l, S.of[i])), cscale(lb, S.of[i + 1]));
-      cplx w = cscale(cdiv(ld(&a.coef[k0 + kk]), gam), 2.0);
-      cplx wl = cmul(w, ld(&S.w[kk][i]));
-      cplx wlb = cmul(w, ld(&S.wb[kk][i]));
-      S.w[kk][i] = make_double2(wl.re, wl.im);
-      S.wb[kk][i] = make_double2(wlb.re, wlb.im);
-    }
-    // carries of this chunk into l[][] scratch rows? use lam-free registers: stage in cbuf as doubles
-    __syncthreads();
-    for (int e = t; e < rows * TR_RT; e += blockDim.x) {
-      int i = e / TR_RT, rr = e - i * TR_RT;
-      int rg = r0 + rr;
-      if (rg >= a.nrhs) continue;
-      double acc = S.F[i][rr];
-      for (int kk = 0; kk < kg; ++kk) {
-        int k = k0 + kk;
-        cplx G = ld(&a.G[(c * a.npairs + k) * a.nrhs + rg]);
-        cplx Gb = ld(&a.Gb[(c * a.npairs + k) * a.nrhs + rg]);
-        cplx wl = ld(&S.w[kk][i]), wlb = ld(&S.wb[kk][i]);
-        acc = fma(wl.re, G.re, acc);
-        acc = fma(-wl.im, G.im, acc);
-        acc = fma(wlb.re, Gb.re, acc);
-        acc = fma(-wlb.im, Gb.im, acc);
+  double2* dst = dir == 0 ? a.G : a.Gb;
+  for (int j0 = 0; j0 < per; j0 += 8) {
+    cplx Lc[8], gc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int q = lane * per + j0 + u;
+      if (j0 + u < per && q < P) {
+        int cc = dir == 0 ? q : P - 1 - q;
+        Lc[u] = ld(&Ls[(int64_t)cc * a.npairs + k]);
+        gc[u] = ld(&gs[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
       }
-      S.F[i][rr] = acc;
     }
-    __syncthreads();
-  }
-  for (int e = t; e < rows * TR_RT; e += blockDim.x) {
-    int i = e / TR_RT, rr = e - i * TR_RT;
-    if (r0 + rr < a.nrhs) {
-      size_t o = (s + i) * a.nrhs + r0 + rr;
-      a.out[o] = a.out[o] + S.F[i][rr];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int q = lane * per + j0 + u;
+      if (j0 + u < per && q < P) {
+        int cc = dir == 0 ? q : P - 1 - q;
+        st(&dst[((int64_t)cc * a.npairs + k) * a.nrhs + rr], x);
+        x = cadd(cmul(Lc[u], x), gc[u]);
+      }
     }
   }
 }
@@ -485,13 +486,42 @@ __global__ void scale_kernel(double* x, size_t n, double s) {
     x[i] *= s;
 }
 
+template <int KM>
+static int launch_stream(const TriArgs& a, cudaStream_t stream, int which) {
+  const int ntile = (a.nrhs + TR_RT - 1) / TR_RT;
+  const int64_t units = (int64_t)a.P * ntile;
+  const unsigned blocks = (unsigned)ceil_div(units, TR_SW_WARPS * 2);
+  const int smem = (int)(sizeof(TriStage<KM>) * TR_SW_WARPS * 2);
+  const int th = TR_SW_WARPS * 32;
+  if (which == 0) {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_LAUNCH("tri_sweep", stream, (tri_stream<KM, 0, 0><<<blocks, th, smem, stream>>>(a)));
+    PFX_LAUNCH("tri_sweep", stream, (tri_stream<KM, 1, 0><<<blocks, th, smem, stream>>>(a)));
+  } else {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_LAUNCH("tri_fix", stream, (tri_stream<KM, 0, 1><<<blocks, th, smem, stream>>>(a)));
+    PFX_LAUNCH("tri_fix", stream, (tri_stream<KM, 1, 1><<<blocks, th, smem, stream>>>(a)));
+  }
+  return PFX_OK;
+}
+
+static int sweeps(const TriArgs& a, cudaStream_t stream, int which) {
+  if (a.npairs <= 8) return launch_stream<8>(a, stream, which);
+  if (a.npairs <= 12) return launch_stream<12>(a, stream, which);
+  if (a.npairs <= 16) return launch_stream<16>(a, stream, which);
+  return launch_stream<32>(a, stream, which);
+}
+
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                 float* launch_ms) {
   const int P = (int)ceil_div(N, TR_L);
   const size_t nP = (size_t)P * npairs;
   const size_t nPR = nP * nrhs;
-  size_t bytes = (nP * 4 * 2 + nP * 4 + nPR * 4) * sizeof(double2);
+  const size_t nN = (size_t)N * npairs;
+  size_t bytes = (nP * 4 * 2 + nP * 4 + nPR * 4 + nN * 3) * sizeof(double2);
   double2* ws = static_cast<double2*>(scratch(1, bytes));
   if (!ws) return fail(PFX_CUDA, "tridiagonal workspace allocation failed");
   TriArgs a;
@@ -515,6 +545,9 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   a.gB = a.gF + nPR;
   a.G = a.gB + nPR;
   a.Gb = a.G + nPR;
+  a.Lf = a.Gb + nPR;
+  a.Lb = a.Lf + nN;
+  a.Wt = a.Lb + nN;
   a.out = out;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (launch_ms) {
@@ -528,20 +561,17 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaGetLastError());
     PFX_LAUNCH("tri_mobius_scan", stream, tri_mobius_scan<<<npairs * 2, TR_SCAN_T, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
+    PFX_LAUNCH("tri_factor", stream, tri_factor<<<(unsigned)ceil_div((int64_t)P * npairs, 128), 128, 0, stream>>>(a));
+    PFX_CUDA_TRY(cudaGetLastError());
   }
-  const int smem = (int)sizeof(TriSmem);
-  const int kg = std::min(npairs, TR_KG);
-  dim3 grid((unsigned)P, (unsigned)ceil_div(nrhs, TR_RT));
-  PFX_CUDA_TRY(cudaFuncSetAttribute(tri_local, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  PFX_LAUNCH("tri_local", stream, tri_local<<<grid, TR_RT * kg, smem, stream>>>(a));
+  if (int rc = sweeps(a, stream, 0)) return rc;
   PFX_CUDA_TRY(cudaGetLastError());
   {
     int warps = npairs * (int)nrhs * 2;
     PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
   }
-  PFX_CUDA_TRY(cudaFuncSetAttribute(tri_correct, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  PFX_LAUNCH("tri_correct", stream, tri_correct<<<grid, TR_RT * kg, smem, stream>>>(a));
+  if (int rc = sweeps(a, stream, 1)) return rc;
   PFX_CUDA_TRY(cudaGetLastError());
   if (shift_c != 0.0) {
     PFX_LAUNCH("scale_kernel", stream, scale_kernel<<<1184, 256, 0, stream>>>(out, (size_t)N * nrhs, exp(shift_c)));
