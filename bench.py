@@ -50,15 +50,17 @@ ALG_FLOPS = {
     "C1": 8.0 * (8.0 / 3.0 * 128**3 + 8.0 * 128**2),
     "C2": 12.0 * (1 << 20) * (12 + 16 * 22),
     "C3": 10.0 * (8.0 / 3.0 * 256**3 + 2 * 8.0 * 256**2),  # per matrix (one eval = one matrix)
+    "C4": 12.0 * (8.0 / 3.0 + 16.0 / 3.0) * 4096**3,
     "C5": 8.0 * (8.0 * 262144 * 512 * 512 + 8.0 * 262144 * 1024 * 8),
 }
 ALG_BYTES = {
     "C1": 1.33e5,
     "C2": 8.0 * (1 << 20) * (2 + 2 * 16),
     "C3": 5.40e8 / 512,
+    "C4": 5.37e8,
     "C5": 8.0 * 2 * 513 * 262144 * 16,
 }
-DOMINANT = {"C1": "dense_batched_kernel", "C2": "tri_local", "C3": "dense_batched_kernel", "C5": "band_lu"}
+DOMINANT = {"C1": "dense_batched_kernel", "C2": "tri_sweep", "C3": "dense_batched_kernel", "C4": "zgemm", "C5": "zgemm"}
 
 
 def load_peaks():
@@ -179,6 +181,15 @@ class Workload:
             self.evals_per_step = float(W.C3["batch"])
             self.desc = {"workload": "C3: 512 dense complex Hermitian d=256, spectrum U[-200,0], exp(A)v, n=20",
                          "batch": 512, "d": 256, "n": 20, "l2": "inputs 537 MB exceed L2; no flush"}
+        elif name == "C4":
+            n = W.C4["n"]
+            A, _ = W.c4_matrix()
+            self.host = dict(A=A)
+            self.h2d = A.nbytes
+            self.d2h = A.nbytes
+            self.evals_per_step = 1.0
+            self.desc = {"workload": "C4: dense complex Hermitian d=4096, spectrum U[-500,0], full exp(A), n=24",
+                         "d": 4096, "n": 24, "l2": "inputs 268 MB exceed L2; no flush"}
         elif name == "C5":
             n = W.C5["n"]
             band = W.c5_band()
@@ -200,8 +211,10 @@ class Workload:
         self.flush = None
         if name == "C1":
             self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-        # pinned host copies for the end-to-end number
+        # pinned host copies (inputs and result) for the end-to-end number
         self.pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in self.host.items()}
+        out_elems = {"C2": 16 << 20, "C1": 128, "C3": 512 * 256 * 2, "C4": 4096 * 4096 * 2, "C5": 262144 * 8}[name]
+        self.pinned_out = torch.empty(out_elems, dtype=torch.float64).pin_memory()
 
     def step(self, stream):
         from paper_2306_16778_b200 import _native
@@ -212,6 +225,9 @@ class Workload:
                                                    out=self.out, stream=stream)
         elif self.name in ("C1", "C3"):
             self.out = _native.expm_dense_device(di["A"], di["V"], self.theta2, self.coef2, 0.0, stream=stream)
+        elif self.name == "C4":
+            self.out = _native.expm_dense_device(di["A"], None, self.theta2, self.coef2, 0.0, out=self.out,
+                                                 stream=stream)
         elif self.name == "C5":
             self.out = _native.expm_banded_device(di["band"], di["V"], self.theta2, self.coef2, 0.0, out=self.out,
                                                   stream=stream)
@@ -222,18 +238,23 @@ class Workload:
         from paper_2306_16778_b200 import _native
 
         p = {k: v.numpy() for k, v in self.pinned.items()}
+        o = self.pinned_out.numpy()
         if self.name == "C2":
-            return _native.expm_tridiag_host(p["diag"], p["off"], p["V"], self.theta2, self.coef2, 0.0)
-        if self.name in ("C1", "C3"):
-            return _native.expm_dense_host(p["A"], p["V"], self.theta2, self.coef2, 0.0)
-        return _native.expm_banded_host(p["band"], p["V"], self.theta2, self.coef2, 0.0)
+            return _native.expm_tridiag_host(p["diag"], p["off"], p["V"], self.theta2, self.coef2, 0.0, out=o)
+        if self.name == "C1":
+            return _native.expm_dense_host(p["A"], p["V"], self.theta2, self.coef2, 0.0, out=o)
+        if self.name in ("C3", "C4"):
+            oc = o.view(np.complex128)
+            return _native.expm_dense_host(p["A"], p.get("V"), self.theta2, self.coef2, 0.0, out=oc)
+        return _native.expm_banded_host(p["band"], p["V"], self.theta2, self.coef2, 0.0, out=o)
 
 
 # ---- CPU baseline (oracle restatement on the host cores) ----------------------------
 
 def _cpu_task(args):
     name, n, cols = args
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    if name != "C4":
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import restate
     from paper_2306_16778_b200 import workloads as W
 
@@ -250,11 +271,26 @@ def _cpu_task(args):
         for b in cols:
             restate.run_tasks_dense(W.c3_matrix(b), W.c3_vector(b), n)
         return float(len(cols))
+    if name == "C4":
+        # one pole pair of the full exp(A): zgesv with 4096 identity RHS (engine.py:208)
+        import scipy.linalg
+        A, _ = W.c4_matrix()
+        th, co = restate.pairs(n)
+        k = cols[0]
+        X = np.linalg.solve(A + th[k] * np.eye(A.shape[0]), np.eye(A.shape[0], dtype=complex))
+        aX = co[k] * X
+        _ = aX + aX.conj().T
+        return 1.0 / len(th)
     if name == "C5":
         band = W.c5_band()
         V = W.c5_rhs()
-        restate.banded_action(band, V[:, cols], n)
-        return len(cols) / 8.0
+        # one pole pair (zgbsv, kl=ku=512) on all 8 RHS
+        th, co = restate.pairs(n)
+        ab = restate.sym_band_to_general(band)
+        ab[2 * band.shape[0] - 2, :] += th[cols[0]]
+        import scipy.linalg.lapack as lapack
+        lapack.zgbsv(band.shape[0] - 1, band.shape[0] - 1, ab, V.astype(complex), overwrite_ab=1)
+        return 1.0 / len(th)
     raise ValueError(name)
 
 
@@ -270,9 +306,12 @@ def cpu_sample_plan(name, cores):
         per = 2
         tasks = [(name, 20, list(range(i * per, (i + 1) * per))) for i in range(cores)]
         return tasks, f"{cores * per} of the 512 C3 matrices ({per} per process)"
+    if name == "C4":
+        tasks = [(name, 24, [0])]
+        return tasks, "1 of the 12 pole pairs of C4 (zgesv d=4096 with identity RHS, all BLAS threads)"
     if name == "C5":
-        tasks = [(name, 16, [c]) for c in range(min(cores, 8))]
-        return tasks, f"{len(tasks)} of the 8 RHS columns of C5 (zgbsv kl=ku=512, all 8 pairs)"
+        tasks = [(name, 16, [k]) for k in range(min(max(cores // 2, 1), 8))]
+        return tasks, f"{len(tasks)} of the 8 pole pairs of C5 (zgbsv kl=ku=512, 8 RHS), one process each"
     raise ValueError(name)
 
 
@@ -301,7 +340,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
@@ -339,7 +378,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2306_16778_b200 import workloads as W
 
-    n = {"C1": 16, "C2": 24, "C3": 20, "C5": 16}[args.workload]
+    n = {"C1": 16, "C2": 24, "C3": 20, "C4": 24, "C5": 16}[args.workload]
     npairs = n // 2
     lo = rank * npairs // world
     hi = (rank + 1) * npairs // world
@@ -400,13 +439,18 @@ def main():
         e2e = {"value": wl.evals_per_step * args.e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h)}
 
-    launches = sum(c for c, _ in kern.values())
+    launches = sum(v[0] for v in kern.values())
     dom = DOMINANT[args.workload]
-    dom_cnt, dom_ms = kern.get(dom, (0, 0.0))
-    flops_per_launch = ALG_FLOPS[args.workload] * wl.evals_per_step * (hi - lo) / npairs
+    dom_cnt, dom_ms, dom_fl = kern.get(dom, (0, 0.0, 0.0))
     roofline = None
     if dom_cnt:
         t_launch = dom_ms / dom_cnt * 1e-3
+        if dom_fl > 0:
+            # the kernel declares its algorithmic flops per launch (GEMM: 8 m n k per complex product)
+            flops_per_launch = dom_fl / dom_cnt
+        else:
+            # one launch of the dominant kernel carries the path's whole algorithmic work per step
+            flops_per_launch = ALG_FLOPS[args.workload] * wl.evals_per_step * (hi - lo) / npairs / (dom_cnt / args.steps)
         achieved = flops_per_launch / t_launch / 1e12
         roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                     "frac": achieved / peaks["fp64_tflops"], "traffic": None, "kernel": dom,
@@ -431,7 +475,7 @@ def main():
             "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic (seeded reference recipes)",
             "config": dict(wl.desc, parallelism=f"pole-shard x{world}" + (" + 1 NCCL reduce" if world > 1 else "")),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
-            "kernels": {k: {"launches": c, "total_ms": t} for k, t in [(k, v[1]) for k, v in kern.items()] for c in [kern[k][0]]},
+            "kernels": {k: {"launches": v[0], "total_ms": v[1], "gflop": v[2] / 1e9} for k, v in kern.items()},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

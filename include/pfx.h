@@ -124,7 +124,8 @@ int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double
  * stream the kernels run on).  When enabled, every kernel launch of the
  * library is bracketed by CUDA events on its stream.  pfx_prof_read()
  * synchronises those events and writes one line per kernel name,
- * "name launches total_ms\n", into buf (NUL-terminated, truncated to buflen),
+ * "name launches total_ms total_flops\n" (flops = algorithmic count of the
+ * launches that declare one, else 0), into buf (NUL-terminated, truncated to buflen),
  * then clears the record.  Returns the number of bytes needed.
  */
 int pfx_prof_enable(int on);

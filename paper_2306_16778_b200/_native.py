@@ -98,13 +98,13 @@ def prof_enable(on: bool) -> None:
 
 
 def prof_read() -> dict:
-    """{kernel name: (launches, total_ms)} since the last read (synchronises the events)."""
+    """{kernel name: (launches, total_ms, total_flops)} since the last read (synchronises the events)."""
     buf = ctypes.create_string_buffer(1 << 16)
     lib().pfx_prof_read(buf, len(buf))
     out = {}
     for line in buf.value.decode().splitlines():
-        name, cnt, tot = line.split()
-        out[name] = (int(cnt), float(tot))
+        name, cnt, tot, fl = line.split()
+        out[name] = (int(cnt), float(tot), float(fl))
     return out
 
 
@@ -201,7 +201,7 @@ def expm_dense_device(A, V, theta2, coef2, shift_c: float, out=None, per_pair_ms
     return res
 
 
-def expm_dense_host(A: np.ndarray, V, theta2, coef2, shift_c: float, per_pair_ms=None):
+def expm_dense_host(A: np.ndarray, V, theta2, coef2, shift_c: float, per_pair_ms=None, out=None):
     """Host-array entry through PFX_MEM_HOST (the library stages H2D/D2H itself)."""
     _torch()  # asserts a device exists
     A = np.ascontiguousarray(A)
@@ -225,7 +225,10 @@ def expm_dense_host(A: np.ndarray, V, theta2, coef2, shift_c: float, per_pair_ms
         V = np.ascontiguousarray(V.astype(np.complex128 if v_complex else np.float64, copy=False))
     real_path = (not a_complex) and (full or not v_complex)
     ncols = d if full else nrhs
-    out = np.empty((batch, d, ncols), dtype=np.float64 if real_path else np.complex128)
+    odt = np.float64 if real_path else np.complex128
+    if out is None or out.dtype != odt or out.size != batch * d * ncols:
+        out = np.empty((batch, d, ncols), dtype=odt)
+    out = out.reshape(batch, d, ncols)
     npairs = len(theta2) // 2
     ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
     st = lib().pfx_expm_dense(
@@ -266,7 +269,7 @@ def expm_tridiag_device(diag, off, V, theta2, coef2, shift_c: float, out=None, p
     return out.squeeze(-1) if squeeze else out
 
 
-def expm_tridiag_host(diag, off, V, theta2, coef2, shift_c: float, per_pair_ms=None):
+def expm_tridiag_host(diag, off, V, theta2, coef2, shift_c: float, per_pair_ms=None, out=None):
     _torch()
     diag = np.ascontiguousarray(diag, dtype=np.float64)
     off = np.ascontiguousarray(off, dtype=np.float64)
@@ -274,7 +277,9 @@ def expm_tridiag_host(diag, off, V, theta2, coef2, shift_c: float, per_pair_ms=N
     squeeze = V.ndim == 1
     V = np.ascontiguousarray(V[:, None] if squeeze else V)
     N, nrhs = V.shape
-    out = np.empty((N, nrhs), dtype=np.float64)
+    if out is None or out.size != N * nrhs:
+        out = np.empty((N, nrhs), dtype=np.float64)
+    out = out.reshape(N, nrhs)
     npairs = len(theta2) // 2
     ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
     st = lib().pfx_expm_tridiag(
@@ -287,7 +292,7 @@ def expm_tridiag_host(diag, off, V, theta2, coef2, shift_c: float, per_pair_ms=N
     return out[:, 0] if squeeze else out
 
 
-def expm_banded_host(band, V, theta2, coef2, shift_c: float, per_pair_ms=None):
+def expm_banded_host(band, V, theta2, coef2, shift_c: float, per_pair_ms=None, out=None):
     _torch()
     band = np.ascontiguousarray(band, dtype=np.float64)
     V = np.asarray(V, dtype=np.float64)
@@ -295,7 +300,9 @@ def expm_banded_host(band, V, theta2, coef2, shift_c: float, per_pair_ms=None):
     V = np.ascontiguousarray(V[:, None] if squeeze else V)
     N, nrhs = V.shape
     kb = band.shape[0] - 1
-    out = np.empty((N, nrhs), dtype=np.float64)
+    if out is None or out.size != N * nrhs:
+        out = np.empty((N, nrhs), dtype=np.float64)
+    out = out.reshape(N, nrhs)
     npairs = len(theta2) // 2
     ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
     st = lib().pfx_expm_banded(

@@ -1,11 +1,139 @@
-// Banded path (config C5): placeholder until the banded LU lands.
-#include "pfx_common.cuh"
+// Real symmetric banded shifted solves with fused residue combine (config C5).
+//
+// The reference is dense-only; this follows its per-pair task and combine
+// (engine.py:194-201: M = A - cI + theta_k I, y = M^{-1} V, 2 Re(a_k y)) and the ascending
+// reduction (engine.py:226-228) with a band LU.
+//
+// Storage: every pole pair gets its own row-band copy of M_k: row i holds columns
+// i-kb-nb .. i+kb+nb (Wd = 2kb+2nb+1 complex entries, the nb extra diagonals on each side
+// stay zero).  Element (i, j) lives at base + i*Wd + (j - i + kb + nb) = p + i*(Wd-1) + j
+// with p = base + kb + nb, i.e. the band IS a dense row-major matrix with ld = Wd - 1 for
+// every access inside |i - j| <= kb + nb.  The zero padding lets the L21/U12 panels of a
+// block step (which reach nb diagonals past the band) be read as plain rectangles.
+//
+// Factorisation (no pivoting, safe by SURVEY finding 7; the band then never fills in),
+// all pole pairs batched in every launch, nb = 64, for each block step j0:
+//   L11 U11 = M11                         zgetf2 (diagonal 64x64 block)
+//   U12 = L11^{-1} M12, L21 = M21 U11^{-1}  ztrsm (kb-wide panels)
+//   M22 -= L21 U12                         zgemm on DMMA (kb x kb x 64)
+//   y1 = L11^{-1} y1, y2 -= L21 y1          forward elimination of the RHS alongside
+// then block back substitution y1 = U11^{-1}(y1 - U12 y2), and the combine kernel.
+#include "zblas.cuh"
 
 namespace pfx {
 
-int banded_run(const double*, int64_t, int64_t, const double*, int64_t, double, const double2*, const double2*, int,
-               double*, cudaStream_t, float*) {
-  return fail(PFX_BADARG, "banded path is not built yet");
+constexpr int BD_NB = 64;
+
+__global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const double* V, int nrhs, double shift_c,
+                         const double2* theta, ZMat M, ZMat X) {
+  const int k = blockIdx.y;
+  const cplx th = ld(&theta[k]);
+  double2* base = M.p - (kb + BD_NB) + k * M.stride;  // row-band base of pair k
+  const int64_t total = N * Wd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / Wd;
+    int off = (int)(e - i * Wd) - (kb + BD_NB);  // j - i
+    int64_t j = i + off;
+    double v = 0.0;
+    int ao = off < 0 ? -off : off;
+    if (ao <= kb && j >= 0 && j < N) v = ao == 0 ? band[i] : band[(int64_t)ao * N + (off < 0 ? j : i)];
+    double2 z = make_double2(v, 0.0);
+    if (off == 0) {
+      z.x = (v - shift_c) + th.re;
+      z.y = th.im;
+    }
+    base[e] = z;
+  }
+  const int64_t nx = N * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nx; e += (int64_t)gridDim.x * blockDim.x)
+    X.p[k * X.stride + e] = make_double2(V[e], 0.0);
+}
+
+__global__ void bd_combine(ZMat X, int64_t n, int npairs, const double2* coef, double scale, double* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < npairs; ++k) {
+      cplx a = ld(&coef[k]);
+      cplx x = ld(&X.p[k * X.stride + e]);
+      double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
+      acc = k == 0 ? sk : acc + sk;
+    }
+    out[e] = scale == 1.0 ? acc : scale * acc;
+  }
+}
+
+int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int64_t nrhs, double shift_c,
+               const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
+               float* per_pair_ms) {
+  const int kb = (int)kb64;
+  const int nb = BD_NB;
+  const int Wd = 2 * kb + 2 * nb + 1;
+  const size_t mbytes = (size_t)npairs * N * Wd * sizeof(double2);
+  const size_t xbytes = (size_t)npairs * N * nrhs * sizeof(double2);
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 256));
+  if (!ws) return fail(PFX_CUDA, "banded workspace allocation failed (needs " + std::to_string((mbytes + xbytes) >> 20) + " MiB)");
+  ZMat M{reinterpret_cast<double2*>(ws) + kb + nb, Wd - 1, (int64_t)N * Wd};
+  ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, N * nrhs};
+  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes);
+  PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (per_pair_ms) {
+    PFX_CUDA_TRY(cudaEventCreate(&e0));
+    PFX_CUDA_TRY(cudaEventCreate(&e1));
+    PFX_CUDA_TRY(cudaEventRecord(e0, stream));
+  }
+  dim3 bg(2368, npairs);
+  PFX_LAUNCH("bd_build", stream, bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X));
+  PFX_CUDA_TRY(cudaGetLastError());
+  auto sub = [](ZMat A, int64_t i, int64_t j) {
+    ZMat r = A;
+    r.p = A.p + i * A.ld + j;
+    return r;
+  };
+  int rc;
+  const int nr = (int)nrhs;
+  for (int64_t j0 = 0; j0 < N; j0 += nb) {
+    const int jb = (int)std::min<int64_t>(nb, N - j0);
+    const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);  // rows/cols coupled below/right
+    if ((rc = zgetf2_panel(stream, npairs, jb, jb, sub(M, j0, j0), nullptr, sing))) return rc;
+    if (rest > 0) {
+      if ((rc = ztrsm_llnu(stream, npairs, jb, rest, sub(M, j0, j0), sub(M, j0, j0 + jb)))) return rc;
+      if ((rc = ztrsm_runn(stream, npairs, rest, jb, sub(M, j0, j0), sub(M, j0 + jb, j0)))) return rc;
+      if ((rc = zgemm(stream, npairs, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
+                      sub(M, j0 + jb, j0 + jb))))
+        return rc;
+    }
+    if ((rc = ztrsm_llnu(stream, npairs, jb, nr, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
+    if (rest > 0 && (rc = zgemm(stream, npairs, rest, nr, jb, -1.0, sub(M, j0 + jb, j0), sub(X, j0, 0),
+                                sub(X, j0 + jb, 0))))
+      return rc;
+  }
+  const int64_t nblk = (N + nb - 1) / nb;
+  for (int64_t pb = nblk - 1; pb >= 0; --pb) {
+    const int64_t j0 = pb * nb;
+    const int jb = (int)std::min<int64_t>(nb, N - j0);
+    const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);
+    if (rest > 0 && (rc = zgemm(stream, npairs, jb, nr, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0),
+                                sub(X, j0, 0))))
+      return rc;
+    if ((rc = ztrsm_lunn(stream, npairs, jb, nr, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
+  }
+  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
+  PFX_LAUNCH("bd_combine", stream, bd_combine<<<1184, 256, 0, stream>>>(X, N * nrhs, npairs, coef_d, scale, out));
+  PFX_CUDA_TRY(cudaGetLastError());
+  int sg = 0;
+  PFX_CUDA_TRY(cudaMemcpyAsync(&sg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (per_pair_ms) PFX_CUDA_TRY(cudaEventRecord(e1, stream));
+  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (per_pair_ms) {
+    float ms = 0.0f;
+    PFX_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (sg) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted band factorization");
+  return PFX_OK;
 }
 
 }  // namespace pfx

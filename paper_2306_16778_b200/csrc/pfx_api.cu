@@ -44,6 +44,7 @@ namespace {
 struct ProfRec {
   std::string name;
   cudaEvent_t e0, e1;
+  double flops;
 };
 std::mutex g_prof_mu;
 std::vector<ProfRec> g_prof;
@@ -52,11 +53,12 @@ bool g_prof_on = false;
 
 bool prof_on() { return g_prof_on; }
 
-void prof_mark(const char* name, cudaStream_t stream, bool begin) {
+void prof_mark(const char* name, cudaStream_t stream, bool begin, double flops) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (begin) {
     ProfRec r;
     r.name = name;
+    r.flops = flops;
     cudaEventCreate(&r.e0);
     cudaEventCreate(&r.e1);
     cudaEventRecord(r.e0, stream);
@@ -180,6 +182,7 @@ int pfx_prof_read(char* buf, int buflen) {
   std::vector<std::string> names;
   std::vector<int> counts;
   std::vector<double> totals;
+  std::vector<double> fl;
   for (auto& r : g_prof) {
     cudaEventSynchronize(r.e1);
     float ms = 0.0f;
@@ -193,15 +196,17 @@ int pfx_prof_read(char* buf, int buflen) {
       names.push_back(r.name);
       counts.push_back(0);
       totals.push_back(0.0);
+      fl.push_back(0.0);
     }
     counts[i] += 1;
     totals[i] += ms;
+    fl[i] += r.flops;
   }
   g_prof.clear();
   std::string out;
   char line[256];
   for (size_t i = 0; i < names.size(); ++i) {
-    snprintf(line, sizeof(line), "%s %d %.6f\n", names[i].c_str(), counts[i], totals[i]);
+    snprintf(line, sizeof(line), "%s %d %.6f %.6e\n", names[i].c_str(), counts[i], totals[i], fl[i]);
     out += line;
   }
   if (buf && buflen > 0) {

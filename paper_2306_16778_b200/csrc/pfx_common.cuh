@@ -30,14 +30,16 @@ void release_scratch();
 
 // Kernel timing (pfx_prof_enable / pfx_prof_read).  PFX_LAUNCH brackets a launch
 // with events when profiling is on; otherwise it is just the launch.
+// PFX_LAUNCH_F also records the launch's algorithmic flop count.
 bool prof_on();
-void prof_mark(const char* name, cudaStream_t stream, bool begin);
-#define PFX_LAUNCH(name, stream, ...)                 \
-  do {                                                \
-    if (::pfx::prof_on()) ::pfx::prof_mark(name, stream, true);  \
-    __VA_ARGS__;                                      \
-    if (::pfx::prof_on()) ::pfx::prof_mark(name, stream, false); \
+void prof_mark(const char* name, cudaStream_t stream, bool begin, double flops = 0.0);
+#define PFX_LAUNCH_F(name, stream, flops, ...)                          \
+  do {                                                                  \
+    if (::pfx::prof_on()) ::pfx::prof_mark(name, stream, true, flops);  \
+    __VA_ARGS__;                                                        \
+    if (::pfx::prof_on()) ::pfx::prof_mark(name, stream, false);        \
   } while (0)
+#define PFX_LAUNCH(name, stream, ...) PFX_LAUNCH_F(name, stream, 0.0, __VA_ARGS__)
 
 // ---- complex arithmetic (device) -----------------------------------------
 struct cplx {

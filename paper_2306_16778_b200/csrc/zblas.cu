@@ -1,0 +1,487 @@
+// Batched complex128 GEMM / TRSM / LU-panel kernels for sm_100a (see zblas.cuh).
+//
+// zgemm: 64x64 output tile per CTA, K staged 16 complex at a time through shared
+// memory with cp.async double buffering, 8 warps each owning a 32x16 sub-tile of
+// 4x2 DMMA 8x8 tiles.  A complex 8x8x4 product is four real DMMA.8x8x4
+// (Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br).  Shared-memory rows are padded by one
+// complex element so both fragment loads spread over all 32 banks (4 wavefronts per
+// 512-byte warp request, the minimum).
+#include "zblas.cuh"
+
+namespace pfx {
+
+constexpr int GM = 64, GN = 64, GK = 16;
+constexpr int GAS = GK + 1, GBS = GN + 1;
+constexpr int G_THREADS = 256;
+
+struct GemmSmem {
+  double2 A[2][GM][GAS];
+  double2 B[2][GK][GBS];
+};
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+
+__global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GemmSmem& S = *reinterpret_cast<GemmSmem*>(smem_raw);
+  const int b = blockIdx.z;
+  const int m0 = blockIdx.y * GM, n0 = blockIdx.x * GN;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;  // warp tile rows [wm*32, +32), cols [wn*16, +16)
+  const double2* Ab = A.p + b * A.stride;
+  const double2* Bb = B.p + b * B.stride;
+  double cr[4][2][2], ci[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+
+  const int ktiles = (k + GK - 1) / GK;
+  auto load = [&](int buf, int kt) {
+    const int k0 = kt * GK;
+#pragma unroll
+    for (int u = 0; u < (GM * GK) / G_THREADS; ++u) {
+      int e = tid + u * G_THREADS;
+      int r = e / GK, c = e % GK;
+      bool v = (m0 + r < m) && (k0 + c < k);
+      const double2* src = v ? Ab + (int64_t)(m0 + r) * A.ld + k0 + c : Ab;
+      cp_async16_zfill(&S.A[buf][r][c], src, v);
+    }
+#pragma unroll
+    for (int u = 0; u < (GK * GN) / G_THREADS; ++u) {
+      int e = tid + u * G_THREADS;
+      int r = e / GN, c = e % GN;
+      bool v = (k0 + r < k) && (n0 + c < n);
+      const double2* src = v ? Bb + (int64_t)(k0 + r) * B.ld + n0 + c : Bb;
+      cp_async16_zfill(&S.B[buf][r][c], src, v);
+    }
+  };
+  if (ktiles > 0) load(0, 0);
+  cp_async_commit();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) load(buf ^ 1, kt + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK; kk += 4) {
+      double ar[4], ai[4], br[2], bi[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double2 x = S.A[buf][wm * 32 + i * 8 + g][kk + t];
+        ar[i] = alpha * x.x;
+        ai[i] = alpha * x.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double2 y = S.B[buf][kk + t][wn * 16 + j * 8 + g];
+        br[j] = y.x;
+        bi[j] = y.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) zmma884(cr[i][j], ci[i][j], ar[i], ai[i], br[j], bi[j]);
+    }
+    __syncthreads();
+  }
+  double2* Cb = C.p + b * C.stride;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    if (row >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn * 16 + j * 8 + 2 * t + h;
+        if (col < n) {
+          double2* p = Cb + (int64_t)row * C.ld + col;
+          double2 v = *p;
+          v.x += cr[i][j][h];
+          v.y += ci[i][j][h];
+          *p = v;
+        }
+      }
+    }
+  }
+}
+
+int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C) {
+  if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
+  static bool attr = false;
+  const int smem = (int)sizeof(GemmSmem);
+  if (!attr) {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(n, GN), (unsigned)ceil_div(m, GM), (unsigned)batch);
+  PFX_LAUNCH_F("zgemm", s, 8.0 * (double)m * n * k * batch,
+               zgemm_kernel<<<grid, G_THREADS, smem, s>>>(m, n, k, alpha, A, B, C));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Unblocked LU of an m x nb panel, one CTA per batch element, panel in global memory
+// (L2-resident).  With ipiv: partial pivoting inside the panel (max |re|+|im|, first
+// index on ties).  nb <= 64.
+constexpr int P_THREADS = 256;
+
+__global__ void __launch_bounds__(P_THREADS) zgetf2_kernel(int m, int nb, ZMat P, int* ipiv, int* sing) {
+  __shared__ double sv[P_THREADS / 32];
+  __shared__ int si[P_THREADS / 32];
+  __shared__ double2 prow[64];
+  __shared__ int s_piv;
+  const int b = blockIdx.x;
+  double2* A = P.p + b * P.stride;
+  const int64_t lda = P.ld;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int j = 0; j < nb && j < m; ++j) {
+    int piv = j;
+    if (ipiv) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int r = j + tid; r < m; r += P_THREADS) {
+        double2 x = A[(int64_t)r * lda + j];
+        double v = fabs(x.x) + fabs(x.y);
+        if (v > bv) {
+          bv = v;
+          bi = r;
+        }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, bv, off);
+        int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        sv[warp] = bv;
+        si[warp] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double best = sv[0];
+        int bidx = si[0];
+        for (int w = 1; w < P_THREADS / 32; ++w)
+          if (sv[w] > best || (sv[w] == best && si[w] < bidx)) {
+            best = sv[w];
+            bidx = si[w];
+          }
+        s_piv = bidx;
+        ipiv[b * nb + j] = bidx;
+      }
+      __syncthreads();
+      piv = s_piv;
+      if (piv != j)
+        for (int c = tid; c < nb; c += P_THREADS) {
+          double2 x = A[(int64_t)j * lda + c];
+          A[(int64_t)j * lda + c] = A[(int64_t)piv * lda + c];
+          A[(int64_t)piv * lda + c] = x;
+        }
+      __syncthreads();
+    }
+    for (int c = tid; c < nb; c += P_THREADS) prow[c] = A[(int64_t)j * lda + c];
+    __syncthreads();
+    cplx pv = ld(&prow[j]);
+    if (pv.re == 0.0 && pv.im == 0.0) {
+      if (tid == 0) *sing = 1;
+      continue;
+    }
+    cplx rp = crcp(pv);
+    // rows below: scale column j, rank-1 update of columns j+1..nb-1
+    const int cols = nb - j - 1;
+    for (int r = j + 1 + tid; r < m; r += P_THREADS) {
+      double2* row = A + (int64_t)r * lda;
+      cplx l = cmul(ld(&row[j]), rp);
+      st(&row[j], l);
+      for (int c = 0; c < cols; ++c) st(&row[j + 1 + c], cfms(ld(&row[j + 1 + c]), l, ld(&prow[j + 1 + c])));
+    }
+    __syncthreads();
+  }
+}
+
+// Shared-memory variant for panels that fit on chip (m*nb <= 4096 complex, e.g. the
+// 64x64 diagonal blocks of the no-pivot LUs): one CTA per batch element, the panel
+// is loaded once, factored with one __syncthreads per column, written back once.
+constexpr int PS_MAXEL = 64 * 65;
+__global__ void __launch_bounds__(P_THREADS) zgetf2_smem_kernel(int m, int nb, ZMat P, int* ipiv, int* sing) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Ps = reinterpret_cast<double2*>(smem_raw);
+  __shared__ double sv[P_THREADS / 32];
+  __shared__ int si[P_THREADS / 32];
+  __shared__ int s_piv;
+  const int b = blockIdx.x;
+  double2* A = P.p + b * P.stride;
+  const int64_t lda = P.ld;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ps = nb + 1;
+  for (int e = tid; e < m * nb; e += P_THREADS) {
+    int r = e / nb, c = e - r * nb;
+    Ps[r * ps + c] = A[(int64_t)r * lda + c];
+  }
+  __syncthreads();
+  for (int j = 0; j < nb && j < m; ++j) {
+    if (ipiv) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int r = j + tid; r < m; r += P_THREADS) {
+        double2 x = Ps[r * ps + j];
+        double v = fabs(x.x) + fabs(x.y);
+        if (v > bv) {
+          bv = v;
+          bi = r;
+        }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, bv, off);
+        int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        sv[warp] = bv;
+        si[warp] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double best = sv[0];
+        int bidx = si[0];
+        for (int w = 1; w < P_THREADS / 32; ++w)
+          if (sv[w] > best || (sv[w] == best && si[w] < bidx)) {
+            best = sv[w];
+            bidx = si[w];
+          }
+        s_piv = bidx;
+        ipiv[b * nb + j] = bidx;
+      }
+      __syncthreads();
+      const int piv = s_piv;
+      if (piv != j)
+        for (int c = tid; c < nb; c += P_THREADS) {
+          double2 x = Ps[j * ps + c];
+          Ps[j * ps + c] = Ps[piv * ps + c];
+          Ps[piv * ps + c] = x;
+        }
+      __syncthreads();
+    }
+    const cplx pv = ld(&Ps[j * ps + j]);
+    if (pv.re == 0.0 && pv.im == 0.0) {
+      if (tid == 0) *sing = 1;
+      __syncthreads();
+      continue;
+    }
+    const cplx rp = crcp(pv);
+    // (row, column) pairs of the trailing part; the multiplier column is recomputed per
+    // element from the unscaled value so every thread works independently
+    const int rows = m - j - 1, cols = nb - j;
+    for (int e = tid; e < rows * cols; e += P_THREADS) {
+      const int r = j + 1 + e / cols, c = j + e % cols;
+      const cplx l = cmul(ld(&Ps[r * ps + j]), rp);
+      if (c == j) continue;
+      st(&Ps[r * ps + c], cfms(ld(&Ps[r * ps + c]), l, ld(&Ps[j * ps + c])));
+    }
+    __syncthreads();
+    for (int r = j + 1 + tid; r < m; r += P_THREADS) st(&Ps[r * ps + j], cmul(ld(&Ps[r * ps + j]), rp));
+    __syncthreads();
+  }
+  for (int e = tid; e < m * nb; e += P_THREADS) {
+    int r = e / nb, c = e - r * nb;
+    A[(int64_t)r * lda + c] = Ps[r * ps + c];
+  }
+}
+
+int zgetf2_panel(cudaStream_t s, int batch, int m, int nb, ZMat P, int* ipiv, int* sing) {
+  if (nb > 64) return fail(PFX_BADARG, "zgetf2_panel: nb > 64");
+  if ((int64_t)m * (nb + 1) <= PS_MAXEL) {
+    const int smem = (int)((int64_t)m * (nb + 1) * sizeof(double2));
+    static bool attr = false;
+    if (!attr) {
+      PFX_CUDA_TRY(cudaFuncSetAttribute(zgetf2_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_MAXEL * 16 + 64));
+      attr = true;
+    }
+    PFX_LAUNCH_F("zgetf2", s, 8.0 / 3.0 * nb * nb * (double)m * batch,
+                 zgetf2_smem_kernel<<<batch, P_THREADS, smem, s>>>(m, nb, P, ipiv, sing));
+    PFX_CUDA_TRY(cudaGetLastError());
+    return PFX_OK;
+  }
+  PFX_LAUNCH("zgetf2", s, zgetf2_kernel<<<batch, P_THREADS, 0, s>>>(m, nb, P, ipiv, sing));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Row interchanges: for each column c in [c0, c1) (one thread per column), apply
+// swaps j = 0..nb-1 (dir = +1) or nb-1..0 (dir = -1) of rows r0+j <-> r0+ipiv[j].
+__global__ void zlaswp_kernel(int nb, ZMat A, int64_t r0, int64_t c0, int64_t c1, const int* ipiv, int dir) {
+  const int b = blockIdx.y;
+  const int64_t c = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  double2* Ab = A.p + b * A.stride;
+  const int* ip = ipiv + b * nb;
+  for (int jj = 0; jj < nb; ++jj) {
+    int j = dir > 0 ? jj : nb - 1 - jj;
+    int p = ip[j];
+    if (p != j) {
+      double2* x = Ab + (r0 + j) * A.ld + c;
+      double2* y = Ab + (r0 + p) * A.ld + c;
+      double2 tmp = *x;
+      *x = *y;
+      *y = tmp;
+    }
+  }
+}
+
+int zlaswp(cudaStream_t s, int batch, int nb, ZMat A, int64_t r0, int64_t c0, int64_t c1, const int* ipiv, int dir) {
+  if (c1 <= c0) return PFX_OK;
+  dim3 grid((unsigned)ceil_div(c1 - c0, 128), (unsigned)batch);
+  PFX_LAUNCH("zlaswp", s, zlaswp_kernel<<<grid, 128, 0, s>>>(nb, A, r0, c0, c1, ipiv, dir));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Left triangular solves on an nb x n block: each CTA owns a strip of 32 columns
+// (one lane per column), the triangle in shared memory.  MODE 0: unit lower
+// (forward), MODE 1: upper non-unit (backward).
+constexpr int T_COLS = 32;
+constexpr int T_THREADS = 256;  // 8 warps: warp w handles rows w, w+8, ... of the update
+
+template <int MODE>
+__global__ void __launch_bounds__(T_THREADS) ztrsm_left_kernel(int nb, int n, ZMat T, ZMat B) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Ts = reinterpret_cast<double2*>(smem_raw);  // nb x (nb+1)
+  double2* Bs = Ts + nb * (nb + 1);                    // nb x (T_COLS+1)
+  const int b = blockIdx.y;
+  const int c0 = blockIdx.x * T_COLS;
+  const int tid = threadIdx.x;
+  const double2* Tb = T.p + b * T.stride;
+  double2* Bb = B.p + b * B.stride;
+  for (int e = tid; e < nb * nb; e += T_THREADS) {
+    int r = e / nb, c = e % nb;
+    Ts[r * (nb + 1) + c] = Tb[(int64_t)r * T.ld + c];
+  }
+  for (int e = tid; e < nb * T_COLS; e += T_THREADS) {
+    int r = e / T_COLS, c = e % T_COLS;
+    Bs[r * (T_COLS + 1) + c] = (c0 + c < n) ? Bb[(int64_t)r * B.ld + c0 + c] : make_double2(0, 0);
+  }
+  __syncthreads();
+  const int col = tid % T_COLS, rg = tid / T_COLS;  // 8 row groups
+  if (MODE == 0) {
+    for (int kk = 0; kk < nb; ++kk) {
+      cplx x = ld(&Bs[kk * (T_COLS + 1) + col]);
+      for (int r = kk + 1 + rg; r < nb; r += T_THREADS / T_COLS)
+        st(&Bs[r * (T_COLS + 1) + col], cfms(ld(&Bs[r * (T_COLS + 1) + col]), ld(&Ts[r * (nb + 1) + kk]), x));
+      __syncthreads();
+    }
+  } else {
+    for (int kk = nb - 1; kk >= 0; --kk) {
+      if (rg == 0) {
+        cplx x = cdiv(ld(&Bs[kk * (T_COLS + 1) + col]), ld(&Ts[kk * (nb + 1) + kk]));
+        st(&Bs[kk * (T_COLS + 1) + col], x);
+      }
+      __syncthreads();
+      cplx x = ld(&Bs[kk * (T_COLS + 1) + col]);
+      for (int r = rg; r < kk; r += T_THREADS / T_COLS)
+        st(&Bs[r * (T_COLS + 1) + col], cfms(ld(&Bs[r * (T_COLS + 1) + col]), ld(&Ts[r * (nb + 1) + kk]), x));
+      __syncthreads();
+    }
+  }
+  for (int e = tid; e < nb * T_COLS; e += T_THREADS) {
+    int r = e / T_COLS, c = e % T_COLS;
+    if (c0 + c < n) Bb[(int64_t)r * B.ld + c0 + c] = Bs[r * (T_COLS + 1) + c];
+  }
+}
+
+// Right upper solve B = B U^{-1} (m x nb): each CTA owns 32 rows (one lane per row).
+__global__ void __launch_bounds__(T_THREADS) ztrsm_runn_kernel(int m, int nb, ZMat U, ZMat B) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Us = reinterpret_cast<double2*>(smem_raw);  // nb x (nb+1)
+  double2* Bs = Us + nb * (nb + 1);                    // T_COLS rows x (nb+1)
+  const int b = blockIdx.y;
+  const int r0 = blockIdx.x * T_COLS;
+  const int tid = threadIdx.x;
+  const double2* Ub = U.p + b * U.stride;
+  double2* Bb = B.p + b * B.stride;
+  for (int e = tid; e < nb * nb; e += T_THREADS) {
+    int r = e / nb, c = e % nb;
+    Us[r * (nb + 1) + c] = Ub[(int64_t)r * U.ld + c];
+  }
+  for (int e = tid; e < T_COLS * nb; e += T_THREADS) {
+    int r = e / nb, c = e % nb;
+    Bs[r * (nb + 1) + c] = (r0 + r < m) ? Bb[(int64_t)(r0 + r) * B.ld + c] : make_double2(0, 0);
+  }
+  __syncthreads();
+  const int row = tid % T_COLS, cg = tid / T_COLS;
+  for (int j = 0; j < nb; ++j) {
+    if (cg == 0) {
+      cplx x = cdiv(ld(&Bs[row * (nb + 1) + j]), ld(&Us[j * (nb + 1) + j]));
+      st(&Bs[row * (nb + 1) + j], x);
+    }
+    __syncthreads();
+    cplx x = ld(&Bs[row * (nb + 1) + j]);
+    for (int c = j + 1 + cg; c < nb; c += T_THREADS / T_COLS)
+      st(&Bs[row * (nb + 1) + c], cfms(ld(&Bs[row * (nb + 1) + c]), x, ld(&Us[j * (nb + 1) + c])));
+    __syncthreads();
+  }
+  for (int e = tid; e < T_COLS * nb; e += T_THREADS) {
+    int r = e / nb, c = e % nb;
+    if (r0 + r < m) Bb[(int64_t)(r0 + r) * B.ld + c] = Bs[r * (nb + 1) + c];
+  }
+}
+
+static int trsm_smem(int nb) { return (int)((size_t)nb * (nb + 1) + (size_t)nb * (T_COLS + 1)) * (int)sizeof(double2); }
+static const int kTrsmSmemMax = (64 * 65 + 64 * 33) * (int)sizeof(double2);
+static int trsm_attrs() {
+  static bool done = false;
+  if (!done) {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_left_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_left_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_runn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
+    done = true;
+  }
+  return PFX_OK;
+}
+
+int ztrsm_llnu(cudaStream_t s, int batch, int nb, int n, ZMat Lm, ZMat B) {
+  if (n <= 0) return PFX_OK;
+  const int smem = trsm_smem(nb);
+  if (int rc = trsm_attrs()) return rc;
+  dim3 grid((unsigned)ceil_div(n, T_COLS), (unsigned)batch);
+  PFX_LAUNCH("ztrsm", s, ztrsm_left_kernel<0><<<grid, T_THREADS, smem, s>>>(nb, n, Lm, B));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+int ztrsm_lunn(cudaStream_t s, int batch, int nb, int n, ZMat Um, ZMat B) {
+  if (n <= 0) return PFX_OK;
+  const int smem = trsm_smem(nb);
+  if (int rc = trsm_attrs()) return rc;
+  dim3 grid((unsigned)ceil_div(n, T_COLS), (unsigned)batch);
+  PFX_LAUNCH("ztrsm", s, ztrsm_left_kernel<1><<<grid, T_THREADS, smem, s>>>(nb, n, Um, B));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+int ztrsm_runn(cudaStream_t s, int batch, int m, int nb, ZMat Um, ZMat B) {
+  if (m <= 0) return PFX_OK;
+  const int smem = trsm_smem(nb);
+  if (int rc = trsm_attrs()) return rc;
+  dim3 grid((unsigned)ceil_div(m, T_COLS), (unsigned)batch);
+  PFX_LAUNCH("ztrsm", s, ztrsm_runn_kernel<<<grid, T_THREADS, smem, s>>>(m, nb, Um, B));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+}  // namespace pfx

@@ -1,0 +1,39 @@
+// Batched complex128 building blocks for blocked LU on sm_100a (used by the large dense
+// path, config C4, and the banded path, config C5).
+//
+// All matrices are row-major complex128 (double2), addressed as base + i*ld + j, with a
+// per-batch stride.  A banded matrix stored by rows with its diagonals padded by zeros
+// is a dense row-major matrix with ld = (row length - 1), so the same kernels run on
+// the band window (banded.cu).
+#pragma once
+#include "pfx_common.cuh"
+
+namespace pfx {
+
+struct ZMat {
+  double2* p;
+  int64_t ld;
+  int64_t stride;  // batch stride (elements)
+  __host__ __device__ double2* at(int b, int64_t i, int64_t j) const { return p + b * stride + i * ld + j; }
+};
+
+// C[b] += alpha * A[b] (m x k) * B[b] (k x n), alpha = +-1.  DMMA m8n8k4, 64x64x16 tiles.
+int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C);
+
+// Unblocked LU of the m x nb panel at P (in place).  ipiv (optional, batch x nb, 0-based
+// rows relative to the panel) -> partial pivoting with row swaps inside the panel only.
+// sing: device int set to 1 on an exactly zero pivot.
+int zgetf2_panel(cudaStream_t s, int batch, int m, int nb, ZMat P, int* ipiv, int* sing);
+
+// Apply the panel's interchanges (rows r0+j <-> r0+ipiv[j], j = 0..nb-1, in order) to
+// columns [c0, c1) of A (skipping nothing; caller passes the column ranges).
+int zlaswp(cudaStream_t s, int batch, int nb, ZMat A, int64_t r0, int64_t c0, int64_t c1, const int* ipiv, int dir);
+
+// B = L^{-1} B, L = unit lower nb x nb at Lm (strictly lower part used), B nb x n.
+int ztrsm_llnu(cudaStream_t s, int batch, int nb, int n, ZMat Lm, ZMat B);
+// B = U^{-1} B, U = upper (non-unit) nb x nb, B nb x n.
+int ztrsm_lunn(cudaStream_t s, int batch, int nb, int n, ZMat Um, ZMat B);
+// B = B U^{-1}, U = upper (non-unit) nb x nb, B m x nb.
+int ztrsm_runn(cudaStream_t s, int batch, int m, int nb, ZMat Um, ZMat B);
+
+}  // namespace pfx

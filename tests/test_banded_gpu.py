@@ -1,0 +1,57 @@
+"""Banded path (config C5 shape) on the GPU vs the CPU restatement (zgbsv per pair)."""
+import numpy as np
+import pytest
+
+from oracle import closed, restate
+from paper_2306_16778_b200 import BandedHermitian, ExpOptions, matexp_action, matexp_shifted, workloads
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("m", [3, 8, 20, 70])
+def test_lap2d_grid(m):
+    # 2-D 5-point Laplacian on m x m (kb = m), spectrum kept O(1..20) so exp(A)V is not tiny
+    band = workloads.c5_band(m, scale=2.0)
+    V = np.random.default_rng(m).standard_normal((m * m, 3))
+    got = matexp_action(BandedHermitian(band), V, ExpOptions(n=16, mode="action")).value
+    want = restate.banded_action(band, V, 16)
+    assert rel(got, want) <= TOL, rel(got, want)
+
+
+@pytest.mark.parametrize("N,kb", [(1, 0), (5, 1), (100, 7), (300, 64), (1000, 65), (2000, 130)])
+def test_random_bands(N, kb):
+    rng = np.random.default_rng(N + kb)
+    band = rng.uniform(-1, 1, (kb + 1, N)) * 0.5
+    band[0] = -4.0 * (kb + 1) * rng.uniform(0.2, 1.0, N) / max(kb, 1)  # negative-ish diagonal
+    V = rng.standard_normal((N, 2))
+    got = matexp_action(BandedHermitian(band), V, ExpOptions(n=20, mode="action")).value
+    want = restate.banded_action(band, V, 20)
+    assert rel(got, want) <= TOL, rel(got, want)
+
+
+def test_vector_and_shift():
+    m = 12
+    band = workloads.c5_band(m, scale=1.0)
+    band = band.copy()
+    band[0] += 5.0  # positive part of the spectrum -> shift method
+    v = np.random.default_rng(1).standard_normal(m * m)
+    res = matexp_shifted(BandedHermitian(band), ExpOptions(n=32, mode="action", shift="auto"), v=v)
+    c = res.c_applied
+    sh = band.copy()
+    sh[0] -= c
+    want = np.exp(c) * restate.banded_action(sh, v[:, None], 32)[:, 0]
+    assert rel(res.value, want) <= TOL
+
+
+def test_c5_shape_scaled_down_vs_dst():
+    m = 40
+    band = workloads.c5_band(m, scale=50.0 * (m + 1) ** 2 / 513.0**2)  # same spectral scaling as C5 per grid
+    V = workloads.c5_rhs(m, 8)
+    got = matexp_action(BandedHermitian(band), V, ExpOptions(n=16, mode="action")).value
+    want = restate.banded_action(band, V, 16)
+    assert rel(got, want) <= TOL
