@@ -77,7 +77,8 @@ __host__ __device__ __forceinline__ cplx crcp(cplx z) {
 }
 __host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) { return cmul(a, crcp(b)); }
 
-// Fast binary64 reciprocal: MUFU seed + two Newton steps (<= 1 ulp for normal x).
+// Fast binary64 reciprocal of a positive normal x: MUFU seed + two Newton steps on the
+// FMA pipe (<= 1 ulp).
 __device__ __forceinline__ double frcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -85,6 +86,13 @@ __device__ __forceinline__ double frcp(double x) {
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
+}
+
+// 2^(1023 - E(m)) for positive normal m (E = biased exponent): scales m into [1, 2)
+// with integer ops only (no frexp/ldexp on the XU pipe).
+__device__ __forceinline__ double pow2_inv_scale(double m) {
+  long long e = (__double_as_longlong(m) >> 52) & 0x7ff;
+  return __longlong_as_double((2046LL - e) << 52);
 }
 // 1/z = conj(z)/|z|^2 with the fast reciprocal; falls back to the scaled form
 // when |z|^2 leaves the comfortable exponent range.

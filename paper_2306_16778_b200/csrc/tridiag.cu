@@ -36,7 +36,7 @@
 
 namespace pfx {
 
-constexpr int TR_L = 128;     // rows per chunk
+constexpr int TR_L = 256;     // rows per chunk
 constexpr int TR_RT = 16;     // RHS per tile (threads per shift)
 constexpr int TR_KG = 16;     // max shifts per pass
 constexpr int TR_WIN = 4;     // rows per combine window
@@ -66,6 +66,8 @@ struct TriArgs {
   double2* Lf;  // N x npairs  forward multipliers l_i
   double2* Lb;  // N x npairs  backward multipliers l'_i
   double2* Wt;  // N x npairs  twisted weights 2a/gamma_i
+  int* contr;   // P          1 if every |l|, |l'| of the chunk is <= 1 (running products shrink)
+  unsigned long long* vmax;  // nrhs  bit pattern of max_i |V[i, r]|
   double* out;  // N x nrhs
 };
 
@@ -93,9 +95,7 @@ __device__ __forceinline__ M22 mmul(const M22& a, const M22& b) {
 // exact power-of-two rescale so the largest |component| is in [1, 2)
 __device__ __forceinline__ void mnorm(M22& a) {
   double mx = fmax(fmax(fmax(cabs1(a.m0), cabs1(a.m1)), fmax(cabs1(a.m2), cabs1(a.m3))), 1e-300);
-  int ex;
-  frexp(mx, &ex);
-  double s = ldexp(1.0, 1 - ex);
+  double s = pow2_inv_scale(mx);
   a.m0 = cscale(a.m0, s);
   a.m1 = cscale(a.m1, s);
   a.m2 = cscale(a.m2, s);
@@ -205,9 +205,7 @@ __global__ void __launch_bounds__(TR_SCAN_T) tri_mobius_scan(TriArgs a) {
     cplx nn = cadd(cmul(T.m0, vn), cmul(T.m1, vd));
     cplx nd = cadd(cmul(T.m2, vn), cmul(T.m3, vd));
     double mx = fmax(fmax(cabs1(nn), cabs1(nd)), 1e-300);
-    int ex;
-    frexp(mx, &ex);
-    double s = ldexp(1.0, 1 - ex);
+    double s = pow2_inv_scale(mx);
     vn = cscale(nn, s);
     vd = cscale(nd, s);
   }
@@ -224,9 +222,7 @@ __global__ void __launch_bounds__(TR_SCAN_T) tri_mobius_scan(TriArgs a) {
 //   Lf = l, Lb = l', Wt = w, and the chunk products LF = prod(-l), LB = prod(-l').
 __device__ __forceinline__ void rescale2(cplx& x, cplx& y) {
   double mx = fmax(fmax(cabs1(x), cabs1(y)), 1e-300);
-  int ex;
-  frexp(mx, &ex);
-  double s = ldexp(1.0, -ex);
+  double s = pow2_inv_scale(mx);
   x = cscale(x, s);
   y = cscale(y, s);
 }
@@ -241,6 +237,7 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
   const cplx th = ld(&a.theta[k]);
   const int np = a.npairs;
   auto offe = [&](int64_t gi) -> double { return (gi >= 0 && gi < a.N - 1) ? a.off[gi] : 0.0; };
+  bool noncontr = false;
   // backward chain
   {
     cplx q1 = mk(1, 0), q2 = ld(&a.rhob_in[c * np + k]);
@@ -253,6 +250,7 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
       double e2 = e * e;
       cplx q0 = cplx{fma(b.re, q1.re, fma(-b.im, q1.im, -e2 * q2.re)), fma(b.re, q1.im, fma(b.im, q1.re, -e2 * q2.im))};
       st(&a.Lb[(s + i) * np + k], lv);
+      if (fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
       lam = cmul(lam, mk(-lv.re, -lv.im));
       q2 = q1;
       q1 = q0;
@@ -279,6 +277,7 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
       cplx w = cdiv_fast(co2, gam);
       st(&a.Lf[(s + i) * np + k], lv);
       st(&a.Wt[(s + i) * np + k], w);
+      if (fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
       lam = cmul(lam, mk(-lv.re, -lv.im));
       p2 = p1;
       p1 = p0;
@@ -287,11 +286,9 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
     }
     st(&a.LF[c * np + k], lam);
   }
+  if (noncontr) atomicAnd(&a.contr[c], 0);
 }
 
-// K_T4 tri_sweep: one thread per (chunk, rhs); the recurrences of all shifts run
-// interleaved in registers (ILP = npairs), the combine over shifts is a register sum
-// in ascending shift order (deterministic).  Zero RHS carry-in; chunk summaries out.
 // K_T4 tri_sweep / K_T5 tri_fix share one streaming skeleton.  Thread layout: a
 // half-warp = one (chunk, 16-RHS tile), lane r = one right-hand side; the
 // recurrences of all shifts of that RHS run interleaved in registers (ILP =
@@ -299,6 +296,16 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
 // half-warp stages its chunk's factor data (l or l', w) and RHS rows through
 // shared memory in TR_T-row tiles with cp.async double buffering, so the global
 // loads of tile t+1 overlap the FP64 work of tile t.
+//   MODE 0 (tri_sweep): forward sweep (writes F_i = sum_k Re(w (g - f))), then the
+//     backward sweep of the same chunk adds sum_k Re(w g') (F read back while L2-hot);
+//     zero RHS carry-in, chunk summaries gF/gB, running max |V[:, r]|.
+//   MODE 1 (tri_fix): true carries through Lambda_i = prod_{j<=i}(-l_j) (forward, from
+//     the chunk top) and Lambda'_i (backward, from the chunk bottom).  In a contractive
+//     chunk (all |l|, |l'| <= 1) |Lambda| never grows, and |w| <= 2|a|/Im(theta) (the
+//     pivots of T + theta I satisfy |gamma| >= Im(theta)), so once
+//     sum_k (2|a_k|/Im theta_k) |Lambda_k| |G_k| <= 2^-60 max|V[:, r]| every remaining
+//     row's correction is below that bound and the pass stops (exact to far below
+//     binary64 rounding of the result; full pass for non-contractive chunks).
 constexpr int TR_T = 8;            // rows per staged tile
 constexpr int TR_SW_WARPS = 4;     // warps per block
 
@@ -312,7 +319,7 @@ struct TriStage {
 // stage rows [r0, r0+cnt) (cnt <= TR_T) of L and Wt plus the RHS tile into buffer b
 template <int KM>
 __device__ __forceinline__ void stage_tile(TriStage<KM>& S, int b, const TriArgs& a, const double2* L, int64_t r0,
-                                           int cnt, int rt0, int lane16) {
+                                           int cnt, int rt0, int lane16, bool want_f) {
   const int np = a.npairs;
   const int nel = cnt * np;  // complex elements per array
   const double2* ls = L + r0 * np;
@@ -325,17 +332,16 @@ __device__ __forceinline__ void stage_tile(TriStage<KM>& S, int b, const TriArgs
     cp_async16(&wd[rr * KM + k], &ws[e]);
   }
   const int rg = rt0 + lane16;
-  if (rg < a.nrhs)
+  if (want_f && rg < a.nrhs)
     for (int rr = 0; rr < cnt; ++rr) cp_async8(&S.f[b][rr][lane16], &a.V[(r0 + rr) * a.nrhs + rg]);
 }
 
-// MODE 0: sweep (zero carry; out = or += contributions, summaries gF/gB)
-// MODE 1: fix   (true carries G/G' through Lambda products; out +=)
-template <int KM, int DIR, int MODE>
-__global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_stream(TriArgs a) {
+template <int KM, int MODE>
+__global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_pass(TriArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, lane16 = lane & 15;
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
   TriStage<KM>& S = reinterpret_cast<TriStage<KM>*>(smem_raw)[warp * 2 + half];
   const int ntile = (a.nrhs + TR_RT - 1) / TR_RT;
   const int64_t unit = (blockIdx.x * (int64_t)TR_SW_WARPS + warp) * 2 + half;  // (chunk, rhs tile)
@@ -347,64 +353,105 @@ __global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_stream(TriArgs a) {
   const int64_t s = c * TR_L;
   const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
   const int np = a.npairs;
-  const double2* L = DIR == 0 ? a.Lf : a.Lb;
-  cplx g[KM], G[KM];
-#pragma unroll
-  for (int k = 0; k < KM; ++k) {
-    if (MODE == 0) {
-      g[k] = mk(0, 0);
-    } else {
-      g[k] = mk(1, 0);  // Lambda
-      const double2* Gs = DIR == 0 ? a.G : a.Gb;
-      G[k] = (k < np && rv) ? ld(&Gs[(c * np + k) * a.nrhs + r]) : mk(0, 0);
-    }
-  }
   const int ntl = (rows + TR_T - 1) / TR_T;
-  // tile t covers local rows [t*TR_T, ...) ; backward sweeps walk tiles and rows in reverse
-  auto tile_first = [&](int t) { return DIR == 0 ? t * TR_T : max(rows - (t + 1) * TR_T, 0); };
-  auto tile_cnt = [&](int t) { return DIR == 0 ? min(TR_T, rows - t * TR_T) : rows - t * TR_T - max(rows - (t + 1) * TR_T, 0); };
-  stage_tile<KM>(S, 0, a, L, s + tile_first(0), tile_cnt(0), rt0, lane16);
-  cp_async_commit();
-  for (int t = 0; t < ntl; ++t) {
-    const int b = t & 1;
-    if (t + 1 < ntl) stage_tile<KM>(S, b ^ 1, a, L, s + tile_first(t + 1), tile_cnt(t + 1), rt0, lane16);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncwarp();
-    const int first = tile_first(t), cnt = tile_cnt(t);
-    for (int jj = 0; jj < cnt; ++jj) {
-      const int j = DIR == 0 ? jj : cnt - 1 - jj;
-      const int64_t row = s + first + j;
-      const double f = S.f[b][j][lane16];
-      double acc = 0.0;
-      if (MODE == 1 || DIR == 1) acc = rv ? a.out[row * a.nrhs + r] : 0.0;
+  double vmx = 0.0;
+  double tau = 0.0;
+  bool contr = false;
+  double beta[KM];
+  if (MODE == 1) {
+    tau = rv ? ldexp(__longlong_as_double((long long)a.vmax[r]), -60) : 1.0;
+    contr = a.contr[c] != 0;
 #pragma unroll
-      for (int k = 0; k < KM; ++k) {
-        if (k < np) {
-          const cplx l = ld(&S.l[b][j][k]);
-          const cplx w = ld(&S.w[b][j][k]);
-          if (MODE == 0) {
-            g[k] = cplx{fma(-l.re, g[k].re, fma(l.im, g[k].im, f)), fma(-l.re, g[k].im, -l.im * g[k].re)};
-            const double gre = DIR == 0 ? g[k].re - f : g[k].re;
-            acc = fma(w.re, gre, fma(-w.im, g[k].im, acc));
-          } else {
-            g[k] = cmul(g[k], mk(-l.re, -l.im));
-            const cplx tt = cmul(g[k], G[k]);
-            acc = fma(w.re, tt.re, fma(-w.im, tt.im, acc));
-          }
-        }
+    for (int k = 0; k < KM; ++k) {
+      if (k < np) {
+        cplx th = ld(&a.theta[k]), co = ld(&a.coef[k]);
+        beta[k] = 2.0 * (fabs(co.re) + fabs(co.im)) / th.im;
+      } else {
+        beta[k] = 0.0;
       }
-      if (rv) a.out[row * a.nrhs + r] = acc;
     }
-    __syncwarp();
   }
-  if (MODE == 0 && rv) {
-    double2* dst = DIR == 0 ? a.gF : a.gB;
+  for (int dir = 0; dir < 2; ++dir) {
+    const double2* L = dir == 0 ? a.Lf : a.Lb;
+    cplx g[KM], G[KM];
 #pragma unroll
-    for (int k = 0; k < KM; ++k)
-      if (k < np) st(&dst[(c * np + k) * a.nrhs + r], g[k]);
+    for (int k = 0; k < KM; ++k) {
+      if (MODE == 0) {
+        g[k] = mk(0, 0);
+      } else {
+        g[k] = mk(1, 0);  // Lambda
+        const double2* Gs = dir == 0 ? a.G : a.Gb;
+        G[k] = (k < np && rv) ? ld(&Gs[(c * np + k) * a.nrhs + r]) : mk(0, 0);
+      }
+    }
+    auto tile_first = [&](int t) { return dir == 0 ? t * TR_T : max(rows - (t + 1) * TR_T, 0); };
+    auto tile_cnt = [&](int t) {
+      return dir == 0 ? min(TR_T, rows - t * TR_T) : rows - t * TR_T - max(rows - (t + 1) * TR_T, 0);
+    };
+    bool done = false;
+    stage_tile<KM>(S, 0, a, L, s + tile_first(0), tile_cnt(0), rt0, lane16, MODE == 0);
+    cp_async_commit();
+    for (int t = 0; t < ntl; ++t) {
+      const int b = t & 1;
+      if (t + 1 < ntl) stage_tile<KM>(S, b ^ 1, a, L, s + tile_first(t + 1), tile_cnt(t + 1), rt0, lane16, MODE == 0);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp(hmask);
+      const int first = tile_first(t), cnt = tile_cnt(t);
+      for (int jj = 0; jj < cnt; ++jj) {
+        const int j = dir == 0 ? jj : cnt - 1 - jj;
+        const int64_t row = s + first + j;
+        double acc = 0.0;
+        if (MODE == 1 || dir == 1) acc = rv ? a.out[row * a.nrhs + r] : 0.0;
+        if (MODE == 0) {
+          const double f = S.f[b][j][lane16];
+          vmx = fmax(vmx, fabs(f));
+#pragma unroll
+          for (int k = 0; k < KM; ++k) {
+            if (k < np) {
+              const cplx l = ld(&S.l[b][j][k]);
+              const cplx w = ld(&S.w[b][j][k]);
+              g[k] = cplx{fma(-l.re, g[k].re, fma(l.im, g[k].im, f)), fma(-l.re, g[k].im, -l.im * g[k].re)};
+              const double gre = dir == 0 ? g[k].re - f : g[k].re;
+              acc = fma(w.re, gre, fma(-w.im, g[k].im, acc));
+            }
+          }
+        } else {
+          double bound = 0.0;
+#pragma unroll
+          for (int k = 0; k < KM; ++k) {
+            if (k < np) {
+              const cplx l = ld(&S.l[b][j][k]);
+              const cplx w = ld(&S.w[b][j][k]);
+              g[k] = cmul(g[k], mk(-l.re, -l.im));
+              const cplx tt = cmul(g[k], G[k]);
+              acc = fma(w.re, tt.re, fma(-w.im, tt.im, acc));
+              bound = fma(beta[k] * cabs1(g[k]), cabs1(G[k]), bound);
+            }
+          }
+          if (contr && bound <= tau) done = true;
+        }
+        if (rv) a.out[row * a.nrhs + r] = acc;
+      }
+      __syncwarp(hmask);
+      if (MODE == 1 && !__any_sync(hmask, !done)) {
+        cp_async_wait<0>();
+        break;
+      }
+    }
+    if (MODE == 0 && rv) {
+      double2* dst = dir == 0 ? a.gF : a.gB;
+#pragma unroll
+      for (int k = 0; k < KM; ++k)
+        if (k < np) st(&dst[(c * np + k) * a.nrhs + r], g[k]);
+    }
+    cp_async_wait<0>();
+    __syncwarp(hmask);
   }
+  if (MODE == 0 && rv) atomicMax(&a.vmax[r], (unsigned long long)__double_as_longlong(vmx));
 }
+
+#include "tridiag_ls.cuh"
 
 // K_T4 ------------------------------------------------------------------------
 // One warp per (shift, rhs, direction).  Affine maps x -> A x + B composed over chunks;
@@ -494,15 +541,11 @@ static int launch_stream(const TriArgs& a, cudaStream_t stream, int which) {
   const int smem = (int)(sizeof(TriStage<KM>) * TR_SW_WARPS * 2);
   const int th = TR_SW_WARPS * 32;
   if (which == 0) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PFX_LAUNCH("tri_sweep", stream, (tri_stream<KM, 0, 0><<<blocks, th, smem, stream>>>(a)));
-    PFX_LAUNCH("tri_sweep", stream, (tri_stream<KM, 1, 0><<<blocks, th, smem, stream>>>(a)));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_pass<KM, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_LAUNCH("tri_sweep", stream, (tri_pass<KM, 0><<<blocks, th, smem, stream>>>(a)));
   } else {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_stream<KM, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PFX_LAUNCH("tri_fix", stream, (tri_stream<KM, 0, 1><<<blocks, th, smem, stream>>>(a)));
-    PFX_LAUNCH("tri_fix", stream, (tri_stream<KM, 1, 1><<<blocks, th, smem, stream>>>(a)));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_pass<KM, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_LAUNCH("tri_fix", stream, (tri_pass<KM, 1><<<blocks, th, smem, stream>>>(a)));
   }
   return PFX_OK;
 }
@@ -521,7 +564,9 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   const size_t nP = (size_t)P * npairs;
   const size_t nPR = nP * nrhs;
   const size_t nN = (size_t)N * npairs;
-  size_t bytes = (nP * 4 * 2 + nP * 4 + nPR * 4 + nN * 3) * sizeof(double2);
+  const size_t nNf = npairs <= 16 ? 0 : nN;  // factor arrays only on the npairs > 16 path
+  size_t bytes = (nP * 4 * 2 + nP * 4 + nPR * 4 + nNf * 3) * sizeof(double2) + (size_t)P * sizeof(int) +
+                 (size_t)nrhs * sizeof(unsigned long long) + 64;
   double2* ws = static_cast<double2*>(scratch(1, bytes));
   if (!ws) return fail(PFX_CUDA, "tridiagonal workspace allocation failed");
   TriArgs a;
@@ -546,9 +591,13 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   a.G = a.gB + nPR;
   a.Gb = a.G + nPR;
   a.Lf = a.Gb + nPR;
-  a.Lb = a.Lf + nN;
-  a.Wt = a.Lb + nN;
+  a.Lb = a.Lf + nNf;
+  a.Wt = a.Lb + nNf;
+  a.contr = reinterpret_cast<int*>(a.Wt + nNf);
+  a.vmax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.contr) + ((P * sizeof(int) + 15) & ~size_t(15)));
   a.out = out;
+  PFX_CUDA_TRY(cudaMemsetAsync(a.contr, 0x01, (size_t)P * sizeof(int), stream));
+  PFX_CUDA_TRY(cudaMemsetAsync(a.vmax, 0, (size_t)nrhs * sizeof(unsigned long long), stream));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (launch_ms) {
     PFX_CUDA_TRY(cudaEventCreate(&e0));
@@ -561,18 +610,41 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaGetLastError());
     PFX_LAUNCH("tri_mobius_scan", stream, tri_mobius_scan<<<npairs * 2, TR_SCAN_T, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
-    PFX_LAUNCH("tri_factor", stream, tri_factor<<<(unsigned)ceil_div((int64_t)P * npairs, 128), 128, 0, stream>>>(a));
-    PFX_CUDA_TRY(cudaGetLastError());
   }
-  if (int rc = sweeps(a, stream, 0)) return rc;
-  PFX_CUDA_TRY(cudaGetLastError());
-  {
+  const bool ls = npairs <= 16;
+  LsArgs lsa{nullptr, nullptr};
+  if (ls) {
+    // checkpoints live in arena slot 2 (L2-resident: 2 x P x 32 x 16 x 32 B)
+    const size_t ckn = (size_t)P * LS_NBLK * 16;
+    LsCk* ckbuf = static_cast<LsCk*>(scratch(2, 2 * ckn * sizeof(LsCk)));
+    if (!ckbuf) return fail(PFX_CUDA, "tridiagonal checkpoint allocation failed");
+    lsa.ckb = ckbuf;
+    lsa.ckf = ckbuf + ckn;
+    const int ntile = (int)ceil_div(nrhs, 16);
+    const unsigned blocks = (unsigned)ceil_div((int64_t)P * ntile, LS_WARPS * 2);
+    const int smem = (int)(sizeof(LsSmem) * LS_WARPS * 2);
+    auto k0 = npairs <= 8 ? tri_ls<8, 0> : npairs <= 12 ? tri_ls<12, 0> : tri_ls<16, 0>;
+    auto k1 = npairs <= 8 ? tri_ls<8, 1> : npairs <= 12 ? tri_ls<12, 1> : tri_ls<16, 1>;
+    PFX_CUDA_TRY(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_LAUNCH("tri_sweep", stream, (k0<<<blocks, LS_WARPS * 32, smem, stream>>>(a, lsa)));
+    PFX_CUDA_TRY(cudaGetLastError());
     int warps = npairs * (int)nrhs * 2;
     PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
+    PFX_LAUNCH("tri_fix", stream, (k1<<<blocks, LS_WARPS * 32, smem, stream>>>(a, lsa)));
+    PFX_CUDA_TRY(cudaGetLastError());
+  } else {
+    PFX_LAUNCH("tri_factor", stream, tri_factor<<<(unsigned)ceil_div((int64_t)P * npairs, 128), 128, 0, stream>>>(a));
+    PFX_CUDA_TRY(cudaGetLastError());
+    if (int rc = sweeps(a, stream, 0)) return rc;
+    PFX_CUDA_TRY(cudaGetLastError());
+    int warps = npairs * (int)nrhs * 2;
+    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, stream>>>(a));
+    PFX_CUDA_TRY(cudaGetLastError());
+    if (int rc = sweeps(a, stream, 1)) return rc;
+    PFX_CUDA_TRY(cudaGetLastError());
   }
-  if (int rc = sweeps(a, stream, 1)) return rc;
-  PFX_CUDA_TRY(cudaGetLastError());
   if (shift_c != 0.0) {
     PFX_LAUNCH("scale_kernel", stream, scale_kernel<<<1184, 256, 0, stream>>>(out, (size_t)N * nrhs, exp(shift_c)));
     PFX_CUDA_TRY(cudaGetLastError());
