@@ -251,7 +251,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
 // Blocked by 32 rows: the contribution of already-solved blocks is a GEMV with
 // coalesced reads of W, the 32x32 diagonal block is solved by warp 0 in registers.
 __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, double2* z, double2* part,
-                             double2* diag) {
+                             double2* diag, const double2* rdiag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool forward = (kind == 0 || kind == 2);
   const int nblk = (d + 31) >> 5;
@@ -306,7 +306,8 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, dou
           xk.re = __shfl_sync(0xffffffffu, x.re, k);
           xk.im = __shfl_sync(0xffffffffu, x.im, k);
           if (!unit) {
-            xk = cdiv(xk, ld(&diag[k * 33 + k]));
+            const cplx rd = ld(&rdiag[i0 + k]);
+            xk = cmul(xk, kind == 2 ? cconj(rd) : rd);
             if (lane == k) x = xk;
           }
           if (lane > k && lane < bs) x = cfms(x, ld(&diag[lane * 33 + k]), xk);
@@ -317,7 +318,8 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, dou
           xk.re = __shfl_sync(0xffffffffu, x.re, k);
           xk.im = __shfl_sync(0xffffffffu, x.im, k);
           if (!unit) {
-            xk = cdiv(xk, ld(&diag[k * 33 + k]));
+            const cplx rd = ld(&rdiag[i0 + k]);
+            xk = cmul(xk, kind == 2 ? cconj(rd) : rd);
             if (lane == k) x = xk;
           }
           if (lane < k) x = cfms(x, ld(&diag[lane * 33 + k]), xk);
@@ -343,6 +345,8 @@ __global__ void __launch_bounds__(DB_THREADS, 1) dense_batched_kernel(DenseBatch
   int* red_i = reinterpret_cast<int*>(red_v + 32);                  // 32
   int* s_piv = red_i + 32;                                          // NB
   int* s_sing = s_piv + NB;                                         // 1
+  int* s_perm = s_sing + 4;                                         // d  (row permutation)
+  double2* rdiag = reinterpret_cast<double2*>(s_perm + ((d + 3) & ~3)); // d  (1 / U_ii)
 
   const int tid = threadIdx.x;
   const int slot = blockIdx.x;
@@ -376,6 +380,32 @@ __global__ void __launch_bounds__(DB_THREADS, 1) dense_batched_kernel(DenseBatch
     // ---- K1/K2: LU with partial pivoting
     lu_blocked<NB>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing);
     __syncthreads();
+    // row permutation of P M = L U (swaps applied in order to the identity) and 1/U_ii
+    for (int i = tid; i < d; i += DB_THREADS) {
+      s_perm[i] = ipiv[i];
+      const cplx u = ld(&W[(size_t)i * d + i]);
+      st(&rdiag[i], (u.re == 0.0 && u.im == 0.0) ? mk(0.0, 0.0) : crcp(u));
+    }
+    __syncthreads();
+    __syncthreads();
+    if (tid == 0) {
+      // s_perm holds ipiv; apply the swaps in order to the identity, in shared memory
+      int* piv = s_perm;
+      // walk backwards-compatible: build perm in rdiag-free scratch (the S strip buffer)
+      int* perm = reinterpret_cast<int*>(S);
+      for (int i = 0; i < d; ++i) perm[i] = i;
+      for (int i = 0; i < d; ++i) {
+        const int pr = piv[i];
+        if (pr != i) {
+          const int t = perm[i];
+          perm[i] = perm[pr];
+          perm[pr] = t;
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < d; i += DB_THREADS) s_perm[i] = reinterpret_cast<int*>(S)[i];
+    __syncthreads();
     if (*s_sing && tid == 0) atomicExch(a.status, PFX_SINGULAR);
     // ---- K3: solves, one RHS column at a time through shared memory
     double2* Yg = a.Y + (size_t)slot * d * nc;
@@ -383,48 +413,26 @@ __global__ void __launch_bounds__(DB_THREADS, 1) dense_batched_kernel(DenseBatch
     const bool want_conj = (!a.full) && (!a.real_path) && (!a.solve_only);
     for (int c = 0; c < nc; ++c) {
       // load RHS column (identity column in full mode)
+      auto rhs = [&](int i) -> double2 {
+        if (a.full) return make_double2(i == c ? 1.0 : 0.0, 0.0);
+        if (a.v_complex) return reinterpret_cast<const double2*>(a.V)[((size_t)b * d + i) * nc + c];
+        return make_double2(a.V[((size_t)b * d + i) * nc + c], 0.0);
+      };
+      // Y = U^{-1} L^{-1} P V : P applied as a gather through the permutation
       for (int i = tid; i < d; i += DB_THREADS) {
-        double2 v;
-        if (a.full) {
-          v = make_double2(i == c ? 1.0 : 0.0, 0.0);
-        } else if (a.v_complex) {
-          v = reinterpret_cast<const double2*>(a.V)[((size_t)b * d + i) * nc + c];
-        } else {
-          v = make_double2(a.V[((size_t)b * d + i) * nc + c], 0.0);
-        }
-        z[i] = v;
-        zc[i] = v;
+        z[i] = rhs(s_perm[i]);
+        zc[i] = rhs(i);
       }
       __syncthreads();
-      // Y = U^{-1} L^{-1} P V : interchanges in order
-      if (tid == 0)
-        for (int i = 0; i < d; ++i) {
-          int pr = ipiv[i];
-          if (pr != i) {
-            double2 x = z[i];
-            z[i] = z[pr];
-            z[pr] = x;
-          }
-        }
-      __syncthreads();
-      trsv_blocked(W, d, 0, z, part, diag);
-      trsv_blocked(W, d, 1, z, part, diag);
+      trsv_blocked(W, d, 0, z, part, diag, rdiag);
+      trsv_blocked(W, d, 1, z, part, diag, rdiag);
       for (int i = tid; i < d; i += DB_THREADS) Yg[(size_t)i * nc + c] = z[i];
       if (want_conj) {
         // Yc = M^{-H} V = P^T L^{-H} U^{-H} V
-        trsv_blocked(W, d, 2, zc, part, diag);
-        trsv_blocked(W, d, 3, zc, part, diag);
-        if (tid == 0)
-          for (int i = d - 1; i >= 0; --i) {
-            int pr = ipiv[i];
-            if (pr != i) {
-              double2 x = zc[i];
-              zc[i] = zc[pr];
-              zc[pr] = x;
-            }
-          }
-        __syncthreads();
-        for (int i = tid; i < d; i += DB_THREADS) Ycg[(size_t)i * nc + c] = zc[i];
+        trsv_blocked(W, d, 2, zc, part, diag, rdiag);
+        trsv_blocked(W, d, 3, zc, part, diag, rdiag);
+        // P^T applied as a scatter through the permutation
+        for (int i = tid; i < d; i += DB_THREADS) Ycg[(size_t)s_perm[i] * nc + c] = zc[i];
       }
       __syncthreads();
     }
@@ -474,7 +482,8 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ stage, double* __
 
 static size_t dense_smem_bytes(int d, int nb) {
   size_t c2 = (size_t)d * (nb + 1) + (size_t)nb * (DB_SW + 1) + 2 * (size_t)d + 32 + 32 * 33;
-  return c2 * sizeof(double2) + 32 * sizeof(double) + (32 + nb + 4) * sizeof(int);
+  return c2 * sizeof(double2) + 32 * sizeof(double) + (32 + nb + 4) * sizeof(int) + ((d + 3) & ~3) * sizeof(int) +
+         (size_t)d * sizeof(double2) + 64;
 }
 
 int dense_batched_supported(int64_t d) { return d >= 1 && d <= 512; }

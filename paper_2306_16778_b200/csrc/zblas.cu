@@ -282,18 +282,17 @@ __global__ void __launch_bounds__(P_THREADS) zgetf2_smem_kernel(int m, int nb, Z
       __syncthreads();
       continue;
     }
-    const cplx rp = crcp(pv);
-    // (row, column) pairs of the trailing part; the multiplier column is recomputed per
-    // element from the unscaled value so every thread works independently
-    const int rows = m - j - 1, cols = nb - j;
-    for (int e = tid; e < rows * cols; e += P_THREADS) {
-      const int r = j + 1 + e / cols, c = j + e % cols;
+    const cplx rp = crcp_fast(pv);
+    // warp w owns rows j+1+w, j+1+w+8, ...: each lane scales its row's multiplier once and
+    // updates columns j+1.. of that row; rows are independent, one barrier per column
+    const int cols = nb - j - 1;
+    for (int r = j + 1 + warp; r < m; r += P_THREADS / 32) {
       const cplx l = cmul(ld(&Ps[r * ps + j]), rp);
-      if (c == j) continue;
-      st(&Ps[r * ps + c], cfms(ld(&Ps[r * ps + c]), l, ld(&Ps[j * ps + c])));
+      for (int c = lane; c < cols; c += 32)
+        st(&Ps[r * ps + j + 1 + c], cfms(ld(&Ps[r * ps + j + 1 + c]), l, ld(&Ps[j * ps + j + 1 + c])));
+      __syncwarp();
+      if (lane == 0) st(&Ps[r * ps + j], l);
     }
-    __syncthreads();
-    for (int r = j + 1 + tid; r < m; r += P_THREADS) st(&Ps[r * ps + j], cmul(ld(&Ps[r * ps + j]), rp));
     __syncthreads();
   }
   for (int e = tid; e < m * nb; e += P_THREADS) {
@@ -377,27 +376,28 @@ __global__ void __launch_bounds__(T_THREADS) ztrsm_left_kernel(int nb, int n, ZM
     Bs[r * (T_COLS + 1) + c] = (c0 + c < n) ? Bb[(int64_t)r * B.ld + c0 + c] : make_double2(0, 0);
   }
   __syncthreads();
-  const int col = tid % T_COLS, rg = tid / T_COLS;  // 8 row groups
+  // warp w owns columns 4w..4w+3 of the strip; lane = (column-in-group, row slice):
+  // lanes 8c..8c+7 share column 4w+c and split the rows 8 ways; only __syncwarp inside
+  const int warp = tid >> 5, lane = tid & 31;
+  const int col = warp * 4 + (lane >> 3), rs = lane & 7;
   if (MODE == 0) {
     for (int kk = 0; kk < nb; ++kk) {
-      cplx x = ld(&Bs[kk * (T_COLS + 1) + col]);
-      for (int r = kk + 1 + rg; r < nb; r += T_THREADS / T_COLS)
+      const cplx x = ld(&Bs[kk * (T_COLS + 1) + col]);
+      for (int r = kk + 1 + rs; r < nb; r += 8)
         st(&Bs[r * (T_COLS + 1) + col], cfms(ld(&Bs[r * (T_COLS + 1) + col]), ld(&Ts[r * (nb + 1) + kk]), x));
-      __syncthreads();
+      __syncwarp();
     }
   } else {
     for (int kk = nb - 1; kk >= 0; --kk) {
-      if (rg == 0) {
-        cplx x = cdiv(ld(&Bs[kk * (T_COLS + 1) + col]), ld(&Ts[kk * (nb + 1) + kk]));
-        st(&Bs[kk * (T_COLS + 1) + col], x);
-      }
-      __syncthreads();
-      cplx x = ld(&Bs[kk * (T_COLS + 1) + col]);
-      for (int r = rg; r < kk; r += T_THREADS / T_COLS)
+      const cplx x = cmul(ld(&Bs[kk * (T_COLS + 1) + col]), crcp_fast(ld(&Ts[kk * (nb + 1) + kk])));
+      __syncwarp();
+      if (rs == 0) st(&Bs[kk * (T_COLS + 1) + col], x);
+      for (int r = rs; r < kk; r += 8)
         st(&Bs[r * (T_COLS + 1) + col], cfms(ld(&Bs[r * (T_COLS + 1) + col]), ld(&Ts[r * (nb + 1) + kk]), x));
-      __syncthreads();
+      __syncwarp();
     }
   }
+  __syncthreads();
   for (int e = tid; e < nb * T_COLS; e += T_THREADS) {
     int r = e / T_COLS, c = e % T_COLS;
     if (c0 + c < n) Bb[(int64_t)r * B.ld + c0 + c] = Bs[r * (T_COLS + 1) + c];
@@ -423,18 +423,18 @@ __global__ void __launch_bounds__(T_THREADS) ztrsm_runn_kernel(int m, int nb, ZM
     Bs[r * (nb + 1) + c] = (r0 + r < m) ? Bb[(int64_t)(r0 + r) * B.ld + c] : make_double2(0, 0);
   }
   __syncthreads();
-  const int row = tid % T_COLS, cg = tid / T_COLS;
+  // warp w owns rows 4w..4w+3; lanes 8r..8r+7 share row 4w+r and split the columns
+  const int warp = tid >> 5, lane = tid & 31;
+  const int row = warp * 4 + (lane >> 3), cs = lane & 7;
   for (int j = 0; j < nb; ++j) {
-    if (cg == 0) {
-      cplx x = cdiv(ld(&Bs[row * (nb + 1) + j]), ld(&Us[j * (nb + 1) + j]));
-      st(&Bs[row * (nb + 1) + j], x);
-    }
-    __syncthreads();
-    cplx x = ld(&Bs[row * (nb + 1) + j]);
-    for (int c = j + 1 + cg; c < nb; c += T_THREADS / T_COLS)
+    const cplx x = cmul(ld(&Bs[row * (nb + 1) + j]), crcp_fast(ld(&Us[j * (nb + 1) + j])));
+    __syncwarp();
+    if (cs == 0) st(&Bs[row * (nb + 1) + j], x);
+    for (int c = j + 1 + cs; c < nb; c += 8)
       st(&Bs[row * (nb + 1) + c], cfms(ld(&Bs[row * (nb + 1) + c]), x, ld(&Us[j * (nb + 1) + c])));
-    __syncthreads();
+    __syncwarp();
   }
+  __syncthreads();
   for (int e = tid; e < T_COLS * nb; e += T_THREADS) {
     int r = e / nb, c = e % nb;
     if (r0 + r < m) Bb[(int64_t)(r0 + r) * B.ld + c] = Bs[r * (nb + 1) + c];
