@@ -16,6 +16,8 @@
 // m8n8k4, four real MMAs per complex 8x8x4 step) straight from the panel/strip
 // in shared memory into accumulator fragments loaded from and stored back to
 // the slot.
+#include <cstdlib>
+
 #include "pfx_common.cuh"
 
 namespace pfx {
@@ -45,6 +47,7 @@ struct DenseBatchArgs {
   double2* Yc;    // slots x d*ncols   (complex action: M^{-H} V)
   double* stage;  // systems x d*ncols (x2 if complex)
   int* status;
+  unsigned long long* dbg;  // optional: per-phase clock totals (PFX_DENSE_PHASES env)
 };
 
 __device__ __forceinline__ void block_argmax(double val, int idx, double* sv, int* si, double& best, int& bidx) {
@@ -91,7 +94,8 @@ __device__ __forceinline__ void block_argmax(double val, int idx, double* sv, in
 // as LAPACK does, and the caller reports PFX_SINGULAR).
 template <int NB>
 __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* P, double2* S,
-                           double* red_v, int* red_i, int* s_piv, int* sing) {
+                           double* red_v, int* red_i, int* s_piv, int* sing, unsigned long long* dbg) {
+  long long tph = 0;
   constexpr int PS = NB + 1;        // padded panel row stride (double2)
   constexpr int SS = DB_SW + 1;     // padded strip row stride
   const int tid = threadIdx.x;
@@ -107,40 +111,86 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       P[r * PS + c] = W[(size_t)(p + r) * d + p + c];
     }
     __syncthreads();
-    // ---- unblocked getf2 on the panel
+    if (dbg && tid == 0) tph = clock64();
+    // ---- unblocked getf2 on the panel, two barriers per column:
+    //   A: per-warp argmax candidates are published; every thread reduces the 8 of them
+    //   B: pivot row and displaced row are staged in prow/trow; then each thread eliminates
+    //      its own rows (the interchange folded in) and tracks the next column's argmax.
+    double2* prow = S;           // strip buffer is idle during the panel
+    double2* trow = S + 64;
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int r = tid; r < m; r += DB_THREADS) {
+      double2 x = P[r * PS];
+      double v = fabs(x.x) + fabs(x.y);
+      if (v > bv) {
+        bv = v;
+        bi = r;
+      }
+    }
     for (int jj = 0; jj < jb; ++jj) {
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-      for (int r = jj + tid; r < m; r += DB_THREADS) {
-        double2 x = P[r * PS + jj];
-        double v = fabs(x.x) + fabs(x.y);
-        if (v > bv) {
-          bv = v;
-          bi = r;
+      for (int off = 16; off > 0; off >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, bv, off);
+        int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
         }
       }
-      double best;
-      int piv;
-      block_argmax(bv, bi, red_v, red_i, best, piv);
+      if (lane == 0) {
+        red_v[warp + 8 * (jj & 1)] = bv;
+        red_i[warp + 8 * (jj & 1)] = bi;
+      }
+      __syncthreads();  // A
+      double best = red_v[8 * (jj & 1)];
+      int piv = red_i[8 * (jj & 1)];
+      for (int w = 1; w < DB_WARPS; ++w) {
+        double v = red_v[w + 8 * (jj & 1)];
+        int i = red_i[w + 8 * (jj & 1)];
+        if (v > best || (v == best && i < piv)) {
+          best = v;
+          piv = i;
+        }
+      }
       if (tid == 0) {
         s_piv[jj] = piv;
         ipiv[p + jj] = p + piv;
         if (best == 0.0) *sing = 1;
       }
-      if (piv != jj && tid < jb) {
-        double2 a = P[jj * PS + tid];
-        P[jj * PS + tid] = P[piv * PS + tid];
-        P[piv * PS + tid] = a;
+      for (int c = tid; c < jb; c += DB_THREADS) {
+        prow[c] = P[piv * PS + c];
+        trow[c] = P[jj * PS + c];
       }
-      __syncthreads();
-      cplx pv = ld(&P[jj * PS + jj]);
-      cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp(pv);
+      __syncthreads();  // B
+      const cplx pv = ld(&prow[jj]);
+      const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp(pv);
+      for (int c = tid; c < jb; c += DB_THREADS) P[jj * PS + c] = prow[c];
+      bv = -1.0;
+      bi = 0x7fffffff;
       for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
-        cplx l = cmul(ld(&P[r * PS + jj]), rp);
-        st(&P[r * PS + jj], l);
-        for (int c = jj + 1; c < jb; ++c) st(&P[r * PS + c], cfms(ld(&P[r * PS + c]), l, ld(&P[jj * PS + c])));
+        const double2* src = (r == piv) ? trow : &P[r * PS];
+        double2* dst = &P[r * PS];
+        if (r == piv)
+          for (int c = 0; c < jj; ++c) dst[c] = trow[c];  // the displaced row's multipliers move too
+        const cplx l = cmul(ld(&src[jj]), rp);
+        for (int c = jj + 1; c < jb; ++c) {
+          const cplx v = cfms(ld(&src[c]), l, ld(&prow[c]));
+          st(&dst[c], v);
+          if (c == jj + 1) {
+            const double av = fabs(v.re) + fabs(v.im);
+            if (av > bv || (av == bv && r < bi)) {
+              bv = av;
+              bi = r;
+            }
+          }
+        }
+        st(&dst[jj], l);
       }
-      __syncthreads();
+    }
+    __syncthreads();
+    if (dbg && tid == 0) {
+      atomicAdd(&dbg[2], (unsigned long long)(clock64() - tph));
+      tph = clock64();
     }
     // ---- write panel back
     for (int e = tid; e < m * jb; e += DB_THREADS) {
@@ -161,6 +211,10 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       }
     }
     __syncthreads();
+    if (dbg && tid == 0) {
+      atomicAdd(&dbg[3], (unsigned long long)(clock64() - tph));
+      tph = clock64();
+    }
     // ---- strips of the trailing columns: U12 = L11^{-1} A12, A22 -= L21 U12
     for (int q = p + jb; q < d; q += DB_SW) {
       const int sw = min(DB_SW, d - q);
@@ -169,18 +223,35 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         S[r * SS + c] = W[(size_t)(p + r) * d + q + c];
       }
       __syncthreads();
-      // unit-lower triangular solve: warp w owns strip columns w, w+8, ... ; lane = row
-      for (int c = warp; c < sw; c += DB_WARPS) {
+      // unit-lower triangular solve: warp w owns strip columns 8w..8w+7, lane = row; the 8
+      // columns are solved together in registers (ILP 8), pivots broadcast by shuffles
+      {
+        const int c0 = warp * 8;
+        cplx x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = (lane < jb && c0 + u < sw) ? ld(&S[lane * SS + c0 + u]) : mk(0.0, 0.0);
         for (int k = 0; k < jb; ++k) {
-          cplx s = ld(&S[k * SS + c]);
-          if (lane > k && lane < jb) st(&S[lane * SS + c], cfms(ld(&S[lane * SS + c]), ld(&P[lane * PS + k]), s));
-          __syncwarp();
+          const cplx l = (lane > k && lane < jb) ? ld(&P[lane * PS + k]) : mk(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            cplx xk;
+            xk.re = __shfl_sync(0xffffffffu, x[u].re, k);
+            xk.im = __shfl_sync(0xffffffffu, x[u].im, k);
+            x[u] = cfms(x[u], l, xk);
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (lane < jb && c0 + u < sw) st(&S[lane * SS + c0 + u], x[u]);
       }
       __syncthreads();
       for (int e = tid; e < jb * sw; e += DB_THREADS) {
         int r = e / sw, c = e - r * sw;
         W[(size_t)(p + r) * d + q + c] = S[r * SS + c];
+      }
+      if (dbg && tid == 0) {
+        atomicAdd(&dbg[4], (unsigned long long)(clock64() - tph));
+        tph = clock64();
       }
       // DMMA trailing update of rows p+jb..d-1, cols q..q+sw-1
       const int mrows = m - jb;
@@ -238,6 +309,10 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         }
       }
       __syncthreads();
+      if (dbg && tid == 0) {
+        atomicAdd(&dbg[5], (unsigned long long)(clock64() - tph));
+        tph = clock64();
+      }
     }
   }
 }
@@ -378,8 +453,11 @@ __global__ void __launch_bounds__(DB_THREADS, 1) dense_batched_kernel(DenseBatch
     }
     __syncthreads();
     // ---- K1/K2: LU with partial pivoting
-    lu_blocked<NB>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing);
+    long long t_lu0 = clock64();
+    lu_blocked<NB>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
+    if (a.dbg && tid == 0) atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t_lu0));
+    long long t_sv0 = clock64();
     // row permutation of P M = L U (swaps applied in order to the identity) and 1/U_ii
     for (int i = tid; i < d; i += DB_THREADS) {
       s_perm[i] = ipiv[i];
@@ -437,6 +515,7 @@ __global__ void __launch_bounds__(DB_THREADS, 1) dense_batched_kernel(DenseBatch
       __syncthreads();
     }
     __syncthreads();
+    if (a.dbg && tid == 0) atomicAdd(&a.dbg[1], (unsigned long long)(clock64() - t_sv0));
     // ---- K5: residue combine into this system's slot of the stage buffer
     const size_t ne = (size_t)d * nc;
     if (a.solve_only) {
@@ -527,6 +606,13 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   args.ipiv = reinterpret_cast<int*>(args.Yc + (size_t)slots * per_sys);
   args.status = args.ipiv + (size_t)slots * d;
   args.stage = stage;
+  args.dbg = nullptr;
+  static unsigned long long* dbg_dev = nullptr;
+  if (getenv("PFX_DENSE_PHASES")) {
+    if (!dbg_dev) PFX_CUDA_TRY(cudaMalloc(&dbg_dev, 8 * sizeof(unsigned long long)));
+    PFX_CUDA_TRY(cudaMemsetAsync(dbg_dev, 0, 8 * sizeof(unsigned long long), stream));
+    args.dbg = dbg_dev;
+  }
   PFX_CUDA_TRY(cudaMemsetAsync(args.status, 0, sizeof(int), stream));
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -558,6 +644,12 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   int st = 0;
   PFX_CUDA_TRY(cudaMemcpyAsync(&st, args.status, sizeof(int), cudaMemcpyDeviceToHost, stream));
   PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (args.dbg) {
+    unsigned long long h[8];
+    PFX_CUDA_TRY(cudaMemcpy(h, args.dbg, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[pfx dense phases, Mcycles summed over CTAs] lu=%.1f solves=%.1f panel=%.1f swaps=%.1f trsm=%.1f gemm=%.1f\n",
+            h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
+  }
   if (st == PFX_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
   return PFX_OK;
 }
