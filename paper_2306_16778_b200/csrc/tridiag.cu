@@ -107,7 +107,7 @@ __device__ __forceinline__ M22 mident() { return M22{mk(1, 0), mk(0, 0), mk(0, 0
 // ---------------------------------------------------------------------------
 // K_T1: transfer matrices.  Forward: (u_i; 1) ~ [b_i, -e_{i-1}^2; 1, 0] (u_{i-1}; 1).
 // Backward: (u'_i; 1) ~ [b_i, -e_i^2; 1, 0] (u'_{i+1}; 1).
-__global__ void tri_mobius_chunks(TriArgs a) {
+__global__ void __launch_bounds__(128) tri_mobius_chunks(TriArgs a) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)a.P * a.npairs * 2;
   if (tid >= total) return;
@@ -116,35 +116,34 @@ __global__ void tri_mobius_chunks(TriArgs a) {
   const int k = (int)(ck % a.npairs);
   const int64_t cidx = ck / a.npairs;
   const int64_t s = cidx * TR_L, e = (s + TR_L < a.N ? s + TR_L : a.N);
+  const int rows = (int)(e - s);
   const cplx th = ld(&a.theta[k]);
   M22 T = mident();
-  int cnt = 0;
-  if (dir == 0) {
-    for (int64_t i = s; i < e; ++i) {
-      cplx b = mk(a.diag[i] - a.c + th.re, th.im);
-      double e2 = off2(a.off, a.N, i - 1);
-      M22 r;
-      r.m0 = csub(cmul(b, T.m0), cscale(T.m2, e2));
-      r.m1 = csub(cmul(b, T.m1), cscale(T.m3, e2));
-      r.m2 = T.m0;
-      r.m3 = T.m1;
-      T = r;
-      if (((++cnt) & 7) == 0) mnorm(T);
+  // rows in processing order, 8 per batch with the loads issued ahead of the product chain
+  for (int i0 = 0; i0 < rows; i0 += 8) {
+    double bre[8], e2v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int ii = i0 + u;
+      const int64_t i = dir == 0 ? s + ii : e - 1 - ii;
+      const bool v = ii < rows;
+      bre[u] = v ? a.diag[i] - a.c + th.re : 0.0;
+      e2v[u] = v ? off2(a.off, a.N, dir == 0 ? i - 1 : i) : 0.0;
     }
-  } else {
-    for (int64_t i = e - 1; i >= s; --i) {
-      cplx b = mk(a.diag[i] - a.c + th.re, th.im);
-      double e2 = off2(a.off, a.N, i);
-      M22 r;
-      r.m0 = csub(cmul(b, T.m0), cscale(T.m2, e2));
-      r.m1 = csub(cmul(b, T.m1), cscale(T.m3, e2));
-      r.m2 = T.m0;
-      r.m3 = T.m1;
-      T = r;
-      if (((++cnt) & 7) == 0) mnorm(T);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0 + u < rows) {
+        const cplx b = mk(bre[u], th.im);
+        M22 r;
+        r.m0 = csub(cmul(b, T.m0), cscale(T.m2, e2v[u]));
+        r.m1 = csub(cmul(b, T.m1), cscale(T.m3, e2v[u]));
+        r.m2 = T.m0;
+        r.m3 = T.m1;
+        T = r;
+      }
     }
+    mnorm(T);
   }
-  mnorm(T);
   double2* dst = (dir == 0 ? a.Tf : a.Tb) + ck * 4;
   st(&dst[0], T.m0);
   st(&dst[1], T.m1);
@@ -454,28 +453,30 @@ __global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_pass(TriArgs a) {
 #include "tridiag_ls.cuh"
 
 // K_T4 ------------------------------------------------------------------------
-// One warp per (shift, rhs, direction).  Affine maps x -> A x + B composed over chunks;
-// each lane owns a contiguous range of chunks, loads are issued 8 at a time.
-__global__ void tri_carry_scan(TriArgs a) {
-  const int warp_global = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  const int total = a.npairs * a.nrhs * 2;
-  if (warp_global >= total) return;
-  const int dir = warp_global & 1;
-  const int kr = warp_global >> 1;
+// One 256-thread block per (shift, rhs, direction).  Affine maps x -> A x + B composed
+// over chunks: each thread composes a contiguous range (loads batched), block scan of the
+// thread composites through shared memory, then each thread replays its range.
+constexpr int CS_T = 256;
+__global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
+  __shared__ cplx sA[CS_T], sB[CS_T];
+  const int bid = blockIdx.x;
+  const int dir = bid & 1;
+  const int kr = bid >> 1;
   const int k = kr / a.nrhs, rr = kr - k * a.nrhs;
   const int P = a.P;
-  const int per = (P + 31) / 32;
+  const int t = threadIdx.x;
+  const int per = (P + CS_T - 1) / CS_T;
   const double2* Ls = dir == 0 ? a.LF : a.LB;
   const double2* gs = dir == 0 ? a.gF : a.gB;
+  auto chunk_of = [&](int q) { return dir == 0 ? q : P - 1 - q; };
   cplx A = mk(1, 0), B = mk(0, 0);
   for (int j0 = 0; j0 < per; j0 += 8) {
     cplx Lc[8], gc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      int q = lane * per + j0 + u;
+      const int q = t * per + j0 + u;
       if (j0 + u < per && q < P) {
-        int cc = dir == 0 ? q : P - 1 - q;
+        const int cc = chunk_of(q);
         Lc[u] = ld(&Ls[(int64_t)cc * a.npairs + k]);
         gc[u] = ld(&gs[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
       } else {
@@ -489,39 +490,38 @@ __global__ void tri_carry_scan(TriArgs a) {
       A = cmul(Lc[u], A);
     }
   }
-  for (int off = 1; off < 32; off <<= 1) {
-    cplx pA, pB;
-    pA.re = __shfl_up_sync(0xffffffffu, A.re, off);
-    pA.im = __shfl_up_sync(0xffffffffu, A.im, off);
-    pB.re = __shfl_up_sync(0xffffffffu, B.re, off);
-    pB.im = __shfl_up_sync(0xffffffffu, B.im, off);
-    if (lane >= off) {
+  sA[t] = A;
+  sB[t] = B;
+  __syncthreads();
+  for (int off = 1; off < CS_T; off <<= 1) {
+    cplx pA = t >= off ? sA[t - off] : mk(1, 0), pB = t >= off ? sB[t - off] : mk(0, 0);
+    __syncthreads();
+    if (t >= off) {
       B = cadd(cmul(A, pB), B);
       A = cmul(A, pA);
+      sA[t] = A;
+      sB[t] = B;
     }
+    __syncthreads();
   }
-  cplx x;
-  x.re = __shfl_up_sync(0xffffffffu, B.re, 1);
-  x.im = __shfl_up_sync(0xffffffffu, B.im, 1);
-  if (lane == 0) x = mk(0, 0);
+  cplx x = t > 0 ? sB[t - 1] : mk(0, 0);
   double2* dst = dir == 0 ? a.G : a.Gb;
   for (int j0 = 0; j0 < per; j0 += 8) {
     cplx Lc[8], gc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      int q = lane * per + j0 + u;
+      const int q = t * per + j0 + u;
       if (j0 + u < per && q < P) {
-        int cc = dir == 0 ? q : P - 1 - q;
+        const int cc = chunk_of(q);
         Lc[u] = ld(&Ls[(int64_t)cc * a.npairs + k]);
         gc[u] = ld(&gs[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
       }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      int q = lane * per + j0 + u;
+      const int q = t * per + j0 + u;
       if (j0 + u < per && q < P) {
-        int cc = dir == 0 ? q : P - 1 - q;
-        st(&dst[((int64_t)cc * a.npairs + k) * a.nrhs + rr], x);
+        st(&dst[((int64_t)chunk_of(q) * a.npairs + k) * a.nrhs + rr], x);
         x = cadd(cmul(Lc[u], x), gc[u]);
       }
     }
@@ -629,8 +629,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     PFX_LAUNCH("tri_sweep", stream, (k0<<<blocks, LS_WARPS * 32, smem, stream>>>(a, lsa)));
     PFX_CUDA_TRY(cudaGetLastError());
-    int warps = npairs * (int)nrhs * 2;
-    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, stream>>>(a));
+    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
     PFX_LAUNCH("tri_fix", stream, (k1<<<blocks, LS_WARPS * 32, smem, stream>>>(a, lsa)));
     PFX_CUDA_TRY(cudaGetLastError());
@@ -639,8 +638,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaGetLastError());
     if (int rc = sweeps(a, stream, 0)) return rc;
     PFX_CUDA_TRY(cudaGetLastError());
-    int warps = npairs * (int)nrhs * 2;
-    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, stream>>>(a));
+    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
     if (int rc = sweeps(a, stream, 1)) return rc;
     PFX_CUDA_TRY(cudaGetLastError());
