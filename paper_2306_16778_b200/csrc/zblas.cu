@@ -25,7 +25,8 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
 }
 
-__global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C) {
+__global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
+                                                          int accumulate) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GemmSmem& S = *reinterpret_cast<GemmSmem*>(smem_raw);
   const int b = blockIdx.z;
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, d
         const int col = n0 + wn * 16 + j * 8 + 2 * t + h;
         if (col < n) {
           double2* p = Cb + (int64_t)row * C.ld + col;
-          double2 v = *p;
+          double2 v = accumulate ? *p : make_double2(0.0, 0.0);
           v.x += cr[i][j][h];
           v.y += ci[i][j][h];
           *p = v;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, d
   }
 }
 
-int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C) {
+int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate) {
   if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
   static bool attr = false;
   const int smem = (int)sizeof(GemmSmem);
@@ -123,7 +124,7 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
   }
   dim3 grid((unsigned)ceil_div(n, GN), (unsigned)ceil_div(m, GM), (unsigned)batch);
   PFX_LAUNCH_F("zgemm", s, 8.0 * (double)m * n * k * batch,
-               zgemm_kernel<<<grid, G_THREADS, smem, s>>>(m, n, k, alpha, A, B, C));
+               zgemm_kernel<<<grid, G_THREADS, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
@@ -480,6 +481,41 @@ int ztrsm_runn(cudaStream_t s, int batch, int m, int nb, ZMat Um, ZMat B) {
   if (int rc = trsm_attrs()) return rc;
   dim3 grid((unsigned)ceil_div(m, T_COLS), (unsigned)batch);
   PFX_LAUNCH("ztrsm", s, ztrsm_runn_kernel<<<grid, T_THREADS, smem, s>>>(m, nb, Um, B));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+
+__global__ void zeye_kernel(ZMat E, int nb) {
+  const int b = blockIdx.y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nb * nb; e += gridDim.x * blockDim.x) {
+    const int r = e / nb, c = e - r * nb;
+    *E.at(b, r, c) = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+}
+
+__global__ void zcopy_kernel(ZMat Src, ZMat Dst, int rows, int cols) {
+  const int b = blockIdx.y;
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    *Dst.at(b, r, c) = *Src.at(b, r, c);
+  }
+}
+
+int ztrsm_left_gemm(cudaStream_t s, int batch, int nb, int n, ZMat T, ZMat B, bool upper) {
+  if (n <= 0) return PFX_OK;
+  const size_t inv_elems = (size_t)batch * nb * nb, tmp_elems = (size_t)batch * nb * n;
+  double2* ws = static_cast<double2*>(scratch(7, (inv_elems + tmp_elems) * sizeof(double2)));
+  if (!ws) return fail(PFX_CUDA, "trsm workspace allocation failed");
+  ZMat Inv{ws, nb, (int64_t)nb * nb};
+  ZMat Tmp{ws + inv_elems, n, (int64_t)nb * n};
+  PFX_LAUNCH("zeye", s, zeye_kernel<<<dim3(16, batch), 256, 0, s>>>(Inv, nb));
+  PFX_CUDA_TRY(cudaGetLastError());
+  int rc = upper ? ztrsm_lunn(s, batch, nb, nb, T, Inv) : ztrsm_llnu(s, batch, nb, nb, T, Inv);
+  if (rc) return rc;
+  if ((rc = zgemm(s, batch, nb, n, nb, 1.0, Inv, B, Tmp, false))) return rc;
+  PFX_LAUNCH("zcopy", s, zcopy_kernel<<<dim3(256, batch), 256, 0, s>>>(Tmp, B, nb, n));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }

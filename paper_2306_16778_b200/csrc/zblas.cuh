@@ -17,8 +17,15 @@ struct ZMat {
   __host__ __device__ double2* at(int b, int64_t i, int64_t j) const { return p + b * stride + i * ld + j; }
 };
 
-// C[b] += alpha * A[b] (m x k) * B[b] (k x n), alpha = +-1.  DMMA m8n8k4, 64x64x16 tiles.
-int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C);
+// C[b] += alpha * A[b] (m x k) * B[b] (k x n) (accumulate = true) or C[b] = alpha * A B.
+// DMMA m8n8k4, 64x64x16 tiles.
+int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
+          bool accumulate = true);
+
+// Wide triangular solves through the tensor cores: T^{-1} (nb x nb) is formed once per
+// batch member (small TRSM on the identity) and applied with zgemm into scratch, then
+// copied back.  Used when n is large (the forward/backward substitutions of C4).
+int ztrsm_left_gemm(cudaStream_t s, int batch, int nb, int n, ZMat T, ZMat B, bool upper);
 
 // Unblocked LU of the m x nb panel at P (in place).  ipiv (optional, batch x nb, 0-based
 // rows relative to the panel) -> partial pivoting with row swaps inside the panel only.
