@@ -119,18 +119,41 @@ void release_scratch() {
   }
 }
 
-// Upload poles (host, interleaved) into arena slot 0.
+// Upload poles (host, interleaved) into a device table.  Tables are cached per device by
+// value and never overwritten (a kernel still reading one on another stream stays valid),
+// so repeated calls with the same order neither copy nor synchronise.
+namespace {
+struct PoleEntry {
+  std::vector<double> host;
+  double2* dev = nullptr;
+};
+std::vector<PoleEntry> g_pole_cache[16];
+std::mutex g_pole_mu;
+}  // namespace
+
 static int upload_poles(const double* theta2, const double* coef2, int npairs, cudaStream_t stream,
                         const double2** th, const double2** co) {
-  double2* p = static_cast<double2*>(scratch(0, 2 * (size_t)npairs * sizeof(double2)));
-  if (!p) return fail(PFX_CUDA, "pole upload allocation failed");
+  int devid = 0;
+  PFX_CUDA_TRY(cudaGetDevice(&devid));
+  if (devid >= 16) return fail(PFX_CUDA, "device index out of range");
   std::vector<double> tmp(4 * (size_t)npairs);
   std::memcpy(tmp.data(), theta2, 2 * npairs * sizeof(double));
   std::memcpy(tmp.data() + 2 * npairs, coef2, 2 * npairs * sizeof(double));
-  PFX_CUDA_TRY(cudaMemcpyAsync(p, tmp.data(), tmp.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+  std::lock_guard<std::mutex> lk(g_pole_mu);
+  for (const PoleEntry& e : g_pole_cache[devid])
+    if (e.host == tmp) {
+      *th = e.dev;
+      *co = e.dev + npairs;
+      return PFX_OK;
+    }
+  PoleEntry e;
+  e.host = tmp;
+  PFX_CUDA_TRY(cudaMalloc(&e.dev, tmp.size() * sizeof(double)));
+  PFX_CUDA_TRY(cudaMemcpyAsync(e.dev, tmp.data(), tmp.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
   PFX_CUDA_TRY(cudaStreamSynchronize(stream));
-  *th = p;
-  *co = p + npairs;
+  g_pole_cache[devid].push_back(e);
+  *th = e.dev;
+  *co = e.dev + npairs;
   return PFX_OK;
 }
 
