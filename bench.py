@@ -14,11 +14,11 @@ and the partial sums meet in ONE NCCL reduce to rank 0 (the path's only exchange
 Total work is fixed as N grows -> "scaling": "strong".
 
 Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA events on
-the launching stream, max over ranks.  C2 inputs (V 128 MB + coefficients 16 MB)
-and output (128 MB) exceed the 126 MB L2, so no explicit flush is needed; the
-dense configs flush L2 between steps by writing a 256 MB buffer (outside the
-timed event pairs of the kernel-only number, inside the step for `value`? no: the
-flush runs before each step's start event and is excluded) — see config.l2.
+the launching stream, max over ranks; library profiling is off in the timed region (a
+separate pass with per-launch CUDA events produces the kernel breakdown and the
+dominant-kernel roofline).  L2 policy per config (config.l2): C2-C5 inputs exceed the
+126 MB L2, so no flush; C1 (256 KB of inputs) writes a 256 MB buffer before every step,
+inside the timed region (so C1's value is a conservative, flush-inclusive number).
 
 `--impl reference` runs the reference's CPU algorithm for the same workload (the
 oracle restatement: zgtsv/zgbsv/LAPACK per pole pair with the 2 Re(a y) combine and

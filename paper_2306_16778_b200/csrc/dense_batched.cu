@@ -406,17 +406,22 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, dou
   }
 }
 
-template <int NB>
-__global__ void __launch_bounds__(DB_THREADS, 1) dense_batched_kernel(DenseBatchArgs a) {
+// NB = panel width; MINB = resident CTAs per SM the register budget is sized for.
+//   <32, 1>: few systems (latency mode, e.g. C1);  <16, 2>: many systems with d <= 256
+//   (two CTAs per SM overlap one system's panel with another's DMMA update, e.g. C3);
+//   <16, 1>: 256 < d <= 512.
+template <int NB, int MINB>
+__global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBatchArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int d = a.d;
   double2* P = reinterpret_cast<double2*>(smem_raw);                // d x (NB+1)
-  double2* S = P + (size_t)d * (NB + 1);                            // NB x (SW+1)
-  double2* z = S + (size_t)NB * (DB_SW + 1);                        // d
+  double2* S = P + (size_t)d * (NB + 1);                            // NB x (SW+1), aliased by diag
+  double2* diag = S;                                                // 32 x 33 (solves only)
+  const size_t sreg = (size_t)NB * (DB_SW + 1) > 32 * 33 ? (size_t)NB * (DB_SW + 1) : 32 * 33;
+  double2* z = S + sreg;                                            // d
   double2* zc = z + d;                                              // d
   double2* part = zc + d;                                           // 32
-  double2* diag = part + 32;                                        // 32 x 33 (>= 8*32)
-  double* red_v = reinterpret_cast<double*>(diag + 32 * 33);        // 32
+  double* red_v = reinterpret_cast<double*>(part + 32);             // 32
   int* red_i = reinterpret_cast<int*>(red_v + 32);                  // 32
   int* s_piv = red_i + 32;                                          // NB
   int* s_sing = s_piv + NB;                                         // 1
@@ -560,7 +565,8 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ stage, double* __
 }
 
 static size_t dense_smem_bytes(int d, int nb) {
-  size_t c2 = (size_t)d * (nb + 1) + (size_t)nb * (DB_SW + 1) + 2 * (size_t)d + 32 + 32 * 33;
+  size_t sreg = (size_t)nb * (DB_SW + 1) > 32 * 33 ? (size_t)nb * (DB_SW + 1) : 32 * 33;
+  size_t c2 = (size_t)d * (nb + 1) + sreg + 2 * (size_t)d + 32;
   return c2 * sizeof(double2) + 32 * sizeof(double) + (32 + nb + 4) * sizeof(int) + ((d + 3) & ~3) * sizeof(int) +
          (size_t)d * sizeof(double2) + 64;
 }
@@ -574,10 +580,13 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   int dev = 0, sms = 0;
   PFX_CUDA_TRY(cudaGetDevice(&dev));
   PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int nb = d <= 256 ? 32 : 16;
+  int dev_sms = sms;
+  const bool many = (int64_t)batch * npairs > dev_sms;
+  const int nb = (d <= 256 && !many) ? 32 : 16;
+  const int minb = (d <= 256 && many) ? 2 : 1;
   const size_t smem = dense_smem_bytes(d, nb);
   const int nsys = batch * npairs;
-  const int slots = nsys < sms ? nsys : sms;
+  const int slots = nsys < minb * sms ? nsys : minb * sms;
   const size_t per_sys = (size_t)d * ncols;
   const size_t stage_elems = (size_t)nsys * per_sys * (real_path ? 1 : 2);
   char* ws = static_cast<char*>(scratch(1, (size_t)slots * ((size_t)d * d + 2 * per_sys) * sizeof(double2) +
@@ -621,13 +630,9 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
     PFX_CUDA_TRY(cudaEventCreate(&e1));
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
-  if (nb == 32) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(dense_batched_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PFX_LAUNCH("dense_batched_kernel", stream, dense_batched_kernel<32><<<slots, DB_THREADS, smem, stream>>>(args));
-  } else {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(dense_batched_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PFX_LAUNCH("dense_batched_kernel", stream, dense_batched_kernel<16><<<slots, DB_THREADS, smem, stream>>>(args));
-  }
+  auto kern = nb == 32 ? dense_batched_kernel<32, 1> : (minb == 2 ? dense_batched_kernel<16, 2> : dense_batched_kernel<16, 1>);
+  PFX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PFX_LAUNCH("dense_batched_kernel", stream, kern<<<slots, DB_THREADS, smem, stream>>>(args));
   PFX_CUDA_TRY(cudaGetLastError());
   const size_t per_out = per_sys * (real_path ? 1 : 2);
   const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
