@@ -13,36 +13,46 @@
 //
 // Factorisation (no pivoting, safe by SURVEY finding 7; the band then never fills in),
 // all pole pairs batched in every launch, nb = 64, for each block step j0:
-//   L11 U11 = M11                         zgetf2 (diagonal 64x64 block)
-//   U12 = L11^{-1} M12, L21 = M21 U11^{-1}  ztrsm (kb-wide panels)
+//   L11 U11 = M11                         zgetrf_diag (diagonal 64x64 block in SMEM)
+//   L11^{-1}, U11^{-1}                     ztrtri_diag (one warp per column; U11^{-1} is kept
+//                                          per block row for the back substitution)
+//   U12 = L11^{-1} M12, L21 = M21 U11^{-1}  ztrmm (in-place DMMA products, kb-wide panels)
 //   M22 -= L21 U12                         zgemm on DMMA (kb x kb x 64)
 //   y1 = L11^{-1} y1, y2 -= L21 y1          forward elimination of the RHS alongside
-// then block back substitution y1 = U11^{-1}(y1 - U12 y2), and the combine kernel.
+// then block back substitution y1 = U11^{-1}(y1 - U12 y2), and the combine kernel.  Applying
+// the explicit inverses keeps every block-step kernel on DMMA with one barrier-free pass
+// instead of a 64-step dependent triangular solve (the latency bound of the TRSM version).
 #include "zblas.cuh"
 
 namespace pfx {
 
 constexpr int BD_NB = 64;
 
+// grid (row groups, pairs): each warp writes whole rows of the padded row band (no index
+// division: the band is ~40 GB for C5, so this is a pure HBM write stream)
 __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const double* V, int nrhs, double shift_c,
                          const double2* theta, ZMat M, ZMat X) {
   const int k = blockIdx.y;
   const cplx th = ld(&theta[k]);
   double2* base = M.p - (kb + BD_NB) + k * M.stride;  // row-band base of pair k
-  const int64_t total = N * Wd;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = e / Wd;
-    int off = (int)(e - i * Wd) - (kb + BD_NB);  // j - i
-    int64_t j = i + off;
-    double v = 0.0;
-    int ao = off < 0 ? -off : off;
-    if (ao <= kb && j >= 0 && j < N) v = ao == 0 ? band[i] : band[(int64_t)ao * N + (off < 0 ? j : i)];
-    double2 z = make_double2(v, 0.0);
-    if (off == 0) {
-      z.x = (v - shift_c) + th.re;
-      z.y = th.im;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = wid; i < N; i += nw) {
+    double2* rowp = base + i * Wd;
+    for (int e = lane; e < Wd; e += 32) {
+      const int off = e - (kb + BD_NB);  // j - i
+      const int64_t j = i + off;
+      const int ao = off < 0 ? -off : off;
+      double v = 0.0;
+      if (ao <= kb && j >= 0 && j < N) v = ao == 0 ? band[i] : band[(int64_t)ao * N + (off < 0 ? j : i)];
+      double2 z = make_double2(v, 0.0);
+      if (off == 0) {
+        z.x = (v - shift_c) + th.re;
+        z.y = th.im;
+      }
+      rowp[e] = z;
     }
-    base[e] = z;
   }
   const int64_t nx = N * nrhs;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nx; e += (int64_t)gridDim.x * blockDim.x)
@@ -65,39 +75,217 @@ __global__ void bd_combine(ZMat X, int64_t n, int npairs, const double2* coef, d
 // The factorisation + solves touch only the workspace, so the ~8 launches per 64-row
 // block step are captured once into a CUDA graph per (shape, workspace) and replayed:
 // the per-launch host overhead was the bound of this path (N/64 = 4096 block steps).
-static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, int64_t N, int kb, int nr, int npairs, int* sing) {
+// Block back substitution y1 = U11^{-1} (y1 - U12 y2) for one 64-row block, all pairs:
+// bd_back_partial splits the kb-long inner dimension into 32-wide chunks (one CTA per chunk
+// and pair: P[q] = U12[:, chunk q] y2[chunk q]), bd_back_finish sums the chunks in
+// ascending order (deterministic), subtracts, and applies the stored U11^{-1}.
+constexpr int BK_C = 32;
+
+__global__ void __launch_bounds__(256) bd_back_partial(ZMat M, ZMat X, int64_t j0, int jb, int rest, int nr,
+                                                       double2* P) {
+  __shared__ __align__(16) double2 us[64][BK_C + 1];
+  __shared__ __align__(16) double2 xs[BK_C][9];
+  const int q = blockIdx.x, b = blockIdx.y, nq = gridDim.x;
+  const int tid = threadIdx.x;
+  const int t0 = q * BK_C, tn = min(BK_C, rest - t0);
+  const int64_t col0 = j0 + jb + t0;
+  for (int e = tid; e < 64 * BK_C; e += 256) {
+    const int r = e >> 5, t = e & 31;
+    if (r < jb && t < tn) cp_async16(&us[r][t], M.at(b, j0 + r, col0 + t));
+    else us[r][t] = make_double2(0, 0);
+  }
+  cp_async_commit();
+  const int r = tid >> 2, cg = tid & 3;
+  for (int c0 = 0; c0 < nr; c0 += 8) {
+    const int nc = min(8, nr - c0);
+    __syncthreads();
+    for (int e = tid; e < BK_C * 8; e += 256) {
+      const int t = e >> 3, c = e & 7;
+      xs[t][c] = (t < tn && c < nc) ? *X.at(b, col0 + t, c0 + c) : make_double2(0, 0);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    cplx a0 = mk(0, 0), a1 = mk(0, 0), b0 = mk(0, 0), b1 = mk(0, 0);
+#pragma unroll 8
+    for (int t = 0; t < BK_C; t += 2) {
+      const cplx u = ld(&us[r][t]), v = ld(&us[r][t + 1]);
+      a0 = cfma(u, ld(&xs[t][cg]), a0);
+      a1 = cfma(u, ld(&xs[t][cg + 4]), a1);
+      b0 = cfma(v, ld(&xs[t + 1][cg]), b0);
+      b1 = cfma(v, ld(&xs[t + 1][cg + 4]), b1);
+    }
+    if (r < jb) {
+      double2* pq = P + (((int64_t)b * nq + q) * 64 + r) * nr + c0;
+      if (cg < nc) pq[cg] = make_double2(a0.re + b0.re, a0.im + b0.im);
+      if (cg + 4 < nc) pq[cg + 4] = make_double2(a1.re + b1.re, a1.im + b1.im);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) bd_back_finish(ZMat X, ZMat Ui, int64_t j0, int jb, int nr, int nq,
+                                                      const double2* P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* us = reinterpret_cast<double2*>(smem_raw);  // 64 x 65 (upper triangle of U11^{-1})
+  double2* ts = us + 64 * 65;                          // 64 x ncl (this CTA's column chunk)
+  const int b = blockIdx.x;
+  const int cc = blockIdx.y * 64, ncl = min(64, nr - cc);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    if (r < jb && c < jb && c >= r) cp_async16(&us[r * 65 + c], Ui.at(b, r, c));
+  }
+  cp_async_commit();
+  for (int e = tid; e < jb * ncl; e += 256) {
+    const int r = e / ncl, c = e - r * ncl;
+    cplx v = ld(X.at(b, j0 + r, cc + c));
+    const double2* pe = P + ((int64_t)b * nq * 64 + r) * nr + cc + c;
+    const int64_t qs = (int64_t)64 * nr;
+    int q = 0;
+    for (; q + 4 <= nq; q += 4) {  // four independent loads per round, subtracted in order
+      const cplx p0 = ld(pe + q * qs), p1 = ld(pe + (q + 1) * qs), p2 = ld(pe + (q + 2) * qs), p3 = ld(pe + (q + 3) * qs);
+      v = csub(csub(csub(csub(v, p0), p1), p2), p3);
+    }
+    for (; q < nq; ++q) v = csub(v, ld(pe + q * qs));
+    ts[r * ncl + c] = make_double2(v.re, v.im);
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int e = tid; e < jb * ncl; e += 256) {
+    const int r = e / ncl, c = e - r * ncl;
+    cplx a0 = mk(0, 0), a1 = mk(0, 0);
+    int k = r;
+    for (; k + 2 <= jb; k += 2) {
+      a0 = cfma(ld(&us[r * 65 + k]), ld(&ts[k * ncl + c]), a0);
+      a1 = cfma(ld(&us[r * 65 + k + 1]), ld(&ts[(k + 1) * ncl + c]), a1);
+    }
+    if (k < jb) a0 = cfma(ld(&us[r * 65 + k]), ld(&ts[k * ncl + c]), a0);
+    *X.at(b, j0 + r, cc + c) = make_double2(a0.re + a1.re, a0.im + a1.im);
+  }
+}
+
+// Three streams inside one captured graph: the critical chain (diagonal LU -> inverses ->
+// L21 -> A22 update -> next LU) stays on `main`; U12 = L11^{-1} M12 runs beside L21 on
+// `s1`; the right-hand-side elimination (y1 = L11^{-1} y1, y2 -= L21 y1) trails on `s2`,
+// where it overlaps the next block steps (its inputs, L11^{-1} per block and the L21
+// columns, are never written again).
+struct BdStreams {
+  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr;
+  cudaEvent_t ev[6] = {};
+};
+static int bd_streams(BdStreams& S) {
+  static BdStreams g;
+  if (!g.s1) {
+    // the critical chain must win the SM slots whenever a trailing-update CTA retires:
+    // s1 (panel beside the critical chain) high priority, s2 / s3 (trailing work) low
+    int lo = 0, hi = 0;
+    PFX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s1, cudaStreamNonBlocking, hi));
+    PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s2, cudaStreamNonBlocking, lo));
+    PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s3, cudaStreamNonBlocking, lo));
+    for (auto& e : g.ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  S = g;
+  return PFX_OK;
+}
+
+static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui, double2* P, int64_t N, int kb,
+                           int nr, int npairs, int* sing) {
   const int nb = BD_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
     r.p = A.p + i * A.ld + j;
     return r;
   };
+  auto blk = [&](ZMat T, int64_t j0) {
+    ZMat r = T;
+    r.p = T.p + (j0 / nb) * nb * nb;
+    return r;
+  };
+  BdStreams S;
   int rc;
+  if ((rc = bd_streams(S))) return rc;
+  // PFX_BD_SKIP (timing experiments only, results are wrong): bit 0 back substitution,
+  // bit 1 rhs chain, bit 2 trailing update, bit 3 diagonal LU + inverses, bit 4 panel products
+  static const int skip = [] {
+    const char* e = getenv("PFX_BD_SKIP");
+    return e ? atoi(e) : 0;
+  }();
+  cudaEvent_t evT = S.ev[0], evU = S.ev[1], evL = S.ev[2], evR = S.ev[3], evP = S.ev[4], evB = S.ev[5];
+  // s2 / s3 start after everything already queued on main (the build kernel)
+  PFX_CUDA_TRY(cudaEventRecord(evT, stream));
+  PFX_CUDA_TRY(cudaStreamWaitEvent(S.s2, evT, 0));
+  PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evT, 0));
+  bool pending_b = false;  // a trailing update of the previous step is queued on s3
   for (int64_t j0 = 0; j0 < N; j0 += nb) {
     const int jb = (int)std::min<int64_t>(nb, N - j0);
     const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);  // rows/cols coupled below/right
-    if ((rc = zgetf2_panel(stream, npairs, jb, jb, sub(M, j0, j0), nullptr, sing))) return rc;
-    if (rest > 0) {
-      if ((rc = ztrsm_llnu(stream, npairs, jb, rest, sub(M, j0, j0), sub(M, j0, j0 + jb)))) return rc;
-      if ((rc = ztrsm_runn(stream, npairs, rest, jb, sub(M, j0, j0), sub(M, j0 + jb, j0)))) return rc;
-      if ((rc = zgemm(stream, npairs, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
-                      sub(M, j0 + jb, j0 + jb))))
-        return rc;
+    if (!(skip & 8) && (rc = zgetrf_diag(stream, npairs, jb, sub(M, j0, j0), sing))) return rc;
+    if (!(skip & 8) && (rc = ztrtri_diag(stream, npairs, jb, sub(M, j0, j0), blk(Li, j0), blk(Ui, j0)))) return rc;
+    if (rest > 0 && !(skip & 16)) {
+      PFX_CUDA_TRY(cudaEventRecord(evT, stream));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(S.s1, evT, 0));
+      if ((rc = ztrmm_inplace(S.s1, npairs, jb, rest, blk(Li, j0), sub(M, j0, j0 + jb), false, false))) return rc;
+      PFX_CUDA_TRY(cudaEventRecord(evU, S.s1));
+      if ((rc = ztrmm_inplace(stream, npairs, jb, rest, blk(Ui, j0), sub(M, j0 + jb, j0), true, true))) return rc;
     }
-    if ((rc = ztrsm_llnu(stream, npairs, jb, nr, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
-    if (rest > 0 && (rc = zgemm(stream, npairs, rest, nr, jb, -1.0, sub(M, j0 + jb, j0), sub(X, j0, 0),
+    PFX_CUDA_TRY(cudaEventRecord(evL, stream));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(S.s2, evL, 0));
+    if (!(skip & 2) && (rc = ztrmm_inplace(S.s2, npairs, jb, nr, blk(Li, j0), sub(X, j0, 0), false, false))) return rc;
+    if (rest > 0 && !(skip & 2) && (rc = zgemm(S.s2, npairs, rest, nr, jb, -1.0, sub(M, j0 + jb, j0), sub(X, j0, 0),
                                 sub(X, j0 + jb, 0))))
       return rc;
+    if (rest > 0) {
+      // look-ahead: the next block's row strip (ra rows, all rest columns) and column strip
+      // are updated first on main; the trailing (rest - ra)^2 part goes to s3, where it
+      // overlaps the next block's LU / inverses / panel products.  The strips lie inside
+      // the previous step's trailing region, so main waits for it (evB) first.
+      const int ra = std::min(nb, rest);
+      PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
+      if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));
+      PFX_CUDA_TRY(cudaEventRecord(evP, stream));  // panels of this step are final
+      if ((rc = zgemm(stream, npairs, ra, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
+                      sub(M, j0 + jb, j0 + jb))))
+        return rc;
+      if (rest > ra && !(skip & 4)) {
+        if ((rc = zgemm(stream, npairs, rest - ra, ra, jb, -1.0, sub(M, j0 + jb + ra, j0), sub(M, j0, j0 + jb),
+                        sub(M, j0 + jb + ra, j0 + jb))))
+          return rc;
+        PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evP, 0));
+        if ((rc = zgemm(S.s3, npairs, rest - ra, rest - ra, jb, -1.0, sub(M, j0 + jb + ra, j0),
+                        sub(M, j0, j0 + jb + ra), sub(M, j0 + jb + ra, j0 + jb + ra))))
+          return rc;
+        PFX_CUDA_TRY(cudaEventRecord(evB, S.s3));
+        pending_b = true;
+      } else {
+        pending_b = false;
+      }
+    }
   }
+  if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));
+  PFX_CUDA_TRY(cudaEventRecord(evR, S.s2));
+  PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evR, 0));
   const int64_t nblk = (N + nb - 1) / nb;
-  for (int64_t pb = nblk - 1; pb >= 0; --pb) {
+  for (int64_t pb = nblk - 1; pb >= 0 && !(skip & 1); --pb) {
     const int64_t j0 = pb * nb;
     const int jb = (int)std::min<int64_t>(nb, N - j0);
     const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);
-    if (rest > 0 && (rc = zgemm(stream, npairs, jb, nr, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0),
-                                sub(X, j0, 0))))
-      return rc;
-    if ((rc = ztrsm_lunn(stream, npairs, jb, nr, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
+    const int nq = (int)ceil_div(rest, BK_C);
+    if (nq > 0) {
+      dim3 g((unsigned)nq, (unsigned)npairs);
+      PFX_LAUNCH_F("bd_back_partial", stream, 8.0 * jb * rest * (double)nr * npairs,
+                   bd_back_partial<<<g, 256, 0, stream>>>(M, X, j0, jb, rest, nr, P));
+      PFX_CUDA_TRY(cudaGetLastError());
+    }
+    const int fsm = (64 * 65 + 64 * std::min(nr, 64)) * (int)sizeof(double2);
+    static int fsm_set = 0;
+    if (fsm > fsm_set) {
+      PFX_CUDA_TRY(cudaFuncSetAttribute(bd_back_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+      fsm_set = fsm;
+    }
+    dim3 gf((unsigned)npairs, (unsigned)ceil_div(nr, 64));
+    PFX_LAUNCH_F("bd_back_finish", stream, 4.0 * jb * jb * (double)nr * npairs,
+                 bd_back_finish<<<gf, 256, fsm, stream>>>(X, blk(Ui, j0), j0, jb, nr, nq, P));
+    PFX_CUDA_TRY(cudaGetLastError());
   }
   return PFX_OK;
 }
@@ -120,11 +308,18 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   const int Wd = 2 * kb + 2 * nb + 1;
   const size_t mbytes = (size_t)npairs * N * Wd * sizeof(double2);
   const size_t xbytes = (size_t)npairs * N * nrhs * sizeof(double2);
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 256));
+  const int64_t nblk = (N + nb - 1) / nb;
+  const size_t libytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
+  const size_t uibytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
+  const size_t pbytes = (size_t)npairs * ceil_div(kb, BK_C) * nb * nrhs * sizeof(double2);
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + libytes + uibytes + pbytes + 256));
   if (!ws) return fail(PFX_CUDA, "banded workspace allocation failed (needs " + std::to_string((mbytes + xbytes) >> 20) + " MiB)");
   ZMat M{reinterpret_cast<double2*>(ws) + kb + nb, Wd - 1, (int64_t)N * Wd};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, N * nrhs};
-  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes);
+  ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), nb, nblk * nb * nb};
+  ZMat Ui{reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes), nb, nblk * nb * nb};
+  double2* P = reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes + uibytes);
+  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + libytes + uibytes + pbytes);
   PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (per_pair_ms) {
@@ -132,12 +327,12 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     PFX_CUDA_TRY(cudaEventCreate(&e1));
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
-  dim3 bg(2368, npairs);
+  dim3 bg(1184, npairs);
   PFX_LAUNCH("bd_build", stream, bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X));
   PFX_CUDA_TRY(cudaGetLastError());
   if (prof_on()) {
     // profiling wants per-kernel events: run the launches directly
-    if (int rc = bd_factor_solve(stream, M, X, N, kb, (int)nrhs, npairs, sing)) return rc;
+    if (int rc = bd_factor_solve(stream, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing)) return rc;
   } else {
     BdGraph& G = g_bd_graph;
     if (!G.exec || G.ws != ws || G.N != N || G.kb != kb || G.nr != (int)nrhs || G.np != npairs) {
@@ -145,15 +340,20 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
         cudaGraphExecDestroy(G.exec);
         G.exec = nullptr;
       }
-      cudaStream_t cs;
-      PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      BdStreams S;  // create the side streams before capturing
+      if (int rc = bd_streams(S)) return rc;
+      cudaStream_t cs;  // capture origin = the critical chain: highest priority
+      int lo = 0, hi = 0;
+      PFX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      PFX_CUDA_TRY(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
       cudaGraph_t graph;
       PFX_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int rc = bd_factor_solve(cs, M, X, N, kb, (int)nrhs, npairs, sing);
+      int rc = bd_factor_solve(cs, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing);
       cudaError_t ce = cudaStreamEndCapture(cs, &graph);
       if (rc) return rc;
       if (ce != cudaSuccess) return fail(PFX_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-      PFX_CUDA_TRY(cudaGraphInstantiate(&G.exec, graph, 0));
+      // kernel nodes keep the priority of the stream they were captured from
+      PFX_CUDA_TRY(cudaGraphInstantiateWithFlags(&G.exec, graph, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(graph);
       cudaStreamDestroy(cs);
       G.ws = ws;

@@ -6,10 +6,11 @@
 // :226-228 ascending reduction):
 //   M_k = A - cI + theta_k I                    (one d x d complex slot per pair)
 //   M_k = L_k U_k                               right-looking blocked LU, nb = 64:
-//        diagonal block LU (zgetf2), U12 = L11^{-1} A12, L21 = A21 U11^{-1} (ztrsm),
-//        A22 -= L21 U12 (zgemm on DMMA)
+//        diagonal block LU (zgetrf_diag) + both triangular inverses (ztrtri_diag, kept per
+//        block row for the substitutions), U12 = L11^{-1} A12, L21 = A21 U11^{-1}
+//        (ztrmm, DMMA), A22 -= L21 U12 (zgemm on DMMA)
 //   X_k = U_k^{-1} L_k^{-1} B                  blocked forward/backward substitution,
-//        B = I (full mode) or V (action); GEMM-rich (zgemm + ztrsm per block row)
+//        B = I (full mode) or V (action); all DMMA (zgemm + ztrmm by the stored inverses)
 //   out = e^c sum_k S_k                          fused combine kernel, k ascending
 // No pivoting on this path: for Hermitian A and Im(theta_k) >= 0.7366 every pivot of
 // A + theta_k I has |Im| >= Im(theta_k) (SURVEY finding 7), so the factorisation cannot
@@ -84,37 +85,46 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
 // LU (no pivoting) of nsys d x d matrices M, then X = U^{-1} L^{-1} X.  identity_rhs: X
 // starts as I, so L^{-1} X is unit lower triangular and the forward substitution of block
 // row p only touches columns < (p+1) nb (one third of the full-RHS work instead of half).
-int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* sing, bool identity_rhs) {
+// Li, Ui: nsys x (d/nb) stored 64x64 L11^{-1} / U11^{-1} tiles (ld 64, stride nblk*64*64).
+int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
+                   bool identity_rhs) {
   const int nb = DL_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
     r.p = A.p + i * A.ld + j;
     return r;
   };
+  auto li = [&](int j0) {
+    ZMat r = Li;
+    r.p = Li.p + (int64_t)(j0 / nb) * nb * nb;
+    return r;
+  };
+  auto ui = [&](int j0) {
+    ZMat r = Ui;
+    r.p = Ui.p + (int64_t)(j0 / nb) * nb * nb;
+    return r;
+  };
   int rc;
   for (int j0 = 0; j0 < d; j0 += nb) {
     const int jb = std::min(nb, d - j0);
     const int rest = d - j0 - jb;
-    if ((rc = zgetf2_panel(s, nsys, jb, jb, sub(M, j0, j0), nullptr, sing))) return rc;
+    if ((rc = zgetrf_diag(s, nsys, jb, sub(M, j0, j0), sing))) return rc;
+    if ((rc = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return rc;
     if (rest > 0) {
-      if ((rc = ztrsm_llnu(s, nsys, jb, rest, sub(M, j0, j0), sub(M, j0, j0 + jb)))) return rc;
-      if ((rc = ztrsm_runn(s, nsys, rest, jb, sub(M, j0, j0), sub(M, j0 + jb, j0)))) return rc;
+      if ((rc = ztrmm_inplace(s, nsys, jb, rest, li(j0), sub(M, j0, j0 + jb), false, false))) return rc;
+      if ((rc = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true))) return rc;
       if ((rc = zgemm(s, nsys, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
                       sub(M, j0 + jb, j0 + jb))))
         return rc;
     }
   }
   // forward: X_p -= L[p, :p] X[:p]; X_p = L_pp^{-1} X_p
-  auto trsm = [&](int jb, int n, ZMat T, ZMat B, bool upper) {
-    if (n >= 512) return ztrsm_left_gemm(s, nsys, jb, n, T, B, upper);
-    return upper ? ztrsm_lunn(s, nsys, jb, n, T, B) : ztrsm_llnu(s, nsys, jb, n, T, B);
-  };
   for (int j0 = 0; j0 < d; j0 += nb) {
     const int jb = std::min(nb, d - j0);
     const int nc = identity_rhs ? j0 : ncols;            // columns the update can touch
     const int ns = identity_rhs ? std::min(ncols, j0 + jb) : ncols;  // columns the solve touches
     if (j0 > 0 && (rc = zgemm(s, nsys, jb, nc, j0, -1.0, sub(M, j0, 0), sub(X, 0, 0), sub(X, j0, 0)))) return rc;
-    if ((rc = trsm(jb, ns, sub(M, j0, j0), sub(X, j0, 0), false))) return rc;
+    if ((rc = ztrmm_inplace(s, nsys, jb, ns, li(j0), sub(X, j0, 0), false, false))) return rc;
   }
   // backward: X_p -= U[p, p+1:] X[p+1:]; X_p = U_pp^{-1} X_p
   const int nblk = (d + nb - 1) / nb;
@@ -125,7 +135,7 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, i
     if (rest > 0 &&
         (rc = zgemm(s, nsys, jb, ncols, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0))))
       return rc;
-    if ((rc = trsm(jb, ncols, sub(M, j0, j0), sub(X, j0, 0), true))) return rc;
+    if ((rc = ztrmm_inplace(s, nsys, jb, ncols, ui(j0), sub(X, j0, 0), false, true))) return rc;
   }
   return PFX_OK;
 }
@@ -137,11 +147,15 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   const int nsys = npairs * (1 + conj_sys);
   const size_t mbytes = (size_t)nsys * d * d * sizeof(double2);
   const size_t xbytes = (size_t)nsys * d * ncols * sizeof(double2);
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 256));
+  const int nblk = (d + DL_NB - 1) / DL_NB;
+  const size_t libytes = (size_t)nsys * nblk * DL_NB * DL_NB * sizeof(double2);
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256));
   if (!ws) return fail(PFX_CUDA, "large dense workspace allocation failed");
+  ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
   ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), ncols, (int64_t)d * ncols};
-  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes);
+  ZMat Ui{reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
+  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + 2 * libytes);
   PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (per_pair_ms) {
@@ -153,7 +167,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full, shift_c,
                                                                     theta_d, npairs, nsys, M, X));
   PFX_CUDA_TRY(cudaGetLastError());
-  int rc = lu_solve_nopiv(stream, nsys, d, M, X, ncols, sing, full != 0);
+  int rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0);
   if (rc) return rc;
   const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
   PFX_LAUNCH("dl_combine", stream,

@@ -60,6 +60,10 @@ __host__ __device__ __forceinline__ cplx cmulc(cplx a, cplx b) {
 __host__ __device__ __forceinline__ cplx cfms(cplx c, cplx a, cplx b) {
   return cplx{fma(-a.re, b.re, fma(a.im, b.im, c.re)), fma(-a.re, b.im, fma(-a.im, b.re, c.im))};
 }
+// c + a*b
+__host__ __device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {
+  return cplx{fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))};
+}
 __host__ __device__ __forceinline__ cplx cconj(cplx a) { return cplx{a.re, -a.im}; }
 __host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cplx{a.re * s, a.im * s}; }
 // 1/z with Smith-style scaling to avoid overflow/underflow of |z|^2

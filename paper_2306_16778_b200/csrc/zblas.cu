@@ -520,4 +520,256 @@ int ztrsm_left_gemm(cudaStream_t s, int batch, int nb, int n, ZMat T, ZMat B, bo
   return PFX_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Diagonal-block LU (nb <= 64, no pivoting), one CTA (256 threads) per batch member,
+// factors written back in place.
+constexpr int DI_MAX = 64;
+constexpr int DI_S = DI_MAX + 1;
+
+// Register-resident: thread (row = tid / 4, phase = tid % 4) holds A[row][phase + 4(q + i)],
+// i < 16 - q, where q is the current 4-column block: after every 4 columns the finished
+// register a[0] is stored and the window rotates, so every register index stays static
+// while the code stays a small loop (a fully unrolled 64-column body overflows the
+// instruction cache).  Step j: row j publishes itself to shared memory (double-buffered:
+// one barrier per column), every lower row takes its multiplier's numerator from the
+// owning lane by shuffle and updates its entries right of j.  nb < 64 pads with I.
+__global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* sing) {
+  // the pivot row buffer runs 64 entries past the block, kept zero: the updates of the
+  // dead registers (a[i], i >= 16 - q) read those zeros, so every update is unconditional
+  // straight-line code the compiler can schedule as one batch of loads + DFMAs
+  __shared__ double2 prow[2][2 * DI_MAX];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int row = tid >> 2, cg = tid & 3;
+  prow[tid >> 7][tid & 127] = make_double2(0, 0);
+  cplx a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int c = cg + 4 * i;
+    if (row < nb && c < nb) a[i] = ld(D.at(b, row, c));
+    else a[i] = mk(row == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int q = 0; q < 16; ++q) {
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * q + jj;
+      double2* pr = prow[jj & 1];
+      if (row == j) {
+        // entries left of j in the first register are stale multipliers: publish only c >= j
+        if (cg >= jj) st(&pr[cg + 4 * q], a[0]);
+#pragma unroll
+        for (int i = 1; i < 16; ++i) st(&pr[cg + 4 * (q + i)], a[i]);  // dead registers are zero
+        if (cg == jj && a[0].re == 0.0 && a[0].im == 0.0) *sing = 1;
+      }
+      __syncthreads();
+      const int src = (lane & ~3) | jj;
+      cplx aj;
+      aj.re = __shfl_sync(0xffffffffu, a[0].re, src);
+      aj.im = __shfl_sync(0xffffffffu, a[0].im, src);
+      if (row > j) {
+        const cplx l = cmul(aj, crcp_fast(ld(&pr[j])));
+        const cplx a0 = cfms(a[0], l, ld(&pr[cg + 4 * q]));
+#pragma unroll
+        for (int i = 1; i < 16; ++i) a[i] = cfms(a[i], l, ld(&pr[cg + 4 * (q + i)]));
+        a[0] = cg == jj ? l : (cg > jj ? a0 : a[0]);
+      }
+    }
+    const int c = cg + 4 * q;
+    if (row < nb && c < nb) *D.at(b, row, c) = make_double2(a[0].re, a[0].im);
+#pragma unroll
+    for (int i = 0; i < 15; ++i) a[i] = a[i + 1];
+    a[15] = mk(0, 0);
+  }
+}
+
+// Triangular inverses of the factored block: grid (nb/8 column groups, 2 triangles, batch);
+// warp w of a CTA owns one column of L^{-1} (blockIdx.y = 0) or U^{-1} (= 1), lanes hold
+// rows lane and lane + 32, and the substitution broadcasts the finished entry by shuffle.
+__global__ void __launch_bounds__(256) ztrtri_diag_kernel(int nb, ZMat D, ZMat Li, ZMat Ui) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* A = reinterpret_cast<double2*>(smem_raw);
+  double2* rdiag = A + DI_MAX * DI_S;
+  const int b = blockIdx.z;
+  const bool upper = blockIdx.y != 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // the zero / identity padding (rows, columns >= nb) makes every update unconditional
+  for (int e = tid; e < DI_MAX * DI_MAX; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    const bool keep = upper ? c >= r : c < r;
+    if (keep && r < nb && c < nb) cp_async16(&A[r * DI_S + c], D.at(b, r, c));
+    else A[r * DI_S + c] = make_double2(r == c && r >= nb ? 1.0 : 0.0, 0.0);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (upper && tid < DI_MAX) {
+    const cplx r = crcp(ld(&A[tid * DI_S + tid]));
+    rdiag[tid] = make_double2(r.re, r.im);
+  }
+  __syncthreads();
+  const int c = blockIdx.x * 8 + warp;
+  if (c >= nb) return;
+  const int r0 = lane, r1 = lane + 32;
+  cplx x0 = mk(r0 == c ? 1.0 : 0.0, 0.0), x1 = mk(r1 == c ? 1.0 : 0.0, 0.0);
+  if (!upper) {
+    // X = L^{-1} e_c (unit diagonal; A holds L strictly below, zeros elsewhere): rows
+    // at or above k see L[r][k] = 0, so the update needs no row test
+    for (int k = c; k < nb - 1; ++k) {
+      const cplx src = k < 32 ? x0 : x1;
+      const cplx l0 = ld(&A[r0 * DI_S + k]), l1 = ld(&A[r1 * DI_S + k]);
+      cplx xk;
+      xk.re = __shfl_sync(0xffffffffu, src.re, k & 31);
+      xk.im = __shfl_sync(0xffffffffu, src.im, k & 31);
+      x0 = cfms(x0, l0, xk);
+      x1 = cfms(x1, l1, xk);
+    }
+    if (r0 < nb) *Li.at(b, r0, c) = make_double2(x0.re, x0.im);
+    if (r1 < nb) *Li.at(b, r1, c) = make_double2(x1.re, x1.im);
+  } else {
+    // X = U^{-1} e_c: step k finalises row k (scale by 1/U_kk) and eliminates it from the
+    // rows above (U[r][k] = 0 for r >= k in A's padded copy except the diagonal)
+    for (int k = c; k >= 0; --k) {
+      const cplx src = k < 32 ? x0 : x1;
+      const cplx rd = ld(&rdiag[k]);
+      const cplx u0 = r0 < k ? ld(&A[r0 * DI_S + k]) : mk(0, 0);
+      const cplx u1 = r1 < k ? ld(&A[r1 * DI_S + k]) : mk(0, 0);
+      cplx xk;
+      xk.re = __shfl_sync(0xffffffffu, src.re, k & 31);
+      xk.im = __shfl_sync(0xffffffffu, src.im, k & 31);
+      xk = cmul(xk, rd);
+      x0 = r0 == k ? xk : cfms(x0, u0, xk);
+      x1 = r1 == k ? xk : cfms(x1, u1, xk);
+    }
+    if (r0 < nb) *Ui.at(b, r0, c) = make_double2(x0.re, x0.im);
+    if (r1 < nb) *Ui.at(b, r1, c) = make_double2(x1.re, x1.im);
+  }
+}
+
+int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing) {
+  if (nb > DI_MAX) return fail(PFX_BADARG, "zgetrf_diag: nb > 64");
+  PFX_LAUNCH_F("zgetrf_diag", s, 8.0 / 3.0 * nb * nb * (double)nb * batch,
+               zgetrf_diag_kernel<<<batch, 256, 0, s>>>(nb, D, sing));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui) {
+  if (nb > DI_MAX) return fail(PFX_BADARG, "ztrtri_diag: nb > 64");
+  static bool attr = false;
+  const int smem = (DI_MAX * DI_S + DI_MAX) * (int)sizeof(double2);
+  if (!attr) {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrtri_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(nb, 8), 2, (unsigned)batch);
+  PFX_LAUNCH_F("ztrtri_diag", s, 8.0 / 3.0 * nb * nb * (double)nb * batch,
+               ztrtri_diag_kernel<<<grid, 256, smem, s>>>(nb, D, Li, Ui));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
+// In-place product with a small triangular inverse T (nb <= 64): left B(nb x n) = T B, or
+// right B(n x nb) = B T.  One CTA per 32-wide strip of B: T and the strip are staged in
+// shared memory by cp.async, the product runs on DMMA m8n8k4 with the k range cut to T's
+// nonzero triangle, and the strip is written back over itself.
+constexpr int TM_T = 64;
+constexpr int TM_S = TM_T + 1;
+constexpr int TM_W = 32;
+
+template <bool RIGHT>
+__global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Ts = reinterpret_cast<double2*>(smem_raw);  // 64 x TM_S
+  double2* Bs = Ts + TM_T * TM_S;                      // left: [k 64][col TM_W+1]; right: [row TM_W][k TM_S]
+  constexpr int BSL = TM_W + 1;
+  const int b = blockIdx.y;
+  const int t0 = blockIdx.x * TM_W;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tt = lane & 3;
+  for (int e = tid; e < TM_T * TM_T; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    if (r < nb && c < nb) cp_async16(&Ts[r * TM_S + c], T.at(b, r, c));
+    else Ts[r * TM_S + c] = make_double2(0, 0);
+  }
+  for (int e = tid; e < TM_T * TM_W; e += 256) {
+    if (!RIGHT) {  // Bs[k][col] = B[k][t0 + col]
+      const int r = e / TM_W, c = e - r * TM_W;
+      if (r < nb && t0 + c < n) cp_async16(&Bs[r * BSL + c], B.at(b, r, t0 + c));
+      else Bs[r * BSL + c] = make_double2(0, 0);
+    } else {  // Bs[row][k] = B[t0 + row][k]
+      const int r = e >> 6, c = e & 63;
+      if (t0 + r < n && c < nb) cp_async16(&Bs[r * TM_S + c], B.at(b, t0 + r, c));
+      else Bs[r * TM_S + c] = make_double2(0, 0);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  // left: R (64 x 32) = T Bs, warp = 8-row slab, 4 column fragments
+  // right: R (32 x 64) = Bs T, warp = (8-row slab wm = warp >> 1, 32-column half wn = warp & 1)
+  const int wm = RIGHT ? (warp >> 1) : warp;
+  const int wn = RIGHT ? (warp & 1) : 0;
+  int klo = 0, khi = TM_T;
+  if (!RIGHT) {
+    if (upper) klo = wm * 8;          // T upper: T[r][k] = 0 for k < r
+    else khi = wm * 8 + 8;            // T lower: T[r][k] = 0 for k > r
+  } else {
+    if (upper) khi = wn * 32 + 32;    // T upper: T[k][c] = 0 for k > c
+    else klo = wn * 32;               // T lower: T[k][c] = 0 for k < c
+  }
+  double cr[4][2], ci[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+  for (int k0 = klo; k0 < khi; k0 += 4) {
+    double2 x;
+    if (!RIGHT) x = Ts[(wm * 8 + g) * TM_S + k0 + tt];
+    else x = Bs[(wm * 8 + g) * TM_S + k0 + tt];
+    double br[4], bi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 y = RIGHT ? Ts[(k0 + tt) * TM_S + wn * 32 + j * 8 + g] : Bs[(k0 + tt) * BSL + j * 8 + g];
+      br[j] = y.x;
+      bi[j] = y.y;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) zmma884(cr[j], ci[j], x.x, x.y, br[j], bi[j]);
+  }
+  const int r = wm * 8 + g;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = wn * 32 + j * 8 + 2 * tt + h;
+      const double2 v = make_double2(cr[j][h], ci[j][h]);
+      if (!RIGHT) {
+        if (r < nb && t0 + c < n) *B.at(b, r, t0 + c) = v;
+      } else {
+        if (t0 + r < n && c < nb) *B.at(b, t0 + r, c) = v;
+      }
+    }
+}
+
+int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper) {
+  if (n <= 0) return PFX_OK;
+  if (nb > TM_T) return fail(PFX_BADARG, "ztrmm_inplace: nb > 64");
+  static bool attr = false;
+  const int smem = (TM_T * TM_S + TM_T * TM_S) * (int)sizeof(double2);
+  if (!attr) {
+    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrmm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrmm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)ceil_div(n, TM_W), (unsigned)batch);
+  const double fl = 4.0 * nb * nb * (double)n * batch;  // triangular: half the square product
+  if (right)
+    PFX_LAUNCH_F("ztrmm", s, fl, ztrmm_kernel<true><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0));
+  else
+    PFX_LAUNCH_F("ztrmm", s, fl, ztrmm_kernel<false><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
 }  // namespace pfx

@@ -27,6 +27,14 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
 // copied back.  Used when n is large (the forward/backward substitutions of C4).
 int ztrsm_left_gemm(cudaStream_t s, int batch, int nb, int n, ZMat T, ZMat B, bool upper);
 
+// No-pivot LU of the nb x nb diagonal block D (nb <= 64) in shared memory, in place.
+int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing);
+// Triangular inverses of a factored diagonal block: Li = L^{-1} (unit lower), Ui = U^{-1}.
+int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui);
+// In place: B = Tinv * B (left, B nb x n) or B = B * Tinv (right, B n x nb), Tinv nb x nb
+// (nb <= 64) triangular (upper or lower), on DMMA; one CTA per 32-wide strip of B.
+int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper);
+
 // Unblocked LU of the m x nb panel at P (in place).  ipiv (optional, batch x nb, 0-based
 // rows relative to the panel) -> partial pivoting with row swaps inside the panel only.
 // sing: device int set to 1 on an exactly zero pivot.

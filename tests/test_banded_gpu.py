@@ -55,3 +55,16 @@ def test_c5_shape_scaled_down_vs_dst():
     got = matexp_action(BandedHermitian(band), V, ExpOptions(n=16, mode="action")).value
     want = restate.banded_action(band, V, 16)
     assert rel(got, want) <= TOL
+
+
+@pytest.mark.parametrize("N,kb,nrhs", [(1500, 600, 1), (1300, 100, 70), (777, 40, 9)])
+def test_wide_band_many_rhs(N, kb, nrhs):
+    # back substitution: > 16 inner chunks (kb > 512), > 64 right-hand sides (column chunks),
+    # and ragged 8-column groups
+    rng = np.random.default_rng(N * 7 + kb)
+    band = rng.uniform(-1, 1, (kb + 1, N)) * (0.5 / np.sqrt(kb + 1))
+    band[0] = -rng.uniform(0.5, 3.0, N)
+    V = rng.standard_normal((N, nrhs))
+    got = matexp_action(BandedHermitian(band), V, ExpOptions(n=16, mode="action")).value
+    want = restate.banded_action(band, V, 16)
+    assert rel(got, want) <= TOL, rel(got, want)
