@@ -60,6 +60,9 @@ ALG_BYTES = {
     "C4": 5.37e8,
     "C5": 8.0 * 2 * 513 * 262144 * 16,
 }
+# dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, from the
+# round's `ncu --set full` capture (profiles/r01_c2_tri_ls_ncu_details.csv); None = not captured
+DOM_TRAFFIC = {"C2": 8.30e8}
 DOMINANT = {"C1": "dense_batched_kernel", "C2": "tri_sweep", "C3": "dense_batched_kernel", "C4": "zgemm", "C5": "zgemm"}
 
 
@@ -282,16 +285,22 @@ def _cpu_task(args):
         _ = aX + aX.conj().T
         return 1.0 / len(th)
     if name == "C5":
+        # one pole pair (zgbsv, kl=ku=512) on all 8 RHS, on the leading C5_ROWS_FRAC of the
+        # rows (the banded LU costs N kb^2: work scales linearly with the rows kept)
         band = W.c5_band()
         V = W.c5_rhs()
-        # one pole pair (zgbsv, kl=ku=512) on all 8 RHS
+        nk = band.shape[1] // C5_ROWS_FRAC
+        band, V = np.ascontiguousarray(band[:, :nk]), np.ascontiguousarray(V[:nk])
         th, co = restate.pairs(n)
         ab = restate.sym_band_to_general(band)
         ab[2 * band.shape[0] - 2, :] += th[cols[0]]
         import scipy.linalg.lapack as lapack
         lapack.zgbsv(band.shape[0] - 1, band.shape[0] - 1, ab, V.astype(complex), overwrite_ab=1)
-        return 1.0 / len(th)
+        return 1.0 / len(th) / C5_ROWS_FRAC
     raise ValueError(name)
+
+
+C5_ROWS_FRAC = 8
 
 
 def cpu_sample_plan(name, cores):
@@ -311,7 +320,8 @@ def cpu_sample_plan(name, cores):
         return tasks, "1 of the 12 pole pairs of C4 (zgesv d=4096 with identity RHS, all BLAS threads)"
     if name == "C5":
         tasks = [(name, 16, [k]) for k in range(min(max(cores // 2, 1), 8))]
-        return tasks, f"{len(tasks)} of the 8 pole pairs of C5 (zgbsv kl=ku=512, 8 RHS), one process each"
+        return tasks, (f"{len(tasks)} of the 8 pole pairs of C5 (zgbsv kl=ku=512, 8 RHS) on the leading 1/{C5_ROWS_FRAC} "
+                       "of the rows (work linear in rows), one process each")
     raise ValueError(name)
 
 
@@ -321,15 +331,16 @@ def run_cpu(name, cores, steps=1, warmup=0):
 
     tasks, desc = cpu_sample_plan(name, cores)
     used = len(tasks)
-    rates = []
+    tot_work = tot_t = 0.0
     with ProcessPoolExecutor(max_workers=used) as pool:
         for it in range(warmup + steps):
             t0 = time.perf_counter()
             work = sum(pool.map(_cpu_task, tasks))
             dt = time.perf_counter() - t0
             if it >= warmup:
-                rates.append(work / dt)
-    return statistics.median(rates), desc, used
+                tot_work += work
+                tot_t += dt
+    return tot_work / tot_t, desc, used
 
 
 # ---- main ------------------------------------------------------------------------
@@ -355,10 +366,11 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        steps = max(1, args.steps if args.steps <= 3 else 3)
-        value, desc, used = run_cpu(args.workload, cores, steps=steps, warmup=0)
+        # every step is one bounded sample of the workload (cpu_sample_plan), K timed after W
+        steps, warmup = max(1, args.steps), max(0, args.warmup)
+        value, desc, used = run_cpu(args.workload, cores, steps=steps, warmup=warmup)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
             "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic (seeded reference recipes)", "impl": "reference",
             "config": {"workload": args.workload, "parallelism": f"cpu x{used} processes"},
@@ -461,7 +473,7 @@ def main():
             flops_per_launch = ALG_FLOPS[args.workload] * wl.evals_per_step * (hi - lo) / npairs / (dom_cnt / prof_steps)
         achieved = flops_per_launch / t_launch / 1e12
         roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                    "frac": achieved / peaks["fp64_tflops"], "traffic": None, "kernel": dom,
+                    "frac": achieved / peaks["fp64_tflops"], "traffic": DOM_TRAFFIC.get(args.workload), "kernel": dom,
                     "kernel_ms": dom_ms / dom_cnt, "peak_source": peaks["fp64_source"],
                     "share_of_step": (dom_ms / prof_steps) / ms_step,
                     "path_frac": ALG_FLOPS[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e12

@@ -20,6 +20,8 @@ LIB = os.path.join(PKG, "libpfx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+# timing experiments only (e.g. PFX_NVCC_FLAGS=-DPFX_TRI_EXP=1 ablates a kernel phase)
+COMMON += os.environ.get("PFX_NVCC_FLAGS", "").split()
 
 
 def _sources():

@@ -199,7 +199,11 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
       const int64_t r0 = blk_r0(b);
       const int cnt = blk_cnt(b);
       // ---- phase A (lane = pair)
+#if defined(PFX_TRI_EXP) && PFX_TRI_EXP == 2
+      if (act && bb == 0) {  // timing ablation: chains of the first block only
+#else
       if (act) {
+#endif
         if (dir == 0) {
           cplx q1 = mk(ckv.a.x, ckv.a.y), q2 = mk(ckv.b.x, ckv.b.y);
 #pragma unroll
@@ -257,6 +261,9 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
       __syncwarp(hmask);
       // ---- phase B (lane = rhs).  Per row: independent per-pair terms, then a fixed
       // pairwise tree over pairs (deterministic); rows unrolled for ILP.
+#if defined(PFX_TRI_EXP) && PFX_TRI_EXP == 1
+      if (bb < 0)  // timing ablation: no RHS sweep
+#endif
 #pragma unroll
       for (int jj = 0; jj < LS_B; ++jj) {
         if (jj < cnt) {

@@ -10,13 +10,13 @@
 
 namespace pfx {
 
-constexpr int GM = 64, GN = 64, GK = 16;
-constexpr int GAS = GK + 1, GBS = GN + 1;
-constexpr int G_THREADS = 256;
+constexpr int GK = 16;
+constexpr int GAS = GK + 1;
 
+template <int TM, int TN>
 struct GemmSmem {
-  double2 A[2][GM][GAS];
-  double2 B[2][GK][GBS];
+  double2 A[2][TM][GAS];
+  double2 B[2][GK][TN + 1];
 };
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
@@ -25,38 +25,45 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
 }
 
-__global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                                                          int accumulate) {
+// TM x TN output tile, NW warps in a 2 x (NW/2) grid, each warp FM x FN DMMA 8x8 tiles.
+// 64x64/8 warps for large problems; 32x32/4 warps when the 64-tile grid would leave SMs
+// idle (one 64x64x64 complex tile is ~16K DMMA cycles of a single SM).
+template <int TM, int TN, int NW>
+__global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
+                                                        int accumulate) {
+  constexpr int NT = NW * 32;
+  constexpr int WN = NW / 2;
+  constexpr int FM = TM / 2 / 8, FN = TN / WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GemmSmem& S = *reinterpret_cast<GemmSmem*>(smem_raw);
+  GemmSmem<TM, TN>& S = *reinterpret_cast<GemmSmem<TM, TN>*>(smem_raw);
   const int b = blockIdx.z;
-  const int m0 = blockIdx.y * GM, n0 = blockIdx.x * GN;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;  // warp tile rows [wm*32, +32), cols [wn*16, +16)
+  const int wm = warp & 1, wn = warp >> 1;  // warp tile rows [wm*TM/2, +TM/2), cols [wn*FN*8, +FN*8)
   const double2* Ab = A.p + b * A.stride;
   const double2* Bb = B.p + b * B.stride;
-  double cr[4][2][2], ci[4][2][2];
+  double cr[FM][FN][2], ci[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
   const int ktiles = (k + GK - 1) / GK;
   auto load = [&](int buf, int kt) {
     const int k0 = kt * GK;
 #pragma unroll
-    for (int u = 0; u < (GM * GK) / G_THREADS; ++u) {
-      int e = tid + u * G_THREADS;
+    for (int u = 0; u < (TM * GK) / NT; ++u) {
+      int e = tid + u * NT;
       int r = e / GK, c = e % GK;
       bool v = (m0 + r < m) && (k0 + c < k);
       const double2* src = v ? Ab + (int64_t)(m0 + r) * A.ld + k0 + c : Ab;
       cp_async16_zfill(&S.A[buf][r][c], src, v);
     }
 #pragma unroll
-    for (int u = 0; u < (GK * GN) / G_THREADS; ++u) {
-      int e = tid + u * G_THREADS;
-      int r = e / GN, c = e % GN;
+    for (int u = 0; u < (GK * TN) / NT; ++u) {
+      int e = tid + u * NT;
+      int r = e / TN, c = e % TN;
       bool v = (k0 + r < k) && (n0 + c < n);
       const double2* src = v ? Bb + (int64_t)(k0 + r) * B.ld + n0 + c : Bb;
       cp_async16_zfill(&S.B[buf][r][c], src, v);
@@ -72,36 +79,36 @@ __global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, d
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < GK; kk += 4) {
-      double ar[4], ai[4], br[2], bi[2];
+      double ar[FM], ai[FM], br[FN], bi[FN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        double2 x = S.A[buf][wm * 32 + i * 8 + g][kk + t];
+      for (int i = 0; i < FM; ++i) {
+        double2 x = S.A[buf][wm * (TM / 2) + i * 8 + g][kk + t];
         ar[i] = alpha * x.x;
         ai[i] = alpha * x.y;
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        double2 y = S.B[buf][kk + t][wn * 16 + j * 8 + g];
+      for (int j = 0; j < FN; ++j) {
+        double2 y = S.B[buf][kk + t][wn * FN * 8 + j * 8 + g];
         br[j] = y.x;
         bi[j] = y.y;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) zmma884(cr[i][j], ci[i][j], ar[i], ai[i], br[j], bi[j]);
+        for (int j = 0; j < FN; ++j) zmma884(cr[i][j], ci[i][j], ar[i], ai[i], br[j], bi[j]);
     }
     __syncthreads();
   }
   double2* Cb = C.p + b * C.stride;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = m0 + wm * 32 + i * 8 + g;
+  for (int i = 0; i < FM; ++i) {
+    const int row = m0 + wm * (TM / 2) + i * 8 + g;
     if (row >= m) continue;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < FN; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int col = n0 + wn * 16 + j * 8 + 2 * t + h;
+        const int col = n0 + wn * FN * 8 + j * 8 + 2 * t + h;
         if (col < n) {
           double2* p = Cb + (int64_t)row * C.ld + col;
           double2 v = accumulate ? *p : make_double2(0.0, 0.0);
@@ -114,19 +121,33 @@ __global__ void __launch_bounds__(G_THREADS) zgemm_kernel(int m, int n, int k, d
   }
 }
 
-int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate) {
-  if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
+template <int TM, int TN, int NW>
+static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
+                        bool accumulate) {
   static bool attr = false;
-  const int smem = (int)sizeof(GemmSmem);
+  const int smem = (int)sizeof(GemmSmem<TM, TN>);
   if (!attr) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<TM, TN, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  dim3 grid((unsigned)ceil_div(n, GN), (unsigned)ceil_div(m, GM), (unsigned)batch);
+  dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch);
   PFX_LAUNCH_F("zgemm", s, 8.0 * (double)m * n * k * batch,
-               zgemm_kernel<<<grid, G_THREADS, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0));
+               (zgemm_kernel<TM, TN, NW><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
+}
+
+int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate) {
+  if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    PFX_CUDA_TRY(cudaGetDevice(&dev));
+    PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, 64) * (int64_t)batch;
+  if (tiles64 < 2 * sms) return zgemm_launch<32, 32, 4>(s, batch, m, n, k, alpha, A, B, C, accumulate);
+  return zgemm_launch<64, 64, 8>(s, batch, m, n, k, alpha, A, B, C, accumulate);
 }
 
 // ---------------------------------------------------------------------------
