@@ -49,17 +49,19 @@ __global__ void dl_build(const double* A, int a_complex, int d, const double* V,
   }
 }
 
-// out = scale * sum_k S_k (k ascending)
+// out = scale * sum_k S_k (k ascending).  sym_lower: X_k holds only its lower triangle
+// (complex symmetric inverse, real-A full mode), read as X(max(i,j), min(i,j)).
 __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* coef, int full, int real_path,
-                           double scale, double* out) {
+                           int sym_lower, double scale, double* out) {
   const int64_t n = (int64_t)d * ncols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = e / ncols, j = e - i * ncols;
     if (real_path) {
+      const int64_t xi = sym_lower && j > i ? j : i, xj = sym_lower && j > i ? i : j;
       double acc = 0.0;
       for (int k = 0; k < npairs; ++k) {
         cplx a = ld(&coef[k]);
-        cplx x = ld(X.at(k, i, j));
+        cplx x = ld(X.at(k, xi, xj));
         double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
         acc = k == 0 ? sk : acc + sk;
       }
@@ -86,8 +88,11 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
 // starts as I, so L^{-1} X is unit lower triangular and the forward substitution of block
 // row p only touches columns < (p+1) nb (one third of the full-RHS work instead of half).
 // Li, Ui: nsys x (d/nb) stored 64x64 L11^{-1} / U11^{-1} tiles (ld 64, stride nblk*64*64).
+// sym_lower (with identity_rhs): M is complex symmetric, so X = M^{-1} is too and the
+// backward pass computes only the lower triangle: block row p needs columns <= p, and the
+// rows below it already hold X[>p, <=p] (a third of the full backward flops).
 int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
-                   bool identity_rhs) {
+                   bool identity_rhs, bool sym_lower) {
   const int nb = DL_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -132,10 +137,11 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
     const int j0 = pb * nb;
     const int jb = std::min(nb, d - j0);
     const int rest = d - j0 - jb;
+    const int nc = sym_lower ? std::min(ncols, j0 + jb) : ncols;
     if (rest > 0 &&
-        (rc = zgemm(s, nsys, jb, ncols, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0))))
+        (rc = zgemm(s, nsys, jb, nc, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0))))
       return rc;
-    if ((rc = ztrmm_inplace(s, nsys, jb, ncols, ui(j0), sub(X, j0, 0), false, true))) return rc;
+    if ((rc = ztrmm_inplace(s, nsys, jb, nc, ui(j0), sub(X, j0, 0), false, true))) return rc;
   }
   return PFX_OK;
 }
@@ -167,11 +173,14 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full, shift_c,
                                                                     theta_d, npairs, nsys, M, X));
   PFX_CUDA_TRY(cudaGetLastError());
-  int rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0);
+  // real A in full mode: A + theta I is complex symmetric -> lower-triangle inverse
+  const int sym_lower = (full && !a_complex && real_path) ? 1 : 0;
+  int rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0);
   if (rc) return rc;
   const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
   PFX_LAUNCH("dl_combine", stream,
-             dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, scale, out));
+             dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
+                                                 out));
   PFX_CUDA_TRY(cudaGetLastError());
   int sg = 0;
   PFX_CUDA_TRY(cudaMemcpyAsync(&sg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));

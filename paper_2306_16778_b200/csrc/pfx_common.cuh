@@ -114,6 +114,16 @@ __device__ __forceinline__ cplx ld(const double2* p) {
   return cplx{v.x, v.y};
 }
 __device__ __forceinline__ void st(double2* p, cplx v) { *p = make_double2(v.re, v.im); }
+// explicit shared-window accesses by 32-bit address (keeps the window-base computation
+// out of latency-critical loops)
+__device__ __forceinline__ cplx lds2(unsigned addr) {
+  double x, y;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
+  return cplx{x, y};
+}
+__device__ __forceinline__ void sts2(unsigned addr, cplx v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.re), "d"(v.im));
+}
 
 // ---- FP64 tensor core (DMMA) ---------------------------------------------
 // D(8x8) += A(8x4, row) * B(4x8, col), binary64.  Fragment ownership for lane l,

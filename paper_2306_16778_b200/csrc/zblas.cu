@@ -559,11 +559,13 @@ __global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* s
   // the pivot row buffer runs 64 entries past the block, kept zero: the updates of the
   // dead registers (a[i], i >= 16 - q) read those zeros, so every update is unconditional
   // straight-line code the compiler can schedule as one batch of loads + DFMAs
-  __shared__ double2 prow[2][2 * DI_MAX];
+  __shared__ __align__(16) double2 prow[2][2 * DI_MAX];
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
   const int row = tid >> 2, cg = tid & 3;
   prow[tid >> 7][tid & 127] = make_double2(0, 0);
+  const unsigned base = (unsigned)__cvta_generic_to_shared(&prow[0][0]);
+  constexpr unsigned BUF = 2 * DI_MAX * 16;  // bytes per pivot-row buffer
   cplx a[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -574,15 +576,16 @@ __global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* s
   __syncthreads();
 #pragma unroll 1
   for (int q = 0; q < 16; ++q) {
+    const unsigned qb = base + (unsigned)(cg + 4 * q) * 16u;  // &prow[0][cg + 4q]
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
       const int j = 4 * q + jj;
-      double2* pr = prow[jj & 1];
+      const unsigned pb = qb + (jj & 1) * BUF;
       if (row == j) {
         // entries left of j in the first register are stale multipliers: publish only c >= j
-        if (cg >= jj) st(&pr[cg + 4 * q], a[0]);
+        if (cg >= jj) sts2(pb, a[0]);
 #pragma unroll
-        for (int i = 1; i < 16; ++i) st(&pr[cg + 4 * (q + i)], a[i]);  // dead registers are zero
+        for (int i = 1; i < 16; ++i) sts2(pb + 64u * i, a[i]);  // dead registers are zero
         if (cg == jj && a[0].re == 0.0 && a[0].im == 0.0) *sing = 1;
       }
       __syncthreads();
@@ -591,10 +594,10 @@ __global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* s
       aj.re = __shfl_sync(0xffffffffu, a[0].re, src);
       aj.im = __shfl_sync(0xffffffffu, a[0].im, src);
       if (row > j) {
-        const cplx l = cmul(aj, crcp_fast(ld(&pr[j])));
-        const cplx a0 = cfms(a[0], l, ld(&pr[cg + 4 * q]));
+        const cplx l = cmul(aj, crcp_fast(lds2(base + (jj & 1) * BUF + (unsigned)j * 16u)));
+        const cplx a0 = cfms(a[0], l, lds2(pb));
 #pragma unroll
-        for (int i = 1; i < 16; ++i) a[i] = cfms(a[i], l, ld(&pr[cg + 4 * (q + i)]));
+        for (int i = 1; i < 16; ++i) a[i] = cfms(a[i], l, lds2(pb + 64u * i));
         a[0] = cg == jj ? l : (cg > jj ? a0 : a[0]);
       }
     }

@@ -42,3 +42,14 @@ def test_action_complex_and_real():
     got = matexp_action(HermitianMatrix(Ar), V, ExpOptions(n=20, mode="action")).value
     for j in range(4):
         assert rel(got[:, j], restate.run_tasks_dense(Ar, V[:, j], 20)) <= TOL
+
+
+@pytest.mark.parametrize("d", [577, 777])
+def test_full_real_symmetric_inverse(d):
+    # real A: the inverse of A + theta I is complex symmetric, only its lower triangle is
+    # computed and the combine mirrors it -> exp(A) comes out exactly symmetric
+    A, _, _ = workloads.random_real_symmetric(d, -50.0, 0.0, seed=d)
+    got = matexp_full(HermitianMatrix(A), ExpOptions(n=20)).value
+    assert got.dtype == np.float64
+    assert rel(got, restate.run_tasks_dense(A, None, 20, threads=8)) <= TOL
+    assert np.array_equal(got, got.T)

@@ -11,10 +11,11 @@ using namespace pfx;
 // ---- ablation copies of zgetrf_diag_kernel (MODE 0 full, 1 no row updates, 2 barriers only)
 template <int MODE>
 __global__ void __launch_bounds__(256) lu_var(int nb, ZMat D, int* sing, long long* clk) {
-  __shared__ double2 prow[2][64];
+  __shared__ double2 prow[2][128];
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
   const int row = tid >> 2, cg = tid & 3;
+  prow[tid >> 7][tid & 127] = make_double2(0, 0);
   long long t0 = clock64();
   cplx a[16];
 #pragma unroll
@@ -23,10 +24,10 @@ __global__ void __launch_bounds__(256) lu_var(int nb, ZMat D, int* sing, long lo
     if (row < nb && c < nb) a[i] = ld(D.at(b, row, c));
     else a[i] = mk(row == c ? 1.0 : 0.0, 0.0);
   }
+  __syncthreads();
   long long t1 = clock64();
 #pragma unroll 1
   for (int q = 0; q < 16; ++q) {
-    const int nq = 16 - q;
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
       const int j = 4 * q + jj;
@@ -34,8 +35,7 @@ __global__ void __launch_bounds__(256) lu_var(int nb, ZMat D, int* sing, long lo
       if (row == j) {
         if (cg >= jj) st(&pr[cg + 4 * q], a[0]);
 #pragma unroll
-        for (int i = 1; i < 16; ++i)
-          if (i < nq) st(&pr[cg + 4 * (q + i)], a[i]);
+        for (int i = 1; i < 16; ++i) st(&pr[cg + 4 * (q + i)], a[i]);
       }
       __syncthreads();
       if (MODE == 2) continue;
@@ -43,15 +43,82 @@ __global__ void __launch_bounds__(256) lu_var(int nb, ZMat D, int* sing, long lo
       cplx aj;
       aj.re = __shfl_sync(0xffffffffu, a[0].re, src);
       aj.im = __shfl_sync(0xffffffffu, a[0].im, src);
-      if (row > j) {
-        const cplx l = cmul(aj, crcp_fast(ld(&pr[j])));
-        if (MODE == 0) {
-          if (cg > jj) a[0] = cfms(a[0], l, ld(&pr[cg + 4 * q]));
+      if (MODE == 3) aj = a[0];
+      if (MODE >= 5) {
+        // branch-free: rows <= j get a zero multiplier (their update is a no-op)
+        const bool below = row > j;
+        cplx l = cmul(aj, crcp_fast(ld(&pr[j])));
+        const cplx lz = below ? l : mk(0, 0);
+        const cplx a0 = cfms(a[0], lz, ld(&pr[cg + 4 * q]));
+        if (MODE == 5) {
 #pragma unroll
-          for (int i = 1; i < 16; ++i)
-            if (i < nq) a[i] = cfms(a[i], l, ld(&pr[cg + 4 * (q + i)]));
+          for (int i = 1; i < 16; ++i) a[i] = cfms(a[i], lz, ld(&pr[cg + 4 * (q + i)]));
         }
-        if (cg == jj) a[0] = l;
+        a[0] = (below && cg == jj) ? l : (cg > jj ? a0 : a[0]);
+      } else if (row > j) {
+        const cplx l = MODE == 4 ? cmul(aj, ld(&pr[j])) : cmul(aj, crcp_fast(ld(&pr[j])));
+        cplx a0 = a[0];
+        if (MODE == 0) {
+          a0 = cfms(a[0], l, ld(&pr[cg + 4 * q]));
+#pragma unroll
+          for (int i = 1; i < 16; ++i) a[i] = cfms(a[i], l, ld(&pr[cg + 4 * (q + i)]));
+        }
+        a[0] = cg == jj ? l : (cg > jj ? a0 : a[0]);
+      }
+    }
+    const int c = cg + 4 * q;
+    if (row < nb && c < nb) *D.at(b, row, c) = make_double2(a[0].re, a[0].im);
+#pragma unroll
+    for (int i = 0; i < 15; ++i) a[i] = a[i + 1];
+    a[15] = mk(0, 0);
+  }
+  long long t2 = clock64();
+  if (tid == 0 && b == 0) { clk[0] = t1 - t0; clk[1] = t2 - t1; }
+}
+
+
+// MODE 0 with explicit 32-bit shared addressing
+__global__ void __launch_bounds__(256) lu_sh(int nb, ZMat D, int* sing, long long* clk) {
+  __shared__ __align__(16) double2 prow[2][128];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int row = tid >> 2, cg = tid & 3;
+  prow[tid >> 7][tid & 127] = make_double2(0, 0);
+  const unsigned base = (unsigned)__cvta_generic_to_shared(&prow[0][0]);
+  long long t0 = clock64();
+  cplx a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int c = cg + 4 * i;
+    if (row < nb && c < nb) a[i] = ld(D.at(b, row, c));
+    else a[i] = mk(row == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+#pragma unroll 1
+  for (int q = 0; q < 16; ++q) {
+    const unsigned qb = base + (unsigned)(cg + 4 * q) * 16u;  // &pr[cg + 4q] in buffer 0
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * q + jj;
+      const unsigned pb = qb + (jj & 1) * 128u * 16u;
+      if (row == j) {
+        if (cg >= jj) sts2(pb, a[0]);
+#pragma unroll
+        for (int i = 1; i < 16; ++i) sts2(pb + 64u * i, a[i]);
+      }
+      __syncthreads();
+      const int src = (lane & ~3) | jj;
+      cplx aj;
+      aj.re = __shfl_sync(0xffffffffu, a[0].re, src);
+      aj.im = __shfl_sync(0xffffffffu, a[0].im, src);
+      if (row > j) {
+        const cplx piv = lds2(base + (jj & 1) * 128u * 16u + (unsigned)j * 16u);
+        const cplx l = cmul(aj, crcp_fast(piv));
+        const cplx a0 = cfms(a[0], l, lds2(pb));
+#pragma unroll
+        for (int i = 1; i < 16; ++i) a[i] = cfms(a[i], l, lds2(pb + 64u * i));
+        a[0] = cg == jj ? l : (cg > jj ? a0 : a[0]);
       }
     }
     const int c = cg + 4 * q;
@@ -164,6 +231,16 @@ int main() {
   timeit("lu_var<0> full", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_var<0><<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
   cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
   timeit("lu_var<1> no update", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_var<1><<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
+  cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
+  timeit("lu_var<3> no upd, no shfl", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_var<3><<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
+  cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
+  timeit("lu_var<4> no upd, no rcp", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_var<4><<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
+  cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
+  timeit("lu_var<5> full branch-free", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_var<5><<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
+  cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
+  timeit("lu_var<6> no upd branch-free", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_var<6><<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
+  cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
+  timeit("lu_sh explicit shared", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_sh<<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
   cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
   timeit("lu_var<2> barriers", [&] { cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s); lu_var<2><<<batch, 256, 0, s>>>(nb, Dm, sing, clk); });
   cudaDeviceSynchronize(); printf("   clk load %lld loop %lld\n", clk[0], clk[1]);
