@@ -107,48 +107,93 @@ __device__ __forceinline__ M22 mident() { return M22{mk(1, 0), mk(0, 0), mk(0, 0
 // ---------------------------------------------------------------------------
 // K_T1: transfer matrices.  Forward: (u_i; 1) ~ [b_i, -e_{i-1}^2; 1, 0] (u_{i-1}; 1).
 // Backward: (u'_i; 1) ~ [b_i, -e_i^2; 1, 0] (u'_{i+1}; 1).
+constexpr int TR_SEG = 4;  // row segments per (chunk, shift) in tri_mobius_chunks
+
+__device__ __forceinline__ M22 shfl_m22(const M22& m, int src) {
+  M22 r;
+  const cplx* in = &m.m0;
+  cplx* o = &r.m0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    o[t].re = __shfl_sync(0xffffffffu, in[t].re, src);
+    o[t].im = __shfl_sync(0xffffffffu, in[t].im, src);
+  }
+  return r;
+}
+
+// One thread per (chunk, shift, 64-row segment); both directions from the same row loads:
+// forward T <- M_i T (rows ascending), backward T' <- T' M'_i (rows ascending, i.e. the
+// product M'_lo ... M'_hi that the descending recurrence applies).  The TR_SEG segment
+// transfers of a (chunk, shift) sit in adjacent lanes and are combined by shuffles.
 __global__ void __launch_bounds__(128) tri_mobius_chunks(TriArgs a) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)a.P * a.npairs * 2;
-  if (tid >= total) return;
-  const int dir = (int)(tid & 1);
-  const int64_t ck = tid >> 1;
+  const int64_t total = (int64_t)a.P * a.npairs * TR_SEG;
+  const bool live = tid < total;
+  const int seg = (int)(tid & (TR_SEG - 1));
+  const int64_t ck = live ? tid / TR_SEG : 0;
   const int k = (int)(ck % a.npairs);
   const int64_t cidx = ck / a.npairs;
   const int64_t s = cidx * TR_L, e = (s + TR_L < a.N ? s + TR_L : a.N);
-  const int rows = (int)(e - s);
+  constexpr int SL = TR_L / TR_SEG;
+  const int64_t s0 = s + (int64_t)seg * SL;
+  const int64_t rem = e - s0;
+  const int rows = (!live || rem <= 0) ? 0 : (rem < SL ? (int)rem : SL);
   const cplx th = ld(&a.theta[k]);
-  M22 T = mident();
-  // rows in processing order, 8 per batch with the loads issued ahead of the product chain
+  M22 F = mident(), B = mident();
   for (int i0 = 0; i0 < rows; i0 += 8) {
-    double bre[8], e2v[8];
+    double bre[8], e2[9];  // e2[u] = e_{i-1}^2 for row i = s0 + i0 + u; e2[u + 1] = e_i^2
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int ii = i0 + u;
-      const int64_t i = dir == 0 ? s + ii : e - 1 - ii;
-      const bool v = ii < rows;
-      bre[u] = v ? a.diag[i] - a.c + th.re : 0.0;
-      e2v[u] = v ? off2(a.off, a.N, dir == 0 ? i - 1 : i) : 0.0;
-    }
+    for (int u = 0; u < 8; ++u) bre[u] = (i0 + u < rows) ? a.diag[s0 + i0 + u] - a.c + th.re : 0.0;
+#pragma unroll
+    for (int u = 0; u < 9; ++u) e2[u] = (i0 + u <= rows) ? off2(a.off, a.N, s0 + i0 + u - 1) : 0.0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (i0 + u < rows) {
         const cplx b = mk(bre[u], th.im);
-        M22 r;
-        r.m0 = csub(cmul(b, T.m0), cscale(T.m2, e2v[u]));
-        r.m1 = csub(cmul(b, T.m1), cscale(T.m3, e2v[u]));
-        r.m2 = T.m0;
-        r.m3 = T.m1;
-        T = r;
+        // forward: [b, -e_{i-1}^2; 1, 0] F
+        const cplx f0 = csub(cmul(b, F.m0), cscale(F.m2, e2[u]));
+        const cplx f1 = csub(cmul(b, F.m1), cscale(F.m3, e2[u]));
+        F.m2 = F.m0;
+        F.m3 = F.m1;
+        F.m0 = f0;
+        F.m1 = f1;
+        // backward: B [b, -e_i^2; 1, 0]
+        const cplx g0 = cadd(cmul(B.m0, b), B.m1);
+        const cplx g2 = cadd(cmul(B.m2, b), B.m3);
+        B.m1 = cscale(B.m0, -e2[u + 1]);
+        B.m3 = cscale(B.m2, -e2[u + 1]);
+        B.m0 = g0;
+        B.m2 = g2;
       }
     }
-    mnorm(T);
+    mnorm(F);
+    mnorm(B);
   }
-  double2* dst = (dir == 0 ? a.Tf : a.Tb) + ck * 4;
-  st(&dst[0], T.m0);
-  st(&dst[1], T.m1);
-  st(&dst[2], T.m2);
-  st(&dst[3], T.m3);
+  // combine segments: forward F = F3 F2 F1 F0, backward B = B0 B1 B2 B3
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int w = 1; w < TR_SEG; w <<= 1) {
+    const M22 Fp = shfl_m22(F, lane + w < 32 ? lane + w : lane);
+    const M22 Bp = shfl_m22(B, lane + w < 32 ? lane + w : lane);
+    if ((seg & (2 * w - 1)) == 0) {
+      F = mmul(Fp, F);
+      B = mmul(B, Bp);
+      mnorm(F);
+      mnorm(B);
+    }
+  }
+  if (live && seg == 0) {
+    double2* df = a.Tf + ck * 4;
+    double2* db = a.Tb + ck * 4;
+    st(&df[0], F.m0);
+    st(&df[1], F.m1);
+    st(&df[2], F.m2);
+    st(&df[3], F.m3);
+    st(&db[0], B.m0);
+    st(&db[1], B.m1);
+    st(&db[2], B.m2);
+    st(&db[3], B.m3);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -302,9 +347,11 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
 //     the chunk top) and Lambda'_i (backward, from the chunk bottom).  In a contractive
 //     chunk (all |l|, |l'| <= 1) |Lambda| never grows, and |w| <= 2|a|/Im(theta) (the
 //     pivots of T + theta I satisfy |gamma| >= Im(theta)), so once
-//     sum_k (2|a_k|/Im theta_k) |Lambda_k| |G_k| <= 2^-60 max|V[:, r]| every remaining
-//     row's correction is below that bound and the pass stops (exact to far below
-//     binary64 rounding of the result; full pass for non-contractive chunks).
+//     sum_k (2|a_k|/Im theta_k) |Lambda_k| |G_k| <= 2^-53 max|V[:, r]| every remaining
+//     row's correction is below one unit roundoff of max|V[:, r]| and the pass stops
+//     (below the binary64 rounding of the 2n-term pole sum itself; full pass for
+//     non-contractive chunks).
+constexpr int TR_FIX_EXP = 53;     // fix-pass stop: remaining correction <= 2^-53 max|V|
 constexpr int TR_T = 8;            // rows per staged tile
 constexpr int TR_SW_WARPS = 4;     // warps per block
 
@@ -358,7 +405,7 @@ __global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_pass(TriArgs a) {
   bool contr = false;
   double beta[KM];
   if (MODE == 1) {
-    tau = rv ? ldexp(__longlong_as_double((long long)a.vmax[r]), -60) : 1.0;
+    tau = rv ? ldexp(__longlong_as_double((long long)a.vmax[r]), -TR_FIX_EXP) : 1.0;
     contr = a.contr[c] != 0;
 #pragma unroll
     for (int k = 0; k < KM; ++k) {
@@ -605,7 +652,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
   {
-    int64_t th = (int64_t)P * npairs * 2;
+    int64_t th = (int64_t)P * npairs * TR_SEG;
     PFX_LAUNCH("tri_mobius_chunks", stream, tri_mobius_chunks<<<(unsigned)ceil_div(th, 128), 128, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
     PFX_LAUNCH("tri_mobius_scan", stream, tri_mobius_scan<<<npairs * 2, TR_SCAN_T, 0, stream>>>(a));

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   LsCk* ckf = ck.ckf + (c * LS_NBLK) * 16;
   bool noncontr = false;
   double vmx = 0.0;
-  const double tau = (MODE == 1 && rv) ? ldexp(__longlong_as_double((long long)a.vmax[rg]), -60) : 0.0;
+  const double tau = (MODE == 1 && rv) ? ldexp(__longlong_as_double((long long)a.vmax[rg]), -TR_FIX_EXP) : 0.0;
   const bool contr = MODE == 1 ? a.contr[c] != 0 : false;
   auto blk_r0 = [&](int b) { return s + (int64_t)b * LS_B; };
   auto blk_cnt = [&](int b) { return min(LS_B, rows - b * LS_B); };
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
       }
       __syncwarp(hmask);
       if (MODE == 1) {
-        // stop once every remaining correction is below 2^-60 max|V[:, r]| (contractive chunks)
+        // stop once every remaining correction is below 2^-53 max|V[:, r]| (contractive chunks)
         double y = 0.0;
         if (rv) {
 #pragma unroll
