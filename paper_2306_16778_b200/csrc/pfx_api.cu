@@ -24,7 +24,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
                     double* out, cudaStream_t stream, float* per_pair_ms);
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
-                float* launch_ms);
+                float* launch_ms, const double* V_host = nullptr, double* out_host = nullptr);
 int banded_run(const double* band, int64_t N, int64_t kb, const double* V, int64_t nrhs, double shift_c,
                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                float* per_pair_ms);
@@ -318,22 +318,32 @@ int pfx_expm_tridiag(int mem, const double* diag, const double* off, int64_t N, 
   const double2 *th = nullptr, *co = nullptr;
   if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
   const double *Dd = nullptr, *Od_ = nullptr, *Vd = nullptr;
+  const size_t vbytes = (size_t)N * nrhs * sizeof(double);
+  // host mode on the on-chip path (npairs <= 16): V and out move in row groups overlapped
+  // with the sweeps / fixes (tridiag_run); otherwise staged whole
+  const bool pipe = mem == PFX_MEM_HOST && npairs <= 16;
   if ((rc = stage_in(mem, 3, diag, N * sizeof(double), stream, &Dd))) return rc;
   if ((rc = stage_in(mem, 4, off, (N - 1) * sizeof(double), stream, &Od_))) return rc;
-  if ((rc = stage_in(mem, 5, V, (size_t)N * nrhs * sizeof(double), stream, &Vd))) return rc;
+  if (pipe) {
+    Vd = static_cast<const double*>(scratch(5, vbytes));
+    if (!Vd) return fail(PFX_CUDA, "staging allocation failed");
+  } else if ((rc = stage_in(mem, 5, V, vbytes, stream, &Vd))) {
+    return rc;
+  }
   double* Out = out;
-  const size_t obytes = (size_t)N * nrhs * sizeof(double);
+  const size_t obytes = vbytes;
   if (mem == PFX_MEM_HOST) {
     Out = static_cast<double*>(scratch(6, obytes));
     if (!Out) return fail(PFX_CUDA, "staging allocation failed");
   }
   float ms = 0.0f;
-  rc = tridiag_run(Dd, Od_, N, Vd, nrhs, shift_c, th, co, npairs, Out, stream, per_pair_ms ? &ms : nullptr);
+  rc = tridiag_run(Dd, Od_, N, Vd, nrhs, shift_c, th, co, npairs, Out, stream, per_pair_ms ? &ms : nullptr,
+                   pipe ? V : nullptr, pipe ? out : nullptr);
   if (rc) return rc;
   if (per_pair_ms)
     for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
   if (mem == PFX_MEM_HOST) {
-    PFX_CUDA_TRY(cudaMemcpyAsync(out, Out, obytes, cudaMemcpyDeviceToHost, stream));
+    if (!pipe) PFX_CUDA_TRY(cudaMemcpyAsync(out, Out, obytes, cudaMemcpyDeviceToHost, stream));
     PFX_CUDA_TRY(cudaStreamSynchronize(stream));
   }
   return PFX_OK;

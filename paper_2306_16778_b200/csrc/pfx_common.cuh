@@ -107,6 +107,12 @@ __device__ __forceinline__ cplx crcp_fast(cplx z) {
   return cplx{z.re * r, -z.im * r};
 }
 __device__ __forceinline__ cplx cdiv_fast(cplx a, cplx b) { return cmul(a, crcp_fast(b)); }
+// 1/z without the range guard: only for values known to be well inside the normal range
+// (rescaled continuants, shifted pivots with |z| >= Im(theta) > 0)
+__device__ __forceinline__ cplx crcp_nc(cplx z) {
+  const double r = frcp(fma(z.re, z.re, z.im * z.im));
+  return cplx{z.re * r, -z.im * r};
+}
 __host__ __device__ __forceinline__ double cabs1(cplx a) { return fabs(a.re) + fabs(a.im); }
 
 __device__ __forceinline__ cplx ld(const double2* p) {

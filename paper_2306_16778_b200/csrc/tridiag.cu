@@ -604,9 +604,45 @@ static int sweeps(const TriArgs& a, cudaStream_t stream, int which) {
   return launch_stream<32>(a, stream, which);
 }
 
+__global__ void scale_rows(double* x, int64_t n, double s) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    x[e] *= s;
+}
+
+namespace {
+constexpr int TR_GROUPS = 8;
+struct TriPipe {
+  cudaStream_t in = nullptr, outs = nullptr;
+  cudaStream_t cs[TR_GROUPS] = {};  // one compute stream per row group (sweeps must co-reside)
+  cudaEvent_t ev[4 * TR_GROUPS + 2] = {};
+};
+int tri_pipe(TriPipe& T) {
+  static TriPipe g;
+  if (!g.in) {
+    PFX_CUDA_TRY(cudaStreamCreateWithFlags(&g.in, cudaStreamNonBlocking));
+    PFX_CUDA_TRY(cudaStreamCreateWithFlags(&g.outs, cudaStreamNonBlocking));
+    // earlier row groups first: their results are the first to go back over PCIe
+    int lo = 0, hi = 0;
+    PFX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int i = 0; i < TR_GROUPS; ++i) {
+      const int pr = hi + (int)((int64_t)(lo - hi) * i / TR_GROUPS);
+      PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.cs[i], cudaStreamNonBlocking, pr));
+    }
+    for (auto& e : g.ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  T = g;
+  return PFX_OK;
+}
+}  // namespace
+
+// V_host / out_host (optional, host mode with npairs <= 16): V is copied into the device
+// buffer V in row groups on a copy stream, each group's sweep starts as soon as its rows
+// have landed, and each group's result goes back as soon as its edge fix is done, so the
+// PCIe transfers hide the compute (out is final only after the global carry scan, so the
+// H2D and D2H phases themselves cannot overlap).
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
-                float* launch_ms) {
+                float* launch_ms, const double* V_host, double* out_host) {
   const int P = (int)ceil_div(N, TR_L);
   const size_t nP = (size_t)P * npairs;
   const size_t nPR = nP * nrhs;
@@ -659,7 +695,9 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaGetLastError());
   }
   const bool ls = npairs <= 16;
-  LsArgs lsa{nullptr, nullptr};
+  const bool pipe = V_host != nullptr;
+  if (pipe && !ls) return fail(PFX_BADARG, "tridiag_run: host pipelining needs npairs <= 16");
+  LsArgs lsa{nullptr, nullptr, 0, 0};
   if (ls) {
     // checkpoints live in arena slot 2 (L2-resident: 2 x P x 32 x 16 x 32 B)
     const size_t ckn = (size_t)P * LS_NBLK * 16;
@@ -668,18 +706,115 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     lsa.ckb = ckbuf;
     lsa.ckf = ckbuf + ckn;
     const int ntile = (int)ceil_div(nrhs, 16);
-    const unsigned blocks = (unsigned)ceil_div((int64_t)P * ntile, LS_WARPS * 2);
     const int smem = (int)(sizeof(LsSmem) * LS_WARPS * 2);
     auto k0 = npairs <= 8 ? tri_ls<8, 0> : npairs <= 12 ? tri_ls<12, 0> : tri_ls<16, 0>;
     auto k1 = npairs <= 8 ? tri_ls<8, 1> : npairs <= 12 ? tri_ls<12, 1> : tri_ls<16, 1>;
     PFX_CUDA_TRY(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     PFX_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PFX_LAUNCH("tri_sweep", stream, (k0<<<blocks, LS_WARPS * 32, smem, stream>>>(a, lsa)));
-    PFX_CUDA_TRY(cudaGetLastError());
-    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
-    PFX_CUDA_TRY(cudaGetLastError());
-    PFX_LAUNCH("tri_fix", stream, (k1<<<blocks, LS_WARPS * 32, smem, stream>>>(a, lsa)));
-    PFX_CUDA_TRY(cudaGetLastError());
+    // row groups: whole chunks, one launch each (a single group in device mode)
+    const int ng = pipe ? (int)std::min<int64_t>(TR_GROUPS, P) : 1;
+    auto grp = [&](int g, int64_t& c0, int64_t& c1) {
+      c0 = (int64_t)P * g / ng;
+      c1 = (int64_t)P * (g + 1) / ng;
+    };
+    auto launch_ls = [&](bool fix, int64_t c0, int64_t c1, cudaStream_t st) -> int {
+      LsArgs la = lsa;
+      la.unit0 = c0 * ntile;
+      la.unit1 = c1 * ntile;
+      const unsigned blocks = (unsigned)ceil_div(la.unit1 - la.unit0, LS_WARPS * 2);
+      if (blocks == 0) return PFX_OK;
+      if (fix)
+        PFX_LAUNCH("tri_fix", st, (k1<<<blocks, LS_WARPS * 32, smem, st>>>(a, la)));
+      else
+        PFX_LAUNCH("tri_sweep", st, (k0<<<blocks, LS_WARPS * 32, smem, st>>>(a, la)));
+      PFX_CUDA_TRY(cudaGetLastError());
+      return PFX_OK;
+    };
+    if (!pipe) {
+      if (int rc = launch_ls(false, 0, P, stream)) return rc;
+      PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
+      PFX_CUDA_TRY(cudaGetLastError());
+      if (int rc = launch_ls(true, 0, P, stream)) return rc;
+    } else {
+      // events: [0, G) V group landed, [G, 2G) sweep done, [2G, 3G) result ready,
+      // 4G: fork point, 4G + 1: all copies back
+      TriPipe TP;
+      if (int rc = tri_pipe(TP)) return rc;
+      cudaEvent_t* ev = TP.ev;
+      const int G = TR_GROUPS;
+      static const bool tl = getenv("PFX_TRI_TIMELINE") != nullptr;
+      static cudaEvent_t tev[5 * TR_GROUPS + 2];
+      static bool tev_init = false;
+      if (tl && !tev_init) {
+        for (auto& e : tev) cudaEventCreate(&e);
+        tev_init = true;
+      }
+      if (tl) cudaEventRecord(tev[5 * G], stream);
+      // the copy-in starts at once: the staging buffers are idle on entry (every host-mode
+      // call ends synchronised) and V does not feed the Moebius kernels
+      PFX_CUDA_TRY(cudaEventRecord(ev[4 * G], stream));  // Moebius scan done
+      for (int g = 0; g < ng; ++g) {
+        int64_t c0, c1;
+        grp(g, c0, c1);
+        const int64_t r0 = c0 * TR_L, r1 = std::min<int64_t>(c1 * TR_L, N);
+        PFX_CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(V) + r0 * nrhs, V_host + r0 * nrhs,
+                                     (size_t)(r1 - r0) * nrhs * sizeof(double), cudaMemcpyHostToDevice, TP.in));
+        PFX_CUDA_TRY(cudaEventRecord(ev[g], TP.in));
+        if (tl) cudaEventRecord(tev[g], TP.in);
+      }
+      for (int g = 0; g < ng; ++g) {
+        int64_t c0, c1;
+        grp(g, c0, c1);
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[4 * G], 0));  // after the Moebius scan
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[g], 0));
+        if (int rc = launch_ls(false, c0, c1, TP.cs[g])) return rc;
+        PFX_CUDA_TRY(cudaEventRecord(ev[G + g], TP.cs[g]));
+        if (tl) cudaEventRecord(tev[G + g], TP.cs[g]);
+        PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[G + g], 0));
+      }
+      PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
+      PFX_CUDA_TRY(cudaGetLastError());
+      PFX_CUDA_TRY(cudaEventRecord(ev[4 * G], stream));  // carry scan done
+      if (tl) cudaEventRecord(tev[5 * G + 1], stream);
+      for (int g = 0; g < ng; ++g) {
+        int64_t c0, c1;
+        grp(g, c0, c1);
+        const int64_t r0 = c0 * TR_L, r1 = std::min<int64_t>(c1 * TR_L, N);
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[4 * G], 0));
+        if (int rc = launch_ls(true, c0, c1, TP.cs[g])) return rc;
+        if (shift_c != 0.0) {
+          PFX_LAUNCH("scale_kernel", TP.cs[g],
+                     scale_rows<<<296, 256, 0, TP.cs[g]>>>(out + r0 * nrhs, (r1 - r0) * nrhs, exp(shift_c)));
+          PFX_CUDA_TRY(cudaGetLastError());
+        }
+        PFX_CUDA_TRY(cudaEventRecord(ev[2 * G + g], TP.cs[g]));
+        if (tl) cudaEventRecord(tev[2 * G + g], TP.cs[g]);
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.outs, ev[2 * G + g], 0));
+        PFX_CUDA_TRY(cudaMemcpyAsync(out_host + r0 * nrhs, out + r0 * nrhs, (size_t)(r1 - r0) * nrhs * sizeof(double),
+                                     cudaMemcpyDeviceToHost, TP.outs));
+        if (tl) cudaEventRecord(tev[3 * G + g], TP.outs);
+      }
+      if (tl) {
+        cudaDeviceSynchronize();
+        auto at = [&](int i) {
+          float ms = 0;
+          cudaEventElapsedTime(&ms, tev[5 * G], tev[i]);
+          return ms;
+        };
+        fprintf(stderr, "[tri timeline ms] in:");
+        for (int g = 0; g < ng; ++g) fprintf(stderr, " %.2f", at(g));
+        fprintf(stderr, " | sweep:");
+        for (int g = 0; g < ng; ++g) fprintf(stderr, " %.2f", at(G + g));
+        fprintf(stderr, " | scan %.2f | fix:", at(5 * G + 1));
+        for (int g = 0; g < ng; ++g) fprintf(stderr, " %.2f", at(2 * G + g));
+        fprintf(stderr, " | out:");
+        for (int g = 0; g < ng; ++g) fprintf(stderr, " %.2f", at(3 * G + g));
+        fprintf(stderr, "\n");
+      }
+      PFX_CUDA_TRY(cudaEventRecord(ev[4 * G + 1], TP.outs));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[4 * G + 1], 0));
+      shift_c = 0.0;  // applied per group above
+    }
   } else {
     PFX_LAUNCH("tri_factor", stream, tri_factor<<<(unsigned)ceil_div((int64_t)P * npairs, 128), 128, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());

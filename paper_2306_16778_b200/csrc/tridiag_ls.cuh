@@ -74,7 +74,7 @@ __device__ __forceinline__ void ls_stage_async(LsBuf& B, const TriArgs& a, int64
 __device__ __forceinline__ cplx ls_bstep(const LsBuf& S, double cshift, int j, int64_t row, cplx th, cplx& q1,
                                          cplx& q2) {
   const double e = S.of[j + 1];
-  const cplx rho = cmul(q2, crcp_fast(q1));
+  const cplx rho = cmul(q2, crcp_nc(q1));  // q1: rescaled continuant, |q1| >= Im(theta) |q2|
   const cplx lv = cscale(rho, e);
   const cplx b = mk(S.dg[j] - cshift + th.re, th.im);
   const double e2 = e * e;
@@ -88,7 +88,7 @@ __device__ __forceinline__ cplx ls_bstep(const LsBuf& S, double cshift, int j, i
 __device__ __forceinline__ cplx ls_fstep(const LsBuf& S, double cshift, int j, int64_t row, cplx th, cplx& p1,
                                          cplx& p2) {
   const double e0 = S.of[j];
-  const cplx rho = cmul(p2, crcp_fast(p1));
+  const cplx rho = cmul(p2, crcp_nc(p1));
   const cplx lv = cscale(rho, e0);
   const cplx b = mk(S.dg[j] - cshift + th.re, th.im);
   const double e2 = e0 * e0;
@@ -102,6 +102,7 @@ __device__ __forceinline__ cplx ls_fstep(const LsBuf& S, double cshift, int j, i
 struct LsArgs {
   LsCk* ckb;  // P x LS_NBLK x 16
   LsCk* ckf;  // P x LS_NBLK x 16
+  int64_t unit0, unit1;  // units [unit0, unit1) of this launch (row-group pipelining)
 };
 
 // MODE 0: main sweeps.  MODE 1: edge fix with the true carries.
@@ -116,8 +117,8 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
   LsSmem& S = reinterpret_cast<LsSmem*>(smem_raw)[warp * 2 + half];
   const int ntile = (a.nrhs + 15) / 16;
-  const int64_t unit = (blockIdx.x * (int64_t)LS_WARPS + warp) * 2 + half;
-  if (unit >= (int64_t)a.P * ntile) return;
+  const int64_t unit = ck.unit0 + (blockIdx.x * (int64_t)LS_WARPS + warp) * 2 + half;
+  if (unit >= ck.unit1) return;
   const int64_t c = unit / ntile;
   const int rt0 = (int)(unit - c * ntile) * 16;
   const int np = a.npairs;
@@ -137,6 +138,11 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   double vmx = 0.0;
   const double tau = (MODE == 1 && rv) ? ldexp(__longlong_as_double((long long)a.vmax[rg]), -TR_FIX_EXP) : 0.0;
   const bool contr = MODE == 1 ? a.contr[c] != 0 : false;
+  if (!act) {  // padded pair slots (k >= np) stay zero: phase B adds exact zeros for them
+#pragma unroll
+    for (int j = 0; j < LS_B; ++j) S.fw[j][k][0] = S.fw[j][k][1] = make_double2(0, 0);
+    S.lamabs[k] = 0.0;
+  }
   auto blk_r0 = [&](int b) { return s + (int64_t)b * LS_B; };
   auto blk_cnt = [&](int b) { return min(LS_B, rows - b * LS_B); };
 
@@ -223,7 +229,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
               const cplx lbv = ld(&S.fw[j][k][0]);
               const cplx bd = mk(B.dg[j] - csh + th.re, th.im);
               const cplx gam = csub(csub(bd, cscale(lv, B.of[j])), cscale(lbv, B.of[j + 1]));
-              cplx w = cdiv_fast(co2, gam);
+              cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
               lam = cmul(lam, mk(-lv.re, -lv.im));
               if (MODE == 0 && fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
               if (MODE == 1) w = cmul(w, lam);
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
               const cplx lv = ld(&S.fw[j][k][0]);
               const cplx bd = mk(B.dg[j] - csh + th.re, th.im);
               const cplx gam = csub(csub(bd, cscale(lv, B.of[j])), cscale(lbv, B.of[j + 1]));
-              cplx w = cdiv_fast(co2, gam);
+              cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
               lam = cmul(lam, mk(-lbv.re, -lbv.im));
               if (MODE == 1) w = cmul(w, lam);
               S.fw[j][k][0] = make_double2(lbv.re, lbv.im);
@@ -275,24 +281,16 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
             vmx = fmax(vmx, fabs(f));
 #pragma unroll
             for (int q = 0; q < KM; ++q) {
-              if (q < np) {
-                const double2 l2 = S.fw[j][q][0], w2 = S.fw[j][q][1];
-                g[q] = cplx{fma(-l2.x, g[q].re, fma(l2.y, g[q].im, f)), fma(-l2.x, g[q].im, -l2.y * g[q].re)};
-                const double gre = dir == 0 ? g[q].re - f : g[q].re;
-                t[q] = fma(w2.x, gre, -w2.y * g[q].im);
-              } else {
-                t[q] = 0.0;
-              }
+              const double2 l2 = S.fw[j][q][0], w2 = S.fw[j][q][1];
+              g[q] = cplx{fma(-l2.x, g[q].re, fma(l2.y, g[q].im, f)), fma(-l2.x, g[q].im, -l2.y * g[q].re)};
+              const double gre = dir == 0 ? g[q].re - f : g[q].re;
+              t[q] = fma(w2.x, gre, -w2.y * g[q].im);
             }
           } else {
 #pragma unroll
             for (int q = 0; q < KM; ++q) {
-              if (q < np) {
-                const double2 w2 = S.fw[j][q][1];  // w * Lambda
-                t[q] = fma(w2.x, g[q].re, -w2.y * g[q].im);
-              } else {
-                t[q] = 0.0;
-              }
+              const double2 w2 = S.fw[j][q][1];  // w * Lambda (zero for padded pairs)
+              t[q] = fma(w2.x, g[q].re, -w2.y * g[q].im);
             }
           }
 #pragma unroll
@@ -316,7 +314,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
         if (rv) {
 #pragma unroll
           for (int q = 0; q < KM; ++q)
-            if (q < np) y = fma(S.lamabs[q], cabs1(g[q]), y);
+            y = fma(S.lamabs[q], cabs1(g[q]), y);
           y = tau > 0.0 ? y / tau : (y > 0.0 ? INFINITY : 0.0);
         }
         for (int off = 8; off > 0; off >>= 1) y = fmax(y, __shfl_xor_sync(hmask, y, off));

@@ -75,3 +75,17 @@ def test_c2_full_size_properties():
     assert rel(got[:, cols], want) <= TOL
     E = closed.dst_exp_lap1d(N, 25.0, V[:, cols])
     assert np.linalg.norm(got[:, cols] - E) <= 10 * np.linalg.norm(want - E)
+
+
+def test_shift_many_groups_ragged_tiles():
+    # host-mode pipelining: 8 row groups (N = 40 chunks), per-group e^c scaling, 2 RHS tiles
+    N, nrhs = 10007, 21
+    d, o = workloads.c2_matrix(N, scale=1.0)
+    d = d + 2.0
+    V = np.random.default_rng(11).standard_normal((N, nrhs))
+    T = TridiagonalHermitian(d, o)
+    res = matexp_shifted(T, ExpOptions(n=24, mode="action", shift="auto"), v=V)
+    c = res.c_applied
+    assert c != 0.0
+    want = np.exp(c) * restate.tridiag_action(d - c, o, V, 24)
+    assert rel(res.value, want) <= TOL
