@@ -81,7 +81,7 @@ __device__ __forceinline__ cplx ls_bstep(const LsBuf& S, double cshift, int j, i
   const cplx q0 = cplx{fma(b.re, q1.re, fma(-b.im, q1.im, -e2 * q2.re)), fma(b.re, q1.im, fma(b.im, q1.re, -e2 * q2.im))};
   q2 = q1;
   q1 = q0;
-  if ((row & 3) == 0) rescale2(q1, q2);
+  if ((row & 7) == 0) rescale2(q1, q2);  // growth over 8 rows stays far inside binary64
   return lv;
 }
 
@@ -95,7 +95,7 @@ __device__ __forceinline__ cplx ls_fstep(const LsBuf& S, double cshift, int j, i
   const cplx p0 = cplx{fma(b.re, p1.re, fma(-b.im, p1.im, -e2 * p2.re)), fma(b.re, p1.im, fma(b.im, p1.re, -e2 * p2.im))};
   p2 = p1;
   p1 = p0;
-  if ((row & 3) == 3) rescale2(p1, p2);
+  if ((row & 7) == 7) rescale2(p1, p2);
   return lv;
 }
 
@@ -270,36 +270,37 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
 #if defined(PFX_TRI_EXP) && PFX_TRI_EXP == 1
       if (bb < 0)  // timing ablation: no RHS sweep
 #endif
+      double* const obase = a.out + r0 * a.nrhs + rg;
 #pragma unroll
       for (int jj = 0; jj < LS_B; ++jj) {
         if (jj < cnt) {
           const int j = dir == 0 ? jj : cnt - 1 - jj;
-          const int64_t row = r0 + j;
-          double t[KM];
+          // sum over pairs: two interleaved FMA chains (even / odd pairs), fixed order
+          double acc0 = 0.0, acc1 = 0.0;
           if (MODE == 0) {
             const double f = B.f[j][k];
-            vmx = fmax(vmx, fabs(f));
+            if (dir == 0) vmx = fmax(vmx, fabs(f));
 #pragma unroll
             for (int q = 0; q < KM; ++q) {
               const double2 l2 = S.fw[j][q][0], w2 = S.fw[j][q][1];
               g[q] = cplx{fma(-l2.x, g[q].re, fma(l2.y, g[q].im, f)), fma(-l2.x, g[q].im, -l2.y * g[q].re)};
               const double gre = dir == 0 ? g[q].re - f : g[q].re;
-              t[q] = fma(w2.x, gre, -w2.y * g[q].im);
+              double& acc = (q & 1) ? acc1 : acc0;
+              acc = fma(w2.x, gre, acc);
+              acc = fma(-w2.y, g[q].im, acc);
             }
           } else {
 #pragma unroll
             for (int q = 0; q < KM; ++q) {
               const double2 w2 = S.fw[j][q][1];  // w * Lambda (zero for padded pairs)
-              t[q] = fma(w2.x, g[q].re, -w2.y * g[q].im);
+              double& acc = (q & 1) ? acc1 : acc0;
+              acc = fma(w2.x, g[q].re, acc);
+              acc = fma(-w2.y, g[q].im, acc);
             }
           }
-#pragma unroll
-          for (int w = 1; w < KM; w <<= 1)
-#pragma unroll
-            for (int q = 0; q + w < KM; q += 2 * w) t[q] += t[q + w];
-          const double acc = t[0];
+          const double acc = acc0 + acc1;
           if (rv) {
-            double* o = &a.out[row * a.nrhs + rg];
+            double* o = obase + j * a.nrhs;
             if (MODE == 0 && dir == 0)
               *o = acc;
             else

@@ -29,7 +29,11 @@ def num(x):
         return 0
 
 
-data = [(num(r[ie]), num(r[iw])) for r in rows[hi + 1:] if len(r) > ie]
+data = []
+for r in rows[hi + 1:]:
+    if not r or not r[0].startswith("0x"):  # next section (another function) starts
+        break
+    data.append((num(r[ie]), num(r[iw])))
 print("sass instructions", len(lines), "ncu rows", len(data))
 agg = collections.defaultdict(lambda: [0, 0])
 for (ins, st), ln in zip(data, lines):
