@@ -613,7 +613,8 @@ namespace {
 constexpr int TR_GROUPS = 8;
 struct TriPipe {
   cudaStream_t in = nullptr, outs = nullptr;
-  cudaStream_t cs[TR_GROUPS] = {};  // one compute stream per row group (sweeps must co-reside)
+  cudaStream_t cs[TR_GROUPS] = {};  // per-group fix streams: earlier groups first (D2H order)
+  cudaStream_t sw[TR_GROUPS] = {};  // per-group sweep streams: later groups first (their rows land last)
   cudaEvent_t ev[4 * TR_GROUPS + 2] = {};
 };
 int tri_pipe(TriPipe& T) {
@@ -621,12 +622,14 @@ int tri_pipe(TriPipe& T) {
   if (!g.in) {
     PFX_CUDA_TRY(cudaStreamCreateWithFlags(&g.in, cudaStreamNonBlocking));
     PFX_CUDA_TRY(cudaStreamCreateWithFlags(&g.outs, cudaStreamNonBlocking));
-    // earlier row groups first: their results are the first to go back over PCIe
+    // sweeps: the last-arriving rows are on the critical path -> later groups higher
+    // priority; fixes: earlier groups go back over PCIe first -> earlier groups higher
     int lo = 0, hi = 0;
     PFX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     for (int i = 0; i < TR_GROUPS; ++i) {
       const int pr = hi + (int)((int64_t)(lo - hi) * i / TR_GROUPS);
       PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.cs[i], cudaStreamNonBlocking, pr));
+      PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.sw[TR_GROUPS - 1 - i], cudaStreamNonBlocking, pr));
     }
     for (auto& e : g.ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -765,11 +768,11 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       for (int g = 0; g < ng; ++g) {
         int64_t c0, c1;
         grp(g, c0, c1);
-        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[4 * G], 0));  // after the Moebius scan
-        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[g], 0));
-        if (int rc = launch_ls(false, c0, c1, TP.cs[g])) return rc;
-        PFX_CUDA_TRY(cudaEventRecord(ev[G + g], TP.cs[g]));
-        if (tl) cudaEventRecord(tev[G + g], TP.cs[g]);
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.sw[g], ev[4 * G], 0));  // after the Moebius scan
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.sw[g], ev[g], 0));
+        if (int rc = launch_ls(false, c0, c1, TP.sw[g])) return rc;
+        PFX_CUDA_TRY(cudaEventRecord(ev[G + g], TP.sw[g]));
+        if (tl) cudaEventRecord(tev[G + g], TP.sw[g]);
         PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[G + g], 0));
       }
       PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
