@@ -152,3 +152,16 @@ def test_no_cpu_fallback_without_gpu():
     A = HermitianMatrix(-np.eye(4))
     with pytest.raises(PfexpmError, match="no CUDA device"):
         matexp_action(A, np.ones(4), ExpOptions(mode="action"))
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    # the product path has no CPU fallback: without libpfx.so every entry raises
+    from paper_2306_16778_b200 import _native
+
+    monkeypatch.setattr(_native, "LIB_PATH", str(tmp_path / "absent" / "libpfx.so"))
+    monkeypatch.setattr(_native, "_lib", None)
+    with pytest.raises(PfexpmError, match="missing"):
+        _native.lib()
+    assert not _native.available()
+    with pytest.raises(PfexpmError):
+        matexp_action(HermitianMatrix(-np.eye(4)), np.ones(4), ExpOptions(mode="action"))
