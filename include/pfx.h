@@ -84,10 +84,12 @@ int pfx_pole_table(int n, double* theta2, double* coef2);
  *        (V = I, out is batch x d x d).
  *   out  batch x d x (nrhs or d); complex iff out_complex.  out_complex must
  *        equal !(real path) as defined above (engine.py:185), else PFX_BADARG.
- * d <= 512: partial pivoting (LAPACK getrf semantics).  d > 512: blocked LU
- * without pivoting, which relies on A being Hermitian (every pivot of A + theta I
- * then has |Im| >= Im theta > 0); for real A in full mode the inverse is taken
- * as complex symmetric (lower triangle computed, mirrored in the combine).
+ * A must be Hermitian: every pivot of A + theta I then has |Im| >= Im theta > 0,
+ * so with all Im theta_k > 0 the LU runs without interchanges (d <= 512: batched
+ * SMEM-panel LU; d > 512: blocked LU on DMMA); a table with some Im theta_k <= 0
+ * (or PFX_DENSE_PIVOT=1 in the environment, d <= 512) selects partial pivoting
+ * (LAPACK getrf semantics).  For real A in full mode and d > 512 the inverse is
+ * taken as complex symmetric (lower triangle computed, mirrored in the combine).
  * An exactly zero pivot returns PFX_SINGULAR.
  */
 int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t batch, const double* V,

@@ -92,7 +92,9 @@ __device__ __forceinline__ void block_argmax(double val, int idx, double* sv, in
 // LU of the d x d row-major slot W (in place), pivots into ipiv (0-based, global rows).
 // Returns nonzero (in *sing) if an exactly zero pivot was met (factorization continues,
 // as LAPACK does, and the caller reports PFX_SINGULAR).
-template <int NB>
+// PIV = false: no interchanges (exp path: A Hermitian and Im(theta) > 0, so every pivot of
+// A + theta I has |Im| >= Im(theta) > 0, SURVEY finding 7); one barrier per panel column.
+template <int NB, bool PIV>
 __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* P, double2* S,
                            double* red_v, int* red_i, int* s_piv, int* sing, unsigned long long* dbg) {
   long long tph = 0;
@@ -116,11 +118,29 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
     //   A: per-warp argmax candidates are published; every thread reduces the 8 of them
     //   B: pivot row and displaced row are staged in prow/trow; then each thread eliminates
     //      its own rows (the interchange folded in) and tracks the next column's argmax.
+    if (!PIV) {
+      for (int jj = 0; jj < jb; ++jj) {
+        __syncthreads();  // panel row jj is final
+        const cplx pv = ld(&P[jj * PS + jj]);
+        if (tid == 0) {
+          s_piv[jj] = jj;
+          ipiv[p + jj] = p + jj;
+          if (pv.re == 0.0 && pv.im == 0.0) *sing = 1;
+        }
+        const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp(pv);
+        for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
+          double2* row = &P[r * PS];
+          const cplx l = cmul(ld(&row[jj]), rp);
+          for (int c = jj + 1; c < jb; ++c) st(&row[c], cfms(ld(&row[c]), l, ld(&P[jj * PS + c])));
+          st(&row[jj], l);
+        }
+      }
+    }
     double2* prow = S;           // strip buffer is idle during the panel
     double2* trow = S + 64;
     double bv = -1.0;
     int bi = 0x7fffffff;
-    for (int r = tid; r < m; r += DB_THREADS) {
+    for (int r = tid; r < m && PIV; r += DB_THREADS) {
       double2 x = P[r * PS];
       double v = fabs(x.x) + fabs(x.y);
       if (v > bv) {
@@ -128,7 +148,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         bi = r;
       }
     }
-    for (int jj = 0; jj < jb; ++jj) {
+    for (int jj = 0; jj < jb && PIV; ++jj) {
       for (int off = 16; off > 0; off >>= 1) {
         double ov = __shfl_down_sync(0xffffffffu, bv, off);
         int oi = __shfl_down_sync(0xffffffffu, bi, off);
@@ -198,7 +218,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       W[(size_t)(p + r) * d + p + c] = P[r * PS + c];
     }
     // ---- row interchanges on the columns outside the panel (in order, per column)
-    for (int c = tid; c < d - jb; c += DB_THREADS) {
+    for (int c = tid; c < d - jb && PIV; c += DB_THREADS) {
       int col = c < p ? c : c + jb;
       for (int jj = 0; jj < jb; ++jj) {
         int pr = s_piv[jj];
@@ -410,7 +430,7 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, dou
 //   <32, 1>: few systems (latency mode, e.g. C1);  <16, 2>: many systems with d <= 256
 //   (two CTAs per SM overlap one system's panel with another's DMMA update, e.g. C3);
 //   <16, 1>: 256 < d <= 512.
-template <int NB, int MINB>
+template <int NB, int MINB, bool PIV>
 __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBatchArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int d = a.d;
@@ -459,7 +479,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     __syncthreads();
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
-    lu_blocked<NB>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
+    lu_blocked<NB, PIV>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t_lu0));
     long long t_sv0 = clock64();
@@ -471,7 +491,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     }
     __syncthreads();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && PIV) {
       // s_perm holds ipiv; apply the swaps in order to the identity, in shared memory
       int* piv = s_perm;
       // walk backwards-compatible: build perm in rdiag-free scratch (the S strip buffer)
@@ -487,7 +507,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
       }
     }
     __syncthreads();
-    for (int i = tid; i < d; i += DB_THREADS) s_perm[i] = reinterpret_cast<int*>(S)[i];
+    for (int i = tid; i < d; i += DB_THREADS) s_perm[i] = PIV ? reinterpret_cast<int*>(S)[i] : i;
     __syncthreads();
     if (*s_sing && tid == 0) atomicExch(a.status, PFX_SINGULAR);
     // ---- K3: solves, one RHS column at a time through shared memory
@@ -576,7 +596,7 @@ int dense_batched_supported(int64_t d) { return d >= 1 && d <= 512; }
 // Launch the batched path.  All pointers are device pointers.
 int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
                       int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,
-                      int npairs, double* out, cudaStream_t stream, float* launch_ms) {
+                      int npairs, double* out, cudaStream_t stream, float* launch_ms, int pivot) {
   int dev = 0, sms = 0;
   PFX_CUDA_TRY(cudaGetDevice(&dev));
   PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -630,7 +650,10 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
     PFX_CUDA_TRY(cudaEventCreate(&e1));
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
-  auto kern = nb == 32 ? dense_batched_kernel<32, 1> : (minb == 2 ? dense_batched_kernel<16, 2> : dense_batched_kernel<16, 1>);
+  auto kern = pivot ? (nb == 32 ? dense_batched_kernel<32, 1, true>
+                                : (minb == 2 ? dense_batched_kernel<16, 2, true> : dense_batched_kernel<16, 1, true>))
+                    : (nb == 32 ? dense_batched_kernel<32, 1, false>
+                                : (minb == 2 ? dense_batched_kernel<16, 2, false> : dense_batched_kernel<16, 1, false>));
   PFX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   PFX_LAUNCH("dense_batched_kernel", stream, kern<<<slots, DB_THREADS, smem, stream>>>(args));
   PFX_CUDA_TRY(cudaGetLastError());

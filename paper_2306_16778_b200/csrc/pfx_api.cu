@@ -18,7 +18,7 @@ namespace pfx {
 int dense_batched_supported(int64_t d);
 int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
                       int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,
-                      int npairs, double* out, cudaStream_t stream, float* launch_ms);
+                      int npairs, double* out, cudaStream_t stream, float* launch_ms, int pivot);
 int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
                     int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
                     double* out, cudaStream_t stream, float* per_pair_ms);
@@ -288,8 +288,15 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
   }
   float ms = 0.0f;
   if (dense_batched_supported(d)) {
+    // Hermitian A and Im(theta_k) > 0 for every pair: no pivot can vanish (|Im u_ii| >=
+    // Im theta_k), so the LU runs without interchanges; PFX_DENSE_PIVOT=1 forces getrf
+    // semantics (partial pivoting) for A/B checks
+    static const bool force_piv = getenv("PFX_DENSE_PIVOT") != nullptr;
+    int pivot = force_piv ? 1 : 0;
+    for (int k = 0; k < npairs && !pivot; ++k)
+      if (!(theta2[2 * k + 1] > 0.0)) pivot = 1;
     rc = dense_batched_run(Ad, a_complex, (int)d, (int)batch, Vd, v_complex, ncols, full, real_path, 0, shift_c, th, co,
-                           npairs, Od, stream, per_pair_ms ? &ms : nullptr);
+                           npairs, Od, stream, per_pair_ms ? &ms : nullptr, pivot);
     if (per_pair_ms)
       for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
   } else {
@@ -403,7 +410,8 @@ int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double
     Yd = static_cast<double*>(scratch(6, vbytes));
     if (!Yd) return fail(PFX_CUDA, "staging allocation failed");
   }
-  rc = dense_batched_run(Ad, a_complex, (int)d, 1, Vd, 1, (int)nrhs, 0, 0, 1, 0.0, th, co, 1, Yd, stream, nullptr);
+  rc = dense_batched_run(Ad, a_complex, (int)d, 1, Vd, 1, (int)nrhs, 0, 0, 1, 0.0, th, co, 1, Yd, stream, nullptr,
+                         1);  // general shift: partial pivoting
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
     PFX_CUDA_TRY(cudaMemcpyAsync(Y, Yd, vbytes, cudaMemcpyDeviceToHost, stream));
