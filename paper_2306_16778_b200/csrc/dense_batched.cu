@@ -460,11 +460,41 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     const int b = sys / a.npairs, k = sys - b * a.npairs;
     const cplx th = ld(&a.theta[k]);
     const cplx co = ld(&a.coef[k]);
+    long long t_sys0 = clock64();
     if (tid == 0) *s_sing = 0;
     // ---- K0: M = A_b - cI + theta I into the slot
+    // (unrolled by 4 so each thread keeps several independent loads in flight)
     if (a.a_complex) {
       const double2* Ab = reinterpret_cast<const double2*>(a.A) + (size_t)b * dd;
-      for (size_t e = tid; e < dd; e += DB_THREADS) W[e] = Ab[e];
+      size_t e = tid;
+      for (; e + 3 * DB_THREADS < dd; e += 4 * DB_THREADS) {
+        const double2 x0 = Ab[e], x1 = Ab[e + DB_THREADS], x2 = Ab[e + 2 * DB_THREADS], x3 = Ab[e + 3 * DB_THREADS];
+        W[e] = x0;
+        W[e + DB_THREADS] = x1;
+        W[e + 2 * DB_THREADS] = x2;
+        W[e + 3 * DB_THREADS] = x3;
+      }
+      for (; e < dd; e += DB_THREADS) W[e] = Ab[e];
+    } else if ((dd & 1) == 0 && (reinterpret_cast<uintptr_t>(a.A) & 15) == 0) {
+      // real A: 16-byte loads of two entries, two complex stores each
+      const double2* Ab2 = reinterpret_cast<const double2*>(a.A + (size_t)b * dd);
+      const size_t h = dd / 2;
+      size_t e = tid;
+      for (; e + 3 * DB_THREADS < h; e += 4 * DB_THREADS) {
+        double2 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = Ab2[e + u * DB_THREADS];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          W[2 * (e + u * DB_THREADS)] = make_double2(x[u].x, 0.0);
+          W[2 * (e + u * DB_THREADS) + 1] = make_double2(x[u].y, 0.0);
+        }
+      }
+      for (; e < h; e += DB_THREADS) {
+        const double2 x = Ab2[e];
+        W[2 * e] = make_double2(x.x, 0.0);
+        W[2 * e + 1] = make_double2(x.y, 0.0);
+      }
     } else {
       const double* Ab = a.A + (size_t)b * dd;
       for (size_t e = tid; e < dd; e += DB_THREADS) W[e] = make_double2(Ab[e], 0.0);
@@ -477,6 +507,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
       W[(size_t)i * d + i] = x;
     }
     __syncthreads();
+    if (a.dbg && tid == 0) atomicAdd(&a.dbg[7], (unsigned long long)(clock64() - t_sys0));
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
     lu_blocked<NB, PIV>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
@@ -568,6 +599,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
       }
     }
     __syncthreads();
+    if (a.dbg && tid == 0) atomicAdd(&a.dbg[6], (unsigned long long)(clock64() - t_sys0));
   }
 }
 
@@ -675,8 +707,10 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   if (args.dbg) {
     unsigned long long h[8];
     PFX_CUDA_TRY(cudaMemcpy(h, args.dbg, sizeof(h), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "[pfx dense phases, Mcycles summed over CTAs] lu=%.1f solves=%.1f panel=%.1f swaps=%.1f trsm=%.1f gemm=%.1f\n",
-            h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
+    fprintf(stderr,
+            "[pfx dense phases, Mcycles summed over CTAs] system=%.1f build=%.1f lu=%.1f solves=%.1f panel=%.1f "
+            "swaps=%.1f trsm=%.1f gemm=%.1f\n",
+            h[6] / 1e6, h[7] / 1e6, h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
   }
   if (st == PFX_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
   return PFX_OK;
