@@ -11,10 +11,10 @@ done
 python bench.py --impl reference > $out/bench_reference_C2.json 2> $out/bench_reference_C2.err
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/c2_launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --prof-steps 0 > $out/ncu_c2_launches.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --prof-steps 0 --e2e-steps 0 > $out/ncu_c2_launches.log 2>&1
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --prof-steps 0 > /dev/null 2>&1 && \
   ncu --set full --import-source on -k regex:tri_ls -c 2 -o $out/c2_tri_ls \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --prof-steps 0 > $out/ncu_c2_full.log 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --prof-steps 0 --e2e-steps 0 > $out/ncu_c2_full.log 2>&1
 python tools/run_c5_once.py 512 1 > /dev/null 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $out/c5_launches.csv \
     python tools/run_c5_once.py 512 1 > $out/ncu_c5_launches.log 2>&1

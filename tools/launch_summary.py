@@ -1,11 +1,13 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list: per-kernel count / median / total."""
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list: per-kernel count / median / total.
+usage: launch_summary.py <csv> [first_n_launches]"""
 import csv, collections, sys
 lines = [l for l in open(sys.argv[1]) if not l.startswith("==")]
 rows = list(csv.reader(lines))
 h = rows[0]
 ik, iv = h.index("Kernel Name"), h.index("Metric Value")
 d = collections.defaultdict(list)
-for r in rows[1:]:
+limit = int(sys.argv[2]) if len(sys.argv) > 2 else None
+for r in rows[1:limit + 1 if limit else None]:
     if len(r) > iv:
         d[r[ik].split("(")[0][:48]].append(float(r[iv].replace(",", "")) / 1000)
 tot = sum(sum(v) for v in d.values())
