@@ -31,6 +31,7 @@
 //   K_T5 tri_correct         per chunk: out_i += sum_k 2 Re(w (Lambda_i G + Lambda'_i G')),
 //                            Lambda = running product of -l (resp. -l') from the chunk edge.
 #include <algorithm>
+#include <type_traits>
 
 #include "pfx_common.cuh"
 
@@ -710,8 +711,20 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     lsa.ckf = ckbuf + ckn;
     const int ntile = (int)ceil_div(nrhs, 16);
     const int smem = (int)(sizeof(LsSmem) * LS_WARPS * 2);
-    auto k0 = npairs <= 8 ? tri_ls<8, 0> : npairs <= 12 ? tri_ls<12, 0> : tri_ls<16, 0>;
-    auto k1 = npairs <= 8 ? tri_ls<8, 1> : npairs <= 12 ? tri_ls<12, 1> : tri_ls<16, 1>;
+    // phase B runs KM (>= npairs) pair slots: exact small widths keep a pole-sharded rank's
+    // work closer to its share of the pairs
+    auto pick = [&](auto m) {
+      using K = decltype(&tri_ls<16, decltype(m)::value>);
+      K k = npairs <= 2    ? tri_ls<2, decltype(m)::value>
+            : npairs <= 4  ? tri_ls<4, decltype(m)::value>
+            : npairs <= 6  ? tri_ls<6, decltype(m)::value>
+            : npairs <= 8  ? tri_ls<8, decltype(m)::value>
+            : npairs <= 12 ? tri_ls<12, decltype(m)::value>
+                           : tri_ls<16, decltype(m)::value>;
+      return k;
+    };
+    auto k0 = pick(std::integral_constant<int, 0>{});
+    auto k1 = pick(std::integral_constant<int, 1>{});
     PFX_CUDA_TRY(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     PFX_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     // row groups: whole chunks, one launch each (a single group in device mode)
