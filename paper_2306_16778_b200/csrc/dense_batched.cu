@@ -41,7 +41,9 @@ struct DenseBatchArgs {
   const double2* theta;  // device, npairs
   const double2* coef;   // device, npairs
   int npairs;
+  int aug;        // RHS columns carried through the LU (W is d x (d + aug)); 0 = separate solves
   double2* W;     // slots x d*d
+  double2* Xa;    // slots x d*aug  carried right-hand sides
   int* ipiv;      // slots x d
   double2* Y;     // slots x d*ncols   (solution Y, or X in full mode)
   double2* Yc;    // slots x d*ncols   (complex action: M^{-H} V)
@@ -94,9 +96,15 @@ __device__ __forceinline__ void block_argmax(double val, int idx, double* sv, in
 // as LAPACK does, and the caller reports PFX_SINGULAR).
 // PIV = false: no interchanges (exp path: A Hermitian and Im(theta) > 0, so every pivot of
 // A + theta I has |Im| >= Im(theta) > 0, SURVEY finding 7); one barrier per panel column.
+// Xa (d x na, row-major): right-hand sides carried through the factorisation (row
+// interchanges + per-panel forward elimination turn them into L^{-1} P v).  The panel head of
+// the carried columns is broadcast through the strip buffer S (idle between the interchanges
+// and the strips; >= 32 x 33 complex >= NB x 4).
 template <int NB, bool PIV>
-__device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* P, double2* S,
-                           double* red_v, int* red_i, int* s_piv, int* sing, unsigned long long* dbg) {
+__device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* __restrict__ Xa, int na,
+                           double2* P, double2* S, double* red_v, int* red_i, int* s_piv, int* sing,
+                           unsigned long long* dbg) {
+  const size_t ldw = (size_t)d;
   long long tph = 0;
   constexpr int PS = NB + 1;        // padded panel row stride (double2)
   constexpr int SS = DB_SW + 1;     // padded strip row stride
@@ -110,7 +118,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
     // ---- load panel rows p..d-1, cols p..p+jb-1
     for (int e = tid; e < m * jb; e += DB_THREADS) {
       int r = e / jb, c = e - r * jb;
-      P[r * PS + c] = W[(size_t)(p + r) * d + p + c];
+      P[r * PS + c] = W[(size_t)(p + r) * ldw + p + c];
     }
     __syncthreads();
     if (dbg && tid == 0) tph = clock64();
@@ -215,18 +223,21 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
     // ---- write panel back
     for (int e = tid; e < m * jb; e += DB_THREADS) {
       int r = e / jb, c = e - r * jb;
-      W[(size_t)(p + r) * d + p + c] = P[r * PS + c];
+      W[(size_t)(p + r) * ldw + p + c] = P[r * PS + c];
     }
     // ---- row interchanges on the columns outside the panel (in order, per column)
-    for (int c = tid; c < d - jb && PIV; c += DB_THREADS) {
-      int col = c < p ? c : c + jb;
+    for (int c = tid; c < d - jb + na && PIV; c += DB_THREADS) {
+      const bool carried = c >= d - jb;  // columns of Xa
+      const int col = carried ? c - (d - jb) : (c < p ? c : c + jb);
+      double2* base = carried ? Xa : W;
+      const size_t ld = carried ? (size_t)na : ldw;
       for (int jj = 0; jj < jb; ++jj) {
         int pr = s_piv[jj];
         if (pr != jj) {
-          size_t a = (size_t)(p + jj) * d + col, b = (size_t)(p + pr) * d + col;
-          double2 x = W[a];
-          W[a] = W[b];
-          W[b] = x;
+          size_t a = (size_t)(p + jj) * ld + col, b = (size_t)(p + pr) * ld + col;
+          double2 x = base[a];
+          base[a] = base[b];
+          base[b] = x;
         }
       }
     }
@@ -236,11 +247,38 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       tph = clock64();
     }
     // ---- strips of the trailing columns: U12 = L11^{-1} A12, A22 -= L21 U12
+    // ---- carried right-hand sides: head = L11^{-1} head (warp per column, shuffles; the
+    // result also goes to shared memory), then tail -= L21 head (thread per row and column)
+    if (na > 0) {
+      double2* xs = S;
+      for (int c = warp; c < na; c += DB_WARPS) {
+        cplx x = lane < jb ? ld(&Xa[(size_t)(p + lane) * na + c]) : mk(0.0, 0.0);
+        for (int k = 0; k < jb; ++k) {
+          cplx xk;
+          xk.re = __shfl_sync(0xffffffffu, x.re, k);
+          xk.im = __shfl_sync(0xffffffffu, x.im, k);
+          if (lane > k && lane < jb) x = cfms(x, ld(&P[lane * PS + k]), xk);
+        }
+        if (lane < jb) {
+          st(&Xa[(size_t)(p + lane) * na + c], x);
+          st(&xs[c * NB + lane], x);
+        }
+      }
+      __syncthreads();  // (also orders the xs reads before the first strip reuses S)
+      for (int e = tid; e < (m - jb) * na; e += DB_THREADS) {
+        const int r = e / na + jb, c = e - (r - jb) * na;
+        cplx y = ld(&Xa[(size_t)(p + r) * na + c]);
+#pragma unroll 4
+        for (int k = 0; k < jb; ++k) y = cfms(y, ld(&P[r * PS + k]), ld(&xs[c * NB + k]));
+        st(&Xa[(size_t)(p + r) * na + c], y);
+      }
+      __syncthreads();
+    }
     for (int q = p + jb; q < d; q += DB_SW) {
       const int sw = min(DB_SW, d - q);
       for (int e = tid; e < jb * sw; e += DB_THREADS) {
         int r = e / sw, c = e - r * sw;
-        S[r * SS + c] = W[(size_t)(p + r) * d + q + c];
+        S[r * SS + c] = W[(size_t)(p + r) * ldw + q + c];
       }
       __syncthreads();
       // unit-lower triangular solve: warp w owns strip columns 8w..8w+7, lane = row; the 8
@@ -267,7 +305,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       __syncthreads();
       for (int e = tid; e < jb * sw; e += DB_THREADS) {
         int r = e / sw, c = e - r * sw;
-        W[(size_t)(p + r) * d + q + c] = S[r * SS + c];
+        W[(size_t)(p + r) * ldw + q + c] = S[r * SS + c];
       }
       if (dbg && tid == 0) {
         atomicAdd(&dbg[4], (unsigned long long)(clock64() - tph));
@@ -286,12 +324,12 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
           if (ct < ctiles && grow < d) {
             int c0 = ct * 8 + 2 * t;
             if (c0 < sw) {
-              double2 x = W[(size_t)grow * d + q + c0];
+              double2 x = W[(size_t)grow * ldw + q + c0];
               cr[ct][0] = x.x;
               ci[ct][0] = x.y;
             }
             if (c0 + 1 < sw) {
-              double2 x = W[(size_t)grow * d + q + c0 + 1];
+              double2 x = W[(size_t)grow * ldw + q + c0 + 1];
               cr[ct][1] = x.x;
               ci[ct][1] = x.y;
             }
@@ -323,8 +361,8 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         for (int ct = 0; ct < DB_SW / 8; ++ct) {
           if (ct < ctiles && grow < d) {
             int c0 = ct * 8 + 2 * t;
-            if (c0 < sw) W[(size_t)grow * d + q + c0] = make_double2(cr[ct][0], ci[ct][0]);
-            if (c0 + 1 < sw) W[(size_t)grow * d + q + c0 + 1] = make_double2(cr[ct][1], ci[ct][1]);
+            if (c0 < sw) W[(size_t)grow * ldw + q + c0] = make_double2(cr[ct][0], ci[ct][0]);
+            if (c0 + 1 < sw) W[(size_t)grow * ldw + q + c0 + 1] = make_double2(cr[ct][1], ci[ct][1]);
           }
         }
       }
@@ -345,7 +383,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
 // kind 3: L^H (unit upper, backward)    z <- L^{-H} z
 // Blocked by 32 rows: the contribution of already-solved blocks is a GEMV with
 // coalesced reads of W, the 32x32 diagonal block is solved by warp 0 in registers.
-__device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, double2* z, double2* part,
+__device__ void trsv_blocked(const double2* __restrict__ W, int d, size_t ldw, int kind, double2* z, double2* part,
                              double2* diag, const double2* rdiag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool forward = (kind == 0 || kind == 2);
@@ -361,7 +399,7 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, dou
     if (kind <= 1) {
       // rows of W are contiguous: warp w handles rows i0+w, i0+w+8, ...; lanes stride j
       for (int ii = warp; ii < bs; ii += DB_WARPS) {
-        const double2* row = W + (size_t)(i0 + ii) * d;
+        const double2* row = W + (size_t)(i0 + ii) * ldw;
         cplx acc = mk(0.0, 0.0);
         for (int j = j0 + lane; j < j1; j += 32) acc = cadd(acc, cmul(ld(&row[j]), ld(&z[j])));
         for (int off = 16; off > 0; off >>= 1) {
@@ -374,7 +412,7 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, dou
       // op(W)[i][j] = conj(W[j][i]): lanes along i (contiguous in row j), warps stride j
       cplx acc = mk(0.0, 0.0);
       if (lane < bs)
-        for (int j = j0 + warp; j < j1; j += DB_WARPS) acc = cadd(acc, cmulc(ld(&z[j]), ld(&W[(size_t)j * d + i0 + lane])));
+        for (int j = j0 + warp; j < j1; j += DB_WARPS) acc = cadd(acc, cmulc(ld(&z[j]), ld(&W[(size_t)j * ldw + i0 + lane])));
       // reduce over warps through shared memory (diag scratch as buffer)
       st(&diag[warp * 32 + lane], acc);
       __syncthreads();
@@ -388,7 +426,7 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, int kind, dou
     // load the diagonal block (op applied) into shared memory: diag[r*33 + c] = op(W)[i0+r][i0+c]
     for (int e = tid; e < bs * bs; e += DB_THREADS) {
       int r = e / bs, c = e - r * bs;
-      cplx v = (kind <= 1) ? ld(&W[(size_t)(i0 + r) * d + i0 + c]) : cconj(ld(&W[(size_t)(i0 + c) * d + i0 + r]));
+      cplx v = (kind <= 1) ? ld(&W[(size_t)(i0 + r) * ldw + i0 + c]) : cconj(ld(&W[(size_t)(i0 + c) * ldw + i0 + r]));
       st(&diag[r * 33 + c], v);
     }
     __syncthreads();
@@ -450,7 +488,9 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
 
   const int tid = threadIdx.x;
   const int slot = blockIdx.x;
-  double2* W = a.W + (size_t)slot * d * d;
+  const size_t ldw = (size_t)d;
+  double2* W = a.W + (size_t)slot * d * ldw;
+  double2* Xa = a.Xa + (size_t)slot * d * a.aug;
   int* ipiv = a.ipiv + (size_t)slot * d;
   const int nsys = a.batch * a.npairs;
   const size_t dd = (size_t)d * d;
@@ -463,61 +503,60 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     long long t_sys0 = clock64();
     if (tid == 0) *s_sing = 0;
     // ---- K0: M = A_b - cI + theta I into the slot
-    // (unrolled by 4 so each thread keeps several independent loads in flight)
-    if (a.a_complex) {
-      const double2* Ab = reinterpret_cast<const double2*>(a.A) + (size_t)b * dd;
-      size_t e = tid;
-      for (; e + 3 * DB_THREADS < dd; e += 4 * DB_THREADS) {
-        const double2 x0 = Ab[e], x1 = Ab[e + DB_THREADS], x2 = Ab[e + 2 * DB_THREADS], x3 = Ab[e + 3 * DB_THREADS];
-        W[e] = x0;
-        W[e + DB_THREADS] = x1;
-        W[e + 2 * DB_THREADS] = x2;
-        W[e + 3 * DB_THREADS] = x3;
-      }
-      for (; e < dd; e += DB_THREADS) W[e] = Ab[e];
-    } else if ((dd & 1) == 0 && (reinterpret_cast<uintptr_t>(a.A) & 15) == 0) {
-      // real A: 16-byte loads of two entries, two complex stores each
-      const double2* Ab2 = reinterpret_cast<const double2*>(a.A + (size_t)b * dd);
-      const size_t h = dd / 2;
-      size_t e = tid;
-      for (; e + 3 * DB_THREADS < h; e += 4 * DB_THREADS) {
-        double2 x[4];
+    // rows of A into the slot (row stride ldw); warp per row, lanes along the row, four rows
+    // per round so each lane keeps several independent loads in flight
+    {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int i0 = warp * 4; i0 < d; i0 += DB_WARPS * 4) {
+        if (a.a_complex) {
+          const double2* Ab = reinterpret_cast<const double2*>(a.A) + (size_t)b * dd;
+          for (int c = lane; c < d; c += 32) {
+            double2 x[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = Ab2[e + u * DB_THREADS];
+            for (int u = 0; u < 4; ++u) x[u] = i0 + u < d ? Ab[(size_t)(i0 + u) * d + c] : make_double2(0, 0);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          W[2 * (e + u * DB_THREADS)] = make_double2(x[u].x, 0.0);
-          W[2 * (e + u * DB_THREADS) + 1] = make_double2(x[u].y, 0.0);
+            for (int u = 0; u < 4; ++u)
+              if (i0 + u < d) W[(size_t)(i0 + u) * ldw + c] = x[u];
+          }
+        } else {
+          const double* Ab = a.A + (size_t)b * dd;
+          for (int c = lane; c < d; c += 32) {
+            double x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = i0 + u < d ? Ab[(size_t)(i0 + u) * d + c] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (i0 + u < d) W[(size_t)(i0 + u) * ldw + c] = make_double2(x[u], 0.0);
+          }
         }
       }
-      for (; e < h; e += DB_THREADS) {
-        const double2 x = Ab2[e];
-        W[2 * e] = make_double2(x.x, 0.0);
-        W[2 * e + 1] = make_double2(x.y, 0.0);
+      // right-hand sides carried through the factorisation
+      for (int e = tid; e < d * a.aug; e += DB_THREADS) {
+        const int i = e / a.aug, c = e - i * a.aug;
+        const size_t vi = ((size_t)b * d + i) * nc + c;
+        Xa[(size_t)i * a.aug + c] =
+            a.v_complex ? reinterpret_cast<const double2*>(a.V)[vi] : make_double2(a.V[vi], 0.0);
       }
-    } else {
-      const double* Ab = a.A + (size_t)b * dd;
-      for (size_t e = tid; e < dd; e += DB_THREADS) W[e] = make_double2(Ab[e], 0.0);
     }
     __syncthreads();
     for (int i = tid; i < d; i += DB_THREADS) {
-      double2 x = W[(size_t)i * d + i];
+      double2 x = W[(size_t)i * ldw + i];
       x.x = (x.x - a.shift_c) + th.re;
       x.y = x.y + th.im;
-      W[(size_t)i * d + i] = x;
+      W[(size_t)i * ldw + i] = x;
     }
     __syncthreads();
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[7], (unsigned long long)(clock64() - t_sys0));
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
-    lu_blocked<NB, PIV>(W, ipiv, d, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
+    lu_blocked<NB, PIV>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t_lu0));
     long long t_sv0 = clock64();
     // row permutation of P M = L U (swaps applied in order to the identity) and 1/U_ii
     for (int i = tid; i < d; i += DB_THREADS) {
       s_perm[i] = ipiv[i];
-      const cplx u = ld(&W[(size_t)i * d + i]);
+      const cplx u = ld(&W[(size_t)i * ldw + i]);
       st(&rdiag[i], (u.re == 0.0 && u.im == 0.0) ? mk(0.0, 0.0) : crcp(u));
     }
     __syncthreads();
@@ -552,19 +591,21 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
         if (a.v_complex) return reinterpret_cast<const double2*>(a.V)[((size_t)b * d + i) * nc + c];
         return make_double2(a.V[((size_t)b * d + i) * nc + c], 0.0);
       };
-      // Y = U^{-1} L^{-1} P V : P applied as a gather through the permutation
+      // Y = U^{-1} L^{-1} P V : P applied as a gather through the permutation; a carried
+      // column already holds L^{-1} P v
+      const bool carried = c < a.aug;
       for (int i = tid; i < d; i += DB_THREADS) {
-        z[i] = rhs(s_perm[i]);
+        z[i] = carried ? Xa[(size_t)i * a.aug + c] : rhs(s_perm[i]);
         zc[i] = rhs(i);
       }
       __syncthreads();
-      trsv_blocked(W, d, 0, z, part, diag, rdiag);
-      trsv_blocked(W, d, 1, z, part, diag, rdiag);
+      if (!carried) trsv_blocked(W, d, ldw, 0, z, part, diag, rdiag);
+      trsv_blocked(W, d, ldw, 1, z, part, diag, rdiag);
       for (int i = tid; i < d; i += DB_THREADS) Yg[(size_t)i * nc + c] = z[i];
       if (want_conj) {
         // Yc = M^{-H} V = P^T L^{-H} U^{-H} V
-        trsv_blocked(W, d, 2, zc, part, diag, rdiag);
-        trsv_blocked(W, d, 3, zc, part, diag, rdiag);
+        trsv_blocked(W, d, ldw, 2, zc, part, diag, rdiag);
+        trsv_blocked(W, d, ldw, 3, zc, part, diag, rdiag);
         // P^T applied as a scatter through the permutation
         for (int i = tid; i < d; i += DB_THREADS) Ycg[(size_t)s_perm[i] * nc + c] = zc[i];
       }
@@ -640,8 +681,11 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   const int nsys = batch * npairs;
   const int slots = nsys < minb * sms ? nsys : minb * sms;
   const size_t per_sys = (size_t)d * ncols;
+  // action mode with a few right-hand sides: carry them through the LU (forward solve free)
+  const int aug = (!full && ncols <= 4) ? ncols : 0;
+
   const size_t stage_elems = (size_t)nsys * per_sys * (real_path ? 1 : 2);
-  char* ws = static_cast<char*>(scratch(1, (size_t)slots * ((size_t)d * d + 2 * per_sys) * sizeof(double2) +
+  char* ws = static_cast<char*>(scratch(1, (size_t)slots * ((size_t)d * (d + aug) + 2 * per_sys) * sizeof(double2) +
                                                (size_t)slots * d * sizeof(int) + sizeof(int) + 256));
   if (!ws) return fail(PFX_CUDA, "dense workspace allocation failed");
   double* stage = static_cast<double*>(scratch(2, stage_elems * sizeof(double)));
@@ -661,8 +705,10 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   args.theta = theta_d;
   args.coef = coef_d;
   args.npairs = npairs;
+  args.aug = aug;
   args.W = reinterpret_cast<double2*>(ws);
-  args.Y = args.W + (size_t)slots * d * d;
+  args.Xa = args.W + (size_t)slots * d * d;
+  args.Y = args.Xa + (size_t)slots * d * aug;
   args.Yc = args.Y + (size_t)slots * per_sys;
   args.ipiv = reinterpret_cast<int*>(args.Yc + (size_t)slots * per_sys);
   args.status = args.ipiv + (size_t)slots * d;
