@@ -479,6 +479,12 @@ def main():
                     "path_frac": ALG_FLOPS[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e12
                     / peaks["fp64_tflops"] / world,
                     "hbm_gbs_alg": ALG_BYTES[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e9}
+        # the HBM axis the north star asks for on the structured paths: compulsory bytes of the
+        # whole step and the dominant kernel's measured DRAM traffic (ncu) over its live time
+        roofline["hbm_peak_gbs"] = peaks["hbm_gbs"]
+        roofline["hbm_frac_alg"] = roofline["hbm_gbs_alg"] / peaks["hbm_gbs"]
+        tr = DOM_TRAFFIC.get(args.workload)
+        roofline["dram_gbs"] = tr / t_launch / 1e9 if tr else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
