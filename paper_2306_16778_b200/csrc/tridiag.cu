@@ -72,6 +72,13 @@ struct TriArgs {
   double* out;  // N x nrhs
 };
 
+// chunk summaries are stored chunk-fastest so the carry scan (one block per pair, rhs and
+// direction, walking the chunks) reads contiguous memory; the producers' stores scatter
+__device__ __forceinline__ int64_t g_at(const TriArgs& a, int64_t c, int k, int r) {
+  return ((int64_t)k * a.nrhs + r) * a.P + c;
+}
+__device__ __forceinline__ int64_t l_at(const TriArgs& a, int64_t c, int k) { return (int64_t)k * a.P + c; }
+
 __device__ __forceinline__ double off2(const double* off, int64_t N, int64_t i) {
   // e_i^2 for the coupling between rows i and i+1 (0 outside the matrix)
   if (i < 0 || i >= N - 1) return 0.0;
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
       if ((i & 3) == 0) rescale2(q1, q2);
       e = offe(s + i - 1);
     }
-    st(&a.LB[c * np + k], lam);
+    st(&a.LB[l_at(a, c, k)], lam);
   }
   // forward chain + twisted weights
   {
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
       if ((i & 3) == 3) rescale2(p1, p2);
       e0 = e1;
     }
-    st(&a.LF[c * np + k], lam);
+    st(&a.LF[l_at(a, c, k)], lam);
   }
   if (noncontr) atomicAnd(&a.contr[c], 0);
 }
@@ -490,7 +497,7 @@ __global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_pass(TriArgs a) {
       double2* dst = dir == 0 ? a.gF : a.gB;
 #pragma unroll
       for (int k = 0; k < KM; ++k)
-        if (k < np) st(&dst[(c * np + k) * a.nrhs + r], g[k]);
+        if (k < np) st(&dst[g_at(a, c, k, r)], g[k]);
     }
     cp_async_wait<0>();
     __syncwarp(hmask);
@@ -525,8 +532,8 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
       const int q = t * per + j0 + u;
       if (j0 + u < per && q < P) {
         const int cc = chunk_of(q);
-        Lc[u] = ld(&Ls[(int64_t)cc * a.npairs + k]);
-        gc[u] = ld(&gs[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
+        Lc[u] = ld(&Ls[l_at(a, cc, k)]);
+        gc[u] = ld(&gs[g_at(a, cc, k, rr)]);
       } else {
         Lc[u] = mk(1, 0);
         gc[u] = mk(0, 0);
@@ -561,8 +568,8 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
       const int q = t * per + j0 + u;
       if (j0 + u < per && q < P) {
         const int cc = chunk_of(q);
-        Lc[u] = ld(&Ls[(int64_t)cc * a.npairs + k]);
-        gc[u] = ld(&gs[((int64_t)cc * a.npairs + k) * a.nrhs + rr]);
+        Lc[u] = ld(&Ls[l_at(a, cc, k)]);
+        gc[u] = ld(&gs[g_at(a, cc, k, rr)]);
       }
     }
 #pragma unroll
@@ -574,6 +581,88 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
       }
     }
   }
+}
+
+// Same scan with the block's whole column staged in shared memory by one round of coalesced
+// cp.async (chunk-fastest summaries: L and g of this (pair, rhs) are two contiguous runs of P
+// complex); used when 2 P complex fit (P <= CS_SMEM_P).
+constexpr int CS_SMEM_P = 4096;
+__global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // one pad slot per 16 chunks: thread t walks chunks 16t.., so unpadded its lanes would sit
+  // 256 B apart in one bank group; padded (272 B) they spread over all banks
+  auto sx = [](int cc) { return cc + (cc >> 4); };
+  const int PP = a.P + (a.P >> 4) + 1;
+  double2* sL = reinterpret_cast<double2*>(smem_raw);  // PP
+  double2* sg = sL + PP;                               // PP
+  __shared__ cplx sA[CS_T], sB[CS_T];
+  const int bid = blockIdx.x;
+  const int dir = bid & 1;
+  const int kr = bid >> 1;
+  const int k = kr / a.nrhs, rr = kr - k * a.nrhs;
+  const int P = a.P;
+  const int t = threadIdx.x;
+  const double2* Ls = (dir == 0 ? a.LF : a.LB) + l_at(a, 0, k);
+  const double2* gs = (dir == 0 ? a.gF : a.gB) + g_at(a, 0, k, rr);
+  for (int e = t; e < P; e += CS_T) {
+    cp_async16(&sL[sx(e)], &Ls[e]);
+    cp_async16(&sg[sx(e)], &gs[e]);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int per = (P + CS_T - 1) / CS_T;
+  auto chunk_of = [&](int q) { return dir == 0 ? q : P - 1 - q; };
+  cplx A = mk(1, 0), B = mk(0, 0);
+  for (int j = 0; j < per; ++j) {
+    const int q = t * per + j;
+    if (q >= P) break;
+    const int cc = sx(chunk_of(q));
+    const cplx L = ld(&sL[cc]);
+    B = cadd(cmul(L, B), ld(&sg[cc]));
+    A = cmul(L, A);
+  }
+  sA[t] = A;
+  sB[t] = B;
+  __syncthreads();
+  for (int off = 1; off < CS_T; off <<= 1) {
+    cplx pA = t >= off ? sA[t - off] : mk(1, 0), pB = t >= off ? sB[t - off] : mk(0, 0);
+    __syncthreads();
+    if (t >= off) {
+      B = cadd(cmul(A, pB), B);
+      A = cmul(A, pA);
+      sA[t] = A;
+      sB[t] = B;
+    }
+    __syncthreads();
+  }
+  cplx x = t > 0 ? sB[t - 1] : mk(0, 0);
+  double2* dst = dir == 0 ? a.G : a.Gb;
+  for (int j = 0; j < per; ++j) {
+    const int q = t * per + j;
+    if (q >= P) break;
+    const int cc = chunk_of(q);
+    st(&dst[((int64_t)cc * a.npairs + k) * a.nrhs + rr], x);
+    x = cadd(cmul(ld(&sL[sx(cc)]), x), ld(&sg[sx(cc)]));
+  }
+}
+
+static int carry_scan(const TriArgs& a, int npairs, int64_t nrhs, cudaStream_t stream) {
+  const unsigned blocks = (unsigned)(npairs * nrhs * 2);
+  if (a.P <= CS_SMEM_P) {
+    const int smem = 2 * (a.P + (a.P >> 4) + 1) * (int)sizeof(double2);
+    static int set = 0;
+    if (smem > set) {
+      const int mx = 2 * (CS_SMEM_P + (CS_SMEM_P >> 4) + 1) * (int)sizeof(double2);
+      PFX_CUDA_TRY(cudaFuncSetAttribute(tri_carry_scan_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      set = mx;
+    }
+    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan_smem<<<blocks, CS_T, smem, stream>>>(a));
+  } else {
+    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<blocks, CS_T, 0, stream>>>(a));
+  }
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
 }
 
 __global__ void scale_kernel(double* x, size_t n, double s) {
@@ -748,8 +837,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     };
     if (!pipe) {
       if (int rc = launch_ls(false, 0, P, stream)) return rc;
-      PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
-      PFX_CUDA_TRY(cudaGetLastError());
+      if (int rc = carry_scan(a, npairs, nrhs, stream)) return rc;
       if (int rc = launch_ls(true, 0, P, stream)) return rc;
     } else {
       // events: [0, G) V group landed, [G, 2G) sweep done, [2G, 3G) result ready,
@@ -788,8 +876,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
         if (tl) cudaEventRecord(tev[G + g], TP.sw[g]);
         PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[G + g], 0));
       }
-      PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
-      PFX_CUDA_TRY(cudaGetLastError());
+      if (int rc = carry_scan(a, npairs, nrhs, stream)) return rc;
       PFX_CUDA_TRY(cudaEventRecord(ev[4 * G], stream));  // carry scan done
       if (tl) cudaEventRecord(tev[5 * G + 1], stream);
       for (int g = 0; g < ng; ++g) {
@@ -836,8 +923,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaGetLastError());
     if (int rc = sweeps(a, stream, 0)) return rc;
     PFX_CUDA_TRY(cudaGetLastError());
-    PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<(unsigned)(npairs * nrhs * 2), CS_T, 0, stream>>>(a));
-    PFX_CUDA_TRY(cudaGetLastError());
+    if (int rc = carry_scan(a, npairs, nrhs, stream)) return rc;
     if (int rc = sweeps(a, stream, 1)) return rc;
     PFX_CUDA_TRY(cudaGetLastError());
   }

@@ -328,9 +328,9 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
       if (rv) {
 #pragma unroll
         for (int q = 0; q < KM; ++q)
-          if (q < np) st(&(dir == 0 ? a.gF : a.gB)[(c * np + q) * a.nrhs + rg], g[q]);
+          if (q < np) st(&(dir == 0 ? a.gF : a.gB)[g_at(a, c, q, rg)], g[q]);
       }
-      if (act && rt0 == 0) st(&(dir == 0 ? a.LF : a.LB)[c * np + k], lam);
+      if (act && rt0 == 0) st(&(dir == 0 ? a.LF : a.LB)[l_at(a, c, k)], lam);
     }
   }
   if (MODE == 0) {
