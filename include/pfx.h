@@ -118,8 +118,9 @@ int pfx_expm_banded(int mem, const double* band, int64_t N, int64_t kb, const do
 
 /*
  * Single-shift solve (reference linalg.shifted_solve, linalg.py:92-103):
- * Y = (A + theta I)^{-1} V for one dense Hermitian A, partial pivoting.
- * V, Y: d x nrhs complex.  Device or host memory as `mem`.
+ * Y = (A + theta I)^{-1} V for one dense Hermitian A, partial pivoting (any d:
+ * d <= 512 the batched SMEM-panel kernel, d > 512 blocked getrf/getrs on DMMA).
+ * theta may be real.  V, Y: d x nrhs complex.  Device or host memory as `mem`.
  */
 int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double theta_re, double theta_im,
                       const double* V, int64_t nrhs, double* Y, void* stream);

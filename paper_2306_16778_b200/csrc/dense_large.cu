@@ -199,4 +199,73 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   return PFX_OK;
 }
 
+// Single shifted solve Y = (A + theta I)^{-1} V for d > 512 (pfx_shifted_solve; the reference
+// linalg.shifted_solve, linalg.py:92-108, has no size limit).  theta is arbitrary here (it may
+// be real), so this is getrf/getrs with partial pivoting: per 64-column panel the pivoting
+// panel kernel (izamax ties), the interchanges on the columns left and right of the panel and
+// on the right-hand sides, U12 = L11^{-1} A12, A22 -= L21 U12; then blocked forward and
+// backward substitution.
+int shifted_solve_large(const double* A, int a_complex, int d, const double2* theta_d, const double* V, int nrhs,
+                        double2* Y, cudaStream_t stream) {
+  const int nb = DL_NB;
+  const size_t mbytes = (size_t)d * d * sizeof(double2);
+  const size_t xbytes = (size_t)d * nrhs * sizeof(double2);
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + (size_t)d * sizeof(int) + 256));
+  if (!ws) return fail(PFX_CUDA, "shifted-solve workspace allocation failed");
+  ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
+  ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, (int64_t)d * nrhs};
+  int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
+  int* sing = ipiv + d;
+  PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+  dim3 bg(1184, 1);
+  PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, 1, nrhs, 0, 0.0, theta_d, 1, 1,
+                                                                    M, X));
+  PFX_CUDA_TRY(cudaGetLastError());
+  auto sub = [](ZMat T, int64_t i, int64_t j) {
+    ZMat r = T;
+    r.p = T.p + i * T.ld + j;
+    return r;
+  };
+  int rc;
+  for (int j0 = 0; j0 < d; j0 += nb) {
+    const int jb = std::min(nb, d - j0);
+    const int rest = d - j0 - jb;
+    if ((rc = zgetf2_panel(stream, 1, d - j0, jb, sub(M, j0, j0), ipiv + j0, sing))) return rc;
+    if ((rc = zlaswp(stream, 1, jb, M, j0, 0, j0, ipiv + j0, +1))) return rc;
+    if ((rc = zlaswp(stream, 1, jb, M, j0, j0 + jb, d, ipiv + j0, +1))) return rc;
+    if ((rc = zlaswp(stream, 1, jb, X, j0, 0, nrhs, ipiv + j0, +1))) return rc;
+    if (rest > 0) {
+      if ((rc = ztrsm_llnu(stream, 1, jb, rest, sub(M, j0, j0), sub(M, j0, j0 + jb)))) return rc;
+      if ((rc = zgemm(stream, 1, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
+                      sub(M, j0 + jb, j0 + jb))))
+        return rc;
+    }
+  }
+  // X = L^{-1} P V (P already applied), then U^{-1}
+  for (int j0 = 0; j0 < d; j0 += nb) {
+    const int jb = std::min(nb, d - j0);
+    const int rest = d - j0 - jb;
+    if ((rc = ztrsm_llnu(stream, 1, jb, nrhs, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
+    if (rest > 0 && (rc = zgemm(stream, 1, rest, nrhs, jb, -1.0, sub(M, j0 + jb, j0), sub(X, j0, 0),
+                                sub(X, j0 + jb, 0))))
+      return rc;
+  }
+  const int nblk = (d + nb - 1) / nb;
+  for (int pb = nblk - 1; pb >= 0; --pb) {
+    const int j0 = pb * nb;
+    const int jb = std::min(nb, d - j0);
+    const int rest = d - j0 - jb;
+    if (rest > 0 && (rc = zgemm(stream, 1, jb, nrhs, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0),
+                                sub(X, j0, 0))))
+      return rc;
+    if ((rc = ztrsm_lunn(stream, 1, jb, nrhs, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
+  }
+  PFX_CUDA_TRY(cudaMemcpyAsync(Y, X.p, xbytes, cudaMemcpyDeviceToDevice, stream));
+  int sg = 0;
+  PFX_CUDA_TRY(cudaMemcpyAsync(&sg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (sg) return fail(PFX_SINGULAR, "exactly zero pivot in the shifted factorization");
+  return PFX_OK;
+}
+
 }  // namespace pfx

@@ -29,6 +29,8 @@ int banded_run(const double* band, int64_t N, int64_t kb, const double* V, int64
                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                float* per_pair_ms);
 int pole_table_host(int n, double* theta2, double* coef2);
+int shifted_solve_large(const double* A, int a_complex, int d, const double2* theta_d, const double* V, int nrhs,
+                        double2* Y, cudaStream_t stream);
 
 static thread_local std::string g_err;
 
@@ -393,7 +395,6 @@ int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (mem != PFX_MEM_DEVICE && mem != PFX_MEM_HOST) return fail(PFX_BADARG, "bad mem kind");
   if (!A || !V || !Y || d < 1 || nrhs < 1) return fail(PFX_BADARG, "need A, V, Y non-null, d >= 1, nrhs >= 1");
-  if (!dense_batched_supported(d)) return fail(PFX_BADARG, "pfx_shifted_solve supports d <= 512");
   if (!std::isfinite(theta_re) || !std::isfinite(theta_im)) return fail(PFX_BADARG, "non-finite shift");
   // one system, residue 1: stage = Y = (A + theta I)^{-1} V (complex V, complex Y)
   double th2[2] = {theta_re, theta_im}, co2[2] = {1.0, 0.0};
@@ -410,8 +411,11 @@ int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double
     Yd = static_cast<double*>(scratch(6, vbytes));
     if (!Yd) return fail(PFX_CUDA, "staging allocation failed");
   }
-  rc = dense_batched_run(Ad, a_complex, (int)d, 1, Vd, 1, (int)nrhs, 0, 0, 1, 0.0, th, co, 1, Yd, stream, nullptr,
-                         1);  // general shift: partial pivoting
+  if (dense_batched_supported(d))
+    rc = dense_batched_run(Ad, a_complex, (int)d, 1, Vd, 1, (int)nrhs, 0, 0, 1, 0.0, th, co, 1, Yd, stream, nullptr,
+                           1);  // general shift: partial pivoting
+  else
+    rc = shifted_solve_large(Ad, a_complex, (int)d, th, Vd, (int)nrhs, reinterpret_cast<double2*>(Yd), stream);
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
     PFX_CUDA_TRY(cudaMemcpyAsync(Y, Yd, vbytes, cudaMemcpyDeviceToHost, stream));

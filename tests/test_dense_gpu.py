@@ -167,3 +167,26 @@ def test_shifted_inverse_and_singular():
     assert np.allclose(shifted_inverse(A, 1j), -1j * np.eye(2), atol=1e-16)
     with pytest.raises(SingularSystem):
         shifted_solve(A, 0.0, np.ones(2))
+
+
+@pytest.mark.parametrize("d,theta", [(513, 0.37), (700, -2.5 + 0.0j), (1024, 0.5 + 0.8j)])
+def test_shifted_solve_large_pivoted(d, theta):
+    # d > 512: blocked getrf/getrs with partial pivoting; real shifts make A + theta I
+    # Hermitian indefinite, where interchanges are needed
+    rng = np.random.default_rng(d)
+    A, _, _ = workloads.random_complex_hermitian(d, -10.0, 10.0, seed=d)
+    H = HermitianMatrix(A)
+    V = rng.standard_normal((d, 3)) + 1j * rng.standard_normal((d, 3))
+    Y = shifted_solve(H, theta, V)
+    M = A + theta * np.eye(d)
+    for j in range(3):
+        assert np.linalg.norm(M @ Y[:, j] - V[:, j]) <= solve_residual_bound(H, theta, Y[:, j])
+    want = np.linalg.solve(M, V)
+    assert np.linalg.norm(Y - want) / np.linalg.norm(want) <= 1e-9
+
+
+def test_shifted_solve_large_singular():
+    d = 600
+    A = HermitianMatrix(np.diag(np.r_[np.ones(d - 1), 0.0]))
+    with pytest.raises(SingularSystem):
+        shifted_solve(A, 0.0, np.ones(d))
