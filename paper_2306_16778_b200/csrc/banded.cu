@@ -250,6 +250,10 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
         if ((rc = zgemm(stream, npairs, rest - ra, ra, jb, -1.0, sub(M, j0 + jb + ra, j0), sub(M, j0, j0 + jb),
                         sub(M, j0 + jb + ra, j0 + jb))))
           return rc;
+        // the trailing update becomes ready together with the next block's LU (both after the
+        // strips), so the higher-priority LU is dispatched first instead of queueing behind a
+        // grid of GEMM CTAs that claimed every SM during the strip updates
+        PFX_CUDA_TRY(cudaEventRecord(evP, stream));
         PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evP, 0));
         if ((rc = zgemm(S.s3, npairs, rest - ra, rest - ra, jb, -1.0, sub(M, j0 + jb + ra, j0),
                         sub(M, j0, j0 + jb + ra), sub(M, j0 + jb + ra, j0 + jb + ra))))
