@@ -28,7 +28,11 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // TM x TN output tile, NW warps in a 2 x (NW/2) grid, each warp FM x FN DMMA 8x8 tiles.
 // 64x64/8 warps for large problems; 32x32/4 warps when the 64-tile grid would leave SMs
 // idle (one 64x64x64 complex tile is ~16K DMMA cycles of a single SM).
-template <int TM, int TN, int NW>
+// M3: the 3M complex product -- three real DMMAs per complex 8x8x4 step instead of four:
+// T1 = sum Ar Br, T2 = sum Ai Bi, T3 = sum (Ar + Ai)(Br + Bi), then Cr = T1 - T2 and
+// Ci = T3 - T1 - T2 (normwise-stable; the imaginary part's error is bounded by eps |A||B|
+// instead of componentwise).
+template <int TM, int TN, int NW, bool M3 = false>
 __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                                                         int accumulate) {
   constexpr int NT = NW * 32;
@@ -44,10 +48,14 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
   const double2* Ab = A.p + b * A.stride;
   const double2* Bb = B.p + b * B.stride;
   double cr[FM][FN][2], ci[FM][FN][2];
+  double t3[M3 ? FM : 1][M3 ? FN : 1][2];  // M3: cr = T1, ci = T2, t3 = T3
 #pragma unroll
   for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < FN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) {
+      cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+      if (M3) t3[M3 ? i : 0][M3 ? j : 0][0] = t3[M3 ? i : 0][M3 ? j : 0][1] = 0.0;
+    }
 
   const int ktiles = (k + GK - 1) / GK;
   auto load = [&](int buf, int kt) {
@@ -92,12 +100,40 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
         br[j] = y.x;
         bi[j] = y.y;
       }
+      if (M3) {
+        double as[FM], bs[FN];
 #pragma unroll
-      for (int i = 0; i < FM; ++i)
+        for (int i = 0; i < FM; ++i) as[i] = ar[i] + ai[i];
 #pragma unroll
-        for (int j = 0; j < FN; ++j) zmma884(cr[i][j], ci[i][j], ar[i], ai[i], br[j], bi[j]);
+        for (int j = 0; j < FN; ++j) bs[j] = br[j] + bi[j];
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            dmma884(cr[i][j][0], cr[i][j][1], ar[i], br[j]);
+            dmma884(ci[i][j][0], ci[i][j][1], ai[i], bi[j]);
+            dmma884(t3[M3 ? i : 0][M3 ? j : 0][0], t3[M3 ? i : 0][M3 ? j : 0][1], as[i], bs[j]);
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) zmma884(cr[i][j], ci[i][j], ar[i], ai[i], br[j], bi[j]);
+      }
     }
     __syncthreads();
+  }
+  if (M3) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double t1 = cr[i][j][h], t2 = ci[i][j][h];
+          cr[i][j][h] = t1 - t2;
+          ci[i][j][h] = t3[M3 ? i : 0][M3 ? j : 0][h] - t1 - t2;
+        }
   }
   double2* Cb = C.p + b * C.stride;
 #pragma unroll
@@ -121,18 +157,19 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
   }
 }
 
-template <int TM, int TN, int NW>
+template <int TM, int TN, int NW, bool M3>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                         bool accumulate) {
   static bool attr = false;
   const int smem = (int)sizeof(GemmSmem<TM, TN>);
   if (!attr) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<TM, TN, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    PFX_CUDA_TRY(
+        cudaFuncSetAttribute(zgemm_kernel<TM, TN, NW, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch);
   PFX_LAUNCH_F("zgemm", s, 8.0 * (double)m * n * k * batch,
-               (zgemm_kernel<TM, TN, NW><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0)));
+               (zgemm_kernel<TM, TN, NW, M3><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
@@ -145,9 +182,13 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
     PFX_CUDA_TRY(cudaGetDevice(&dev));
     PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
   const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, 64) * (int64_t)batch;
-  if (tiles64 < 2 * sms) return zgemm_launch<32, 32, 4>(s, batch, m, n, k, alpha, A, B, C, accumulate);
-  return zgemm_launch<64, 64, 8>(s, batch, m, n, k, alpha, A, B, C, accumulate);
+  if (tiles64 < 2 * sms)
+    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate)
+              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate);
+  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate)
+            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate);
 }
 
 // ---------------------------------------------------------------------------

@@ -222,6 +222,31 @@ int main() {
     });
     timeit("LU alone (no memcpy)", [&] { zgetrf_diag(s, batch, nb, Dm, sing); });
   }
+  {
+    // C4 shapes (12 systems): LU trailing update, and the skinny block-row updates of the solves
+    const int nb4 = 12, D4 = 4096;
+    double2* Mb;
+    cudaMalloc(&Mb, (size_t)nb4 * D4 * D4 * 16);
+    cudaMemset(Mb, 0, (size_t)nb4 * D4 * D4 * 16);
+    ZMat A4{Mb, D4, (int64_t)D4 * D4};
+    auto sub4 = [&](int64_t i, int64_t j) { ZMat r = A4; r.p = Mb + i * D4 + j; return r; };
+    auto gf = [&](const char* nm, int m, int n, int k, ZMat A, ZMat Bm, ZMat C) {
+      for (int i = 0; i < 2; ++i) zgemm(s, nb4, m, n, k, -1.0, A, Bm, C);
+      cudaEventRecord(e0, s);
+      for (int i = 0; i < 5; ++i) zgemm(s, nb4, m, n, k, -1.0, A, Bm, C);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double t = ms / 5 * 1e-3, fl = 8.0 * m * n * (double)k * nb4;
+      printf("%-34s %9.1f us  %6.1f TFLOP/s  (%.0f%% of 36.9)\n", nm, t * 1e6, fl / t / 1e12, fl / t / 1e12 / 36.9 * 100);
+    };
+    gf("C4 LU update 4032x4032x64", 4032, 4032, 64, sub4(64, 0), sub4(0, 64), sub4(64, 64));
+    gf("C4 LU update 2048x2048x64", 2048, 2048, 64, sub4(64, 0), sub4(0, 64), sub4(64, 64));
+    gf("C4 fwd 64x2048xK2048", 64, 2048, 2048, sub4(2048, 0), sub4(0, 0), sub4(2048, 0));
+    gf("C4 bwd 64x4096xK2048", 64, 4096, 2048, sub4(0, 2048), sub4(2048, 0), sub4(0, 0));
+    cudaFree(Mb);
+  }
   timeit("zgetf2_panel 64x64 (old)", [&] {
     cudaMemcpyAsync(D, D0, dsz * 16, cudaMemcpyDeviceToDevice, s);
     zgetf2_panel(s, batch, nb, nb, Dm, nullptr, sing);
