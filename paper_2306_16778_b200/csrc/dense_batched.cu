@@ -100,7 +100,9 @@ __device__ __forceinline__ void block_argmax(double val, int idx, double* sv, in
 // interchanges + per-panel forward elimination turn them into L^{-1} P v).  The panel head of
 // the carried columns is broadcast through the strip buffer S (idle between the interchanges
 // and the strips; >= 32 x 33 complex >= NB x 4).
-template <int NB, bool PIV>
+// M3: the trailing update uses the 3M complex product (three DMMAs per step); only for the
+// one-CTA-per-SM variants, where its extra accumulators fit without spilling.
+template <int NB, bool PIV, bool M3>
 __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* __restrict__ Xa, int na,
                            double2* P, double2* S, double* red_v, int* red_i, int* s_piv, int* sing,
                            unsigned long long* dbg) {
@@ -315,6 +317,72 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       const int mrows = m - jb;
       const int rtiles = (mrows + 7) >> 3;
       const int ctiles = (sw + 7) >> 3;
+      if (M3) {
+      // 3M complex product (three DMMAs per complex 8x8x4 step): T1 = sum Lr Ur,
+      // T2 = sum Li Ui, T3 = sum (Lr + Li)(Ur + Ui); C -= (T1 - T2, T3 - T1 - T2).  The strip's
+      // column tiles go in two halves (half the live accumulators) and each half's C values
+      // are fetched before its k loop, so the loads overlap the DMMAs.
+      constexpr int CH = DB_SW / 16;  // column tiles per half
+      for (int rt = warp; rt < rtiles; rt += DB_WARPS) {
+        const int grow = p + jb + rt * 8 + g;  // C row owned by this lane
+        const int prow = jb + rt * 8 + g;      // panel row of the A fragment
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          const int cb = hf * CH;
+          if (cb >= ctiles) break;
+          double t1[CH][2], t2[CH][2], t3[CH][2];
+          double2 cv[CH][2];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            t1[u][0] = t1[u][1] = t2[u][0] = t2[u][1] = t3[u][0] = t3[u][1] = 0.0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c0 = (cb + u) * 8 + 2 * t + h;
+              cv[u][h] = (cb + u < ctiles && grow < d && c0 < sw) ? W[(size_t)grow * ldw + q + c0] : make_double2(0, 0);
+            }
+          }
+          for (int k0 = 0; k0 < jb; k0 += 4) {
+            double ar = 0.0, ai = 0.0;
+            if (prow < m && k0 + t < jb) {
+              double2 x = P[prow * PS + k0 + t];
+              ar = x.x;
+              ai = x.y;
+            }
+            const double as = ar + ai;
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+              if (cb + u < ctiles) {
+                double br = 0.0, bi = 0.0;
+                int col = (cb + u) * 8 + g;
+                if (k0 + t < jb && col < sw) {
+                  double2 y = S[(k0 + t) * SS + col];
+                  br = y.x;
+                  bi = y.y;
+                }
+                dmma884(t1[u][0], t1[u][1], ar, br);
+                dmma884(t2[u][0], t2[u][1], ai, bi);
+                dmma884(t3[u][0], t3[u][1], as, br + bi);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            if (cb + u < ctiles && grow < d) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int c0 = (cb + u) * 8 + 2 * t + h;
+                if (c0 < sw) {
+                  double2 x = cv[u][h];
+                  x.x -= t1[u][h] - t2[u][h];
+                  x.y -= t3[u][h] - t1[u][h] - t2[u][h];
+                  W[(size_t)grow * ldw + q + c0] = x;
+                }
+              }
+            }
+          }
+        }
+      }
+      } else {
       for (int rt = warp; rt < rtiles; rt += DB_WARPS) {
         double cr[DB_SW / 8][2], ci[DB_SW / 8][2];
         const int grow = p + jb + rt * 8 + g;  // C row owned by this lane
@@ -365,6 +433,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
             if (c0 + 1 < sw) W[(size_t)grow * ldw + q + c0 + 1] = make_double2(cr[ct][1], ci[ct][1]);
           }
         }
+      }
       }
       __syncthreads();
       if (dbg && tid == 0) {
@@ -549,7 +618,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[7], (unsigned long long)(clock64() - t_sys0));
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
-    lu_blocked<NB, PIV>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
+    lu_blocked<NB, PIV, MINB == 1>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t_lu0));
     long long t_sv0 = clock64();
