@@ -785,23 +785,31 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
     if (upper) khi = wn * 32 + 32;    // T upper: T[k][c] = 0 for k > c
     else klo = wn * 32;               // T lower: T[k][c] = 0 for k < c
   }
-  double cr[4][2], ci[4][2];
+  // 3M complex product: T1 = sum Xr Yr, T2 = sum Xi Yi, T3 = sum (Xr + Xi)(Yr + Yi)
+  double t1[4][2], t2[4][2], t3[4][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+  for (int j = 0; j < 4; ++j) t1[j][0] = t1[j][1] = t2[j][0] = t2[j][1] = t3[j][0] = t3[j][1] = 0.0;
   for (int k0 = klo; k0 < khi; k0 += 4) {
     double2 x;
     if (!RIGHT) x = Ts[(wm * 8 + g) * TM_S + k0 + tt];
     else x = Bs[(wm * 8 + g) * TM_S + k0 + tt];
-    double br[4], bi[4];
+    const double xs = x.x + x.y;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const double2 y = RIGHT ? Ts[(k0 + tt) * TM_S + wn * 32 + j * 8 + g] : Bs[(k0 + tt) * BSL + j * 8 + g];
-      br[j] = y.x;
-      bi[j] = y.y;
+      const double2 y = RIGHT ? Ts[(k0 + tt) * TM_S + wn * 32 + j * 8 + g] : Bs[(k0 + tt) * (TM_W + 1) + j * 8 + g];
+      dmma884(t1[j][0], t1[j][1], x.x, y.x);
+      dmma884(t2[j][0], t2[j][1], x.y, y.y);
+      dmma884(t3[j][0], t3[j][1], xs, y.x + y.y);
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) zmma884(cr[j], ci[j], x.x, x.y, br[j], bi[j]);
   }
+  double cr[4][2], ci[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      cr[j][h] = t1[j][h] - t2[j][h];
+      ci[j][h] = t3[j][h] - t1[j][h] - t2[j][h];
+    }
   const int r = wm * 8 + g;
 #pragma unroll
   for (int j = 0; j < 4; ++j)
