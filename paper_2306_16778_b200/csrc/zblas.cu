@@ -596,27 +596,14 @@ constexpr int DI_S = DI_MAX + 1;
 // instruction cache).  Step j: row j publishes itself to shared memory (double-buffered:
 // one barrier per column), every lower row takes its multiplier's numerator from the
 // owning lane by shuffle and updates its entries right of j.  nb < 64 pads with I.
-__global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* sing) {
-  // the pivot row buffer runs 64 entries past the block, kept zero: the updates of the
-  // dead registers (a[i], i >= 16 - q) read those zeros, so every update is unconditional
-  // straight-line code the compiler can schedule as one batch of loads + DFMAs
-  __shared__ __align__(16) double2 prow[2][2 * DI_MAX];
-  const int b = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int row = tid >> 2, cg = tid & 3;
-  prow[tid >> 7][tid & 127] = make_double2(0, 0);
-  const unsigned base = (unsigned)__cvta_generic_to_shared(&prow[0][0]);
+// One phase of four 4-column blocks with NL live registers (the window holds columns
+// phase + 4 (q + i), i < NL; NL >= 16 - q for every q of the phase, the excess are zeros).
+template <int NL>
+__device__ __forceinline__ void lu_diag_phase(int q0, cplx (&a)[16], int nb, ZMat D, int b, int row, int cg,
+                                              int lane, unsigned base, int* sing) {
   constexpr unsigned BUF = 2 * DI_MAX * 16;  // bytes per pivot-row buffer
-  cplx a[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int c = cg + 4 * i;
-    if (row < nb && c < nb) a[i] = ld(D.at(b, row, c));
-    else a[i] = mk(row == c ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
 #pragma unroll 1
-  for (int q = 0; q < 16; ++q) {
+  for (int q = q0; q < q0 + 4; ++q) {
     const unsigned qb = base + (unsigned)(cg + 4 * q) * 16u;  // &prow[0][cg + 4q]
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
@@ -626,7 +613,7 @@ __global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* s
         // entries left of j in the first register are stale multipliers: publish only c >= j
         if (cg >= jj) sts2(pb, a[0]);
 #pragma unroll
-        for (int i = 1; i < 16; ++i) sts2(pb + 64u * i, a[i]);  // dead registers are zero
+        for (int i = 1; i < NL; ++i) sts2(pb + 64u * i, a[i]);
         if (cg == jj && a[0].re == 0.0 && a[0].im == 0.0) *sing = 1;
       }
       __syncthreads();
@@ -638,16 +625,47 @@ __global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* s
         const cplx l = cmul(aj, crcp_fast(lds2(base + (jj & 1) * BUF + (unsigned)j * 16u)));
         const cplx a0 = cfms(a[0], l, lds2(pb));
 #pragma unroll
-        for (int i = 1; i < 16; ++i) a[i] = cfms(a[i], l, lds2(pb + 64u * i));
+        for (int i = 1; i < NL; ++i) a[i] = cfms(a[i], l, lds2(pb + 64u * i));
         a[0] = cg == jj ? l : (cg > jj ? a0 : a[0]);
       }
     }
     const int c = cg + 4 * q;
     if (row < nb && c < nb) *D.at(b, row, c) = make_double2(a[0].re, a[0].im);
 #pragma unroll
-    for (int i = 0; i < 15; ++i) a[i] = a[i + 1];
-    a[15] = mk(0, 0);
+    for (int i = 0; i < NL - 1; ++i) a[i] = a[i + 1];
+    a[NL - 1] = mk(0, 0);
   }
+}
+
+// Register-resident: thread (row = tid / 4, phase = tid % 4) holds A[row][phase + 4(q + i)]
+// where q is the current 4-column block: after every 4 columns the finished register a[0]
+// is stored and the window rotates, so register indices stay static.  The column loop runs
+// in four phases whose live width (16, 12, 8, 4 registers) tracks the shrinking trailing
+// matrix, so dead registers are not updated.  Step j: row j publishes itself to shared
+// memory (double-buffered: one barrier per column), every lower row takes its multiplier's
+// numerator from the owning lane by shuffle and updates its entries right of j.
+// nb < 64 pads with the identity.
+__global__ void __launch_bounds__(256) zgetrf_diag_kernel(int nb, ZMat D, int* sing) {
+  // the pivot row buffer runs 64 entries past the block, kept zero: updates of registers
+  // past the live window read those zeros
+  __shared__ __align__(16) double2 prow[2][2 * DI_MAX];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int row = tid >> 2, cg = tid & 3;
+  prow[tid >> 7][tid & 127] = make_double2(0, 0);
+  const unsigned base = (unsigned)__cvta_generic_to_shared(&prow[0][0]);
+  cplx a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int c = cg + 4 * i;
+    if (row < nb && c < nb) a[i] = ld(D.at(b, row, c));
+    else a[i] = mk(row == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  lu_diag_phase<16>(0, a, nb, D, b, row, cg, lane, base, sing);
+  lu_diag_phase<12>(4, a, nb, D, b, row, cg, lane, base, sing);
+  lu_diag_phase<8>(8, a, nb, D, b, row, cg, lane, base, sing);
+  lu_diag_phase<4>(12, a, nb, D, b, row, cg, lane, base, sing);
 }
 
 // Triangular inverses of the factored block: grid (nb/8 column groups, 2 triangles, batch);
