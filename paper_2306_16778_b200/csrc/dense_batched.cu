@@ -249,17 +249,45 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       tph = clock64();
     }
     // ---- strips of the trailing columns: U12 = L11^{-1} A12, A22 -= L21 U12
-    // ---- carried right-hand sides: head = L11^{-1} head (warp per column, shuffles; the
-    // result also goes to shared memory), then tail -= L21 head (thread per row and column)
-    if (na > 0) {
-      double2* xs = S;
-      for (int c = warp; c < na; c += DB_WARPS) {
-        cplx x = lane < jb ? ld(&Xa[(size_t)(p + lane) * na + c]) : mk(0.0, 0.0);
-        for (int k = 0; k < jb; ++k) {
+    // ---- L11^{-1} (unit lower) over the panel's top block (the panel is already back in W,
+    // and only L21 below it is read from here on): warp per column, lane = row, forward
+    // substitution by shuffles.  The strips then apply it on DMMA instead of a dependent
+    // triangular solve.
+    {
+      constexpr int CPW = NB / DB_WARPS;  // columns per warp
+      cplx inv[CPW];
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) {
+        const int c = warp + u * DB_WARPS;
+        cplx x = mk(lane == c ? 1.0 : 0.0, 0.0);
+        for (int k = c; k < jb; ++k) {
           cplx xk;
           xk.re = __shfl_sync(0xffffffffu, x.re, k);
           xk.im = __shfl_sync(0xffffffffu, x.im, k);
           if (lane > k && lane < jb) x = cfms(x, ld(&P[lane * PS + k]), xk);
+        }
+        inv[u] = x;
+      }
+      __syncthreads();  // every read of L11 is done
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) {
+        const int c = warp + u * DB_WARPS;
+        if (lane < jb && c < jb) st(&P[lane * PS + c], inv[u]);
+      }
+      __syncthreads();
+    }
+    // ---- carried right-hand sides: head = L11^{-1} head (warp per column; the result also
+    // goes to shared memory), then tail -= L21 head (thread per row and column)
+    if (na > 0) {
+      double2* xs = S;
+      for (int c = warp; c < na; c += DB_WARPS) {
+        const cplx h = lane < jb ? ld(&Xa[(size_t)(p + lane) * na + c]) : mk(0.0, 0.0);
+        cplx x = mk(0.0, 0.0);
+        for (int k = 0; k < jb; ++k) {
+          cplx hk;
+          hk.re = __shfl_sync(0xffffffffu, h.re, k);
+          hk.im = __shfl_sync(0xffffffffu, h.im, k);
+          if (lane >= k && lane < jb) x = cfma(ld(&P[lane * PS + k]), hk, x);
         }
         if (lane < jb) {
           st(&Xa[(size_t)(p + lane) * na + c], x);
@@ -283,26 +311,44 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         S[r * SS + c] = W[(size_t)(p + r) * ldw + q + c];
       }
       __syncthreads();
-      // unit-lower triangular solve: warp w owns strip columns 8w..8w+7, lane = row; the 8
-      // columns are solved together in registers (ILP 8), pivots broadcast by shuffles
+      // U12 = L11^{-1} A12 on DMMA: output 8x8 tiles (NB/8 row tiles x sw/8 column tiles)
+      // spread over the warps; results held in registers until every read of S is done
       {
-        const int c0 = warp * 8;
-        cplx x[8];
+        constexpr int MT = NB / 8;
+        constexpr int TPW = (MT * (DB_SW / 8) + DB_WARPS - 1) / DB_WARPS;  // tiles per warp
+        const int ntl = MT * ((sw + 7) >> 3);
+        double cr[TPW][2], ci[TPW][2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = (lane < jb && c0 + u < sw) ? ld(&S[lane * SS + c0 + u]) : mk(0.0, 0.0);
-        for (int k = 0; k < jb; ++k) {
-          const cplx l = (lane > k && lane < jb) ? ld(&P[lane * PS + k]) : mk(0.0, 0.0);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            cplx xk;
-            xk.re = __shfl_sync(0xffffffffu, x[u].re, k);
-            xk.im = __shfl_sync(0xffffffffu, x[u].im, k);
-            x[u] = cfms(x[u], l, xk);
+        for (int u = 0; u < TPW; ++u) {
+          cr[u][0] = cr[u][1] = ci[u][0] = ci[u][1] = 0.0;
+          const int tl = warp + u * DB_WARPS;
+          if (tl < ntl) {
+            const int mt = tl % MT, nt = tl / MT;
+            for (int k0 = 0; k0 < jb; k0 += 4) {
+              const int kk = k0 + t;
+              double2 x = make_double2(0, 0), y = make_double2(0, 0);
+              if (kk < jb) {
+                x = P[(mt * 8 + g) * PS + kk];
+                if (nt * 8 + g < sw) y = S[kk * SS + nt * 8 + g];
+              }
+              zmma884(cr[u], ci[u], x.x, x.y, y.x, y.y);
+            }
           }
         }
+        __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (lane < jb && c0 + u < sw) st(&S[lane * SS + c0 + u], x[u]);
+        for (int u = 0; u < TPW; ++u) {
+          const int tl = warp + u * DB_WARPS;
+          if (tl < ntl) {
+            const int mt = tl % MT, nt = tl / MT;
+            const int r = mt * 8 + g;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = nt * 8 + 2 * t + h;
+              if (r < jb && c < sw) S[r * SS + c] = make_double2(cr[u][h], ci[u][h]);
+            }
+          }
+        }
       }
       __syncthreads();
       for (int e = tid; e < jb * sw; e += DB_THREADS) {
