@@ -1,11 +1,13 @@
-// Batched complex128 GEMM / TRSM / LU-panel kernels for sm_100a (see zblas.cuh).
+// Batched complex128 block toolkit for sm_100a (see zblas.cuh): GEMM, diagonal-block LU and
+// triangular inverses, in-place triangular products, and the pivoting panel / row
+// interchange / TRSM kernels of the general shifted solve.
 //
-// zgemm: 64x64 output tile per CTA, K staged 16 complex at a time through shared
-// memory with cp.async double buffering, 8 warps each owning a 32x16 sub-tile of
-// 4x2 DMMA 8x8 tiles.  A complex 8x8x4 product is four real DMMA.8x8x4
-// (Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br).  Shared-memory rows are padded by one
-// complex element so both fragment loads spread over all 32 banks (4 wavefronts per
-// 512-byte warp request, the minimum).
+// zgemm: 64x64 (8 warps, 32x16 per warp) or 32x32 (4 warps) output tile per CTA, K staged
+// 16 complex at a time through shared memory with cp.async double buffering.  A complex
+// 8x8x4 step is three real DMMA.8x8x4 (3M: T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi);
+// Cr = T1 - T2, Ci = T3 - T1 - T2), or four with PFX_ZGEMM_4M=1.  Shared-memory rows are
+// padded by one complex element so both fragment loads spread over all 32 banks (4
+// wavefronts per 512-byte warp request, the minimum).
 #include "zblas.cuh"
 
 namespace pfx {
@@ -467,43 +469,6 @@ __global__ void __launch_bounds__(T_THREADS) ztrsm_left_kernel(int nb, int n, ZM
   }
 }
 
-// Right upper solve B = B U^{-1} (m x nb): each CTA owns 32 rows (one lane per row).
-__global__ void __launch_bounds__(T_THREADS) ztrsm_runn_kernel(int m, int nb, ZMat U, ZMat B) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* Us = reinterpret_cast<double2*>(smem_raw);  // nb x (nb+1)
-  double2* Bs = Us + nb * (nb + 1);                    // T_COLS rows x (nb+1)
-  const int b = blockIdx.y;
-  const int r0 = blockIdx.x * T_COLS;
-  const int tid = threadIdx.x;
-  const double2* Ub = U.p + b * U.stride;
-  double2* Bb = B.p + b * B.stride;
-  for (int e = tid; e < nb * nb; e += T_THREADS) {
-    int r = e / nb, c = e % nb;
-    Us[r * (nb + 1) + c] = Ub[(int64_t)r * U.ld + c];
-  }
-  for (int e = tid; e < T_COLS * nb; e += T_THREADS) {
-    int r = e / nb, c = e % nb;
-    Bs[r * (nb + 1) + c] = (r0 + r < m) ? Bb[(int64_t)(r0 + r) * B.ld + c] : make_double2(0, 0);
-  }
-  __syncthreads();
-  // warp w owns rows 4w..4w+3; lanes 8r..8r+7 share row 4w+r and split the columns
-  const int warp = tid >> 5, lane = tid & 31;
-  const int row = warp * 4 + (lane >> 3), cs = lane & 7;
-  for (int j = 0; j < nb; ++j) {
-    const cplx x = cmul(ld(&Bs[row * (nb + 1) + j]), crcp_fast(ld(&Us[j * (nb + 1) + j])));
-    __syncwarp();
-    if (cs == 0) st(&Bs[row * (nb + 1) + j], x);
-    for (int c = j + 1 + cs; c < nb; c += 8)
-      st(&Bs[row * (nb + 1) + c], cfms(ld(&Bs[row * (nb + 1) + c]), x, ld(&Us[j * (nb + 1) + c])));
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int e = tid; e < T_COLS * nb; e += T_THREADS) {
-    int r = e / nb, c = e % nb;
-    if (r0 + r < m) Bb[(int64_t)(r0 + r) * B.ld + c] = Bs[r * (nb + 1) + c];
-  }
-}
-
 static int trsm_smem(int nb) { return (int)((size_t)nb * (nb + 1) + (size_t)nb * (T_COLS + 1)) * (int)sizeof(double2); }
 static const int kTrsmSmemMax = (64 * 65 + 64 * 33) * (int)sizeof(double2);
 static int trsm_attrs() {
@@ -511,7 +476,6 @@ static int trsm_attrs() {
   if (!done) {
     PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_left_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
     PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_left_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
-    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_runn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
     done = true;
   }
   return PFX_OK;
@@ -536,52 +500,6 @@ int ztrsm_lunn(cudaStream_t s, int batch, int nb, int n, ZMat Um, ZMat B) {
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
-
-int ztrsm_runn(cudaStream_t s, int batch, int m, int nb, ZMat Um, ZMat B) {
-  if (m <= 0) return PFX_OK;
-  const int smem = trsm_smem(nb);
-  if (int rc = trsm_attrs()) return rc;
-  dim3 grid((unsigned)ceil_div(m, T_COLS), (unsigned)batch);
-  PFX_LAUNCH("ztrsm", s, ztrsm_runn_kernel<<<grid, T_THREADS, smem, s>>>(m, nb, Um, B));
-  PFX_CUDA_TRY(cudaGetLastError());
-  return PFX_OK;
-}
-
-
-__global__ void zeye_kernel(ZMat E, int nb) {
-  const int b = blockIdx.y;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nb * nb; e += gridDim.x * blockDim.x) {
-    const int r = e / nb, c = e - r * nb;
-    *E.at(b, r, c) = make_double2(r == c ? 1.0 : 0.0, 0.0);
-  }
-}
-
-__global__ void zcopy_kernel(ZMat Src, ZMat Dst, int rows, int cols) {
-  const int b = blockIdx.y;
-  const int64_t n = (int64_t)rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / cols, c = e - r * cols;
-    *Dst.at(b, r, c) = *Src.at(b, r, c);
-  }
-}
-
-int ztrsm_left_gemm(cudaStream_t s, int batch, int nb, int n, ZMat T, ZMat B, bool upper) {
-  if (n <= 0) return PFX_OK;
-  const size_t inv_elems = (size_t)batch * nb * nb, tmp_elems = (size_t)batch * nb * n;
-  double2* ws = static_cast<double2*>(scratch(7, (inv_elems + tmp_elems) * sizeof(double2)));
-  if (!ws) return fail(PFX_CUDA, "trsm workspace allocation failed");
-  ZMat Inv{ws, nb, (int64_t)nb * nb};
-  ZMat Tmp{ws + inv_elems, n, (int64_t)nb * n};
-  PFX_LAUNCH("zeye", s, zeye_kernel<<<dim3(16, batch), 256, 0, s>>>(Inv, nb));
-  PFX_CUDA_TRY(cudaGetLastError());
-  int rc = upper ? ztrsm_lunn(s, batch, nb, nb, T, Inv) : ztrsm_llnu(s, batch, nb, nb, T, Inv);
-  if (rc) return rc;
-  if ((rc = zgemm(s, batch, nb, n, nb, 1.0, Inv, B, Tmp, false))) return rc;
-  PFX_LAUNCH("zcopy", s, zcopy_kernel<<<dim3(256, batch), 256, 0, s>>>(Tmp, B, nb, n));
-  PFX_CUDA_TRY(cudaGetLastError());
-  return PFX_OK;
-}
-
 
 // ---------------------------------------------------------------------------
 // Diagonal-block LU (nb <= 64, no pivoting), one CTA (256 threads) per batch member,

@@ -22,11 +22,6 @@ struct ZMat {
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
           bool accumulate = true);
 
-// Wide triangular solves through the tensor cores: T^{-1} (nb x nb) is formed once per
-// batch member (small TRSM on the identity) and applied with zgemm into scratch, then
-// copied back.  Used when n is large (the forward/backward substitutions of C4).
-int ztrsm_left_gemm(cudaStream_t s, int batch, int nb, int n, ZMat T, ZMat B, bool upper);
-
 // No-pivot LU of the nb x nb diagonal block D (nb <= 64) in shared memory, in place.
 int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing);
 // Triangular inverses of a factored diagonal block: Li = L^{-1} (unit lower), Ui = U^{-1}.
@@ -48,7 +43,5 @@ int zlaswp(cudaStream_t s, int batch, int nb, ZMat A, int64_t r0, int64_t c0, in
 int ztrsm_llnu(cudaStream_t s, int batch, int nb, int n, ZMat Lm, ZMat B);
 // B = U^{-1} B, U = upper (non-unit) nb x nb, B nb x n.
 int ztrsm_lunn(cudaStream_t s, int batch, int nb, int n, ZMat Um, ZMat B);
-// B = B U^{-1}, U = upper (non-unit) nb x nb, B m x nb.
-int ztrsm_runn(cudaStream_t s, int batch, int m, int nb, ZMat Um, ZMat B);
 
 }  // namespace pfx
