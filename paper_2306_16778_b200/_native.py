@@ -117,12 +117,18 @@ def pole_table(n: int):
 
 # ---- device plumbing (torch) --------------------------------------------------
 
-def _torch():
-    import torch
+_torch_ok = None
 
-    if not torch.cuda.is_available():
-        raise PfexpmError("no CUDA device: the B200 engine has no CPU fallback")
-    return torch
+
+def _torch():
+    global _torch_ok
+    if _torch_ok is None:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise PfexpmError("no CUDA device: the B200 engine has no CPU fallback")
+        _torch_ok = torch
+    return _torch_ok
 
 
 def _stream_ptr(stream=None) -> int:

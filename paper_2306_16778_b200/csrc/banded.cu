@@ -371,8 +371,9 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
   PFX_LAUNCH("bd_combine", stream, bd_combine<<<1184, 256, 0, stream>>>(X, N * nrhs, npairs, coef_d, scale, out));
   PFX_CUDA_TRY(cudaGetLastError());
-  int sg = 0;
-  PFX_CUDA_TRY(cudaMemcpyAsync(&sg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  int* hsg = pinned_word();
+  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
+  PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (per_pair_ms) PFX_CUDA_TRY(cudaEventRecord(e1, stream));
   PFX_CUDA_TRY(cudaStreamSynchronize(stream));
   if (per_pair_ms) {
@@ -382,7 +383,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  if (sg) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted band factorization");
+  if (*hsg) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted band factorization");
   return PFX_OK;
 }
 

@@ -18,6 +18,8 @@
 // the slot.
 #include <cstdlib>
 
+#include <vector>
+
 #include "pfx_common.cuh"
 
 namespace pfx {
@@ -785,9 +787,11 @@ int dense_batched_supported(int64_t d) { return d >= 1 && d <= 512; }
 int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
                       int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,
                       int npairs, double* out, cudaStream_t stream, float* launch_ms, int pivot) {
-  int dev = 0, sms = 0;
+  int dev = 0;
   PFX_CUDA_TRY(cudaGetDevice(&dev));
-  PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static int sms_of[16] = {};
+  if (dev < 16 && !sms_of[dev]) PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
+  int sms = dev < 16 ? sms_of[dev] : 148;
   int dev_sms = sms;
   const bool many = (int64_t)batch * npairs > dev_sms;
   const int nb = (d <= 256 && !many) ? 32 : 16;
@@ -847,7 +851,7 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
                                 : (minb == 2 ? dense_batched_kernel<16, 2, true> : dense_batched_kernel<16, 1, true>))
                     : (nb == 32 ? dense_batched_kernel<32, 1, false>
                                 : (minb == 2 ? dense_batched_kernel<16, 2, false> : dense_batched_kernel<16, 1, false>));
-  PFX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(kern), smem)) return rc;
   PFX_LAUNCH("dense_batched_kernel", stream, kern<<<slots, DB_THREADS, smem, stream>>>(args));
   PFX_CUDA_TRY(cudaGetLastError());
   const size_t per_out = per_sys * (real_path ? 1 : 2);
@@ -862,9 +866,11 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  int st = 0;
-  PFX_CUDA_TRY(cudaMemcpyAsync(&st, args.status, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  int* hst = pinned_word();
+  if (!hst) return fail(PFX_CUDA, "pinned status word allocation failed");
+  PFX_CUDA_TRY(cudaMemcpyAsync(hst, args.status, sizeof(int), cudaMemcpyDeviceToHost, stream));
   PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  const int st = *hst;
   if (args.dbg) {
     unsigned long long h[8];
     PFX_CUDA_TRY(cudaMemcpy(h, args.dbg, sizeof(h), cudaMemcpyDeviceToHost));

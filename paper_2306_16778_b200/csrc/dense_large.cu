@@ -182,8 +182,9 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
              dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
                                                  out));
   PFX_CUDA_TRY(cudaGetLastError());
-  int sg = 0;
-  PFX_CUDA_TRY(cudaMemcpyAsync(&sg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  int* hsg = pinned_word();
+  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
+  PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (per_pair_ms) {
     PFX_CUDA_TRY(cudaEventRecord(e1, stream));
   }
@@ -195,7 +196,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  if (sg) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
+  if (*hsg) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
   return PFX_OK;
 }
 
@@ -261,10 +262,11 @@ int shifted_solve_large(const double* A, int a_complex, int d, const double2* th
     if ((rc = ztrsm_lunn(stream, 1, jb, nrhs, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
   }
   PFX_CUDA_TRY(cudaMemcpyAsync(Y, X.p, xbytes, cudaMemcpyDeviceToDevice, stream));
-  int sg = 0;
-  PFX_CUDA_TRY(cudaMemcpyAsync(&sg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  int* hsg = pinned_word();
+  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
+  PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   PFX_CUDA_TRY(cudaStreamSynchronize(stream));
-  if (sg) return fail(PFX_SINGULAR, "exactly zero pivot in the shifted factorization");
+  if (*hsg) return fail(PFX_SINGULAR, "exactly zero pivot in the shifted factorization");
   return PFX_OK;
 }
 

@@ -86,6 +86,31 @@ Arena g_arena[kMaxDev];
 std::mutex g_arena_mu;
 }  // namespace
 
+int* pinned_word() {
+  thread_local int* p = nullptr;
+  if (!p && cudaMallocHost(reinterpret_cast<void**>(&p), 64) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+  }
+  return p;
+}
+
+int raise_smem_limit(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> set;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : set)
+    if (e.first == kernel) {
+      if (e.second >= bytes) return PFX_OK;
+      PFX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      e.second = bytes;
+      return PFX_OK;
+    }
+  PFX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  set.emplace_back(kernel, bytes);
+  return PFX_OK;
+}
+
 void* scratch(int slot, size_t bytes) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev || slot >= kSlots) return nullptr;

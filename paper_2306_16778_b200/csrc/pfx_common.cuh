@@ -26,6 +26,12 @@ int fail(int status, const std::string& msg);
 // Grow-only device scratch arena, one per (device, slot).  Slots let one call
 // hold several live buffers.  Freed by pfx_release().
 void* scratch(int slot, size_t bytes);
+// a pinned host word per thread for the status readback (a pageable 4-byte copy is staged
+// through a driver bounce buffer: tens of microseconds on the small configs)
+int* pinned_word();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `bytes` exceeds what was set
+// before for this kernel (the call itself costs host time on every launch otherwise)
+int raise_smem_limit(const void* kernel, size_t bytes);
 void release_scratch();
 
 // Kernel timing (pfx_prof_enable / pfx_prof_read).  PFX_LAUNCH brackets a launch

@@ -814,8 +814,8 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     };
     auto k0 = pick(std::integral_constant<int, 0>{});
     auto k1 = pick(std::integral_constant<int, 1>{});
-    PFX_CUDA_TRY(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PFX_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(k0), smem)) return rc;
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(k1), smem)) return rc;
     // row groups: whole chunks, one launch each (a single group in device mode)
     const int ng = pipe ? (int)std::min<int64_t>(TR_GROUPS, P) : 1;
     auto grp = [&](int g, int64_t& c0, int64_t& c1) {
