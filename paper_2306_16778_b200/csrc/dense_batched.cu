@@ -143,7 +143,20 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
           double2* row = &P[r * PS];
           const cplx l = cmul(ld(&row[jj]), rp);
-          for (int c = jj + 1; c < jb; ++c) st(&row[c], cfms(ld(&row[c]), l, ld(&P[jj * PS + c])));
+          const double2* prow_j = &P[jj * PS];
+          // four columns per round: all loads first (this row is never the pivot row, but
+          // the compiler cannot prove it), then the updates and stores
+          for (int c = jj + 1; c < jb; c += 4) {
+            cplx x[4], y[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              x[u] = c + u < jb ? ld(&row[c + u]) : mk(0.0, 0.0);
+              y[u] = c + u < jb ? ld(&prow_j[c + u]) : mk(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c + u < jb) st(&row[c + u], cfms(x[u], l, y[u]));
+          }
           st(&row[jj], l);
         }
       }
