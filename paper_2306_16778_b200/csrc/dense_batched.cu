@@ -527,16 +527,34 @@ __device__ void trsv_blocked(const double2* __restrict__ W, int d, size_t ldw, i
     const int j1 = forward ? i0 : d;
     // GEMV: part[i] = sum_j op(W)[i][j] z[j]
     if (kind <= 1) {
-      // rows of W are contiguous: warp w handles rows i0+w, i0+w+8, ...; lanes stride j
-      for (int ii = warp; ii < bs; ii += DB_WARPS) {
-        const double2* row = W + (size_t)(i0 + ii) * ldw;
-        cplx acc = mk(0.0, 0.0);
-        for (int j = j0 + lane; j < j1; j += 32) acc = cadd(acc, cmul(ld(&row[j]), ld(&z[j])));
-        for (int off = 16; off > 0; off >>= 1) {
-          acc.re += __shfl_down_sync(0xffffffffu, acc.re, off);
-          acc.im += __shfl_down_sync(0xffffffffu, acc.im, off);
+      // rows of W are contiguous: warp w handles rows i0+w, i0+w+8, i0+w+16, i0+w+24 together
+      // (four independent L2 loads per column step, two column steps per round); lanes stride j
+      constexpr int RW = 32 / DB_WARPS;  // rows per warp
+      cplx acc[RW];
+#pragma unroll
+      for (int u = 0; u < RW; ++u) acc[u] = mk(0.0, 0.0);
+      for (int j = j0 + lane; j < j1; j += 64) {
+        const bool j2 = j + 32 < j1;
+        const cplx z0 = ld(&z[j]), z1 = j2 ? ld(&z[j + 32]) : mk(0.0, 0.0);
+        cplx w0[RW], w1[RW];
+#pragma unroll
+        for (int u = 0; u < RW; ++u) {
+          const int ii = warp + u * DB_WARPS;
+          const double2* row = W + (size_t)(i0 + ii) * ldw;
+          w0[u] = ii < bs ? ld(&row[j]) : mk(0.0, 0.0);
+          w1[u] = (ii < bs && j2) ? ld(&row[j + 32]) : mk(0.0, 0.0);
         }
-        if (lane == 0) st(&part[ii], acc);
+#pragma unroll
+        for (int u = 0; u < RW; ++u) acc[u] = cfma(w1[u], z1, cfma(w0[u], z0, acc[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < RW; ++u) {
+        for (int off = 16; off > 0; off >>= 1) {
+          acc[u].re += __shfl_down_sync(0xffffffffu, acc[u].re, off);
+          acc[u].im += __shfl_down_sync(0xffffffffu, acc[u].im, off);
+        }
+        const int ii = warp + u * DB_WARPS;
+        if (lane == 0 && ii < bs) st(&part[ii], acc[u]);
       }
     } else {
       // op(W)[i][j] = conj(W[j][i]): lanes along i (contiguous in row j), warps stride j
