@@ -169,8 +169,8 @@ __global__ void __launch_bounds__(256) bd_back_finish(ZMat X, ZMat Ui, int64_t j
 // where it overlaps the next block steps (its inputs, L11^{-1} per block and the L21
 // columns, are never written again).
 struct BdStreams {
-  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
+  cudaEvent_t ev[8] = {};
 };
 static int bd_streams(BdStreams& S) {
   static BdStreams g;
@@ -180,6 +180,7 @@ static int bd_streams(BdStreams& S) {
     int lo = 0, hi = 0;
     PFX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s1, cudaStreamNonBlocking, hi));
+    PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s4, cudaStreamNonBlocking, hi));
     PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s2, cudaStreamNonBlocking, lo));
     PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s3, cudaStreamNonBlocking, lo));
     for (auto& e : g.ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -211,6 +212,8 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
     return e ? atoi(e) : 0;
   }();
   cudaEvent_t evT = S.ev[0], evU = S.ev[1], evL = S.ev[2], evR = S.ev[3], evP = S.ev[4], evB = S.ev[5];
+  cudaEvent_t evS = S.ev[6], evA = S.ev[7];
+  bool pending_s = false;  // strips of the previous step queued on s4
   // s2 / s3 start after everything already queued on main (the build kernel)
   PFX_CUDA_TRY(cudaEventRecord(evT, stream));
   PFX_CUDA_TRY(cudaStreamWaitEvent(S.s2, evT, 0));
@@ -221,6 +224,8 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
     const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);  // rows/cols coupled below/right
     if (!(skip & 8) && (rc = zgetrf_diag(stream, npairs, jb, sub(M, j0, j0), sing))) return rc;
     if (!(skip & 8) && (rc = ztrtri_diag(stream, npairs, jb, sub(M, j0, j0), blk(Li, j0), blk(Ui, j0)))) return rc;
+    // this block's panels are the previous step's strips (s4)
+    if (pending_s) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evS, 0));
     if (rest > 0 && !(skip & 16)) {
       PFX_CUDA_TRY(cudaEventRecord(evT, stream));
       PFX_CUDA_TRY(cudaStreamWaitEvent(S.s1, evT, 0));
@@ -235,36 +240,45 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
                                 sub(X, j0 + jb, 0))))
       return rc;
     if (rest > 0) {
-      // look-ahead: the next block's row strip (ra rows, all rest columns) and column strip
-      // are updated first on main; the trailing (rest - ra)^2 part goes to s3, where it
-      // overlaps the next block's LU / inverses / panel products.  The strips lie inside
-      // the previous step's trailing region, so main waits for it (evB) first.
+      // look-ahead: only the next diagonal block (ra x ra) is updated on main before the next
+      // LU; the rest of the next row / column strips (needed by the next panel products)
+      // go to s4, and the trailing (rest - ra)^2 part to s3, both overlapping the next LU /
+      // inverses.  Everything here lies inside the previous step's trailing region, so main
+      // waits for it (evB) first.
       const int ra = std::min(nb, rest);
       PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
       if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));
       PFX_CUDA_TRY(cudaEventRecord(evP, stream));  // panels of this step are final
-      if ((rc = zgemm(stream, npairs, ra, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
+      if ((rc = zgemm(stream, npairs, ra, ra, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
                       sub(M, j0 + jb, j0 + jb))))
         return rc;
-      if (rest > ra && !(skip & 4)) {
-        if ((rc = zgemm(stream, npairs, rest - ra, ra, jb, -1.0, sub(M, j0 + jb + ra, j0), sub(M, j0, j0 + jb),
+      pending_s = false;
+      pending_b = false;
+      if (rest > ra) {
+        PFX_CUDA_TRY(cudaStreamWaitEvent(S.s4, evP, 0));
+        if ((rc = zgemm(S.s4, npairs, ra, rest - ra, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb + ra),
+                        sub(M, j0 + jb, j0 + jb + ra))))
+          return rc;
+        if ((rc = zgemm(S.s4, npairs, rest - ra, ra, jb, -1.0, sub(M, j0 + jb + ra, j0), sub(M, j0, j0 + jb),
                         sub(M, j0 + jb + ra, j0 + jb))))
           return rc;
-        // the trailing update becomes ready together with the next block's LU (both after the
-        // strips), so the higher-priority LU is dispatched first instead of queueing behind a
-        // grid of GEMM CTAs that claimed every SM during the strip updates
-        PFX_CUDA_TRY(cudaEventRecord(evP, stream));
-        PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evP, 0));
-        if ((rc = zgemm(S.s3, npairs, rest - ra, rest - ra, jb, -1.0, sub(M, j0 + jb + ra, j0),
-                        sub(M, j0, j0 + jb + ra), sub(M, j0 + jb + ra, j0 + jb + ra))))
-          return rc;
-        PFX_CUDA_TRY(cudaEventRecord(evB, S.s3));
-        pending_b = true;
-      } else {
-        pending_b = false;
+        PFX_CUDA_TRY(cudaEventRecord(evS, S.s4));
+        pending_s = true;
+        if (!(skip & 4)) {
+          // the trailing update becomes ready together with the next block's LU (both after
+          // the diagonal-block update), so the higher-priority LU is dispatched first
+          PFX_CUDA_TRY(cudaEventRecord(evA, stream));
+          PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evA, 0));
+          if ((rc = zgemm(S.s3, npairs, rest - ra, rest - ra, jb, -1.0, sub(M, j0 + jb + ra, j0),
+                          sub(M, j0, j0 + jb + ra), sub(M, j0 + jb + ra, j0 + jb + ra))))
+            return rc;
+          PFX_CUDA_TRY(cudaEventRecord(evB, S.s3));
+          pending_b = true;
+        }
       }
     }
   }
+  if (pending_s) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evS, 0));
   if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));
   PFX_CUDA_TRY(cudaEventRecord(evR, S.s2));
   PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evR, 0));
