@@ -386,10 +386,37 @@ def main():
 
     from paper_2306_16778_b200 import _native
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # PFX_BENCH_GLOO=1 (tests only): gloo collectives on host tensors and every rank on the
+    # visible GPU(s) round-robin -- exercises the multi-rank logic on a single-GPU box (the
+    # ranks' kernels never wait on one another; only the host-side collectives synchronise)
+    gloo = os.environ.get("PFX_BENCH_GLOO") == "1"
+    local_dev = local % max(1, torch.cuda.device_count()) if gloo else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def reduce_sum(t):
+        """One reduce (sum) of t to rank 0: NCCL on the device tensor (gloo: via the host)."""
+        if world == 1:
+            return t
+        if gloo:
+            h = t.cpu()
+            dist.reduce(h, dst=0, op=dist.ReduceOp.SUM)
+            t.copy_(h)
+        else:
+            dist.reduce(t, dst=0, op=dist.ReduceOp.SUM)
+        return t
+
+    def all_max(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     from paper_2306_16778_b200 import workloads as W
 
     n = {"C1": 16, "C2": 24, "C3": 20, "C4": 24, "C5": 16}[args.workload]
@@ -401,7 +428,10 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if gloo:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     def one_step(ev=None):
         # ev: (start, end) events bracketing the step's compute; the L2 flush (C1) runs
@@ -410,9 +440,7 @@ def main():
             wl.flush.zero_()
         if ev is not None:
             ev[0].record(stream)
-        out = wl.step(stream)
-        if world > 1:
-            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
+        out = reduce_sum(wl.step(stream))
         if ev is not None:
             ev[1].record(stream)
         return out
@@ -451,22 +479,31 @@ def main():
     torch.cuda.synchronize()
     kern = _native.prof_read()
     _native.prof_enable(False)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = all_max(ms)
     ms_step = ms / args.steps
     value = wl.evals_per_step * args.steps / (ms * 1e-3)
 
-    # end-to-end through the C-ABI with host buffers (H2D + compute + D2H per step)
+    # end-to-end through the C-ABI with host buffers (H2D + compute + D2H per step).  N > 1:
+    # every rank calls the host entry on its pole slice, the host partials meet in one
+    # reduce to rank 0 (device tensors over NCCL), and rank 0 reads the sum back; the time is
+    # the max over ranks of the wall clock between two barriers
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
-        wl.step_host()
+    if args.e2e_steps > 0:
+        def e2e_step():
+            part = wl.step_host()
+            if world > 1:
+                t = reduce_sum(torch.from_numpy(np.ascontiguousarray(part)).reshape(-1).to(dev))
+                if rank == 0:
+                    t.cpu()
+        e2e_step()
         torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            wl.step_host()
-        dt = time.perf_counter() - t0
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        dt = all_max(time.perf_counter() - t0)
         e2e = {"value": wl.evals_per_step * args.e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h)}
 
