@@ -102,9 +102,9 @@ __device__ __forceinline__ void block_argmax(double val, int idx, double* sv, in
 // interchanges + per-panel forward elimination turn them into L^{-1} P v).  The panel head of
 // the carried columns is broadcast through the strip buffer S (idle between the interchanges
 // and the strips; >= 32 x 33 complex >= NB x 4).
-// M3: the trailing update uses the 3M complex product (three DMMAs per step); only for the
-// one-CTA-per-SM variants, where its extra accumulators fit without spilling.
-template <int NB, bool PIV, bool M3>
+// M3: the trailing update uses the 3M complex product (three DMMAs per step) over NCH column
+// chunks of the strip (fewer live accumulators per chunk for the register-capped variant).
+template <int NB, bool PIV, bool M3, int NCH = 2>
 __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* __restrict__ Xa, int na,
                            double2* P, double2* S, double* red_v, int* red_i, int* s_piv, int* sing,
                            unsigned long long* dbg) {
@@ -383,12 +383,12 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       // T2 = sum Li Ui, T3 = sum (Lr + Li)(Ur + Ui); C -= (T1 - T2, T3 - T1 - T2).  The strip's
       // column tiles go in two halves (half the live accumulators) and each half's C values
       // are fetched before its k loop, so the loads overlap the DMMAs.
-      constexpr int CH = DB_SW / 16;  // column tiles per half
+      constexpr int CH = DB_SW / 8 / NCH;  // column tiles per chunk
       for (int rt = warp; rt < rtiles; rt += DB_WARPS) {
         const int grow = p + jb + rt * 8 + g;  // C row owned by this lane
         const int prow = jb + rt * 8 + g;      // panel row of the A fragment
 #pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < NCH; ++hf) {
           const int cb = hf * CH;
           if (cb >= ctiles) break;
           double t1[CH][2], t2[CH][2], t3[CH][2];
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[7], (unsigned long long)(clock64() - t_sys0));
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
-    lu_blocked<NB, PIV, MINB == 1>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
+    lu_blocked<NB, PIV, true, MINB == 1 ? 2 : 4>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t_lu0));
     long long t_sv0 = clock64();
