@@ -102,9 +102,9 @@ __device__ __forceinline__ void block_argmax(double val, int idx, double* sv, in
 // interchanges + per-panel forward elimination turn them into L^{-1} P v).  The panel head of
 // the carried columns is broadcast through the strip buffer S (idle between the interchanges
 // and the strips; >= 32 x 33 complex >= NB x 4).
-// M3: the trailing update uses the 3M complex product (three DMMAs per step) over NCH column
+// The trailing update uses the 3M complex product (three DMMAs per step) over NCH column
 // chunks of the strip (fewer live accumulators per chunk for the register-capped variant).
-template <int NB, bool PIV, bool M3, int NCH = 2>
+template <int NB, bool PIV, int NCH>
 __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* __restrict__ Xa, int na,
                            double2* P, double2* S, double* red_v, int* red_i, int* s_piv, int* sing,
                            unsigned long long* dbg) {
@@ -378,11 +378,10 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       const int mrows = m - jb;
       const int rtiles = (mrows + 7) >> 3;
       const int ctiles = (sw + 7) >> 3;
-      if (M3) {
       // 3M complex product (three DMMAs per complex 8x8x4 step): T1 = sum Lr Ur,
       // T2 = sum Li Ui, T3 = sum (Lr + Li)(Ur + Ui); C -= (T1 - T2, T3 - T1 - T2).  The strip's
-      // column tiles go in two halves (half the live accumulators) and each half's C values
-      // are fetched before its k loop, so the loads overlap the DMMAs.
+      // column tiles go in NCH chunks (fewer live accumulators) and each chunk's C values are
+      // fetched before its k loop, so the loads overlap the DMMAs.
       constexpr int CH = DB_SW / 8 / NCH;  // column tiles per chunk
       for (int rt = warp; rt < rtiles; rt += DB_WARPS) {
         const int grow = p + jb + rt * 8 + g;  // C row owned by this lane
@@ -442,59 +441,6 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
             }
           }
         }
-      }
-      } else {
-      for (int rt = warp; rt < rtiles; rt += DB_WARPS) {
-        double cr[DB_SW / 8][2], ci[DB_SW / 8][2];
-        const int grow = p + jb + rt * 8 + g;  // C row owned by this lane
-#pragma unroll
-        for (int ct = 0; ct < DB_SW / 8; ++ct) {
-          cr[ct][0] = cr[ct][1] = ci[ct][0] = ci[ct][1] = 0.0;
-          if (ct < ctiles && grow < d) {
-            int c0 = ct * 8 + 2 * t;
-            if (c0 < sw) {
-              double2 x = W[(size_t)grow * ldw + q + c0];
-              cr[ct][0] = x.x;
-              ci[ct][0] = x.y;
-            }
-            if (c0 + 1 < sw) {
-              double2 x = W[(size_t)grow * ldw + q + c0 + 1];
-              cr[ct][1] = x.x;
-              ci[ct][1] = x.y;
-            }
-          }
-        }
-        const int prow = jb + rt * 8 + g;  // panel row of the A fragment
-        for (int k0 = 0; k0 < jb; k0 += 4) {
-          double ar = 0.0, ai = 0.0;
-          if (prow < m && k0 + t < jb) {
-            double2 x = P[prow * PS + k0 + t];
-            ar = -x.x;  // C -= L*U  ==  C += (-L)*U
-            ai = -x.y;
-          }
-#pragma unroll
-          for (int ct = 0; ct < DB_SW / 8; ++ct) {
-            if (ct < ctiles) {
-              double br = 0.0, bi = 0.0;
-              int col = ct * 8 + g;
-              if (k0 + t < jb && col < sw) {
-                double2 y = S[(k0 + t) * SS + col];
-                br = y.x;
-                bi = y.y;
-              }
-              zmma884(cr[ct], ci[ct], ar, ai, br, bi);
-            }
-          }
-        }
-#pragma unroll
-        for (int ct = 0; ct < DB_SW / 8; ++ct) {
-          if (ct < ctiles && grow < d) {
-            int c0 = ct * 8 + 2 * t;
-            if (c0 < sw) W[(size_t)grow * ldw + q + c0] = make_double2(cr[ct][0], ci[ct][0]);
-            if (c0 + 1 < sw) W[(size_t)grow * ldw + q + c0 + 1] = make_double2(cr[ct][1], ci[ct][1]);
-          }
-        }
-      }
       }
       __syncthreads();
       if (dbg && tid == 0) {
@@ -697,7 +643,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[7], (unsigned long long)(clock64() - t_sys0));
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
-    lu_blocked<NB, PIV, true, MINB == 1 ? 2 : 4>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
+    lu_blocked<NB, PIV, MINB == 1 ? 2 : 4>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t_lu0));
     long long t_sv0 = clock64();
