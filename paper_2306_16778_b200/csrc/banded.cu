@@ -389,7 +389,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
   PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (per_pair_ms) PFX_CUDA_TRY(cudaEventRecord(e1, stream));
-  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (int rc_ = sync_stream(stream)) return rc_;
   if (per_pair_ms) {
     float ms = 0.0f;
     PFX_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));

@@ -846,7 +846,7 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   int* hst = pinned_word();
   if (!hst) return fail(PFX_CUDA, "pinned status word allocation failed");
   PFX_CUDA_TRY(cudaMemcpyAsync(hst, args.status, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (int rc_ = sync_stream(stream)) return rc_;
   const int st = *hst;
   if (args.dbg) {
     unsigned long long h[8];

@@ -188,7 +188,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   if (per_pair_ms) {
     PFX_CUDA_TRY(cudaEventRecord(e1, stream));
   }
-  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (int rc_ = sync_stream(stream)) return rc_;
   if (per_pair_ms) {
     float ms = 0.0f;
     PFX_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
@@ -265,7 +265,7 @@ int shifted_solve_large(const double* A, int a_complex, int d, const double2* th
   int* hsg = pinned_word();
   if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
   PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (int rc_ = sync_stream(stream)) return rc_;
   if (*hsg) return fail(PFX_SINGULAR, "exactly zero pivot in the shifted factorization");
   return PFX_OK;
 }

@@ -2,6 +2,7 @@
 // device arena, pole-table upload, dispatch to the kernels.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <algorithm>
 #include <cstdio>
@@ -95,6 +96,18 @@ int* pinned_word() {
   return p;
 }
 
+int sync_stream(cudaStream_t stream) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(stream);
+    if (q == cudaSuccess) return PFX_OK;
+    if (q != cudaErrorNotReady) return fail(PFX_CUDA, std::string("cudaStreamQuery: ") + cudaGetErrorString(q));
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) break;
+  }
+  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  return PFX_OK;
+}
+
 int raise_smem_limit(const void* kernel, size_t bytes) {
   static std::mutex mu;
   static std::vector<std::pair<const void*, size_t>> set;
@@ -177,7 +190,7 @@ static int upload_poles(const double* theta2, const double* coef2, int npairs, c
   e.host = tmp;
   PFX_CUDA_TRY(cudaMalloc(&e.dev, tmp.size() * sizeof(double)));
   PFX_CUDA_TRY(cudaMemcpyAsync(e.dev, tmp.data(), tmp.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
-  PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (int rc_ = sync_stream(stream)) return rc_;
   g_pole_cache[devid].push_back(e);
   *th = e.dev;
   *co = e.dev + npairs;
@@ -333,7 +346,7 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
     PFX_CUDA_TRY(cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, stream));
-    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+    if (int rc_ = sync_stream(stream)) return rc_;
   }
   return PFX_OK;
 }
@@ -378,7 +391,7 @@ int pfx_expm_tridiag(int mem, const double* diag, const double* off, int64_t N, 
     for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
   if (mem == PFX_MEM_HOST) {
     if (!pipe) PFX_CUDA_TRY(cudaMemcpyAsync(out, Out, obytes, cudaMemcpyDeviceToHost, stream));
-    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+    if (int rc_ = sync_stream(stream)) return rc_;
   }
   return PFX_OK;
 }
@@ -409,7 +422,7 @@ int pfx_expm_banded(int mem, const double* band, int64_t N, int64_t kb, const do
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
     PFX_CUDA_TRY(cudaMemcpyAsync(out, Out, obytes, cudaMemcpyDeviceToHost, stream));
-    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+    if (int rc_ = sync_stream(stream)) return rc_;
   }
   return PFX_OK;
 }
@@ -444,7 +457,7 @@ int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
     PFX_CUDA_TRY(cudaMemcpyAsync(Y, Yd, vbytes, cudaMemcpyDeviceToHost, stream));
-    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+    if (int rc_ = sync_stream(stream)) return rc_;
   }
   return PFX_OK;
 }

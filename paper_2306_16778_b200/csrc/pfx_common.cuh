@@ -29,6 +29,9 @@ void* scratch(int slot, size_t bytes);
 // a pinned host word per thread for the status readback (a pageable 4-byte copy is staged
 // through a driver bounce buffer: tens of microseconds on the small configs)
 int* pinned_word();
+// wait for `stream`: spin on cudaStreamQuery for up to ~200 us (short calls return without
+// the blocking-sync wake-up latency), then fall back to a blocking synchronise
+int sync_stream(cudaStream_t stream);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `bytes` exceeds what was set
 // before for this kernel (the call itself costs host time on every launch otherwise)
 int raise_smem_limit(const void* kernel, size_t bytes);
