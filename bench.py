@@ -30,7 +30,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -277,7 +276,6 @@ def _cpu_task(args):
         return float(len(cols))
     if name == "C4":
         # one pole pair of the full exp(A): zgesv with 4096 identity RHS (engine.py:208)
-        import scipy.linalg
         A, _ = W.c4_matrix()
         th, co = restate.pairs(n)
         k = cols[0]

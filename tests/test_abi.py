@@ -5,7 +5,6 @@ import os
 import re
 
 import numpy as np
-import pytest
 
 from paper_2306_16778_b200 import _native
 from paper_2306_16778_b200.errors import PFX_BADARG

@@ -2,7 +2,7 @@
 import numpy as np
 import pytest
 
-from oracle import closed, restate
+from oracle import restate
 from paper_2306_16778_b200 import BandedHermitian, ExpOptions, matexp_action, matexp_shifted, workloads
 
 pytestmark = pytest.mark.gpu

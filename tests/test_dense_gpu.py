@@ -8,7 +8,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle import closed, restate
+from oracle import restate
 from paper_2306_16778_b200 import (
     ExpOptions,
     HermitianMatrix,
