@@ -39,8 +39,6 @@ namespace pfx {
 
 constexpr int TR_L = 256;     // rows per chunk
 constexpr int TR_RT = 16;     // RHS per tile (threads per shift)
-constexpr int TR_KG = 16;     // max shifts per pass
-constexpr int TR_WIN = 4;     // rows per combine window
 constexpr int TR_SCAN_T = 512;
 
 struct TriArgs {
