@@ -788,32 +788,40 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   const bool ls = npairs <= 16;
   const bool pipe = V_host != nullptr;
   if (pipe && !ls) return fail(PFX_BADARG, "tridiag_run: host pipelining needs npairs <= 16");
-  LsArgs lsa{nullptr, nullptr, 0, 0};
+  LsArgs lsa{};
   if (ls) {
-    // checkpoints live in arena slot 2 (L2-resident: 2 x P x 32 x 16 x 32 B)
+    // checkpoints live in arena slot 2 (L2-resident: 2 x P x 32 x 16 x 32 B); the fix data
+    // (z per row and pair, both directions, plus the per-block bounds) in slot 7
     const size_t ckn = (size_t)P * LS_NBLK * 16;
     LsCk* ckbuf = static_cast<LsCk*>(scratch(2, 2 * ckn * sizeof(LsCk)));
-    if (!ckbuf) return fail(PFX_CUDA, "tridiagonal checkpoint allocation failed");
+    char* zbuf = static_cast<char*>(scratch(7, 2 * nN * sizeof(double2) + 2 * ckn * sizeof(double)));
+    if (!ckbuf || !zbuf) return fail(PFX_CUDA, "tridiagonal checkpoint allocation failed");
     lsa.ckb = ckbuf;
     lsa.ckf = ckbuf + ckn;
+    lsa.zf = reinterpret_cast<double2*>(zbuf);
+    lsa.zb = lsa.zf + nN;
+    lsa.lamf = reinterpret_cast<double*>(lsa.zb + nN);
+    lsa.lamb = lsa.lamf + ckn;
     const int ntile = (int)ceil_div(nrhs, 16);
     const int smem = (int)(sizeof(LsSmem) * LS_WARPS * 2);
+    const int smem_fix = (int)(sizeof(FzBuf) * 2 * LS_WARPS * 2);
     // phase B runs KM (>= npairs) pair slots: exact small widths keep a pole-sharded rank's
     // work closer to its share of the pairs
-    auto pick = [&](auto m) {
-      using K = decltype(&tri_ls<16, decltype(m)::value>);
-      K k = npairs <= 2    ? tri_ls<2, decltype(m)::value>
-            : npairs <= 4  ? tri_ls<4, decltype(m)::value>
-            : npairs <= 6  ? tri_ls<6, decltype(m)::value>
-            : npairs <= 8  ? tri_ls<8, decltype(m)::value>
-            : npairs <= 12 ? tri_ls<12, decltype(m)::value>
-                           : tri_ls<16, decltype(m)::value>;
-      return k;
-    };
-    auto k0 = pick(std::integral_constant<int, 0>{});
-    auto k1 = pick(std::integral_constant<int, 1>{});
+    using K = decltype(&tri_ls<16>);
+    const K k0 = npairs <= 2    ? tri_ls<2>
+                 : npairs <= 4  ? tri_ls<4>
+                 : npairs <= 6  ? tri_ls<6>
+                 : npairs <= 8  ? tri_ls<8>
+                 : npairs <= 12 ? tri_ls<12>
+                                : tri_ls<16>;
+    const K k1 = npairs <= 2    ? tri_fixz<2>
+                 : npairs <= 4  ? tri_fixz<4>
+                 : npairs <= 6  ? tri_fixz<6>
+                 : npairs <= 8  ? tri_fixz<8>
+                 : npairs <= 12 ? tri_fixz<12>
+                                : tri_fixz<16>;
     if (int rc = raise_smem_limit(reinterpret_cast<const void*>(k0), smem)) return rc;
-    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(k1), smem)) return rc;
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(k1), smem_fix)) return rc;
     // row groups: whole chunks, one launch each (a single group in device mode)
     const int ng = pipe ? (int)std::min<int64_t>(TR_GROUPS, P) : 1;
     auto grp = [&](int g, int64_t& c0, int64_t& c1) {
@@ -827,7 +835,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       const unsigned blocks = (unsigned)ceil_div(la.unit1 - la.unit0, LS_WARPS * 2);
       if (blocks == 0) return PFX_OK;
       if (fix)
-        PFX_LAUNCH("tri_fix", st, (k1<<<blocks, LS_WARPS * 32, smem, st>>>(a, la)));
+        PFX_LAUNCH("tri_fix", st, (k1<<<blocks, LS_WARPS * 32, smem_fix, st>>>(a, la)));
       else
         PFX_LAUNCH("tri_sweep", st, (k0<<<blocks, LS_WARPS * 32, smem, st>>>(a, la)));
       PFX_CUDA_TRY(cudaGetLastError());

@@ -13,8 +13,10 @@
 //       w = 2a/gamma -> forward RHS sweep, F_i = sum_k Re(w (g - f)) -> out
 //   P3  per block, bottom-up: recompute l (from P2 checkpoints) -> backward chain, gamma,
 //       w -> backward RHS sweep, out_i += sum_k Re(w g')
-//   summaries gF/gB, LF/LB, contractivity flag, max|V| -> the same carry scan and a fix
-//   pass (tri_ls_fix) that recomputes the chains only near chunk edges.
+//   summaries gF/gB, LF/LB, contractivity flag, max|V| -> the same carry scan.  P2/P3 also
+//   store z = w Lambda per (row, pair) (Lambda = running product of -l, resp. -l', from the
+//   chunk edge) and the per-block bounds beta |Lambda|, so the edge fix (tri_fixz) is a
+//   streaming pass out_i += sum_k Re(z_f G + z_b G') with no chain recomputation.
 #pragma once
 // (included inside namespace pfx)
 
@@ -102,14 +104,19 @@ __device__ __forceinline__ cplx ls_fstep(const LsBuf& S, double cshift, int j, i
 struct LsArgs {
   LsCk* ckb;  // P x LS_NBLK x 16
   LsCk* ckf;  // P x LS_NBLK x 16
+  double2* zf;    // N x npairs  w_i Lambda_i, Lambda_i = prod_{s <= j <= i} (-l_j)   (chunk top s)
+  double2* zb;    // N x npairs  w_i Lambda'_i, Lambda'_i = prod_{i <= j <= e} (-l'_j) (chunk bottom e)
+  double* lamf;   // P x LS_NBLK x 16  beta_k |Lambda_k| after each block (forward)
+  double* lamb;   // P x LS_NBLK x 16  beta_k |Lambda'_k| after each block (backward)
   int64_t unit0, unit1;  // units [unit0, unit1) of this launch (row-group pipelining)
 };
 
-// MODE 0: main sweeps.  MODE 1: edge fix with the true carries.
-// Phase A of a block: lane k = pole pair k computes its chain -> (l, w) in shared memory.
+// The sweep (zero RHS carry-in).
+// Phase A of a block: lane k = pole pair k computes its chain -> (l, w) in shared memory,
+// and z = w Lambda plus the block-end bound beta |Lambda| to global memory for the fix.
 // Phase B of a block: lane r = right-hand side r sweeps all pairs from broadcast loads and
 // sums over pairs in registers (ascending k).
-template <int KM, int MODE>
+template <int KM>
 __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -123,6 +130,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   const int rt0 = (int)(unit - c * ntile) * 16;
   const int np = a.npairs;
   const bool act = k < np;                 // lane is a live pair in phase A
+  const bool wz = act && rt0 == 0;         // z and the bounds are per (row, pair): one tile stores them
   const int rg = rt0 + k;                  // rhs of this lane in phase B
   const bool rv = rg < a.nrhs;
   const int64_t s = c * TR_L;
@@ -136,18 +144,15 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   LsCk* ckf = ck.ckf + (c * LS_NBLK) * 16;
   bool noncontr = false;
   double vmx = 0.0;
-  const double tau = (MODE == 1 && rv) ? ldexp(__longlong_as_double((long long)a.vmax[rg]), -TR_FIX_EXP) : 0.0;
-  const bool contr = MODE == 1 ? a.contr[c] != 0 : false;
   if (!act) {  // padded pair slots (k >= np) stay zero: phase B adds exact zeros for them
 #pragma unroll
     for (int j = 0; j < LS_B; ++j) S.fw[j][k][0] = S.fw[j][k][1] = make_double2(0, 0);
-    S.lamabs[k] = 0.0;
   }
   auto blk_r0 = [&](int b) { return s + (int64_t)b * LS_B; };
   auto blk_cnt = [&](int b) { return min(LS_B, rows - b * LS_B); };
 
-  // ---- P1 (main only): backward continuant, checkpoints entering each block from below
-  if (MODE == 0) {
+  // ---- P1: backward continuant, checkpoints entering each block from below
+  {
     cplx q1 = mk(1, 0), q2 = act ? ld(&a.rhob_in[c * np + k]) : mk(0, 0);
     ls_stage_async(S.buf[0], a, blk_r0(nblk - 1), blk_cnt(nblk - 1), rt0, k, false);
     cp_async_commit();
@@ -176,18 +181,15 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   for (int dir = 0; dir < 2; ++dir) {
     cplx g[KM];
 #pragma unroll
-    for (int q = 0; q < KM; ++q) {
-      if (MODE == 0)
-        g[q] = mk(0, 0);
-      else
-        g[q] = (q < np && rv) ? ld(&(dir == 0 ? a.G : a.Gb)[(c * np + q) * a.nrhs + rg]) : mk(0, 0);
-    }
+    for (int q = 0; q < KM; ++q) g[q] = mk(0, 0);
     cplx x1 = mk(1, 0);
     cplx x2 = act ? ld(dir == 0 ? &a.rho_in[c * np + k] : &a.rhob_in[c * np + k]) : mk(0, 0);
     cplx lam = mk(1, 0);
+    double2* const zo = (dir == 0 ? ck.zf : ck.zb) + k;
+    double* const lo = (dir == 0 ? ck.lamf : ck.lamb) + (c * LS_NBLK) * 16 + k;
     auto blk_of = [&](int bb) { return dir == 0 ? bb : nblk - 1 - bb; };
     __syncwarp(hmask);
-    ls_stage_async(S.buf[0], a, blk_r0(blk_of(0)), blk_cnt(blk_of(0)), rt0, k, MODE == 0);
+    ls_stage_async(S.buf[0], a, blk_r0(blk_of(0)), blk_cnt(blk_of(0)), rt0, k, true);
     cp_async_commit();
     LsCk ck_next = act ? (dir == 0 ? ckb[blk_of(0) * 16 + k] : ckf[blk_of(0) * 16 + k]) : LsCk{};
     for (int bb = 0; bb < nblk; ++bb) {
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
       const int cur = bb & 1;
       const LsCk ckv = ck_next;
       if (bb + 1 < nblk) {
-        ls_stage_async(S.buf[cur ^ 1], a, blk_r0(blk_of(bb + 1)), blk_cnt(blk_of(bb + 1)), rt0, k, MODE == 0);
+        ls_stage_async(S.buf[cur ^ 1], a, blk_r0(blk_of(bb + 1)), blk_cnt(blk_of(bb + 1)), rt0, k, true);
         if (act) ck_next = dir == 0 ? ckb[blk_of(bb + 1) * 16 + k] : ckf[blk_of(bb + 1) * 16 + k];
       }
       cp_async_commit();
@@ -218,10 +220,10 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
             if (j < cnt) {
               cplx lv = ls_bstep(B, csh, j, r0 + j, th, q1, q2);
               S.fw[j][k][0] = make_double2(lv.re, lv.im);
-              if (MODE == 0 && fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
+              if (fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
             }
           }
-          if (MODE == 0) ckf[b * 16 + k] = LsCk{make_double2(x1.re, x1.im), make_double2(x2.re, x2.im)};
+          ckf[b * 16 + k] = LsCk{make_double2(x1.re, x1.im), make_double2(x2.re, x2.im)};
 #pragma unroll
           for (int j = 0; j < LS_B; ++j) {
             if (j < cnt) {
@@ -229,12 +231,12 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
               const cplx lbv = ld(&S.fw[j][k][0]);
               const cplx bd = mk(B.dg[j] - csh + th.re, th.im);
               const cplx gam = csub(csub(bd, cscale(lv, B.of[j])), cscale(lbv, B.of[j + 1]));
-              cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
+              const cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
               lam = cmul(lam, mk(-lv.re, -lv.im));
-              if (MODE == 0 && fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
-              if (MODE == 1) w = cmul(w, lam);
+              if (fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
               S.fw[j][k][0] = make_double2(lv.re, lv.im);
               S.fw[j][k][1] = make_double2(w.re, w.im);
+              if (wz) st(&zo[(r0 + j) * np], cmul(w, lam));
             }
           }
         } else {
@@ -254,15 +256,15 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
               const cplx lv = ld(&S.fw[j][k][0]);
               const cplx bd = mk(B.dg[j] - csh + th.re, th.im);
               const cplx gam = csub(csub(bd, cscale(lv, B.of[j])), cscale(lbv, B.of[j + 1]));
-              cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
+              const cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
               lam = cmul(lam, mk(-lbv.re, -lbv.im));
-              if (MODE == 1) w = cmul(w, lam);
               S.fw[j][k][0] = make_double2(lbv.re, lbv.im);
               S.fw[j][k][1] = make_double2(w.re, w.im);
+              if (wz) st(&zo[(r0 + j) * np], cmul(w, lam));
             }
           }
         }
-        if (MODE == 1) S.lamabs[k] = beta * cabs1(lam);
+        if (wz) lo[b * 16] = beta * cabs1(lam);
       }
       __syncwarp(hmask);
       // ---- phase B (lane = rhs).  Per row: independent per-pair terms, then a fixed
@@ -277,31 +279,21 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
           const int j = dir == 0 ? jj : cnt - 1 - jj;
           // sum over pairs: two interleaved FMA chains (even / odd pairs), fixed order
           double acc0 = 0.0, acc1 = 0.0;
-          if (MODE == 0) {
-            const double f = B.f[j][k];
-            if (dir == 0) vmx = fmax(vmx, fabs(f));
+          const double f = B.f[j][k];
+          if (dir == 0) vmx = fmax(vmx, fabs(f));
 #pragma unroll
-            for (int q = 0; q < KM; ++q) {
-              const double2 l2 = S.fw[j][q][0], w2 = S.fw[j][q][1];
-              g[q] = cplx{fma(-l2.x, g[q].re, fma(l2.y, g[q].im, f)), fma(-l2.x, g[q].im, -l2.y * g[q].re)};
-              const double gre = dir == 0 ? g[q].re - f : g[q].re;
-              double& acc = (q & 1) ? acc1 : acc0;
-              acc = fma(w2.x, gre, acc);
-              acc = fma(-w2.y, g[q].im, acc);
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < KM; ++q) {
-              const double2 w2 = S.fw[j][q][1];  // w * Lambda (zero for padded pairs)
-              double& acc = (q & 1) ? acc1 : acc0;
-              acc = fma(w2.x, g[q].re, acc);
-              acc = fma(-w2.y, g[q].im, acc);
-            }
+          for (int q = 0; q < KM; ++q) {
+            const double2 l2 = S.fw[j][q][0], w2 = S.fw[j][q][1];
+            g[q] = cplx{fma(-l2.x, g[q].re, fma(l2.y, g[q].im, f)), fma(-l2.x, g[q].im, -l2.y * g[q].re)};
+            const double gre = dir == 0 ? g[q].re - f : g[q].re;
+            double& acc = (q & 1) ? acc1 : acc0;
+            acc = fma(w2.x, gre, acc);
+            acc = fma(-w2.y, g[q].im, acc);
           }
           const double acc = acc0 + acc1;
           if (rv) {
             double* o = obase + j * a.nrhs;
-            if (MODE == 0 && dir == 0)
+            if (dir == 0)
               *o = acc;
             else
               *o = *o + acc;
@@ -309,32 +301,156 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
         }
       }
       __syncwarp(hmask);
-      if (MODE == 1) {
-        // stop once every remaining correction is below 2^-53 max|V[:, r]| (contractive chunks)
-        double y = 0.0;
-        if (rv) {
-#pragma unroll
-          for (int q = 0; q < KM; ++q)
-            y = fma(S.lamabs[q], cabs1(g[q]), y);
-          y = tau > 0.0 ? y / tau : (y > 0.0 ? INFINITY : 0.0);
-        }
-        for (int off = 8; off > 0; off >>= 1) y = fmax(y, __shfl_xor_sync(hmask, y, off));
-        if (contr && y <= 1.0) break;
-      }
     }
     cp_async_wait<0>();
     __syncwarp(hmask);
-    if (MODE == 0) {
-      if (rv) {
+    if (rv) {
 #pragma unroll
-        for (int q = 0; q < KM; ++q)
-          if (q < np) st(&(dir == 0 ? a.gF : a.gB)[g_at(a, c, q, rg)], g[q]);
-      }
-      if (act && rt0 == 0) st(&(dir == 0 ? a.LF : a.LB)[l_at(a, c, k)], lam);
+      for (int q = 0; q < KM; ++q)
+        if (q < np) st(&(dir == 0 ? a.gF : a.gB)[g_at(a, c, q, rg)], g[q]);
     }
+    if (act && rt0 == 0) st(&(dir == 0 ? a.LF : a.LB)[l_at(a, c, k)], lam);
   }
-  if (MODE == 0) {
-    if (noncontr) atomicAnd(&a.contr[c], 0);
-    if (rv) atomicMax(&a.vmax[rg], (unsigned long long)__double_as_longlong(vmx));
+  if (noncontr) atomicAnd(&a.contr[c], 0);
+  if (rv) atomicMax(&a.vmax[rg], (unsigned long long)__double_as_longlong(vmx));
+}
+
+// Edge fix with the true carries G (from above) and G' (from below), from the sweep's
+// stored z:   out_i += sum_k Re(zf_{k,i} G_k) + Re(zb_{k,i} G'_k).
+// In a contractive chunk (every |l|, |l'| <= 1) |Lambda| never grows and |w| <= 2|a|/Im(theta)
+// (|gamma| >= Im(theta)), so after the first block whose end bound
+// sum_k beta_k |Lambda_k| |G_k| is <= 2^-53 max|V[:, r]| every later row's correction is below
+// one unit roundoff of max|V[:, r]| (below the binary64 rounding of the pole sum itself):
+// the forward terms cover blocks [0, endF), the backward terms [begB, nblk), and only their
+// union is visited (all blocks in a non-contractive chunk).
+// Layout: a half-warp = one (chunk, 16-RHS tile), lane = right-hand side; the z rows of a
+// block are staged by cp.async (double buffered) and read back as broadcasts.
+struct FzBuf {
+  double2 z[2][LS_B][16];  // [direction][row][pair]
+};
+
+template <int KM>
+__global__ void __launch_bounds__(LS_WARPS * 32, 3) tri_fixz(TriArgs a, LsArgs ck) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, k = lane & 15;
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  FzBuf* const Z = reinterpret_cast<FzBuf*>(smem_raw) + (warp * 2 + half) * 2;
+  const int ntile = (a.nrhs + 15) / 16;
+  const int64_t unit = ck.unit0 + (blockIdx.x * (int64_t)LS_WARPS + warp) * 2 + half;
+  if (unit >= ck.unit1) return;
+  const int64_t c = unit / ntile;
+  const int rt0 = (int)(unit - c * ntile) * 16;
+  const int np = a.npairs;
+  const int rg = rt0 + k;
+  const bool rv = rg < a.nrhs;
+  const int64_t s = c * TR_L;
+  const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
+  const int nblk = (rows + LS_B - 1) / LS_B;
+  cplx gf[KM], gb[KM];
+#pragma unroll
+  for (int q = 0; q < KM; ++q) {
+    const bool on = q < np && rv;
+    gf[q] = on ? ld(&a.G[(c * np + q) * a.nrhs + rg]) : mk(0, 0);
+    gb[q] = on ? ld(&a.Gb[(c * np + q) * a.nrhs + rg]) : mk(0, 0);
   }
+  // padded pair slots read as zeros
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+    for (int e = k; e < 2 * LS_B * 16; e += 16)
+      if ((e & 15) >= np) (&Z[t].z[0][0][0])[e] = make_double2(0, 0);
+  int endF = nblk, begB = 0;
+  if (a.contr[c] != 0) {
+    const double tau = rv ? ldexp(__longlong_as_double((long long)a.vmax[rg]), -TR_FIX_EXP) : 0.0;
+    const double* lf = ck.lamf + (c * LS_NBLK) * 16;
+    const double* lb = ck.lamb + (c * LS_NBLK) * 16;
+    int ef = nblk, eb = nblk;  // blocks this lane needs, per direction
+    for (int bb = 0; bb < nblk; ++bb) {
+      double y = 0.0;
+#pragma unroll
+      for (int q = 0; q < KM; ++q) y = fma(lf[bb * 16 + q], cabs1(gf[q]), y);
+      if (y <= tau) {
+        ef = bb + 1;
+        break;
+      }
+    }
+    for (int bb = 0; bb < nblk; ++bb) {
+      double y = 0.0;
+#pragma unroll
+      for (int q = 0; q < KM; ++q) y = fma(lb[(nblk - 1 - bb) * 16 + q], cabs1(gb[q]), y);
+      if (y <= tau) {
+        eb = bb + 1;
+        break;
+      }
+    }
+    for (int off = 8; off > 0; off >>= 1) {
+      ef = max(ef, __shfl_xor_sync(hmask, ef, off));
+      eb = max(eb, __shfl_xor_sync(hmask, eb, off));
+    }
+    endF = ef;
+    begB = nblk - eb;
+  }
+  const bool gap = begB > endF;
+  auto next_blk = [&](int b) { return (gap && b + 1 == endF) ? begB : b + 1; };
+  auto stage = [&](FzBuf& D, int b) {
+    const int64_t r0 = s + (int64_t)b * LS_B;
+    const int n = min(LS_B, rows - b * LS_B) * np;
+    if (b < endF)
+      for (int e = k; e < n; e += 16) {
+        const int j = e / np;
+        cp_async16(&D.z[0][j][e - j * np], &ck.zf[r0 * np + e]);
+      }
+    if (b >= begB)
+      for (int e = k; e < n; e += 16) {
+        const int j = e / np;
+        cp_async16(&D.z[1][j][e - j * np], &ck.zb[r0 * np + e]);
+      }
+  };
+  __syncwarp(hmask);
+  int b = 0, cur = 0;
+  stage(Z[0], 0);
+  cp_async_commit();
+  while (b < nblk) {
+    const int bn = next_blk(b);
+    if (bn < nblk) stage(Z[cur ^ 1], bn);
+    cp_async_commit();
+    const int64_t r0 = s + (int64_t)b * LS_B;
+    const int cnt = min(LS_B, rows - b * LS_B);
+    double ov[LS_B];
+    double* const obase = a.out + r0 * a.nrhs + rg;
+#pragma unroll
+    for (int j = 0; j < LS_B; ++j) ov[j] = (rv && j < cnt) ? obase[j * a.nrhs] : 0.0;
+    cp_async_wait<1>();
+    __syncwarp(hmask);
+    const FzBuf& D = Z[cur];
+    const bool uf = b < endF, ub = b >= begB;
+#pragma unroll
+    for (int j = 0; j < LS_B; ++j) {
+      double acc0 = 0.0, acc1 = 0.0;
+      if (uf) {
+#pragma unroll
+        for (int q = 0; q < KM; ++q) {
+          const double2 z = D.z[0][j][q];
+          acc0 = fma(z.x, gf[q].re, acc0);
+          acc1 = fma(-z.y, gf[q].im, acc1);
+        }
+      }
+      if (ub) {
+#pragma unroll
+        for (int q = 0; q < KM; ++q) {
+          const double2 z = D.z[1][j][q];
+          acc0 = fma(z.x, gb[q].re, acc0);
+          acc1 = fma(-z.y, gb[q].im, acc1);
+        }
+      }
+      ov[j] += acc0 + acc1;
+    }
+#pragma unroll
+    for (int j = 0; j < LS_B; ++j)
+      if (rv && j < cnt) obase[j * a.nrhs] = ov[j];
+    __syncwarp(hmask);
+    b = bn;
+    cur ^= 1;
+  }
+  cp_async_wait<0>();
 }
