@@ -37,7 +37,7 @@
 
 namespace pfx {
 
-constexpr int TR_L = 256;     // rows per chunk
+constexpr int TR_L = 256;     // maximum rows per chunk (the chunk length a.L is chosen per call)
 constexpr int TR_RT = 16;     // RHS per tile (threads per shift)
 constexpr int TR_SCAN_T = 512;
 
@@ -51,6 +51,7 @@ struct TriArgs {
   const double2* theta;
   const double2* coef;
   int npairs;
+  int L;  // rows per chunk (multiple of 32, <= TR_L)
   int P;  // chunks
   double2* Tf;  // P x npairs x 4   forward transfers
   double2* Tb;  // P x npairs x 4   backward transfers
@@ -139,8 +140,8 @@ __global__ void __launch_bounds__(128) tri_mobius_chunks(TriArgs a) {
   const int64_t ck = live ? tid / TR_SEG : 0;
   const int k = (int)(ck % a.npairs);
   const int64_t cidx = ck / a.npairs;
-  const int64_t s = cidx * TR_L, e = (s + TR_L < a.N ? s + TR_L : a.N);
-  constexpr int SL = TR_L / TR_SEG;
+  const int64_t s = cidx * a.L, e = (s + a.L < a.N ? s + a.L : a.N);
+  const int SL = a.L / TR_SEG;
   const int64_t s0 = s + (int64_t)seg * SL;
   const int64_t rem = e - s0;
   const int rows = (!live || rem <= 0) ? 0 : (rem < SL ? (int)rem : SL);
@@ -282,8 +283,8 @@ __global__ void __launch_bounds__(128) tri_factor(TriArgs a) {
   if (tid >= (int64_t)a.P * a.npairs) return;
   const int k = (int)(tid % a.npairs);
   const int64_t c = tid / a.npairs;
-  const int64_t s = c * TR_L;
-  const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
+  const int64_t s = c * a.L;
+  const int rows = (int)(a.L < a.N - s ? a.L : a.N - s);
   const cplx th = ld(&a.theta[k]);
   const int np = a.npairs;
   auto offe = [&](int64_t gi) -> double { return (gi >= 0 && gi < a.N - 1) ? a.off[gi] : 0.0; };
@@ -402,8 +403,8 @@ __global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_pass(TriArgs a) {
   const int rt0 = (int)(unit - c * ntile) * TR_RT;
   const int r = rt0 + lane16;
   const bool rv = r < a.nrhs;
-  const int64_t s = c * TR_L;
-  const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
+  const int64_t s = c * a.L;
+  const int rows = (int)(a.L < a.N - s ? a.L : a.N - s);
   const int np = a.npairs;
   const int ntl = (rows + TR_T - 1) / TR_T;
   double vmx = 0.0;
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
 // Same scan with the block's whole column staged in shared memory by one round of coalesced
 // cp.async (chunk-fastest summaries: L and g of this (pair, rhs) are two contiguous runs of P
 // complex); used when 2 P complex fit (P <= CS_SMEM_P).
-constexpr int CS_SMEM_P = 4096;
+constexpr int CS_SMEM_P = 6144;
 __global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // one pad slot per 16 chunks: thread t walks chunks 16t.., so unpadded its lanes would sit
@@ -734,7 +735,17 @@ int tri_pipe(TriPipe& T) {
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                 float* launch_ms, const double* V_host, double* out_host) {
-  const int P = (int)ceil_div(N, TR_L);
+  // Chunk length: the sweep keeps 32 (chunk, 16-RHS tile) units resident per SM, so the
+  // chunks are sized to fill every SM in one wave (C2: 224 rows -> 4682 units on 148 SMs,
+  // where 256 rows left 20 SMs idle), within [64, TR_L] rows and a multiple of 32.
+  int dev = 0;
+  PFX_CUDA_TRY(cudaGetDevice(&dev));
+  static int sms_of[16] = {};
+  if (dev < 16 && !sms_of[dev]) PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
+  const int64_t slots = (int64_t)(dev < 16 ? sms_of[dev] : 148) * 2 * LS_WARPS * 4;
+  const int64_t per = ceil_div(N * ceil_div(nrhs, 16), slots);
+  const int L = (int)std::min<int64_t>(TR_L, std::max<int64_t>(64, ceil_div(per, 32) * 32));
+  const int P = (int)ceil_div(N, L);
   const size_t nP = (size_t)P * npairs;
   const size_t nPR = nP * nrhs;
   const size_t nN = (size_t)N * npairs;
@@ -753,6 +764,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   a.theta = theta_d;
   a.coef = coef_d;
   a.npairs = npairs;
+  a.L = L;
   a.P = P;
   a.Tf = ws;
   a.Tb = a.Tf + nP * 4;
@@ -866,7 +878,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       for (int g = 0; g < ng; ++g) {
         int64_t c0, c1;
         grp(g, c0, c1);
-        const int64_t r0 = c0 * TR_L, r1 = std::min<int64_t>(c1 * TR_L, N);
+        const int64_t r0 = c0 * L, r1 = std::min<int64_t>(c1 * L, N);
         PFX_CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(V) + r0 * nrhs, V_host + r0 * nrhs,
                                      (size_t)(r1 - r0) * nrhs * sizeof(double), cudaMemcpyHostToDevice, TP.in));
         PFX_CUDA_TRY(cudaEventRecord(ev[g], TP.in));
@@ -888,7 +900,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       for (int g = 0; g < ng; ++g) {
         int64_t c0, c1;
         grp(g, c0, c1);
-        const int64_t r0 = c0 * TR_L, r1 = std::min<int64_t>(c1 * TR_L, N);
+        const int64_t r0 = c0 * L, r1 = std::min<int64_t>(c1 * L, N);
         PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[4 * G], 0));
         if (int rc = launch_ls(true, c0, c1, TP.cs[g])) return rc;
         if (shift_c != 0.0) {

@@ -1,7 +1,7 @@
 // On-chip ("lane = pole pair") variant of the tridiagonal sweeps, used when npairs <= 16.
 // Included by tridiag.cu after TriArgs / the Moebius kernels.
 //
-// One half-warp = one (chunk of TR_L rows, 16-RHS tile).  Lane k owns pole pair k: it
+// One half-warp = one (chunk of a.L <= TR_L rows, 16-RHS tile).  Lane k owns pole pair k: it
 // runs pair k's pivot chains itself and the recurrences of all 16 right-hand sides
 // (ILP 16).  The per-row sum over pairs goes through a shared-memory transpose and is
 // added in ascending k (deterministic, the reference's order).  No factor data leaves
@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   const bool wz = act && rt0 == 0;         // z and the bounds are per (row, pair): one tile stores them
   const int rg = rt0 + k;                  // rhs of this lane in phase B
   const bool rv = rg < a.nrhs;
-  const int64_t s = c * TR_L;
-  const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
+  const int64_t s = c * a.L;
+  const int rows = (int)(a.L < a.N - s ? a.L : a.N - s);
   const int nblk = (rows + LS_B - 1) / LS_B;
   const double csh = a.c;
   const cplx th = act ? ld(&a.theta[k]) : mk(0, 1);
@@ -344,8 +344,8 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 3) tri_fixz(TriArgs a, LsArgs c
   const int np = a.npairs;
   const int rg = rt0 + k;
   const bool rv = rg < a.nrhs;
-  const int64_t s = c * TR_L;
-  const int rows = (int)(TR_L < a.N - s ? TR_L : a.N - s);
+  const int64_t s = c * a.L;
+  const int rows = (int)(a.L < a.N - s ? a.L : a.N - s);
   const int nblk = (rows + LS_B - 1) / LS_B;
   cplx gf[KM], gb[KM];
 #pragma unroll
