@@ -452,6 +452,318 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
 }
 
 // ---------------------------------------------------------------------------
+// Interchange-free LU (exp path) with a delayed, two-panel trailing update (NB = 16 panels):
+// the trailing matrix is streamed through L2 once per 32 columns instead of once per 16,
+// which halves the dominant L2/DRAM traffic of the factorisation and doubles the DMMA work
+// per C tile.  Per 32-column step at p (panels a = [p, p+16), b = [p+16, p+32)):
+//   1. panel a: getf2 in shared memory, written back; L11a and Lba (its rows 16..31) are
+//      copied into T; Ia = L11a^{-1} over T's top-left block; carried RHS updated.
+//   2. look-ahead: panel b's columns get panel a's update only (a 16-column strip, K = 16).
+//   3. panel b: getf2, written back; Ib = L11b^{-1}; carried RHS updated.
+//      T becomes the full inverse of the 32 x 32 unit lower block:
+//      [Ia 0; -Ib Lba Ia  Ib].
+//   4. 32-column strips right of the step: U12 = T A12 (one product, K = 32), then
+//      A22 -= [L21a L21b] U12 on DMMA (3M product, K = 32, A fragments from the slot).
+// T: 32 x 33 complex (stride TS).  Same results as lu_blocked<16, false> up to rounding order.
+constexpr int TS = 33;
+constexpr int DP_SW = 32;  // strip width of the two-panel update
+
+// this warp's 8 x 8 complex tile (rt, ct) of C = A (rows x K, stride lda) * S (K x sw rows
+// brow0.., stride TS); rows >= arows and k >= K read as zero
+__device__ __forceinline__ void dp_tile(const double2* A, size_t lda, int arows, int K, const double2* Sb, int sw,
+                                        int rt, int ct, int kbeg, double (&cr)[2], double (&ci)[2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  cr[0] = cr[1] = ci[0] = ci[1] = 0.0;
+  const int r = rt * 8 + g, col = ct * 8 + g;
+  for (int k0 = kbeg; k0 < K; k0 += 4) {
+    const int kk = k0 + t;
+    double2 x = make_double2(0, 0), y = make_double2(0, 0);
+    if (kk < K) {
+      if (r < arows) x = A[(size_t)r * lda + kk];
+      if (col < sw) y = Sb[kk * TS + col];
+    }
+    zmma884(cr, ci, x.x, x.y, y.x, y.y);
+  }
+}
+
+// unit lower inverse of the jb x jb block at T + off*(TS+1) (in place), warp per column
+__device__ __forceinline__ void dp_inv16(double2* T, int off, int jb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* B = T + off * (TS + 1);
+  cplx inv[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = warp + u * DB_WARPS;
+    cplx x = mk(lane == c ? 1.0 : 0.0, 0.0);
+    for (int k = c; k < jb; ++k) {
+      cplx xk;
+      xk.re = __shfl_sync(0xffffffffu, x.re, k);
+      xk.im = __shfl_sync(0xffffffffu, x.im, k);
+      if (lane > k && lane < jb) x = cfms(x, ld(&B[lane * TS + k]), xk);
+    }
+    inv[u] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = warp + u * DB_WARPS;
+    if (lane < jb && c < jb) st(&B[lane * TS + c], lane >= c ? inv[u] : mk(0.0, 0.0));
+  }
+  __syncthreads();
+}
+
+template <int CH>
+__device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int d, double2* __restrict__ Xa, int na,
+                            double2* P, double2* S, double2* T, int* s_piv, int* sing, unsigned long long* dbg) {
+  constexpr int NB = 16;
+  constexpr int PS = NB + 1;
+  const size_t ldw = (size_t)d;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  long long tph = 0;
+
+  // panel [p, p+jb) x rows [p, d): load, getf2 without interchanges, write back; L11 (and,
+  // for panel a, the next 16 rows of L21) into T at toff; L11^{-1} over it; carried RHS.
+  auto panel = [&](int p, int jb, int toff, bool keep_below) {
+    const int m = d - p;
+    for (int e = tid; e < m * jb; e += DB_THREADS) {
+      const int r = e / jb, c = e - r * jb;
+      P[r * PS + c] = W[(size_t)(p + r) * ldw + p + c];
+    }
+    __syncthreads();
+    if (dbg && tid == 0) tph = clock64();
+    for (int jj = 0; jj < jb; ++jj) {
+      __syncthreads();  // panel row jj is final
+      const cplx pv = ld(&P[jj * PS + jj]);
+      if (tid == 0) {
+        s_piv[jj] = jj;
+        ipiv[p + jj] = p + jj;
+        if (pv.re == 0.0 && pv.im == 0.0) *sing = 1;
+      }
+      const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp(pv);
+      for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
+        double2* row = &P[r * PS];
+        const cplx l = cmul(ld(&row[jj]), rp);
+        const double2* prow_j = &P[jj * PS];
+        for (int c = jj + 1; c < jb; c += 4) {
+          cplx x[4], y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            x[u] = c + u < jb ? ld(&row[c + u]) : mk(0.0, 0.0);
+            y[u] = c + u < jb ? ld(&prow_j[c + u]) : mk(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c + u < jb) st(&row[c + u], cfms(x[u], l, y[u]));
+        }
+        st(&row[jj], l);
+      }
+    }
+    __syncthreads();
+    if (dbg && tid == 0) {
+      atomicAdd(&dbg[2], (unsigned long long)(clock64() - tph));
+      tph = clock64();
+    }
+    for (int e = tid; e < m * jb; e += DB_THREADS) {
+      const int r = e / jb, c = e - r * jb;
+      W[(size_t)(p + r) * ldw + p + c] = P[r * PS + c];
+    }
+    // L11 (rows 0..jb) and, for panel a, the L21 rows jb..2 NB (Lba) into T
+    const int tr = keep_below ? min(2 * NB, m) : jb;
+    for (int e = tid; e < tr * NB; e += DB_THREADS) {
+      const int r = e / NB, c = e - r * NB;
+      T[(toff + r) * TS + toff + c] = c < jb ? P[r * PS + c] : make_double2(0, 0);
+    }
+    __syncthreads();
+    dp_inv16(T, toff, jb);
+    // carried right-hand sides: head = L11^{-1} head, tail -= L21 head
+    if (na > 0) {
+      double2* xs = S;
+      const double2* I = T + toff * (TS + 1);
+      for (int c = warp; c < na; c += DB_WARPS) {
+        const cplx h = lane < jb ? ld(&Xa[(size_t)(p + lane) * na + c]) : mk(0.0, 0.0);
+        cplx x = mk(0.0, 0.0);
+        for (int k = 0; k < jb; ++k) {
+          cplx hk;
+          hk.re = __shfl_sync(0xffffffffu, h.re, k);
+          hk.im = __shfl_sync(0xffffffffu, h.im, k);
+          if (lane >= k && lane < jb) x = cfma(ld(&I[lane * TS + k]), hk, x);
+        }
+        if (lane < jb) {
+          st(&Xa[(size_t)(p + lane) * na + c], x);
+          st(&xs[c * NB + lane], x);
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < (m - jb) * na; e += DB_THREADS) {
+        const int r = e / na + jb, c = e - (r - jb) * na;
+        cplx y = ld(&Xa[(size_t)(p + r) * na + c]);
+#pragma unroll 4
+        for (int k = 0; k < jb; ++k) y = cfms(y, ld(&P[r * PS + k]), ld(&xs[c * NB + k]));
+        st(&Xa[(size_t)(p + r) * na + c], y);
+      }
+      __syncthreads();
+    }
+  };
+
+  // trailing update of rows [r0, d) x cols [q, q + sw): C -= L (slot columns [p, p + K)) * S
+  // (K x sw at S, stride TS), 3M product on DMMA; CH column tiles per chunk
+  auto trailing = [&](int p, int K, int r0, int q, int sw) {
+    const int rtiles = (d - r0 + 7) >> 3;
+    const int ctiles = (sw + 7) >> 3;
+    for (int rt = warp; rt < rtiles; rt += DB_WARPS) {
+      const int grow = r0 + rt * 8 + g;
+      // A fragments of this row tile for the whole K (<= 32): loaded once, reused by every chunk
+      double ar[2 * NB / 4], ai[2 * NB / 4];
+#pragma unroll
+      for (int s4 = 0; s4 < 2 * NB / 4; ++s4) {
+        const int kk = s4 * 4 + t;
+        double2 x = make_double2(0, 0);
+        if (grow < d && kk < K) x = W[(size_t)grow * ldw + p + kk];
+        ar[s4] = x.x;
+        ai[s4] = x.y;
+      }
+#pragma unroll 1
+      for (int cb = 0; cb < ctiles; cb += CH) {
+        double t1[CH][2], t2[CH][2], t3[CH][2];
+        double2 cv[CH][2];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          t1[u][0] = t1[u][1] = t2[u][0] = t2[u][1] = t3[u][0] = t3[u][1] = 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c0 = (cb + u) * 8 + 2 * t + h;
+            cv[u][h] = (grow < d && c0 < sw) ? W[(size_t)grow * ldw + q + c0] : make_double2(0, 0);
+          }
+        }
+#pragma unroll
+        for (int s4 = 0; s4 < 2 * NB / 4; ++s4) {
+          if (s4 * 4 < K) {
+            const int kk = s4 * 4 + t;
+            const double as = ar[s4] + ai[s4];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+              const int col = (cb + u) * 8 + g;
+              double2 y = make_double2(0, 0);
+              if (kk < K && col < sw) y = S[kk * TS + col];
+              dmma884(t1[u][0], t1[u][1], ar[s4], y.x);
+              dmma884(t2[u][0], t2[u][1], ai[s4], y.y);
+              dmma884(t3[u][0], t3[u][1], as, y.x + y.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c0 = (cb + u) * 8 + 2 * t + h;
+            if (grow < d && c0 < sw) {
+              double2 x = cv[u][h];
+              x.x -= t1[u][h] - t2[u][h];
+              x.y -= t3[u][h] - t1[u][h] - t2[u][h];
+              W[(size_t)grow * ldw + q + c0] = x;
+            }
+          }
+        }
+      }
+    }
+  };
+
+  // strip rows [p, p + K) x cols [q, q + sw) of the slot -> S; U12 = T(K x K, lower) S in
+  // place (written back to the slot); then the trailing update below it
+  auto strip = [&](int p, int K, int q, int sw) {
+    for (int e = tid; e < K * sw; e += DB_THREADS) {
+      const int r = e / sw, c = e - r * sw;
+      S[r * TS + c] = W[(size_t)(p + r) * ldw + q + c];
+    }
+    __syncthreads();
+    // K x sw output: (K/8) x (sw/8) tiles, at most 16 over 8 warps; T is lower triangular,
+    // so row tile rt only needs k < 8 (rt + 1)
+    const int mtl = (K + 7) >> 3, ntl = (sw + 7) >> 3;
+    double cr[2][2], ci[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int tl = warp + u * DB_WARPS;
+      if (tl < mtl * ntl) {
+        const int rt = tl % mtl, ct = tl / mtl;
+        dp_tile(T, TS, K, min(K, 8 * (rt + 1)), S, sw, rt, ct, 0, cr[u], ci[u]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int tl = warp + u * DB_WARPS;
+      if (tl < mtl * ntl) {
+        const int rt = tl % mtl, ct = tl / mtl;
+        const int r = rt * 8 + g;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = ct * 8 + 2 * t + h;
+          if (r < K && c < sw) S[r * TS + c] = make_double2(cr[u][h], ci[u][h]);
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < K * sw; e += DB_THREADS) {
+      const int r = e / sw, c = e - r * sw;
+      W[(size_t)(p + r) * ldw + q + c] = S[r * TS + c];
+    }
+    if (dbg && tid == 0) {
+      atomicAdd(&dbg[4], (unsigned long long)(clock64() - tph));
+      tph = clock64();
+    }
+    trailing(p, K, p + K, q, sw);
+    __syncthreads();
+    if (dbg && tid == 0) {
+      atomicAdd(&dbg[5], (unsigned long long)(clock64() - tph));
+      tph = clock64();
+    }
+  };
+
+  for (int p = 0; p < d; p += 2 * NB) {
+    const int ja = min(NB, d - p);
+    const int jb = min(NB, d - p - ja);  // 0: panel a is the last
+    for (int e = tid; e < 2 * NB * TS; e += DB_THREADS) T[e] = make_double2(0, 0);
+    __syncthreads();
+    panel(p, ja, 0, jb > 0);
+    if (jb == 0) {
+      // last (partial) step: the columns right of panel a are none
+      break;
+    }
+    // look-ahead: panel b's columns with panel a's update (T's top-left block holds Ia)
+    strip(p, ja, p + ja, jb);
+    panel(p + ja, jb, NB, false);
+    // T's bottom-left block: -Ib Lba Ia (two 16 x 16 x 16 products, four warps)
+    {
+      double2* L = T + NB * TS;  // Lba
+      double cr[2], ci[2];
+      const int rt = warp & 1, ct = (warp >> 1) & 1;
+      if (warp < 4) dp_tile(L, TS, jb, ja, T, ja, rt, ct, 0, cr, ci);  // Lba Ia (Ia at T, stride TS)
+      __syncthreads();
+      if (warp < 4) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) L[(rt * 8 + g) * TS + ct * 8 + 2 * t + h] = make_double2(cr[h], ci[h]);
+      }
+      __syncthreads();
+      // -Ib (Lba Ia): B operand = rows of L (stride TS) -> through dp_tile with Sb = L
+      if (warp < 4) dp_tile(T + NB * (TS + 1), TS, jb, jb, L, ja, rt, ct, 0, cr, ci);
+      __syncthreads();
+      if (warp < 4) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = rt * 8 + g, c = ct * 8 + 2 * t + h;
+          L[r * TS + c] = (r < jb && c < ja) ? make_double2(-cr[h], -ci[h]) : make_double2(0, 0);
+        }
+      }
+      __syncthreads();
+    }
+    const int K = ja + jb;
+    for (int q = p + K; q < d; q += DP_SW) strip(p, K, q, min(DP_SW, d - q));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Triangular solves on one RHS column z (shared memory, length d) against the LU in W.
 // kind 0: L  (unit lower, forward)      z <- L^{-1} z
 // kind 1: U  (upper, backward)          z <- U^{-1} z
@@ -570,15 +882,17 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
   double2* S = P + (size_t)d * (NB + 1);                            // NB x (SW+1), aliased by diag
   double2* diag = S;                                                // 32 x 33 (solves only)
   const size_t sreg = (size_t)NB * (DB_SW + 1) > 32 * 33 ? (size_t)NB * (DB_SW + 1) : 32 * 33;
-  double2* z = S + sreg;                                            // d
-  double2* zc = z + d;                                              // d
-  double2* part = zc + d;                                           // 32
+  double2* T = S + sreg;                                            // 32 x 33 (two-panel LU)
+  double2* part = T + 32 * TS;                                      // 32
   double* red_v = reinterpret_cast<double*>(part + 32);             // 32
   int* red_i = reinterpret_cast<int*>(red_v + 32);                  // 32
   int* s_piv = red_i + 32;                                          // NB
   int* s_sing = s_piv + NB;                                         // 1
   int* s_perm = s_sing + 4;                                         // d  (row permutation)
-  double2* rdiag = reinterpret_cast<double2*>(s_perm + ((d + 3) & ~3)); // d  (1 / U_ii)
+  // solve-phase vectors live in the panel buffer (idle after the factorisation)
+  double2* z = P;                                                   // d
+  double2* zc = z + d;                                              // d
+  double2* rdiag = zc + d;                                          // d  (1 / U_ii)
 
   const int tid = threadIdx.x;
   const int slot = blockIdx.x;
@@ -643,7 +957,10 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[7], (unsigned long long)(clock64() - t_sys0));
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
-    lu_blocked<NB, PIV, MINB == 1 ? 2 : 4>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
+    if constexpr (NB == 16 && !PIV)
+      lu_nopiv_dp<MINB == 1 ? 4 : 2>(W, ipiv, d, Xa, a.aug, P, S, T, s_piv, s_sing, a.dbg);
+    else
+      lu_blocked<NB, PIV, MINB == 1 ? 2 : 4>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
     if (a.dbg && tid == 0) atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t_lu0));
     long long t_sv0 = clock64();
@@ -753,9 +1070,9 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ stage, double* __
 
 static size_t dense_smem_bytes(int d, int nb) {
   size_t sreg = (size_t)nb * (DB_SW + 1) > 32 * 33 ? (size_t)nb * (DB_SW + 1) : 32 * 33;
-  size_t c2 = (size_t)d * (nb + 1) + sreg + 2 * (size_t)d + 32;
-  return c2 * sizeof(double2) + 32 * sizeof(double) + (32 + nb + 4) * sizeof(int) + ((d + 3) & ~3) * sizeof(int) +
-         (size_t)d * sizeof(double2) + 64;
+  // panel (z, zc, 1/U_ii alias it in the solves) + strip + T (32 x 33) + part
+  size_t c2 = (size_t)d * (nb + 1) + sreg + 32 * 33 + 32;
+  return c2 * sizeof(double2) + 32 * sizeof(double) + (32 + nb + 4) * sizeof(int) + ((d + 3) & ~3) * sizeof(int) + 64;
 }
 
 int dense_batched_supported(int64_t d) { return d >= 1 && d <= 512; }
