@@ -466,6 +466,9 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
 //      A22 -= [L21a L21b] U12 on DMMA (3M product, K = 32, A fragments from the slot).
 // T: 32 x 33 complex (stride TS).  Same results as lu_blocked<16, false> up to rounding order.
 constexpr int TS = 33;
+#ifndef PFX_DP_CH
+#define PFX_DP_CH 1  // column tiles per chunk of the two-panel update in the two-CTA variant
+#endif
 constexpr int DP_SW = 32;  // strip width of the two-panel update
 
 // this warp's 8 x 8 complex tile (rt, ct) of C = A (rows x K, stride lda) * S (K x sw rows
@@ -958,7 +961,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     // ---- K1/K2: LU with partial pivoting
     long long t_lu0 = clock64();
     if constexpr (NB == 16 && !PIV)
-      lu_nopiv_dp<MINB == 1 ? 4 : 2>(W, ipiv, d, Xa, a.aug, P, S, T, s_piv, s_sing, a.dbg);
+      lu_nopiv_dp<MINB == 1 ? 4 : PFX_DP_CH>(W, ipiv, d, Xa, a.aug, P, S, T, s_piv, s_sing, a.dbg);
     else
       lu_blocked<NB, PIV, MINB == 1 ? 2 : 4>(W, ipiv, d, Xa, a.aug, P, S, red_v, red_i, s_piv, s_sing, a.dbg);
     __syncthreads();
