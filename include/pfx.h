@@ -108,6 +108,25 @@ int pfx_expm_tridiag(int mem, const double* diag, const double* off, int64_t N, 
                      float* per_pair_ms, void* stream);
 
 /*
+ * Row-sharded tridiagonal path: multi-GPU domain decomposition of the call above
+ * (one process per GPU; device memory on the caller's stream).  The chunk rows are
+ * split into nranks contiguous blocks; pfx_tridiag_shard_rows gives this rank's rows
+ * [r0, r1).  diag, off, V are the full arrays (only the rank's rows and the couplings
+ * at its edges are read); out (N x nrhs) receives rows [r0, r1) only, each final (no
+ * reduction: the pole sum is complete per row).  The two chunk scans that cross rank
+ * edges (pivot carries, right-hand-side carries) each exchange one small aggregate
+ * per rank, through allgather(ctx, buf, count): buf holds nranks x count doubles,
+ * this rank's block at buf + rank * count filled by the library, the callback fills
+ * the others (a torch.distributed all-gather on the Python side) and returns 0.
+ * Same results as pfx_expm_tridiag up to the rounding of a different chunking.
+ * npairs <= 16.
+ */
+typedef int (*pfx_allgather_fn)(void* ctx, double* buf, int64_t count);
+int pfx_tridiag_shard_rows(int64_t N, int64_t nrhs, int rank, int nranks, int64_t* r0, int64_t* r1);
+int pfx_expm_tridiag_shard(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs,
+                           double shift_c, const double* theta2, const double* coef2, int npairs, double* out,
+                           int rank, int nranks, pfx_allgather_fn allgather, void* ctx, void* stream);
+/*
  * Real symmetric banded path.
  *   band (kb+1) x N, lower symmetric band storage: band[r][j] = A[j+r][j].
  *   V, out: N x nrhs real.  No pivoting (same argument as above).

@@ -47,6 +47,11 @@ SIGNATURES = {
         _int,
         [_int, _vp, _i64, _i64, _vp, _i64, ctypes.c_double, _dp, _dp, _int, _vp, _fp, _vp],
     ),
+    "pfx_tridiag_shard_rows": (_int, [_i64, _i64, _int, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "pfx_expm_tridiag_shard": (
+        _int,
+        [_vp, _vp, _i64, _vp, _i64, ctypes.c_double, _dp, _dp, _int, _vp, _int, _int, _vp, _vp, _vp],
+    ),
     "pfx_prof_enable": (_int, [_int]),
     "pfx_prof_read": (_int, [ctypes.c_char_p, _int]),
     "pfx_shifted_solve": (
@@ -272,6 +277,56 @@ def expm_tridiag_device(diag, off, V, theta2, coef2, shift_c: float, out=None, p
     _check(st, "pfx_expm_tridiag")
     if per_pair_ms is not None:
         per_pair_ms[:] = list(ms)
+    return out.squeeze(-1) if squeeze else out
+
+
+# pfx_allgather_fn: int (*)(void* ctx, double* buf, int64_t count)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _dp, ctypes.c_int64)
+
+
+def tridiag_shard_rows(N: int, nrhs: int, rank: int, nranks: int):
+    """Rows [r0, r1) that rank `rank` of `nranks` owns in pfx_expm_tridiag_shard."""
+    r0, r1 = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().pfx_tridiag_shard_rows(N, nrhs, rank, nranks, ctypes.byref(r0), ctypes.byref(r1)),
+           "pfx_tridiag_shard_rows")
+    return r0.value, r1.value
+
+
+def expm_tridiag_shard(diag, off, V, theta2, coef2, shift_c: float, rank: int, nranks: int, allgather, out=None,
+                       stream=None):
+    """Row-sharded tridiagonal exp(A)V (include/pfx.h pfx_expm_tridiag_shard): this rank's
+    rows [r0, r1) of `out` (N x nrhs, device) are written, final.  `allgather(mine)` takes this
+    rank's float64 block and returns all ranks' blocks concatenated in rank order."""
+    torch = _torch()
+    squeeze = V.dim() == 1
+    if squeeze:
+        V = V.unsqueeze(-1)
+    N, nrhs = V.shape
+    if out is None:
+        out = torch.zeros((N, nrhs), dtype=torch.float64, device=V.device)
+    failure = []
+
+    def _cb(ctx, buf, count):
+        try:
+            full = np.ctypeslib.as_array(buf, shape=(nranks * count,))
+            mine = full[rank * count:(rank + 1) * count].copy()
+            got = np.asarray(allgather(mine), dtype=np.float64).reshape(-1)
+            if got.size != nranks * count:
+                raise ValueError(f"allgather returned {got.size} values, expected {nranks * count}")
+            full[:] = got
+            return 0
+        except Exception as exc:  # reported through the status below
+            failure.append(exc)
+            return 1
+
+    cb = ALLGATHER_FN(_cb)
+    st = lib().pfx_expm_tridiag_shard(
+        _ptr(diag), _ptr(off) if N > 1 else None, N, _ptr(V.contiguous()), nrhs, float(shift_c), _f64p(theta2),
+        _f64p(coef2), len(theta2) // 2, _ptr(out), rank, nranks, ctypes.cast(cb, _vp), None, _stream_ptr(stream),
+    )
+    if failure:
+        raise failure[0]
+    _check(st, "pfx_expm_tridiag_shard")
     return out.squeeze(-1) if squeeze else out
 
 

@@ -25,7 +25,8 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
                     double* out, cudaStream_t stream, float* per_pair_ms);
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
-                float* launch_ms, const double* V_host = nullptr, double* out_host = nullptr);
+                float* launch_ms, const double* V_host = nullptr, double* out_host = nullptr,
+                const TriShard* sh = nullptr);
 int banded_run(const double* band, int64_t N, int64_t kb, const double* V, int64_t nrhs, double shift_c,
                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                float* per_pair_ms);
@@ -394,6 +395,36 @@ int pfx_expm_tridiag(int mem, const double* diag, const double* off, int64_t N, 
     if (int rc_ = sync_stream(stream)) return rc_;
   }
   return PFX_OK;
+}
+
+int pfx_tridiag_shard_rows(int64_t N, int64_t nrhs, int rank, int nranks, int64_t* r0, int64_t* r1) {
+  g_err.clear();
+  if (N < 1 || nrhs < 1 || nranks < 1 || rank < 0 || rank >= nranks || !r0 || !r1)
+    return fail(PFX_BADARG, "bad shard arguments");
+  int L = 0, P = 0;
+  int64_t c0 = 0, c1 = 0;
+  if (int rc = tri_partition(N, nrhs, rank, nranks, &L, &P, &c0, &c1)) return rc;
+  *r0 = std::min<int64_t>(c0 * L, N);
+  *r1 = std::min<int64_t>(c1 * L, N);
+  return PFX_OK;
+}
+
+int pfx_expm_tridiag_shard(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs,
+                           double shift_c, const double* theta2, const double* coef2, int npairs, double* out,
+                           int rank, int nranks, pfx_allgather_fn allgather, void* ctx, void* stream_) {
+  g_err.clear();
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (N < 1 || nrhs < 1) return fail(PFX_BADARG, "need N >= 1 and nrhs >= 1");
+  if (!diag || !V || !out || (N > 1 && !off)) return fail(PFX_BADARG, "null array");
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !allgather)) return fail(PFX_BADARG, "bad shard arguments");
+  if (!std::isfinite(shift_c)) return fail(PFX_BADARG, "shift must be finite");
+  int rc = check_poles(theta2, coef2, npairs);
+  if (rc) return rc;
+  if (npairs > 16) return fail(PFX_BADARG, "row sharding needs npairs <= 16 (n <= 32)");
+  const double2 *th = nullptr, *co = nullptr;
+  if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
+  TriShard sh{rank, nranks, allgather, ctx};
+  return tridiag_run(diag, off, N, V, nrhs, shift_c, th, co, npairs, out, stream, nullptr, nullptr, nullptr, &sh);
 }
 
 int pfx_expm_banded(int mem, const double* band, int64_t N, int64_t kb, const double* V, int64_t nrhs,

@@ -32,6 +32,14 @@ int* pinned_word();
 // wait for `stream`: spin on cudaStreamQuery for up to ~200 us (short calls return without
 // the blocking-sync wake-up latency), then fall back to a blocking synchronise
 int sync_stream(cudaStream_t stream);
+// Row sharding of the tridiagonal path (pfx_expm_tridiag_shard): this process is `rank` of
+// `nranks`; allgather(ctx, buf, count) fills buf[j*count, (j+1)*count) with rank j's block.
+struct TriShard {
+  int rank, nranks;
+  int (*allgather)(void* ctx, double* buf, int64_t count);
+  void* ctx;
+};
+int tri_partition(int64_t N, int64_t nrhs, int rank, int nranks, int* L, int* P, int64_t* c0, int64_t* c1);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `bytes` exceeds what was set
 // before for this kernel (the call itself costs host time on every launch otherwise)
 int raise_smem_limit(const void* kernel, size_t bytes);

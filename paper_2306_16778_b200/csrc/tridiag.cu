@@ -31,7 +31,10 @@
 //   K_T5 tri_correct         per chunk: out_i += sum_k 2 Re(w (Lambda_i G + Lambda'_i G')),
 //                            Lambda = running product of -l (resp. -l') from the chunk edge.
 #include <algorithm>
+#include <complex>
+#include <cstring>
 #include <type_traits>
+#include <vector>
 
 #include "pfx_common.cuh"
 
@@ -69,6 +72,16 @@ struct TriArgs {
   int* contr;   // P          1 if every |l|, |l'| of the chunk is <= 1 (running products shrink)
   unsigned long long* vmax;  // nrhs  bit pattern of max_i |V[i, r]|
   double* out;  // N x nrhs
+  // Row sharding (pfx_expm_tridiag_shard): this call owns chunks [c0, c1) of the P; the two
+  // chunk scans then run in two passes, an aggregate pass (agg != 0: the range's composite
+  // goes to magg / cagg) and a replay pass entering the range with the state the other
+  // ranks' aggregates give (msin / csin; null = the start of the matrix).
+  int64_t c0, c1;
+  int agg;
+  const double2* msin;  // npairs x 2 dirs x (vn, vd)      Moebius state entering the range
+  double2* magg;        // npairs x 2 dirs x 4              transfer over the range
+  const double2* csin;  // npairs x nrhs x 2 dirs           RHS carry entering the range
+  double2* cagg;        // npairs x nrhs x 2 dirs x (A, B)  affine map over the range
 };
 
 // chunk summaries are stored chunk-fastest so the carry scan (one block per pair, rhs and
@@ -134,10 +147,10 @@ __device__ __forceinline__ M22 shfl_m22(const M22& m, int src) {
 // transfers of a (chunk, shift) sit in adjacent lanes and are combined by shuffles.
 __global__ void __launch_bounds__(128) tri_mobius_chunks(TriArgs a) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)a.P * a.npairs * TR_SEG;
+  const int64_t total = (a.c1 - a.c0) * a.npairs * TR_SEG;
   const bool live = tid < total;
   const int seg = (int)(tid & (TR_SEG - 1));
-  const int64_t ck = live ? tid / TR_SEG : 0;
+  const int64_t ck = live ? tid / TR_SEG + a.c0 * a.npairs : 0;
   const int k = (int)(ck % a.npairs);
   const int64_t cidx = ck / a.npairs;
   const int64_t s = cidx * a.L, e = (s + a.L < a.N ? s + a.L : a.N);
@@ -210,17 +223,18 @@ __global__ void __launch_bounds__(128) tri_mobius_chunks(TriArgs a) {
 __global__ void __launch_bounds__(TR_SCAN_T) tri_mobius_scan(TriArgs a) {
   __shared__ M22 sm[TR_SCAN_T];
   const int k = blockIdx.x >> 1, dir = blockIdx.x & 1;
-  const int P = a.P;
+  const int P = (int)(a.c1 - a.c0);  // chunks of this call's range
   const int per = (P + TR_SCAN_T - 1) / TR_SCAN_T;
   const int t = threadIdx.x;
   const double2* Tsrc = dir == 0 ? a.Tf : a.Tb;
   double2* dst = dir == 0 ? a.rho_in : a.rhob_in;
+  auto chunk_of = [&](int q) { return dir == 0 ? a.c0 + q : a.c1 - 1 - q; };
   // composite of this thread's range (in processing order)
   M22 acc = mident();
   for (int j = 0; j < per; ++j) {
     int q = t * per + j;
     if (q >= P) break;
-    int c = dir == 0 ? q : P - 1 - q;
+    const int64_t c = chunk_of(q);
     const double2* src = Tsrc + ((int64_t)c * a.npairs + k) * 4;
     M22 T{ld(&src[0]), ld(&src[1]), ld(&src[2]), ld(&src[3])};
     acc = mmul(T, acc);
@@ -240,16 +254,27 @@ __global__ void __launch_bounds__(TR_SCAN_T) tri_mobius_scan(TriArgs a) {
     }
     __syncthreads();
   }
+  if (a.agg) {  // aggregate pass: the range's transfer only
+    if (t == TR_SCAN_T - 1) {
+      double2* o = a.magg + (k * 2 + dir) * 4;
+      st(&o[0], sm[t].m0);
+      st(&o[1], sm[t].m1);
+      st(&o[2], sm[t].m2);
+      st(&o[3], sm[t].m3);
+    }
+    return;
+  }
   M22 pre = t > 0 ? sm[t - 1] : mident();
-  // state entering this thread's range
-  cplx vn = pre.m0, vd = pre.m2;  // pre * (1; 0)
+  // state entering this thread's range: pre * s0, s0 = (1; 0) at the start of the matrix
+  const cplx s0n = a.msin ? ld(&a.msin[(k * 2 + dir) * 2]) : mk(1, 0);
+  const cplx s0d = a.msin ? ld(&a.msin[(k * 2 + dir) * 2 + 1]) : mk(0, 0);
+  cplx vn = cadd(cmul(pre.m0, s0n), cmul(pre.m1, s0d)), vd = cadd(cmul(pre.m2, s0n), cmul(pre.m3, s0d));
   for (int j = 0; j < per; ++j) {
     int q = t * per + j;
     if (q >= P) break;
-    int c = dir == 0 ? q : P - 1 - q;
-    // rho = den / num
+    const int64_t c = chunk_of(q);
+    // rho = den / num (0 entering the first chunk of the matrix: no coupling)
     cplx rho = (vn.re == 0.0 && vn.im == 0.0) ? mk(0, 0) : cdiv(vd, vn);
-    if (q == 0) rho = mk(0, 0);
     st(&dst[(int64_t)c * a.npairs + k], rho);
     const double2* src = Tsrc + ((int64_t)c * a.npairs + k) * 4;
     M22 T{ld(&src[0]), ld(&src[1]), ld(&src[2]), ld(&src[3])};
@@ -517,12 +542,12 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
   const int dir = bid & 1;
   const int kr = bid >> 1;
   const int k = kr / a.nrhs, rr = kr - k * a.nrhs;
-  const int P = a.P;
+  const int P = (int)(a.c1 - a.c0);  // chunks of this call's range
   const int t = threadIdx.x;
   const int per = (P + CS_T - 1) / CS_T;
   const double2* Ls = dir == 0 ? a.LF : a.LB;
   const double2* gs = dir == 0 ? a.gF : a.gB;
-  auto chunk_of = [&](int q) { return dir == 0 ? q : P - 1 - q; };
+  auto chunk_of = [&](int q) { return dir == 0 ? a.c0 + q : a.c1 - 1 - q; };
   cplx A = mk(1, 0), B = mk(0, 0);
   for (int j0 = 0; j0 < per; j0 += 8) {
     cplx Lc[8], gc[8];
@@ -558,7 +583,15 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
     }
     __syncthreads();
   }
-  cplx x = t > 0 ? sB[t - 1] : mk(0, 0);
+  if (a.agg) {  // aggregate pass: the range's affine map only
+    if (t == CS_T - 1) {
+      st(&a.cagg[((k * a.nrhs + rr) * 2 + dir) * 2], A);
+      st(&a.cagg[((k * a.nrhs + rr) * 2 + dir) * 2 + 1], B);
+    }
+    return;
+  }
+  const cplx x0 = a.csin ? ld(&a.csin[(k * a.nrhs + rr) * 2 + dir]) : mk(0, 0);
+  cplx x = t > 0 ? cadd(cmul(sA[t - 1], x0), sB[t - 1]) : x0;
   double2* dst = dir == 0 ? a.G : a.Gb;
   for (int j0 = 0; j0 < per; j0 += 8) {
     cplx Lc[8], gc[8];
@@ -591,7 +624,8 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
   // one pad slot per 16 chunks: thread t walks chunks 16t.., so unpadded its lanes would sit
   // 256 B apart in one bank group; padded (272 B) they spread over all banks
   auto sx = [](int cc) { return cc + (cc >> 4); };
-  const int PP = a.P + (a.P >> 4) + 1;
+  const int P = (int)(a.c1 - a.c0);  // chunks of this call's range (local index = chunk - c0)
+  const int PP = P + (P >> 4) + 1;
   double2* sL = reinterpret_cast<double2*>(smem_raw);  // PP
   double2* sg = sL + PP;                               // PP
   __shared__ cplx sA[CS_T], sB[CS_T];
@@ -599,10 +633,9 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
   const int dir = bid & 1;
   const int kr = bid >> 1;
   const int k = kr / a.nrhs, rr = kr - k * a.nrhs;
-  const int P = a.P;
   const int t = threadIdx.x;
-  const double2* Ls = (dir == 0 ? a.LF : a.LB) + l_at(a, 0, k);
-  const double2* gs = (dir == 0 ? a.gF : a.gB) + g_at(a, 0, k, rr);
+  const double2* Ls = (dir == 0 ? a.LF : a.LB) + l_at(a, a.c0, k);
+  const double2* gs = (dir == 0 ? a.gF : a.gB) + g_at(a, a.c0, k, rr);
   for (int e = t; e < P; e += CS_T) {
     cp_async16(&sL[sx(e)], &Ls[e]);
     cp_async16(&sg[sx(e)], &gs[e]);
@@ -611,7 +644,7 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
   cp_async_wait<0>();
   __syncthreads();
   const int per = (P + CS_T - 1) / CS_T;
-  auto chunk_of = [&](int q) { return dir == 0 ? q : P - 1 - q; };
+  auto chunk_of = [&](int q) { return dir == 0 ? q : P - 1 - q; };  // local
   cplx A = mk(1, 0), B = mk(0, 0);
   for (int j = 0; j < per; ++j) {
     const int q = t * per + j;
@@ -635,21 +668,30 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
     }
     __syncthreads();
   }
-  cplx x = t > 0 ? sB[t - 1] : mk(0, 0);
+  if (a.agg) {  // aggregate pass: the range's affine map only
+    if (t == CS_T - 1) {
+      st(&a.cagg[((k * a.nrhs + rr) * 2 + dir) * 2], A);
+      st(&a.cagg[((k * a.nrhs + rr) * 2 + dir) * 2 + 1], B);
+    }
+    return;
+  }
+  const cplx x0 = a.csin ? ld(&a.csin[(k * a.nrhs + rr) * 2 + dir]) : mk(0, 0);
+  cplx x = t > 0 ? cadd(cmul(sA[t - 1], x0), sB[t - 1]) : x0;
   double2* dst = dir == 0 ? a.G : a.Gb;
   for (int j = 0; j < per; ++j) {
     const int q = t * per + j;
     if (q >= P) break;
     const int cc = chunk_of(q);
-    st(&dst[((int64_t)cc * a.npairs + k) * a.nrhs + rr], x);
+    st(&dst[((a.c0 + cc) * a.npairs + k) * a.nrhs + rr], x);
     x = cadd(cmul(ld(&sL[sx(cc)]), x), ld(&sg[sx(cc)]));
   }
 }
 
 static int carry_scan(const TriArgs& a, int npairs, int64_t nrhs, cudaStream_t stream) {
   const unsigned blocks = (unsigned)(npairs * nrhs * 2);
-  if (a.P <= CS_SMEM_P) {
-    const int smem = 2 * (a.P + (a.P >> 4) + 1) * (int)sizeof(double2);
+  const int64_t np_ = a.c1 - a.c0;
+  if (np_ <= CS_SMEM_P) {
+    const int smem = 2 * (int)(np_ + (np_ >> 4) + 1) * (int)sizeof(double2);
     static int set = 0;
     if (smem > set) {
       const int mx = 2 * (CS_SMEM_P + (CS_SMEM_P >> 4) + 1) * (int)sizeof(double2);
@@ -732,25 +774,47 @@ int tri_pipe(TriPipe& T) {
 // have landed, and each group's result goes back as soon as its edge fix is done, so the
 // PCIe transfers hide the compute (out is final only after the global carry scan, so the
 // H2D and D2H phases themselves cannot overlap).
-int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
-                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
-                float* launch_ms, const double* V_host, double* out_host) {
-  // Chunk length: the sweep keeps 32 (chunk, 16-RHS tile) units resident per SM, so the
-  // chunks are sized to fill every SM in one wave (C2: 224 rows -> 4682 units on 148 SMs,
-  // where 256 rows left 20 SMs idle), within [64, TR_L] rows and a multiple of 32.
+// Chunk partition: the sweep keeps 32 (chunk, 16-RHS tile) units resident per SM, so the
+// chunks are sized to fill every SM in one wave (C2: 224 rows -> 4682 units on 148 SMs, where
+// 256 rows left 20 SMs idle), within [32, TR_L] rows and a multiple of 32.  Row-sharded calls
+// size them for one rank's share of the rows; rank r owns chunks [P r / R, P (r + 1) / R).
+int tri_partition(int64_t N, int64_t nrhs, int rank, int nranks, int* L_, int* P_, int64_t* c0, int64_t* c1) {
   int dev = 0;
   PFX_CUDA_TRY(cudaGetDevice(&dev));
   static int sms_of[16] = {};
   if (dev < 16 && !sms_of[dev]) PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
   const int64_t slots = (int64_t)(dev < 16 ? sms_of[dev] : 148) * 2 * LS_WARPS * 4;
-  const int64_t per = ceil_div(N * ceil_div(nrhs, 16), slots);
-  const int L = (int)std::min<int64_t>(TR_L, std::max<int64_t>(64, ceil_div(per, 32) * 32));
+  const int64_t per = ceil_div(ceil_div(N, nranks) * ceil_div(nrhs, 16), slots);
+  const int L = (int)std::min<int64_t>(TR_L, std::max<int64_t>(nranks > 1 ? 32 : 64, ceil_div(per, 32) * 32));
   const int P = (int)ceil_div(N, L);
+  *L_ = L;
+  *P_ = P;
+  *c0 = (int64_t)P * rank / nranks;
+  *c1 = (int64_t)P * (rank + 1) / nranks;
+  return PFX_OK;
+}
+
+namespace {
+// host-side composition of the ranks' aggregates (row sharding)
+using zc = std::complex<double>;
+inline zc zl(const double* p) { return zc(p[0], p[1]); }
+}  // namespace
+
+int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
+                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
+                float* launch_ms, const double* V_host, double* out_host, const TriShard* sh) {
+  const int rank = sh ? sh->rank : 0, nranks = sh ? sh->nranks : 1;
+  int L = 0, P = 0;
+  int64_t c0 = 0, c1 = 0;
+  if (int rc = tri_partition(N, nrhs, rank, nranks, &L, &P, &c0, &c1)) return rc;
   const size_t nP = (size_t)P * npairs;
   const size_t nPR = nP * nrhs;
   const size_t nN = (size_t)N * npairs;
   const size_t nNf = npairs <= 16 ? 0 : nN;  // factor arrays only on the npairs > 16 path
-  size_t bytes = (nP * 4 * 2 + nP * 4 + nPR * 4 + nNf * 3) * sizeof(double2) + (size_t)P * sizeof(int) +
+  // + row-sharding exchange buffers: Moebius aggregates (4 per pair and direction) and entry
+  // states (2), RHS-carry aggregates (2 per pair, rhs and direction) and entry carries (1)
+  const size_t nX = (size_t)npairs * 2 * 6 + (size_t)npairs * nrhs * 2 * 3;
+  size_t bytes = (nP * 4 * 2 + nP * 4 + nPR * 4 + nNf * 3 + nX) * sizeof(double2) + (size_t)P * sizeof(int) +
                  (size_t)nrhs * sizeof(unsigned long long) + 64;
   double2* ws = static_cast<double2*>(scratch(1, bytes));
   if (!ws) return fail(PFX_CUDA, "tridiagonal workspace allocation failed");
@@ -779,7 +843,16 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   a.Lf = a.Gb + nPR;
   a.Lb = a.Lf + nNf;
   a.Wt = a.Lb + nNf;
-  a.contr = reinterpret_cast<int*>(a.Wt + nNf);
+  a.c0 = c0;
+  a.c1 = c1;
+  a.agg = 0;
+  a.msin = nullptr;
+  a.csin = nullptr;
+  a.magg = a.Wt + nNf;
+  double2* msin_d = a.magg + (size_t)npairs * 2 * 4;
+  a.cagg = msin_d + (size_t)npairs * 2 * 2;
+  double2* csin_d = a.cagg + (size_t)npairs * nrhs * 2 * 2;
+  a.contr = reinterpret_cast<int*>(csin_d + (size_t)npairs * nrhs * 2);
   a.vmax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.contr) + ((P * sizeof(int) + 15) & ~size_t(15)));
   a.out = out;
   PFX_CUDA_TRY(cudaMemsetAsync(a.contr, 0x01, (size_t)P * sizeof(int), stream));
@@ -790,16 +863,97 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaEventCreate(&e1));
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
+  // all-gather of this rank's `cnt` doubles (host) through the caller's callback
+  std::vector<double> xbuf;
+  auto exchange = [&](const double2* dev_src, int64_t cnt, const double* extra, int64_t nextra) -> int {
+    xbuf.assign((size_t)nranks * (cnt + nextra), 0.0);
+    double* mine = xbuf.data() + (size_t)rank * (cnt + nextra);
+    PFX_CUDA_TRY(cudaMemcpyAsync(mine, dev_src, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+    for (int64_t i = 0; i < nextra; ++i) mine[cnt + i] = extra[i];
+    if (sh->allgather(sh->ctx, xbuf.data(), cnt + nextra) != 0) return fail(PFX_CUDA, "row-shard all-gather failed");
+    return PFX_OK;
+  };
   {
-    int64_t th = (int64_t)P * npairs * TR_SEG;
-    PFX_LAUNCH("tri_mobius_chunks", stream, tri_mobius_chunks<<<(unsigned)ceil_div(th, 128), 128, 0, stream>>>(a));
-    PFX_CUDA_TRY(cudaGetLastError());
+    int64_t th = (c1 - c0) * npairs * TR_SEG;
+    if (th > 0) {
+      PFX_LAUNCH("tri_mobius_chunks", stream, tri_mobius_chunks<<<(unsigned)ceil_div(th, 128), 128, 0, stream>>>(a));
+      PFX_CUDA_TRY(cudaGetLastError());
+    }
+    if (nranks > 1) {
+      // pivot carries across ranks: aggregate transfer of every rank's chunks, then the
+      // state entering this rank's range (forward: ranks below, backward: ranks above)
+      a.agg = 1;
+      PFX_LAUNCH("tri_mobius_scan", stream, tri_mobius_scan<<<npairs * 2, TR_SCAN_T, 0, stream>>>(a));
+      PFX_CUDA_TRY(cudaGetLastError());
+      const int64_t cnt = (int64_t)npairs * 2 * 4 * 2;
+      if (int rc = exchange(a.magg, cnt, nullptr, 0)) return rc;
+      std::vector<double> s0((size_t)npairs * 2 * 2 * 2);
+      for (int k = 0; k < npairs; ++k)
+        for (int dir = 0; dir < 2; ++dir) {
+          zc vn(1, 0), vd(0, 0);
+          for (int j = dir == 0 ? 0 : nranks - 1; dir == 0 ? j < rank : j > rank; j += dir == 0 ? 1 : -1) {
+            const double* m = xbuf.data() + (size_t)j * cnt + (size_t)(k * 2 + dir) * 8;
+            const zc nn = zl(m) * vn + zl(m + 2) * vd, nd = zl(m + 4) * vn + zl(m + 6) * vd;
+            const double mx = std::max({std::abs(nn.real()), std::abs(nn.imag()), std::abs(nd.real()),
+                                        std::abs(nd.imag()), 1e-300});
+            const double sc = std::ldexp(1.0, -std::ilogb(mx));
+            vn = nn * sc;
+            vd = nd * sc;
+          }
+          double* o = s0.data() + (size_t)(k * 2 + dir) * 4;
+          o[0] = vn.real(), o[1] = vn.imag(), o[2] = vd.real(), o[3] = vd.imag();
+        }
+      PFX_CUDA_TRY(cudaMemcpyAsync(msin_d, s0.data(), s0.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+      a.agg = 0;
+      a.msin = msin_d;
+    }
     PFX_LAUNCH("tri_mobius_scan", stream, tri_mobius_scan<<<npairs * 2, TR_SCAN_T, 0, stream>>>(a));
     PFX_CUDA_TRY(cudaGetLastError());
   }
   const bool ls = npairs <= 16;
   const bool pipe = V_host != nullptr;
   if (pipe && !ls) return fail(PFX_BADARG, "tridiag_run: host pipelining needs npairs <= 16");
+  if (nranks > 1 && (pipe || !ls)) return fail(PFX_BADARG, "tridiag_run: row sharding needs device memory and npairs <= 16");
+  // RHS carries across ranks (row sharding): aggregate affine maps + max|V| of every rank,
+  // then the carries entering this rank's range and the global max|V| (fix-pass stop rule)
+  auto carry_exchange = [&]() -> int {
+    a.agg = 1;
+    if (int rc = carry_scan(a, npairs, nrhs, stream)) return rc;
+    std::vector<unsigned long long> vm((size_t)nrhs);
+    PFX_CUDA_TRY(cudaMemcpyAsync(vm.data(), a.vmax, (size_t)nrhs * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 stream));
+    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+    std::vector<double> vmd((size_t)nrhs);
+    for (int64_t r = 0; r < nrhs; ++r) std::memcpy(&vmd[r], &vm[r], sizeof(double));
+    const int64_t cnt = (int64_t)npairs * nrhs * 2 * 2 * 2;
+    if (int rc = exchange(a.cagg, cnt, vmd.data(), nrhs)) return rc;
+    const int64_t stride = cnt + nrhs;
+    std::vector<double> x0((size_t)npairs * nrhs * 2 * 2);
+    for (int64_t kr = 0; kr < (int64_t)npairs * nrhs; ++kr)
+      for (int dir = 0; dir < 2; ++dir) {
+        zc x(0, 0);
+        for (int j = dir == 0 ? 0 : nranks - 1; dir == 0 ? j < rank : j > rank; j += dir == 0 ? 1 : -1) {
+          const double* m = xbuf.data() + (size_t)j * stride + (size_t)(kr * 2 + dir) * 4;
+          x = zl(m) * x + zl(m + 2);
+        }
+        x0[(size_t)(kr * 2 + dir) * 2] = x.real();
+        x0[(size_t)(kr * 2 + dir) * 2 + 1] = x.imag();
+      }
+    for (int64_t r = 0; r < nrhs; ++r) {
+      double m = 0.0;
+      for (int j = 0; j < nranks; ++j) m = std::max(m, xbuf[(size_t)j * stride + cnt + r]);
+      std::memcpy(&vm[r], &m, sizeof(double));
+    }
+    PFX_CUDA_TRY(cudaMemcpyAsync(csin_d, x0.data(), x0.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+    PFX_CUDA_TRY(cudaMemcpyAsync(a.vmax, vm.data(), (size_t)nrhs * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                                 stream));
+    // the host vectors die with this scope: the copies must land first
+    PFX_CUDA_TRY(cudaStreamSynchronize(stream));
+    a.agg = 0;
+    a.csin = csin_d;
+    return PFX_OK;
+  };
   LsArgs lsa{};
   if (ls) {
     // checkpoints live in arena slot 2 (L2-resident: 2 x P x 32 x 16 x 32 B); the fix data
@@ -854,9 +1008,11 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       return PFX_OK;
     };
     if (!pipe) {
-      if (int rc = launch_ls(false, 0, P, stream)) return rc;
+      if (int rc = launch_ls(false, c0, c1, stream)) return rc;
+      if (nranks > 1)
+        if (int rc = carry_exchange()) return rc;
       if (int rc = carry_scan(a, npairs, nrhs, stream)) return rc;
-      if (int rc = launch_ls(true, 0, P, stream)) return rc;
+      if (int rc = launch_ls(true, c0, c1, stream)) return rc;
     } else {
       // events: [0, G) V group landed, [G, 2G) sweep done, [2G, 3G) result ready,
       // 4G: fork point, 4G + 1: all copies back
@@ -946,7 +1102,9 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
     PFX_CUDA_TRY(cudaGetLastError());
   }
   if (shift_c != 0.0) {
-    PFX_LAUNCH("scale_kernel", stream, scale_kernel<<<1184, 256, 0, stream>>>(out, (size_t)N * nrhs, exp(shift_c)));
+    const int64_t r0 = c0 * L, r1 = std::min<int64_t>(c1 * L, N);
+    PFX_LAUNCH("scale_kernel", stream,
+               scale_kernel<<<1184, 256, 0, stream>>>(out + r0 * nrhs, (size_t)(r1 - r0) * nrhs, exp(shift_c)));
     PFX_CUDA_TRY(cudaGetLastError());
   }
   if (launch_ms) {
