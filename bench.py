@@ -8,10 +8,16 @@ One eval (= one step) = exp(tA)V for the whole 16-column block.  --workload C1/C
 selects the other configs (C4 when built).  Inputs are seeded synthetic data with
 the reference recipes (paper_2306_16778_b200/workloads.py); there is no dataset.
 
-Multi-GPU (torchrun, one process per GPU): the n/2 pole pairs are sharded across
-ranks (contiguous ascending blocks); each rank factors and solves its own shifts
-and the partial sums meet in ONE NCCL reduce to rank 0 (the path's only exchange).
-Total work is fixed as N grows -> "scaling": "strong".
+Multi-GPU (torchrun, one process per GPU), total work fixed as N grows ("scaling":
+"strong"), --shard selects how it is split:
+  pole   the n/2 pole pairs in contiguous ascending blocks; each rank factors and solves
+         its own shifts and the partial sums meet in ONE NCCL reduce to rank 0 (the
+         north-star mechanism; every config);
+  rows   C2 only: each rank owns a contiguous block of the tridiagonal's row chunks
+         (pfx_expm_tridiag_shard); the two chunk scans exchange one small all-gather each
+         and every output row is final on its rank (no reduction of the 134 MB result);
+  batch  C3 only: each rank solves its block of the 512 matrices (no collective);
+  auto   (default) rows for C2, batch for C3, pole otherwise.
 
 Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA events on
 the launching stream, max over ranks; library profiling is off in the timed region (a
@@ -149,7 +155,7 @@ class ClockSampler:
 class Workload:
     """Inputs resident on the device + a step function calling the native library."""
 
-    def __init__(self, name, torch, dev, pairs_lo, pairs_hi):
+    def __init__(self, name, torch, dev, pairs_lo, pairs_hi, batch_range=None):
         from paper_2306_16778_b200 import workloads as W
         from paper_2306_16778_b200.roots import default_table
 
@@ -205,6 +211,9 @@ class Workload:
                          "N": 262144, "kb": 512, "nrhs": 8, "n": 16, "l2": "inputs > L2; no flush"}
         else:
             raise SystemExit(f"unknown workload {name}")
+        if batch_range is not None:  # batch sharding (C3): this rank's matrices only
+            b0, b1 = batch_range
+            self.host = {k: v[b0:b1] for k, v in self.host.items()}
         self.n = n
         t2, c2 = default_table(n).interleaved()
         self.theta2 = np.ascontiguousarray(t2[2 * pairs_lo: 2 * pairs_hi])
@@ -354,6 +363,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--prof-steps", type=int, default=3)
+    ap.add_argument("--shard", choices=["auto", "pole", "rows", "batch"], default="auto")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -419,10 +429,42 @@ def main():
 
     n = {"C1": 16, "C2": 24, "C3": 20, "C4": 24, "C5": 16}[args.workload]
     npairs = n // 2
-    lo = rank * npairs // world
-    hi = (rank + 1) * npairs // world
-    wl = Workload(args.workload, torch, dev, lo, hi)
+    shard = args.shard
+    if shard == "auto":
+        shard = {"C2": "rows", "C3": "batch"}.get(args.workload, "pole")
+    if (shard == "rows" and args.workload != "C2") or (shard == "batch" and args.workload != "C3"):
+        raise SystemExit(f"--shard {shard} does not apply to {args.workload}")
+    if world == 1:
+        shard = "pole"  # one rank: every mode is the plain call
+    lo, hi = (rank * npairs // world, (rank + 1) * npairs // world) if shard == "pole" else (0, npairs)
+    nbatch = W.C3["batch"]
+    brange = (rank * nbatch // world, (rank + 1) * nbatch // world) if shard == "batch" else None
+    wl = Workload(args.workload, torch, dev, lo, hi, batch_range=brange)
     stream = torch.cuda.current_stream()
+
+    def allgather(mine):
+        """All-gather of a small float64 host block (row sharding's scan aggregates)."""
+        if gloo:
+            parts = [torch.empty(mine.size, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(parts, torch.from_numpy(mine))
+            return torch.cat(parts).numpy()
+        full = torch.empty(world * mine.size, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(full, torch.from_numpy(mine).to(dev))
+        return full.cpu().numpy()
+
+    rows = None
+    if shard == "rows":
+        rows = _native.tridiag_shard_rows(1 << 20, 16, rank, world)
+
+    def compute(st):
+        """This rank's share of one eval; pole sharding adds the one reduce to rank 0."""
+        if shard == "rows":
+            di = wl.dev_in
+            wl.out = _native.expm_tridiag_shard(di["diag"], di["off"], di["V"], wl.theta2, wl.coef2, 0.0, rank, world,
+                                                allgather, out=wl.out, stream=st)
+            return wl.out
+        out = wl.step(st)
+        return reduce_sum(out) if shard == "pole" else out
 
     def barrier():
         if world > 1:
@@ -438,7 +480,7 @@ def main():
             wl.flush.zero_()
         if ev is not None:
             ev[0].record(stream)
-        out = reduce_sum(wl.step(stream))
+        out = compute(stream)
         if ev is not None:
             ev[1].record(stream)
         return out
@@ -487,9 +529,33 @@ def main():
     # the max over ranks of the wall clock between two barriers
     e2e = None
     if args.e2e_steps > 0:
-        def e2e_step():
-            part = wl.step_host()
+        h2d, d2h = wl.h2d, wl.d2h
+        if shard == "rows":
+            # this rank's rows in (V, diag, the couplings at its edges), its rows of out back
+            r0, r1 = rows
+            o0 = max(r0 - 1, 0)
+            o1 = min(r1, (1 << 20) - 1)
+            pin, di = wl.pinned, wl.dev_in
+            pout = wl.pinned_out.view(1 << 20, 16)
+            h2d = (r1 - r0) * (16 + 1) * 8 + (o1 - o0) * 8
+            d2h = (r1 - r0) * 16 * 8
             if world > 1:
+                t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device="cpu" if gloo else dev)
+                dist.all_reduce(t)
+                h2d, d2h = int(t[0].item()), int(t[1].item())
+
+        def e2e_step():
+            if shard == "rows":
+                di["V"][r0:r1].copy_(pin["V"][r0:r1], non_blocking=True)
+                di["diag"][r0:r1].copy_(pin["diag"][r0:r1], non_blocking=True)
+                if o1 > o0:
+                    di["off"][o0:o1].copy_(pin["off"][o0:o1], non_blocking=True)
+                out = compute(stream)
+                pout[r0:r1].copy_(out[r0:r1], non_blocking=True)
+                stream.synchronize()
+                return
+            part = wl.step_host()
+            if world > 1 and shard == "pole":
                 t = reduce_sum(torch.from_numpy(np.ascontiguousarray(part)).reshape(-1).to(dev))
                 if rank == 0:
                     t.cpu()
@@ -503,7 +569,7 @@ def main():
         barrier()
         dt = all_max(time.perf_counter() - t0)
         e2e = {"value": wl.evals_per_step * args.e2e_steps / dt, "unit": UNIT,
-               "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     launches = sum(v[0] for v in kern.values())
     dom = DOMINANT[args.workload]
@@ -516,7 +582,8 @@ def main():
             flops_per_launch = dom_fl / dom_cnt
         else:
             # one launch of the dominant kernel carries the path's whole algorithmic work per step
-            flops_per_launch = ALG_FLOPS[args.workload] * wl.evals_per_step * (hi - lo) / npairs / (dom_cnt / prof_steps)
+            share = {"pole": (hi - lo) / npairs, "rows": 1.0 / world, "batch": 1.0 / world}[shard]
+            flops_per_launch = ALG_FLOPS[args.workload] * wl.evals_per_step * share / (dom_cnt / prof_steps)
         achieved = flops_per_launch / t_launch / 1e12
         roofline = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                     "frac": achieved / peaks["fp64_tflops"], "traffic": DOM_TRAFFIC.get(args.workload), "kernel": dom,
@@ -545,7 +612,10 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic (seeded reference recipes)",
-            "config": dict(wl.desc, parallelism=f"pole-shard x{world}" + (" + 1 NCCL reduce" if world > 1 else "")),
+            "config": dict(wl.desc, parallelism={
+                "pole": f"pole-shard x{world}" + (" + 1 NCCL reduce" if world > 1 else ""),
+                "rows": f"row-shard x{world} + 2 small all-gathers (scan aggregates); output rows stay on their rank",
+                "batch": f"batch-shard x{world} (no collective)"}[shard]),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches * args.steps // prof_steps,
             "kernels": {k: {"launches": v[0], "total_ms": v[1], "gflop": v[2] / 1e9} for k, v in kern.items()},

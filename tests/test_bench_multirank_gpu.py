@@ -1,5 +1,6 @@
-"""bench.py under torchrun with two ranks (gloo emulation on one GPU): the pole-sharded
-timed region, the max-over-ranks timing, the N > 1 e2e leg and rank 0's single JSON line."""
+"""bench.py under torchrun with two ranks (gloo emulation on one GPU): the pole-, row- and
+batch-sharded timed regions, the max-over-ranks timing, the N > 1 e2e leg and rank 0's
+single JSON line."""
 import json
 import os
 import socket
@@ -20,11 +21,14 @@ def _port():
     return p
 
 
-def test_two_rank_bench_line():
+@pytest.mark.parametrize("workload,shard,tag", [("C1", "auto", "pole-shard x2"), ("C2", "auto", "row-shard x2"),
+                                               ("C2", "pole", "pole-shard x2"), ("C3", "auto", "batch-shard x2")])
+def test_two_rank_bench_line(workload, shard, tag):
     env = dict(os.environ, PFX_BENCH_GLOO="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--workload", "C1", "--steps", "3", "--warmup", "3", "--e2e-steps", "2"]
+           "--gpus", "2", "--workload", workload, "--shard", shard, "--steps", "3", "--warmup", "3",
+           "--e2e-steps", "2"]
     res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
@@ -32,4 +36,4 @@ def test_two_rank_bench_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["warmup"] == 3
     assert d["value"] > 0 and d["e2e"] is not None and d["e2e"]["value"] > 0
-    assert "pole-shard x2" in d["config"]["parallelism"]
+    assert tag in d["config"]["parallelism"]
