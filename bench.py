@@ -68,7 +68,7 @@ ALG_BYTES = {
 }
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, from the
 # round's `ncu --set full` capture (profiles/r01_c2_tri_ls_ncu_details.csv); None = not captured
-DOM_TRAFFIC = {"C2": 8.30e8}
+DOM_TRAFFIC = {"C2": 1.288e9, "C3": 4.566e10}
 DOMINANT = {"C1": "dense_batched_kernel", "C2": "tri_sweep", "C3": "dense_batched_kernel", "C4": "zgemm", "C5": "zgemm"}
 
 
