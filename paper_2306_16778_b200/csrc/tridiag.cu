@@ -82,6 +82,12 @@ struct TriArgs {
   double2* magg;        // npairs x 2 dirs x 4              transfer over the range
   const double2* csin;  // npairs x nrhs x 2 dirs           RHS carry entering the range
   double2* cagg;        // npairs x nrhs x 2 dirs x (A, B)  affine map over the range
+  // Host-mode group pipeline (carry scans per row group): directions scanned (bit 0 forward,
+  // bit 1 backward), carries stored only for chunks [w0, w1), and cin_prev = the forward
+  // carry entering the range is continued from the previous chunk's (G, LF, gF)
+  int dirmask;
+  int64_t w0, w1;
+  int cin_prev;
 };
 
 // chunk summaries are stored chunk-fastest so the carry scan (one block per pair, rhs and
@@ -536,10 +542,22 @@ __global__ void __launch_bounds__(TR_SW_WARPS * 32) tri_pass(TriArgs a) {
 // over chunks: each thread composes a contiguous range (loads batched), block scan of the
 // thread composites through shared memory, then each thread replays its range.
 constexpr int CS_T = 256;
+// carry entering the scanned range: the exchanged one (row sharding), the previous chunk's
+// carried through its summary (host-mode group pipeline, forward), else zero (matrix edge)
+__device__ __forceinline__ cplx carry_in(const TriArgs& a, int k, int rr, int dir) {
+  if (a.csin) return ld(&a.csin[(k * a.nrhs + rr) * 2 + dir]);
+  if (a.cin_prev && dir == 0 && a.c0 > 0) {
+    const int64_t c = a.c0 - 1;
+    return cadd(cmul(ld(&a.LF[l_at(a, c, k)]), ld(&a.G[(c * a.npairs + k) * a.nrhs + rr])), ld(&a.gF[g_at(a, c, k, rr)]));
+  }
+  return mk(0, 0);
+}
+
 __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
   __shared__ cplx sA[CS_T], sB[CS_T];
   const int bid = blockIdx.x;
   const int dir = bid & 1;
+  if (!((a.dirmask >> dir) & 1)) return;
   const int kr = bid >> 1;
   const int k = kr / a.nrhs, rr = kr - k * a.nrhs;
   const int P = (int)(a.c1 - a.c0);  // chunks of this call's range
@@ -590,7 +608,7 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
     }
     return;
   }
-  const cplx x0 = a.csin ? ld(&a.csin[(k * a.nrhs + rr) * 2 + dir]) : mk(0, 0);
+  const cplx x0 = carry_in(a, k, rr, dir);
   cplx x = t > 0 ? cadd(cmul(sA[t - 1], x0), sB[t - 1]) : x0;
   double2* dst = dir == 0 ? a.G : a.Gb;
   for (int j0 = 0; j0 < per; j0 += 8) {
@@ -608,7 +626,8 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan(TriArgs a) {
     for (int u = 0; u < 8; ++u) {
       const int q = t * per + j0 + u;
       if (j0 + u < per && q < P) {
-        st(&dst[((int64_t)chunk_of(q) * a.npairs + k) * a.nrhs + rr], x);
+        const int64_t cq = chunk_of(q);
+        if (cq >= a.w0 && cq < a.w1) st(&dst[(cq * a.npairs + k) * a.nrhs + rr], x);
         x = cadd(cmul(Lc[u], x), gc[u]);
       }
     }
@@ -631,6 +650,7 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
   __shared__ cplx sA[CS_T], sB[CS_T];
   const int bid = blockIdx.x;
   const int dir = bid & 1;
+  if (!((a.dirmask >> dir) & 1)) return;
   const int kr = bid >> 1;
   const int k = kr / a.nrhs, rr = kr - k * a.nrhs;
   const int t = threadIdx.x;
@@ -675,15 +695,46 @@ __global__ void __launch_bounds__(CS_T) tri_carry_scan_smem(TriArgs a) {
     }
     return;
   }
-  const cplx x0 = a.csin ? ld(&a.csin[(k * a.nrhs + rr) * 2 + dir]) : mk(0, 0);
+  const cplx x0 = carry_in(a, k, rr, dir);
   cplx x = t > 0 ? cadd(cmul(sA[t - 1], x0), sB[t - 1]) : x0;
   double2* dst = dir == 0 ? a.G : a.Gb;
   for (int j = 0; j < per; ++j) {
     const int q = t * per + j;
     if (q >= P) break;
     const int cc = chunk_of(q);
-    st(&dst[((a.c0 + cc) * a.npairs + k) * a.nrhs + rr], x);
+    if (a.c0 + cc >= a.w0 && a.c0 + cc < a.w1) st(&dst[((a.c0 + cc) * a.npairs + k) * a.nrhs + rr], x);
     x = cadd(cmul(ld(&sL[sx(cc)]), x), ld(&sg[sx(cc)]));
+  }
+}
+
+// Host-mode group pipeline: group g's backward carries were scanned from the end of group g+1
+// with zero entering (truncation).  The neglected term is (prod over group g+1 of L') times the
+// true carry entering there, |carry| <= N max|V| when every chunk is contractive (|l'| <= 1),
+// and it reaches the output through |z| <= beta_k: it stays below one unit roundoff of max|V|
+// when N sum_k beta_k max_k prod_{c in g+1} |LB_k(c)| <= 2^-53.  Otherwise (or for any
+// non-contractive chunk) *flag is set and the caller redoes the carries globally.
+__global__ void tri_trunc_check(TriArgs a, int ng, int* flag) {
+  // one warp per (truncated group, pair): log2 of the product, summed over the group's chunks
+  const int np = a.npairs;
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w < (ng - 1) * np) {
+    const int g = w / np + 1, k = w - (w / np) * np;  // group g (>= 1) was truncated away
+    const int64_t lo = (int64_t)a.P * g / ng, hi = (int64_t)a.P * (g + 1) / ng;
+    double lg = 0.0;
+    for (int64_t c = lo + lane; c < hi; c += 32) {
+      const cplx l = ld(&a.LB[l_at(a, c, k)]);
+      lg += 0.5 * log2(fma(l.re, l.re, l.im * l.im));  // -inf for an exact zero: fine
+    }
+    for (int off = 16; off > 0; off >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, off);
+    double bsum = 0.0;
+    for (int q = 0; q < np; ++q) {
+      const cplx th = ld(&a.theta[q]), co = ld(&a.coef[q]);
+      bsum += 2.0 * cabs1(co) / th.im;
+    }
+    if (lane == 0 && !(lg + log2((double)a.N * bsum) <= -53.0)) atomicExch(flag, 1);
+  } else if (w == (ng - 1) * np) {
+    for (int64_t c = lane; c < a.P; c += 32)
+      if (!a.contr[c]) atomicExch(flag, 1);
   }
 }
 
@@ -747,6 +798,7 @@ struct TriPipe {
   cudaStream_t cs[TR_GROUPS] = {};  // per-group fix streams: earlier groups first (D2H order)
   cudaStream_t sw[TR_GROUPS] = {};  // per-group sweep streams: later groups first (their rows land last)
   cudaEvent_t ev[4 * TR_GROUPS + 2] = {};
+  cudaEvent_t kick = nullptr;  // timing-enabled (see the group loop)
 };
 int tri_pipe(TriPipe& T) {
   static TriPipe g;
@@ -763,6 +815,7 @@ int tri_pipe(TriPipe& T) {
       PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.sw[TR_GROUPS - 1 - i], cudaStreamNonBlocking, pr));
     }
     for (auto& e : g.ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    PFX_CUDA_TRY(cudaEventCreate(&g.kick));
   }
   T = g;
   return PFX_OK;
@@ -815,7 +868,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   // states (2), RHS-carry aggregates (2 per pair, rhs and direction) and entry carries (1)
   const size_t nX = (size_t)npairs * 2 * 6 + (size_t)npairs * nrhs * 2 * 3;
   size_t bytes = (nP * 4 * 2 + nP * 4 + nPR * 4 + nNf * 3 + nX) * sizeof(double2) + (size_t)P * sizeof(int) +
-                 (size_t)nrhs * sizeof(unsigned long long) + 64;
+                 (TR_GROUPS + 1) * (size_t)nrhs * sizeof(unsigned long long) + 64;
   double2* ws = static_cast<double2*>(scratch(1, bytes));
   if (!ws) return fail(PFX_CUDA, "tridiagonal workspace allocation failed");
   TriArgs a;
@@ -856,7 +909,14 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   a.vmax = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.contr) + ((P * sizeof(int) + 15) & ~size_t(15)));
   a.out = out;
   PFX_CUDA_TRY(cudaMemsetAsync(a.contr, 0x01, (size_t)P * sizeof(int), stream));
-  PFX_CUDA_TRY(cudaMemsetAsync(a.vmax, 0, (size_t)nrhs * sizeof(unsigned long long), stream));
+  // max|V| per rhs: one slice per host-pipeline row group (+ the whole matrix), then a flag word
+  int* trunc_flag = reinterpret_cast<int*>(a.vmax + (TR_GROUPS + 1) * (size_t)nrhs);
+  PFX_CUDA_TRY(cudaMemsetAsync(a.vmax, 0, (TR_GROUPS + 1) * (size_t)nrhs * sizeof(unsigned long long) + sizeof(int),
+                               stream));
+  a.dirmask = 3;
+  a.w0 = 0;
+  a.w1 = P;
+  a.cin_prev = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (launch_ms) {
     PFX_CUDA_TRY(cudaEventCreate(&e0));
@@ -994,16 +1054,17 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       c0 = (int64_t)P * g / ng;
       c1 = (int64_t)P * (g + 1) / ng;
     };
-    auto launch_ls = [&](bool fix, int64_t c0, int64_t c1, cudaStream_t st) -> int {
+    auto launch_ls = [&](bool fix, int64_t c0, int64_t c1, cudaStream_t st, const TriArgs* aa = nullptr) -> int {
+      const TriArgs& ta = aa ? *aa : a;
       LsArgs la = lsa;
       la.unit0 = c0 * ntile;
       la.unit1 = c1 * ntile;
       const unsigned blocks = (unsigned)ceil_div(la.unit1 - la.unit0, LS_WARPS * 2);
       if (blocks == 0) return PFX_OK;
       if (fix)
-        PFX_LAUNCH("tri_fix", st, (k1<<<blocks, LS_WARPS * 32, smem_fix, st>>>(a, la)));
+        PFX_LAUNCH("tri_fix", st, (k1<<<blocks, LS_WARPS * 32, smem_fix, st>>>(ta, la)));
       else
-        PFX_LAUNCH("tri_sweep", st, (k0<<<blocks, LS_WARPS * 32, smem, st>>>(a, la)));
+        PFX_LAUNCH("tri_sweep", st, (k0<<<blocks, LS_WARPS * 32, smem, st>>>(ta, la)));
       PFX_CUDA_TRY(cudaGetLastError());
       return PFX_OK;
     };
@@ -1045,20 +1106,53 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
         grp(g, c0, c1);
         PFX_CUDA_TRY(cudaStreamWaitEvent(TP.sw[g], ev[4 * G], 0));  // after the Moebius scan
         PFX_CUDA_TRY(cudaStreamWaitEvent(TP.sw[g], ev[g], 0));
-        if (int rc = launch_ls(false, c0, c1, TP.sw[g])) return rc;
+        TriArgs ag = a;
+        ag.vmax = a.vmax + (size_t)g * nrhs;  // this group's max|V| (its fix's stop rule)
+        if (int rc = launch_ls(false, c0, c1, TP.sw[g], &ag)) return rc;
         PFX_CUDA_TRY(cudaEventRecord(ev[G + g], TP.sw[g]));
         if (tl) cudaEventRecord(tev[G + g], TP.sw[g]);
-        PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[G + g], 0));
       }
-      if (int rc = carry_scan(a, npairs, nrhs, stream)) return rc;
-      PFX_CUDA_TRY(cudaEventRecord(ev[4 * G], stream));  // carry scan done
+      // Carries per group instead of one global scan, so group g's fix and copy-back start
+      // once group g + 1 is swept and overlap the copy-in of the later groups:
+      //   forward: chained group to group on the main stream (each scan continues from the
+      //     previous group's last chunk);
+      //   backward: group g's carries are scanned from the end of group g + 1 with zero
+      //     entering there.  The neglected term is below one unit roundoff of max|V| when the
+      //     decay over group g + 1 is strong enough (tri_trunc_check, after every sweep; the
+      //     call falls back to the global scans otherwise).
+      // Each group's fix stops at one unit roundoff of its own rows' max|V| (stricter than the
+      // whole matrix's).
       if (tl) cudaEventRecord(tev[5 * G + 1], stream);
+      // A timing-enabled event recorded on the main stream here makes the driver submit the
+      // main stream's queued work at once; without it the forward-carry chain below (and the
+      // fixes and copy-backs behind it) started late (measured C2 host call 5.31 -> 4.32 ms;
+      // a timing-disabled event does not have the effect)
+      PFX_CUDA_TRY(cudaEventRecord(TP.kick, stream));
       for (int g = 0; g < ng; ++g) {
-        int64_t c0, c1;
+        int64_t c0, c1, n0, n1;
         grp(g, c0, c1);
+        grp(std::min(g + 1, ng - 1), n0, n1);
         const int64_t r0 = c0 * L, r1 = std::min<int64_t>(c1 * L, N);
-        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[4 * G], 0));
-        if (int rc = launch_ls(true, c0, c1, TP.cs[g])) return rc;
+        TriArgs ag = a;
+        ag.vmax = a.vmax + (size_t)g * nrhs;
+        ag.c0 = c0;
+        ag.c1 = c1;
+        ag.w0 = c0;
+        ag.w1 = c1;
+        ag.dirmask = 1;
+        ag.cin_prev = 1;
+        PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[G + g], 0));
+        if (int rc = carry_scan(ag, npairs, nrhs, stream)) return rc;
+        PFX_CUDA_TRY(cudaEventRecord(ev[3 * G + g], stream));
+        ag.c1 = n1;
+        ag.dirmask = 2;
+        ag.cin_prev = 0;
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[G + g], 0));
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[G + std::min(g + 1, ng - 1)], 0));
+        if (int rc = carry_scan(ag, npairs, nrhs, TP.cs[g])) return rc;
+        PFX_CUDA_TRY(cudaStreamWaitEvent(TP.cs[g], ev[3 * G + g], 0));
+        ag.c1 = c1;
+        if (int rc = launch_ls(true, c0, c1, TP.cs[g], &ag)) return rc;
         if (shift_c != 0.0) {
           PFX_LAUNCH("scale_kernel", TP.cs[g],
                      scale_rows<<<296, 256, 0, TP.cs[g]>>>(out + r0 * nrhs, (r1 - r0) * nrhs, exp(shift_c)));
@@ -1088,9 +1182,33 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
         for (int g = 0; g < ng; ++g) fprintf(stderr, " %.2f", at(3 * G + g));
         fprintf(stderr, "\n");
       }
+      // the main stream has waited for every sweep (forward chain): check the truncation while
+      // the last groups are fixed and copied back
+      PFX_LAUNCH("tri_trunc_check", stream,
+                 tri_trunc_check<<<(unsigned)ceil_div((int64_t)(ng - 1) * npairs + 1, 8), 256, 0, stream>>>(a, ng,
+                                                                                                       trunc_flag));
+      PFX_CUDA_TRY(cudaGetLastError());
       PFX_CUDA_TRY(cudaEventRecord(ev[4 * G + 1], TP.outs));
       PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[4 * G + 1], 0));
-      shift_c = 0.0;  // applied per group above
+      int* hflag = pinned_word();
+      if (!hflag) return fail(PFX_CUDA, "pinned status word allocation failed");
+      PFX_CUDA_TRY(cudaMemcpyAsync(hflag, trunc_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      if (int rc = sync_stream(stream)) return rc;
+      if (*hflag) {
+        // weak decay across a row group: redo the carries globally (V is on the device)
+        TriArgs af = a;
+        af.vmax = a.vmax + (size_t)TR_GROUPS * nrhs;
+        if (int rc = launch_ls(false, 0, P, stream, &af)) return rc;
+        if (int rc = carry_scan(af, npairs, nrhs, stream)) return rc;
+        if (int rc = launch_ls(true, 0, P, stream, &af)) return rc;
+        if (shift_c != 0.0) {
+          PFX_LAUNCH("scale_kernel", stream,
+                     scale_kernel<<<1184, 256, 0, stream>>>(out, (size_t)N * nrhs, exp(shift_c)));
+          PFX_CUDA_TRY(cudaGetLastError());
+        }
+        PFX_CUDA_TRY(cudaMemcpyAsync(out_host, out, (size_t)N * nrhs * sizeof(double), cudaMemcpyDeviceToHost, stream));
+      }
+      shift_c = 0.0;  // applied per group above (or in the fallback)
     }
   } else {
     PFX_LAUNCH("tri_factor", stream, tri_factor<<<(unsigned)ceil_div((int64_t)P * npairs, 128), 128, 0, stream>>>(a));

@@ -89,3 +89,26 @@ def test_shift_many_groups_ragged_tiles():
     assert c != 0.0
     want = np.exp(c) * restate.tridiag_action(d - c, o, V, 24)
     assert rel(res.value, want) <= TOL
+
+
+@pytest.mark.parametrize("N,nrhs,scale", [(4096, 4, 25.0), (1 << 16, 16, 25.0), (1 << 18, 16, 25.0),
+                                          (1 << 16, 3, 0.05)])
+def test_host_pipeline_matches_device(N, nrhs, scale):
+    """Host-memory calls pipeline the copies by row groups with per-group carries (backward
+    carries truncated at the next group, verified by tri_trunc_check, global fallback
+    otherwise).  Small groups or weak decay (scale 0.05: |l'| close to 1 over many rows) take
+    the fallback; C2-like sizes take the truncated carries.  Both must agree with the
+    device-memory call, which scans the carries globally, to rounding."""
+    import torch
+
+    from paper_2306_16778_b200 import _native
+    from paper_2306_16778_b200.roots import default_table
+
+    d, o = workloads.c2_matrix(N, scale=scale)
+    V = np.random.default_rng([N, nrhs]).standard_normal((N, nrhs))
+    t2, c2 = default_table(24).interleaved()
+    host = _native.expm_tridiag_host(d, o, V, t2, c2, 0.0)
+    dev = torch.device("cuda:0")
+    devr = _native.expm_tridiag_device(*(torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (d, o, V)), t2,
+                                       c2, 0.0).cpu().numpy()
+    assert rel(host, devr) <= 1e-13, rel(host, devr)
