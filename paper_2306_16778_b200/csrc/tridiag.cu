@@ -792,7 +792,7 @@ __global__ void scale_rows(double* x, int64_t n, double s) {
 }
 
 namespace {
-constexpr int TR_GROUPS = 8;
+constexpr int TR_GROUPS = 16;
 struct TriPipe {
   cudaStream_t in = nullptr, outs = nullptr;
   cudaStream_t cs[TR_GROUPS] = {};  // per-group fix streams: earlier groups first (D2H order)
@@ -1101,7 +1101,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
         PFX_CUDA_TRY(cudaEventRecord(ev[g], TP.in));
         if (tl) cudaEventRecord(tev[g], TP.in);
       }
-      for (int g = 0; g < ng; ++g) {
+      auto sweep_group = [&](int g) -> int {
         int64_t c0, c1;
         grp(g, c0, c1);
         PFX_CUDA_TRY(cudaStreamWaitEvent(TP.sw[g], ev[4 * G], 0));  // after the Moebius scan
@@ -1111,7 +1111,8 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
         if (int rc = launch_ls(false, c0, c1, TP.sw[g], &ag)) return rc;
         PFX_CUDA_TRY(cudaEventRecord(ev[G + g], TP.sw[g]));
         if (tl) cudaEventRecord(tev[G + g], TP.sw[g]);
-      }
+        return PFX_OK;
+      };
       // Carries per group instead of one global scan, so group g's fix and copy-back start
       // once group g + 1 is swept and overlap the copy-in of the later groups:
       //   forward: chained group to group on the main stream (each scan continues from the
@@ -1122,13 +1123,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       //     call falls back to the global scans otherwise).
       // Each group's fix stops at one unit roundoff of its own rows' max|V| (stricter than the
       // whole matrix's).
-      if (tl) cudaEventRecord(tev[5 * G + 1], stream);
-      // A timing-enabled event recorded on the main stream here makes the driver submit the
-      // main stream's queued work at once; without it the forward-carry chain below (and the
-      // fixes and copy-backs behind it) started late (measured C2 host call 5.31 -> 4.32 ms;
-      // a timing-disabled event does not have the effect)
-      PFX_CUDA_TRY(cudaEventRecord(TP.kick, stream));
-      for (int g = 0; g < ng; ++g) {
+      auto finish_group = [&](int g) -> int {
         int64_t c0, c1, n0, n1;
         grp(g, c0, c1);
         grp(std::min(g + 1, ng - 1), n0, n1);
@@ -1144,6 +1139,11 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
         PFX_CUDA_TRY(cudaStreamWaitEvent(stream, ev[G + g], 0));
         if (int rc = carry_scan(ag, npairs, nrhs, stream)) return rc;
         PFX_CUDA_TRY(cudaEventRecord(ev[3 * G + g], stream));
+        // A timing-enabled event recorded on the main stream makes the driver submit its
+        // queued work at once; without it the forward-carry chain (and the fixes and
+        // copy-backs behind it) started late (C2 host call 5.31 -> 4.32 ms; a timing-disabled
+        // event does not have the effect)
+        PFX_CUDA_TRY(cudaEventRecord(TP.kick, stream));
         ag.c1 = n1;
         ag.dirmask = 2;
         ag.cin_prev = 0;
@@ -1164,7 +1164,17 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
         PFX_CUDA_TRY(cudaMemcpyAsync(out_host + r0 * nrhs, out + r0 * nrhs, (size_t)(r1 - r0) * nrhs * sizeof(double),
                                      cudaMemcpyDeviceToHost, TP.outs));
         if (tl) cudaEventRecord(tev[3 * G + g], TP.outs);
+        return PFX_OK;
+      };
+      // enqueue order: a group's carries, fix and copy-back right after the next group's sweep
+      // (the host reaches the first fix after two sweeps, not after all of them)
+      if (tl) cudaEventRecord(tev[5 * G + 1], stream);
+      for (int g = 0; g < ng; ++g) {
+        if (int rc = sweep_group(g)) return rc;
+        if (g > 0)
+          if (int rc = finish_group(g - 1)) return rc;
       }
+      if (int rc = finish_group(ng - 1)) return rc;
       if (tl) {
         cudaDeviceSynchronize();
         auto at = [&](int i) {
