@@ -1080,6 +1080,14 @@ static size_t dense_smem_bytes(int d, int nb) {
 
 int dense_batched_supported(int64_t d) { return d >= 1 && d <= 512; }
 
+// resident CTAs (= concurrently factored systems) of dense_batched_run for nsys systems of size d
+int dense_batched_slots(int d, int64_t nsys) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool many = nsys > sms;
+  return (d <= 256 && many) ? 2 * sms : sms;
+}
+
 // Launch the batched path.  All pointers are device pointers.
 int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
                       int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,

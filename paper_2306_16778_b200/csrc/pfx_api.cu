@@ -17,6 +17,7 @@ namespace pfx {
 
 // kernels (defined in the other translation units)
 int dense_batched_supported(int64_t d);
+int dense_batched_slots(int d, int64_t nsys);
 int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
                       int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,
                       int npairs, double* out, cudaStream_t stream, float* launch_ms, int pivot);
@@ -319,6 +320,71 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
   const double2 *th = nullptr, *co = nullptr;
   rc = upload_poles(theta2, coef2, npairs, stream, &th, &co);
   if (rc) return rc;
+  if (mem == PFX_MEM_HOST && dense_batched_supported(d) && batch > 1) {
+    // Host batches: the matrices go in by chunks on a copy stream and each chunk is factored
+    // as soon as it has landed, so the copy-in hides behind the factorisations.  Chunks hold
+    // five rounds of the resident CTAs' systems (whole rounds: no extra tail); the remainder
+    // goes first, where its short copy starts the pipeline.
+    const int64_t slots = dense_batched_slots((int)d, batch * npairs);
+    const int64_t per = std::max<int64_t>(1, slots * 5 / npairs);
+    if (batch >= 2 * per) {
+      static cudaStream_t cin = nullptr;
+      static std::vector<cudaEvent_t> evs;
+      if (!cin) PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+      const int64_t first = batch % per ? batch % per : per;
+      const int64_t nch = 1 + (batch - first + per - 1) / per;
+      while ((int64_t)evs.size() < nch + 1) {
+        cudaEvent_t e;
+        PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+      }
+      const size_t am = abytes / batch, vm = vbytes / batch, om = obytes / batch;  // bytes per matrix
+      char* Ad = static_cast<char*>(scratch(3, abytes));
+      char* Vd = vbytes ? static_cast<char*>(scratch(4, vbytes)) : nullptr;
+      char* Od = static_cast<char*>(scratch(6, obytes));
+      if (!Ad || (vbytes && !Vd) || !Od) return fail(PFX_CUDA, "staging allocation failed");
+      // the staging buffers are idle on entry (host-mode calls end synchronised)
+      PFX_CUDA_TRY(cudaEventRecord(evs[nch], stream));  // poles uploaded
+      PFX_CUDA_TRY(cudaStreamWaitEvent(cin, evs[nch], 0));
+      auto chunk = [&](int64_t i, int64_t& b0, int64_t& nb) {
+        b0 = i == 0 ? 0 : first + (i - 1) * per;
+        nb = i == 0 ? first : std::min(per, batch - b0);
+      };
+      for (int64_t i = 0; i < nch; ++i) {
+        int64_t b0, nb;
+        chunk(i, b0, nb);
+        PFX_CUDA_TRY(cudaMemcpyAsync(Ad + b0 * am, reinterpret_cast<const char*>(A) + b0 * am, nb * am,
+                                     cudaMemcpyHostToDevice, cin));
+        if (vbytes)
+          PFX_CUDA_TRY(cudaMemcpyAsync(Vd + b0 * vm, reinterpret_cast<const char*>(V) + b0 * vm, nb * vm,
+                                       cudaMemcpyHostToDevice, cin));
+        PFX_CUDA_TRY(cudaEventRecord(evs[i], cin));
+      }
+      static const bool force_piv = getenv("PFX_DENSE_PIVOT") != nullptr;
+      int pivot = force_piv ? 1 : 0;
+      for (int k = 0; k < npairs && !pivot; ++k)
+        if (!(theta2[2 * k + 1] > 0.0)) pivot = 1;
+      float tot = 0.0f;
+      for (int64_t i = 0; i < nch; ++i) {
+        int64_t b0, nb;
+        chunk(i, b0, nb);
+        PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evs[i], 0));
+        float ms = 0.0f;
+        // returns synchronised (status word); the next chunk's copy is already in flight
+        rc = dense_batched_run(reinterpret_cast<const double*>(Ad + b0 * am), a_complex, (int)d, (int)nb,
+                               vbytes ? reinterpret_cast<const double*>(Vd + b0 * vm) : nullptr, v_complex, ncols, full,
+                               real_path, 0, shift_c, th, co, npairs, reinterpret_cast<double*>(Od + b0 * om), stream,
+                               per_pair_ms ? &ms : nullptr, pivot);
+        if (rc) return rc;
+        tot += ms;
+        PFX_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(out) + b0 * om, Od + b0 * om, nb * om,
+                                     cudaMemcpyDeviceToHost, stream));
+      }
+      if (per_pair_ms)
+        for (int k = 0; k < npairs; ++k) per_pair_ms[k] = tot;
+      return sync_stream(stream);
+    }
+  }
   const double *Ad = nullptr, *Vd = nullptr;
   if ((rc = stage_in(mem, 3, A, abytes, stream, &Ad))) return rc;
   if ((rc = stage_in(mem, 4, V, vbytes, stream, &Vd))) return rc;
