@@ -139,7 +139,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
           ipiv[p + jj] = p + jj;
           if (pv.re == 0.0 && pv.im == 0.0) *sing = 1;
         }
-        const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp(pv);
+        const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp_fast(pv);
         for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
           double2* row = &P[r * PS];
           const cplx l = cmul(ld(&row[jj]), rp);
@@ -544,7 +544,7 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
         ipiv[p + jj] = p + jj;
         if (pv.re == 0.0 && pv.im == 0.0) *sing = 1;
       }
-      const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp(pv);
+      const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp_fast(pv);
       for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
         double2* row = &P[r * PS];
         const cplx l = cmul(ld(&row[jj]), rp);
