@@ -269,13 +269,15 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
       __syncwarp(hmask);
       // ---- phase B (lane = rhs).  Per row: independent per-pair terms, then a fixed
       // pairwise tree over pairs (deterministic); rows unrolled for ILP.
-#if defined(PFX_TRI_EXP) && PFX_TRI_EXP == 1
-      if (bb < 0)  // timing ablation: no RHS sweep
-#endif
       double* const obase = a.out + r0 * a.nrhs + rg;
+#if defined(PFX_TRI_EXP) && PFX_TRI_EXP == 1
+      const int cnt_b = bb < 0 ? cnt : 0;  // timing ablation: no RHS sweep
+#else
+      const int cnt_b = cnt;
+#endif
 #pragma unroll
       for (int jj = 0; jj < LS_B; ++jj) {
-        if (jj < cnt) {
+        if (jj < cnt_b) {
           const int j = dir == 0 ? jj : cnt - 1 - jj;
           // sum over pairs: two interleaved FMA chains (even / odd pairs), fixed order
           double acc0 = 0.0, acc1 = 0.0;
