@@ -860,6 +860,16 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
   int L = 0, P = 0;
   int64_t c0 = 0, c1 = 0;
   if (int rc = tri_partition(N, nrhs, rank, nranks, &L, &P, &c0, &c1)) return rc;
+  if (V_host && npairs <= 16) {
+    // host-memory pipeline: each row group is swept as its rows land, a partial wave whose
+    // duration is one unit's latency (proportional to the chunk length); the compute hides
+    // behind the copies, so short chunks (more, faster units per group) shorten the tail
+    static const int hl = getenv("PFX_TRI_HOST_L") ? atoi(getenv("PFX_TRI_HOST_L")) : 96;
+    L = std::max(32, std::min(TR_L, hl / 32 * 32));
+    P = (int)ceil_div(N, L);
+    c0 = 0;
+    c1 = P;
+  }
   const size_t nP = (size_t)P * npairs;
   const size_t nPR = nP * nrhs;
   const size_t nN = (size_t)N * npairs;

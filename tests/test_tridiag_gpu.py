@@ -98,7 +98,8 @@ def test_host_pipeline_matches_device(N, nrhs, scale):
     carries truncated at the next group, verified by tri_trunc_check, global fallback
     otherwise).  Small groups or weak decay (scale 0.05: |l'| close to 1 over many rows) take
     the fallback; C2-like sizes take the truncated carries.  Both must agree with the
-    device-memory call, which scans the carries globally, to rounding."""
+    device-memory call, which scans the carries globally (and uses longer chunks), to
+    rounding."""
     import torch
 
     from paper_2306_16778_b200 import _native
@@ -111,4 +112,4 @@ def test_host_pipeline_matches_device(N, nrhs, scale):
     dev = torch.device("cuda:0")
     devr = _native.expm_tridiag_device(*(torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (d, o, V)), t2,
                                        c2, 0.0).cpu().numpy()
-    assert rel(host, devr) <= 1e-13, rel(host, devr)
+    assert rel(host, devr) <= 1e-12, rel(host, devr)
