@@ -327,12 +327,15 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
 // union is visited (all blocks in a non-contractive chunk).
 // Layout: a half-warp = one (chunk, 16-RHS tile), lane = right-hand side; the z rows of a
 // block are staged by cp.async (double buffered) and read back as broadcasts.
+#ifndef PFX_FIXZ_MINB
+#define PFX_FIXZ_MINB 4  // resident CTAs per SM the fix kernel's registers are sized for
+#endif
 struct FzBuf {
-  double2 z[2][LS_B][16];  // [direction][row][pair]
+  double2 z[LS_B][16];  // [row][pair] of one direction
 };
 
 template <int KM>
-__global__ void __launch_bounds__(LS_WARPS * 32, 3) tri_fixz(TriArgs a, LsArgs ck) {
+__global__ void __launch_bounds__(LS_WARPS * 32, PFX_FIXZ_MINB) tri_fixz(TriArgs a, LsArgs ck) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, k = lane & 15;
@@ -349,110 +352,80 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 3) tri_fixz(TriArgs a, LsArgs c
   const int64_t s = c * a.L;
   const int rows = (int)(a.L < a.N - s ? a.L : a.N - s);
   const int nblk = (rows + LS_B - 1) / LS_B;
-  cplx gf[KM], gb[KM];
-#pragma unroll
-  for (int q = 0; q < KM; ++q) {
-    const bool on = q < np && rv;
-    gf[q] = on ? ld(&a.G[(c * np + q) * a.nrhs + rg]) : mk(0, 0);
-    gb[q] = on ? ld(&a.Gb[(c * np + q) * a.nrhs + rg]) : mk(0, 0);
-  }
   // padded pair slots read as zeros
 #pragma unroll
   for (int t = 0; t < 2; ++t)
-    for (int e = k; e < 2 * LS_B * 16; e += 16)
-      if ((e & 15) >= np) (&Z[t].z[0][0][0])[e] = make_double2(0, 0);
-  int endF = nblk, begB = 0;
-  if (a.contr[c] != 0) {
-    const double tau = rv ? ldexp(__longlong_as_double((long long)a.vmax[rg]), -TR_FIX_EXP) : 0.0;
-    const double* lf = ck.lamf + (c * LS_NBLK) * 16;
-    const double* lb = ck.lamb + (c * LS_NBLK) * 16;
-    int ef = nblk, eb = nblk;  // blocks this lane needs, per direction
-    for (int bb = 0; bb < nblk; ++bb) {
-      double y = 0.0;
+    for (int e = k; e < LS_B * 16; e += 16)
+      if ((e & 15) >= np) (&Z[t].z[0][0])[e] = make_double2(0, 0);
+  const bool contr = a.contr[c] != 0;
+  const double tau = rv ? ldexp(__longlong_as_double((long long)a.vmax[rg]), -TR_FIX_EXP) : 0.0;
+  // the two directions one after the other (only one set of carries live at a time): the
+  // forward terms over blocks [0, endF), then the backward terms over [begB, nblk)
+  for (int dir = 0; dir < 2; ++dir) {
+    cplx g[KM];
+    const double2* Gs = dir == 0 ? a.G : a.Gb;
 #pragma unroll
-      for (int q = 0; q < KM; ++q) y = fma(lf[bb * 16 + q], cabs1(gf[q]), y);
-      if (y <= tau) {
-        ef = bb + 1;
-        break;
-      }
-    }
-    for (int bb = 0; bb < nblk; ++bb) {
-      double y = 0.0;
+    for (int q = 0; q < KM; ++q) g[q] = (q < np && rv) ? ld(&Gs[(c * np + q) * a.nrhs + rg]) : mk(0, 0);
+    int need = nblk;  // blocks from this direction's edge that can carry a correction
+    if (contr) {
+      const double* lb = (dir == 0 ? ck.lamf : ck.lamb) + (c * LS_NBLK) * 16;
+      int e = nblk;
+      for (int bb = 0; bb < nblk; ++bb) {
+        double y = 0.0;
 #pragma unroll
-      for (int q = 0; q < KM; ++q) y = fma(lb[(nblk - 1 - bb) * 16 + q], cabs1(gb[q]), y);
-      if (y <= tau) {
-        eb = bb + 1;
-        break;
+        for (int q = 0; q < KM; ++q) y = fma(lb[(dir == 0 ? bb : nblk - 1 - bb) * 16 + q], cabs1(g[q]), y);
+        if (y <= tau) {
+          e = bb + 1;
+          break;
+        }
       }
+      for (int off = 8; off > 0; off >>= 1) e = max(e, __shfl_xor_sync(hmask, e, off));
+      need = e;
     }
-    for (int off = 8; off > 0; off >>= 1) {
-      ef = max(ef, __shfl_xor_sync(hmask, ef, off));
-      eb = max(eb, __shfl_xor_sync(hmask, eb, off));
-    }
-    endF = ef;
-    begB = nblk - eb;
-  }
-  const bool gap = begB > endF;
-  auto next_blk = [&](int b) { return (gap && b + 1 == endF) ? begB : b + 1; };
-  auto stage = [&](FzBuf& D, int b) {
-    const int64_t r0 = s + (int64_t)b * LS_B;
-    const int n = min(LS_B, rows - b * LS_B) * np;
-    if (b < endF)
+    const int b0 = dir == 0 ? 0 : nblk - need, b1 = dir == 0 ? need : nblk;
+    const double2* zs = dir == 0 ? ck.zf : ck.zb;
+    auto stage = [&](FzBuf& D, int b) {
+      const int64_t r0 = s + (int64_t)b * LS_B;
+      const int n = min(LS_B, rows - b * LS_B) * np;
       for (int e = k; e < n; e += 16) {
         const int j = e / np;
-        cp_async16(&D.z[0][j][e - j * np], &ck.zf[r0 * np + e]);
+        cp_async16(&D.z[j][e - j * np], &zs[r0 * np + e]);
       }
-    if (b >= begB)
-      for (int e = k; e < n; e += 16) {
-        const int j = e / np;
-        cp_async16(&D.z[1][j][e - j * np], &ck.zb[r0 * np + e]);
-      }
-  };
-  __syncwarp(hmask);
-  int b = 0, cur = 0;
-  stage(Z[0], 0);
-  cp_async_commit();
-  while (b < nblk) {
-    const int bn = next_blk(b);
-    if (bn < nblk) stage(Z[cur ^ 1], bn);
+    };
+    __syncwarp(hmask);
+    int cur = 0;
+    if (b0 < b1) stage(Z[0], b0);
     cp_async_commit();
-    const int64_t r0 = s + (int64_t)b * LS_B;
-    const int cnt = min(LS_B, rows - b * LS_B);
-    double ov[LS_B];
-    double* const obase = a.out + r0 * a.nrhs + rg;
+    for (int b = b0; b < b1; ++b) {
+      if (b + 1 < b1) stage(Z[cur ^ 1], b + 1);
+      cp_async_commit();
+      const int64_t r0 = s + (int64_t)b * LS_B;
+      const int cnt = min(LS_B, rows - b * LS_B);
+      double ov[LS_B];
+      double* const obase = a.out + r0 * a.nrhs + rg;
 #pragma unroll
-    for (int j = 0; j < LS_B; ++j) ov[j] = (rv && j < cnt) ? obase[j * a.nrhs] : 0.0;
-    cp_async_wait<1>();
-    __syncwarp(hmask);
-    const FzBuf& D = Z[cur];
-    const bool uf = b < endF, ub = b >= begB;
+      for (int j = 0; j < LS_B; ++j) ov[j] = (rv && j < cnt) ? obase[j * a.nrhs] : 0.0;
+      cp_async_wait<1>();
+      __syncwarp(hmask);
+      const FzBuf& D = Z[cur];
 #pragma unroll
-    for (int j = 0; j < LS_B; ++j) {
-      double acc0 = 0.0, acc1 = 0.0;
-      if (uf) {
-#pragma unroll
-        for (int q = 0; q < KM; ++q) {
-          const double2 z = D.z[0][j][q];
-          acc0 = fma(z.x, gf[q].re, acc0);
-          acc1 = fma(-z.y, gf[q].im, acc1);
-        }
-      }
-      if (ub) {
+      for (int j = 0; j < LS_B; ++j) {
+        double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
         for (int q = 0; q < KM; ++q) {
-          const double2 z = D.z[1][j][q];
-          acc0 = fma(z.x, gb[q].re, acc0);
-          acc1 = fma(-z.y, gb[q].im, acc1);
+          const double2 z = D.z[j][q];
+          acc0 = fma(z.x, g[q].re, acc0);
+          acc1 = fma(-z.y, g[q].im, acc1);
         }
+        ov[j] += acc0 + acc1;
       }
-      ov[j] += acc0 + acc1;
+#pragma unroll
+      for (int j = 0; j < LS_B; ++j)
+        if (rv && j < cnt) obase[j * a.nrhs] = ov[j];
+      __syncwarp(hmask);
+      cur ^= 1;
     }
-#pragma unroll
-    for (int j = 0; j < LS_B; ++j)
-      if (rv && j < cnt) obase[j * a.nrhs] = ov[j];
+    cp_async_wait<0>();
     __syncwarp(hmask);
-    b = bn;
-    cur ^= 1;
   }
-  cp_async_wait<0>();
 }
