@@ -165,60 +165,62 @@ __global__ void __launch_bounds__(128) tri_mobius_chunks(TriArgs a) {
   const int64_t rem = e - s0;
   const int rows = (!live || rem <= 0) ? 0 : (rem < SL ? (int)rem : SL);
   const cplx th = ld(&a.theta[k]);
-  M22 F = mident(), B = mident();
+  // Only the forward product is formed.  With the first row's coupling replaced by 1 it is
+  // F' = [A, -C; D, -E] in the chunk's continuants (A: rows 1..n, C: 2..n, D: 1..n-1,
+  // E: 2..n-1), and both transfers follow from it: F = F' diag(1, e_0^2) and
+  // B = [A, -e_n^2 D; C, -e_n^2 E] (e_0, e_n: couplings into the chunk from above / below).
+  // Every entry is a forward continuant, so nothing is lost by not running the backward
+  // recurrence; the scan uses the transfers only up to a common scale.
+  M22 F = mident();
   for (int i0 = 0; i0 < rows; i0 += 8) {
-    double bre[8], e2[9];  // e2[u] = e_{i-1}^2 for row i = s0 + i0 + u; e2[u + 1] = e_i^2
+    double bre[8], e2[8];  // e2[u] = e_{i-1}^2 for row i = s0 + i0 + u (1 for the segment's first row)
 #pragma unroll
     for (int u = 0; u < 8; ++u) bre[u] = (i0 + u < rows) ? a.diag[s0 + i0 + u] - a.c + th.re : 0.0;
 #pragma unroll
-    for (int u = 0; u < 9; ++u) e2[u] = (i0 + u <= rows) ? off2(a.off, a.N, s0 + i0 + u - 1) : 0.0;
+    for (int u = 0; u < 8; ++u) e2[u] = (i0 + u == 0) ? 1.0 : (i0 + u < rows) ? off2(a.off, a.N, s0 + i0 + u - 1) : 0.0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (i0 + u < rows) {
         const cplx b = mk(bre[u], th.im);
-        // forward: [b, -e_{i-1}^2; 1, 0] F
+        // [b, -e_{i-1}^2; 1, 0] F
         const cplx f0 = csub(cmul(b, F.m0), cscale(F.m2, e2[u]));
         const cplx f1 = csub(cmul(b, F.m1), cscale(F.m3, e2[u]));
         F.m2 = F.m0;
         F.m3 = F.m1;
         F.m0 = f0;
         F.m1 = f1;
-        // backward: B [b, -e_i^2; 1, 0]
-        const cplx g0 = cadd(cmul(B.m0, b), B.m1);
-        const cplx g2 = cadd(cmul(B.m2, b), B.m3);
-        B.m1 = cscale(B.m0, -e2[u + 1]);
-        B.m3 = cscale(B.m2, -e2[u + 1]);
-        B.m0 = g0;
-        B.m2 = g2;
       }
     }
     mnorm(F);
-    mnorm(B);
   }
-  // combine segments: forward F = F3 F2 F1 F0, backward B = B0 B1 B2 B3
+  // segments after the first carry their true coupling into the product
+  if (seg > 0 && rows > 0) {
+    const double es = off2(a.off, a.N, s0 - 1);
+    F.m1 = cscale(F.m1, es);
+    F.m3 = cscale(F.m3, es);
+  }
+  // combine segments: F' = F3 F2 F1 F'0
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int w = 1; w < TR_SEG; w <<= 1) {
     const M22 Fp = shfl_m22(F, lane + w < 32 ? lane + w : lane);
-    const M22 Bp = shfl_m22(B, lane + w < 32 ? lane + w : lane);
     if ((seg & (2 * w - 1)) == 0) {
       F = mmul(Fp, F);
-      B = mmul(B, Bp);
       mnorm(F);
-      mnorm(B);
     }
   }
   if (live && seg == 0) {
+    const double e0 = off2(a.off, a.N, s - 1), en = off2(a.off, a.N, e - 1);
     double2* df = a.Tf + ck * 4;
     double2* db = a.Tb + ck * 4;
     st(&df[0], F.m0);
-    st(&df[1], F.m1);
+    st(&df[1], cscale(F.m1, e0));
     st(&df[2], F.m2);
-    st(&df[3], F.m3);
-    st(&db[0], B.m0);
-    st(&db[1], B.m1);
-    st(&db[2], B.m2);
-    st(&db[3], B.m3);
+    st(&df[3], cscale(F.m3, e0));
+    st(&db[0], F.m0);
+    st(&db[1], cscale(F.m2, -en));
+    st(&db[2], cscale(F.m1, -1.0));
+    st(&db[3], cscale(F.m3, en));
   }
 }
 
