@@ -31,8 +31,10 @@ struct LsBuf {
 };
 
 struct LsSmem {
-  double2 fw[LS_B][16][2];  // per (row, pair): (l or l', w); first holds the recomputed
-                            // opposite-direction multiplier until the lane overwrites it
+  double2 fw[LS_B][2][16];  // per row: [0][pair] l or l', [1][pair] w (pair-fastest: a
+                            // phase-A store of 16 lanes is one conflict-free 256-byte row);
+                            // [0] holds the recomputed opposite-direction multiplier until
+                            // the lane overwrites it
   LsBuf buf[2];             // cp.async double buffer of the staged rows
   double lamabs[16];        // |Lambda_k| after the block (fix pass stop test)
 };
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
   double vmx = 0.0;
   if (!act) {  // padded pair slots (k >= np) stay zero: phase B adds exact zeros for them
 #pragma unroll
-    for (int j = 0; j < LS_B; ++j) S.fw[j][k][0] = S.fw[j][k][1] = make_double2(0, 0);
+    for (int j = 0; j < LS_B; ++j) S.fw[j][0][k] = S.fw[j][1][k] = make_double2(0, 0);
   }
   auto blk_r0 = [&](int b) { return s + (int64_t)b * LS_B; };
   auto blk_cnt = [&](int b) { return min(LS_B, rows - b * LS_B); };
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
             const int j = LS_B - 1 - jj;
             if (j < cnt) {
               cplx lv = ls_bstep(B, csh, j, r0 + j, th, q1, q2);
-              S.fw[j][k][0] = make_double2(lv.re, lv.im);
+              S.fw[j][0][k] = make_double2(lv.re, lv.im);
               if (fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
             }
           }
@@ -228,14 +230,14 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
           for (int j = 0; j < LS_B; ++j) {
             if (j < cnt) {
               const cplx lv = ls_fstep(B, csh, j, r0 + j, th, x1, x2);
-              const cplx lbv = ld(&S.fw[j][k][0]);
+              const cplx lbv = ld(&S.fw[j][0][k]);
               const cplx bd = mk(B.dg[j] - csh + th.re, th.im);
               const cplx gam = csub(csub(bd, cscale(lv, B.of[j])), cscale(lbv, B.of[j + 1]));
               const cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
               lam = cmul(lam, mk(-lv.re, -lv.im));
               if (fma(lv.re, lv.re, lv.im * lv.im) > 1.0) noncontr = true;
-              S.fw[j][k][0] = make_double2(lv.re, lv.im);
-              S.fw[j][k][1] = make_double2(w.re, w.im);
+              S.fw[j][0][k] = make_double2(lv.re, lv.im);
+              S.fw[j][1][k] = make_double2(w.re, w.im);
               if (wz) st(&zo[(r0 + j) * np], cmul(w, lam));
             }
           }
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
           for (int j = 0; j < LS_B; ++j) {
             if (j < cnt) {
               cplx lv = ls_fstep(B, csh, j, r0 + j, th, p1, p2);
-              S.fw[j][k][0] = make_double2(lv.re, lv.im);
+              S.fw[j][0][k] = make_double2(lv.re, lv.im);
             }
           }
 #pragma unroll
@@ -253,13 +255,13 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
             const int j = LS_B - 1 - jj;
             if (j < cnt) {
               const cplx lbv = ls_bstep(B, csh, j, r0 + j, th, x1, x2);
-              const cplx lv = ld(&S.fw[j][k][0]);
+              const cplx lv = ld(&S.fw[j][0][k]);
               const cplx bd = mk(B.dg[j] - csh + th.re, th.im);
               const cplx gam = csub(csub(bd, cscale(lv, B.of[j])), cscale(lbv, B.of[j + 1]));
               const cplx w = cmul(co2, crcp_nc(gam));  // |gamma| >= Im(theta)
               lam = cmul(lam, mk(-lbv.re, -lbv.im));
-              S.fw[j][k][0] = make_double2(lbv.re, lbv.im);
-              S.fw[j][k][1] = make_double2(w.re, w.im);
+              S.fw[j][0][k] = make_double2(lbv.re, lbv.im);
+              S.fw[j][1][k] = make_double2(w.re, w.im);
               if (wz) st(&zo[(r0 + j) * np], cmul(w, lam));
             }
           }
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(LS_WARPS * 32, 4) tri_ls(TriArgs a, LsArgs ck)
           if (dir == 0) vmx = fmax(vmx, fabs(f));
 #pragma unroll
           for (int q = 0; q < KM; ++q) {
-            const double2 l2 = S.fw[j][q][0], w2 = S.fw[j][q][1];
+            const double2 l2 = S.fw[j][0][q], w2 = S.fw[j][1][q];
             g[q] = cplx{fma(-l2.x, g[q].re, fma(l2.y, g[q].im, f)), fma(-l2.x, g[q].im, -l2.y * g[q].re)};
             const double gre = dir == 0 ? g[q].re - f : g[q].re;
             double& acc = (q & 1) ? acc1 : acc0;
