@@ -464,16 +464,21 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
 //      [Ia 0; -Ib Lba Ia  Ib].
 //   4. 32-column strips right of the step: U12 = T A12 (one product, K = 32), then
 //      A22 -= [L21a L21b] U12 on DMMA (3M product, K = 32, A fragments from the slot).
-// T: 32 x 33 complex (stride TS).  Same results as lu_blocked<16, false> up to rounding order.
-constexpr int TS = 33;
+// T: 32 x TST complex, S: 32 x TSS complex.  Same results as lu_blocked<16, false> up to rounding order.
+// Strides chosen for conflict-free DMMA fragment loads: a quarter-warp reads rows t (0..3) and
+// columns g (0..1) of an A operand (row stride = 4 mod 8 in 16-byte words) or rows t, columns g
+// of a B operand stored k-major (row stride = 2 mod 8); with 33 both patterns were 2-way
+// conflicted.
+constexpr int TST = 36;  // T (A operand of the strip products)
+constexpr int TSS = 34;  // S (B operand of the strip and trailing products)
 #ifndef PFX_DP_CH
 #define PFX_DP_CH 1  // column tiles per chunk of the two-panel update in the two-CTA variant
 #endif
 constexpr int DP_SW = 32;  // strip width of the two-panel update
 
 // this warp's 8 x 8 complex tile (rt, ct) of C = A (rows x K, stride lda) * S (K x sw rows
-// brow0.., stride TS); rows >= arows and k >= K read as zero
-__device__ __forceinline__ void dp_tile(const double2* A, size_t lda, int arows, int K, const double2* Sb, int sw,
+// brow0.., stride ldb); rows >= arows and k >= K read as zero
+__device__ __forceinline__ void dp_tile(const double2* A, size_t lda, int arows, int K, const double2* Sb, int ldb, int sw,
                                         int rt, int ct, int kbeg, double (&cr)[2], double (&ci)[2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   cr[0] = cr[1] = ci[0] = ci[1] = 0.0;
@@ -483,16 +488,16 @@ __device__ __forceinline__ void dp_tile(const double2* A, size_t lda, int arows,
     double2 x = make_double2(0, 0), y = make_double2(0, 0);
     if (kk < K) {
       if (r < arows) x = A[(size_t)r * lda + kk];
-      if (col < sw) y = Sb[kk * TS + col];
+      if (col < sw) y = Sb[kk * ldb + col];
     }
     zmma884(cr, ci, x.x, x.y, y.x, y.y);
   }
 }
 
-// unit lower inverse of the jb x jb block at T + off*(TS+1) (in place), warp per column
+// unit lower inverse of the jb x jb block at T + off*(TST+1) (in place), warp per column
 __device__ __forceinline__ void dp_inv16(double2* T, int off, int jb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* B = T + off * (TS + 1);
+  double2* B = T + off * (TST + 1);
   cplx inv[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
@@ -502,7 +507,7 @@ __device__ __forceinline__ void dp_inv16(double2* T, int off, int jb) {
       cplx xk;
       xk.re = __shfl_sync(0xffffffffu, x.re, k);
       xk.im = __shfl_sync(0xffffffffu, x.im, k);
-      if (lane > k && lane < jb) x = cfms(x, ld(&B[lane * TS + k]), xk);
+      if (lane > k && lane < jb) x = cfms(x, ld(&B[lane * TST + k]), xk);
     }
     inv[u] = x;
   }
@@ -510,7 +515,7 @@ __device__ __forceinline__ void dp_inv16(double2* T, int off, int jb) {
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int c = warp + u * DB_WARPS;
-    if (lane < jb && c < jb) st(&B[lane * TS + c], lane >= c ? inv[u] : mk(0.0, 0.0));
+    if (lane < jb && c < jb) st(&B[lane * TST + c], lane >= c ? inv[u] : mk(0.0, 0.0));
   }
   __syncthreads();
 }
@@ -576,14 +581,14 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
     const int tr = keep_below ? min(2 * NB, m) : jb;
     for (int e = tid; e < tr * NB; e += DB_THREADS) {
       const int r = e / NB, c = e - r * NB;
-      T[(toff + r) * TS + toff + c] = c < jb ? P[r * PS + c] : make_double2(0, 0);
+      T[(toff + r) * TST + toff + c] = c < jb ? P[r * PS + c] : make_double2(0, 0);
     }
     __syncthreads();
     dp_inv16(T, toff, jb);
     // carried right-hand sides: head = L11^{-1} head, tail -= L21 head
     if (na > 0) {
       double2* xs = S;
-      const double2* I = T + toff * (TS + 1);
+      const double2* I = T + toff * (TST + 1);
       for (int c = warp; c < na; c += DB_WARPS) {
         const cplx h = lane < jb ? ld(&Xa[(size_t)(p + lane) * na + c]) : mk(0.0, 0.0);
         cplx x = mk(0.0, 0.0);
@@ -591,7 +596,7 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
           cplx hk;
           hk.re = __shfl_sync(0xffffffffu, h.re, k);
           hk.im = __shfl_sync(0xffffffffu, h.im, k);
-          if (lane >= k && lane < jb) x = cfma(ld(&I[lane * TS + k]), hk, x);
+          if (lane >= k && lane < jb) x = cfma(ld(&I[lane * TST + k]), hk, x);
         }
         if (lane < jb) {
           st(&Xa[(size_t)(p + lane) * na + c], x);
@@ -611,7 +616,7 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
   };
 
   // trailing update of rows [r0, d) x cols [q, q + sw): C -= L (slot columns [p, p + K)) * S
-  // (K x sw at S, stride TS), 3M product on DMMA; CH column tiles per chunk
+  // (K x sw at S, stride TSS), 3M product on DMMA; CH column tiles per chunk
   auto trailing = [&](int p, int K, int r0, int q, int sw) {
     const int rtiles = (d - r0 + 7) >> 3;
     const int ctiles = (sw + 7) >> 3;
@@ -649,7 +654,7 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
             for (int u = 0; u < CH; ++u) {
               const int col = (cb + u) * 8 + g;
               double2 y = make_double2(0, 0);
-              if (kk < K && col < sw) y = S[kk * TS + col];
+              if (kk < K && col < sw) y = S[kk * TSS + col];
               dmma884(t1[u][0], t1[u][1], ar[s4], y.x);
               dmma884(t2[u][0], t2[u][1], ai[s4], y.y);
               dmma884(t3[u][0], t3[u][1], as, y.x + y.y);
@@ -678,7 +683,7 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
   auto strip = [&](int p, int K, int q, int sw) {
     for (int e = tid; e < K * sw; e += DB_THREADS) {
       const int r = e / sw, c = e - r * sw;
-      S[r * TS + c] = W[(size_t)(p + r) * ldw + q + c];
+      S[r * TSS + c] = W[(size_t)(p + r) * ldw + q + c];
     }
     __syncthreads();
     // K x sw output: (K/8) x (sw/8) tiles, at most 16 over 8 warps; T is lower triangular,
@@ -690,7 +695,7 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
       const int tl = warp + u * DB_WARPS;
       if (tl < mtl * ntl) {
         const int rt = tl % mtl, ct = tl / mtl;
-        dp_tile(T, TS, K, min(K, 8 * (rt + 1)), S, sw, rt, ct, 0, cr[u], ci[u]);
+        dp_tile(T, TST, K, min(K, 8 * (rt + 1)), S, TSS, sw, rt, ct, 0, cr[u], ci[u]);
       }
     }
     __syncthreads();
@@ -703,14 +708,14 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = ct * 8 + 2 * t + h;
-          if (r < K && c < sw) S[r * TS + c] = make_double2(cr[u][h], ci[u][h]);
+          if (r < K && c < sw) S[r * TSS + c] = make_double2(cr[u][h], ci[u][h]);
         }
       }
     }
     __syncthreads();
     for (int e = tid; e < K * sw; e += DB_THREADS) {
       const int r = e / sw, c = e - r * sw;
-      W[(size_t)(p + r) * ldw + q + c] = S[r * TS + c];
+      W[(size_t)(p + r) * ldw + q + c] = S[r * TSS + c];
     }
     if (dbg && tid == 0) {
       atomicAdd(&dbg[4], (unsigned long long)(clock64() - tph));
@@ -727,7 +732,7 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
   for (int p = 0; p < d; p += 2 * NB) {
     const int ja = min(NB, d - p);
     const int jb = min(NB, d - p - ja);  // 0: panel a is the last
-    for (int e = tid; e < 2 * NB * TS; e += DB_THREADS) T[e] = make_double2(0, 0);
+    for (int e = tid; e < 2 * NB * TST; e += DB_THREADS) T[e] = make_double2(0, 0);
     __syncthreads();
     panel(p, ja, 0, jb > 0);
     if (jb == 0) {
@@ -739,24 +744,24 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
     panel(p + ja, jb, NB, false);
     // T's bottom-left block: -Ib Lba Ia (two 16 x 16 x 16 products, four warps)
     {
-      double2* L = T + NB * TS;  // Lba
+      double2* L = T + NB * TST;  // Lba
       double cr[2], ci[2];
       const int rt = warp & 1, ct = (warp >> 1) & 1;
-      if (warp < 4) dp_tile(L, TS, jb, ja, T, ja, rt, ct, 0, cr, ci);  // Lba Ia (Ia at T, stride TS)
+      if (warp < 4) dp_tile(L, TST, jb, ja, T, TST, ja, rt, ct, 0, cr, ci);  // Lba Ia (Ia at T)
       __syncthreads();
       if (warp < 4) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) L[(rt * 8 + g) * TS + ct * 8 + 2 * t + h] = make_double2(cr[h], ci[h]);
+        for (int h = 0; h < 2; ++h) L[(rt * 8 + g) * TST + ct * 8 + 2 * t + h] = make_double2(cr[h], ci[h]);
       }
       __syncthreads();
-      // -Ib (Lba Ia): B operand = rows of L (stride TS) -> through dp_tile with Sb = L
-      if (warp < 4) dp_tile(T + NB * (TS + 1), TS, jb, jb, L, ja, rt, ct, 0, cr, ci);
+      // -Ib (Lba Ia): B operand = rows of L -> through dp_tile with Sb = L
+      if (warp < 4) dp_tile(T + NB * (TST + 1), TST, jb, jb, L, TST, ja, rt, ct, 0, cr, ci);
       __syncthreads();
       if (warp < 4) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = rt * 8 + g, c = ct * 8 + 2 * t + h;
-          L[r * TS + c] = (r < jb && c < ja) ? make_double2(-cr[h], -ci[h]) : make_double2(0, 0);
+          L[r * TST + c] = (r < jb && c < ja) ? make_double2(-cr[h], -ci[h]) : make_double2(0, 0);
         }
       }
       __syncthreads();
@@ -884,9 +889,9 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
   double2* P = reinterpret_cast<double2*>(smem_raw);                // d x (NB+1)
   double2* S = P + (size_t)d * (NB + 1);                            // NB x (SW+1), aliased by diag
   double2* diag = S;                                                // 32 x 33 (solves only)
-  const size_t sreg = (size_t)NB * (DB_SW + 1) > 32 * 33 ? (size_t)NB * (DB_SW + 1) : 32 * 33;
-  double2* T = S + sreg;                                            // 32 x 33 (two-panel LU)
-  double2* part = T + 32 * TS;                                      // 32
+  const size_t sreg = (size_t)NB * (DB_SW + 1) > 32 * TSS ? (size_t)NB * (DB_SW + 1) : 32 * TSS;
+  double2* T = S + sreg;                                            // 32 x TST (two-panel LU)
+  double2* part = T + 32 * TST;                                     // 32
   double* red_v = reinterpret_cast<double*>(part + 32);             // 32
   int* red_i = reinterpret_cast<int*>(red_v + 32);                  // 32
   int* s_piv = red_i + 32;                                          // NB
@@ -1072,9 +1077,9 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ stage, double* __
 }
 
 static size_t dense_smem_bytes(int d, int nb) {
-  size_t sreg = (size_t)nb * (DB_SW + 1) > 32 * 33 ? (size_t)nb * (DB_SW + 1) : 32 * 33;
+  size_t sreg = (size_t)nb * (DB_SW + 1) > 32 * TSS ? (size_t)nb * (DB_SW + 1) : 32 * TSS;
   // panel (z, zc, 1/U_ii alias it in the solves) + strip + T (32 x 33) + part
-  size_t c2 = (size_t)d * (nb + 1) + sreg + 32 * 33 + 32;
+  size_t c2 = (size_t)d * (nb + 1) + sreg + 32 * TST + 32;
   return c2 * sizeof(double2) + 32 * sizeof(double) + (32 + nb + 4) * sizeof(int) + ((d + 3) & ~3) * sizeof(int) + 64;
 }
 
