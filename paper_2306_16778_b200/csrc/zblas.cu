@@ -6,19 +6,22 @@
 // 16 complex at a time through shared memory with cp.async double buffering.  A complex
 // 8x8x4 step is three real DMMA.8x8x4 (3M: T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi);
 // Cr = T1 - T2, Ci = T3 - T1 - T2), or four with PFX_ZGEMM_4M=1.  Shared-memory rows are
-// padded by one complex element so both fragment loads spread over all 32 banks (4
-// wavefronts per 512-byte warp request, the minimum).
+// padded (GAS, TN + 2) so both fragment loads spread over all 32 banks (4 wavefronts per
+// 512-byte warp request, the minimum).
 #include "zblas.cuh"
 
 namespace pfx {
 
 constexpr int GK = 16;
-constexpr int GAS = GK + 1;
+// Row strides (in 16-byte words) for conflict-free DMMA fragment loads: a quarter-warp reads
+// A at rows g (0..1) x columns t (0..3) -> stride 4 mod 8; B at rows t x columns g -> stride
+// 2 mod 8 (GK + 1 and TN + 1 were 2-way conflicted: ncu counted half the wavefronts as excess)
+constexpr int GAS = GK + 4;
 
 template <int TM, int TN>
 struct GemmSmem {
   double2 A[2][TM][GAS];
-  double2 B[2][GK][TN + 1];
+  double2 B[2][GK][TN + 2];
 };
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
