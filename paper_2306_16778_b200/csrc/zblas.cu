@@ -680,23 +680,27 @@ int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui) {
 // shared memory by cp.async, the product runs on DMMA m8n8k4 with the k range cut to T's
 // nonzero triangle, and the strip is written back over itself.
 constexpr int TM_T = 64;
-constexpr int TM_S = TM_T + 1;
 constexpr int TM_W = 32;
 
 template <bool RIGHT>
 __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* Ts = reinterpret_cast<double2*>(smem_raw);  // 64 x TM_S
-  double2* Bs = Ts + TM_T * TM_S;                      // left: [k 64][col TM_W+1]; right: [row TM_W][k TM_S]
-  constexpr int BSL = TM_W + 1;
+  // row strides (16-byte words) for conflict-free DMMA fragment loads: an A-operand array
+  // (read at rows g x columns tt of a quarter-warp) 4 mod 8, a B-operand array (rows tt x
+  // columns g) 2 mod 8.  T is the A operand on the left and the B operand on the right.
+  constexpr int TSS_ = RIGHT ? TM_T + 2 : TM_T + 4;  // Ts
+  constexpr int BSL = TM_W + 2;                      // Bs, left: [k][col] (B operand)
+  constexpr int BSR = TM_T + 4;                      // Bs, right: [row][k] (A operand)
+  double2* Ts = reinterpret_cast<double2*>(smem_raw);  // 64 x TSS_
+  double2* Bs = Ts + TM_T * (TM_T + 4);                // left: [k 64][col BSL]; right: [row TM_W][k BSR]
   const int b = blockIdx.y;
   const int t0 = blockIdx.x * TM_W;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tt = lane & 3;
   for (int e = tid; e < TM_T * TM_T; e += 256) {
     const int r = e >> 6, c = e & 63;
-    if (r < nb && c < nb) cp_async16(&Ts[r * TM_S + c], T.at(b, r, c));
-    else Ts[r * TM_S + c] = make_double2(0, 0);
+    if (r < nb && c < nb) cp_async16(&Ts[r * TSS_ + c], T.at(b, r, c));
+    else Ts[r * TSS_ + c] = make_double2(0, 0);
   }
   for (int e = tid; e < TM_T * TM_W; e += 256) {
     if (!RIGHT) {  // Bs[k][col] = B[k][t0 + col]
@@ -705,8 +709,8 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
       else Bs[r * BSL + c] = make_double2(0, 0);
     } else {  // Bs[row][k] = B[t0 + row][k]
       const int r = e >> 6, c = e & 63;
-      if (t0 + r < n && c < nb) cp_async16(&Bs[r * TM_S + c], B.at(b, t0 + r, c));
-      else Bs[r * TM_S + c] = make_double2(0, 0);
+      if (t0 + r < n && c < nb) cp_async16(&Bs[r * BSR + c], B.at(b, t0 + r, c));
+      else Bs[r * BSR + c] = make_double2(0, 0);
     }
   }
   cp_async_commit();
@@ -730,12 +734,12 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
   for (int j = 0; j < 4; ++j) t1[j][0] = t1[j][1] = t2[j][0] = t2[j][1] = t3[j][0] = t3[j][1] = 0.0;
   for (int k0 = klo; k0 < khi; k0 += 4) {
     double2 x;
-    if (!RIGHT) x = Ts[(wm * 8 + g) * TM_S + k0 + tt];
-    else x = Bs[(wm * 8 + g) * TM_S + k0 + tt];
+    if (!RIGHT) x = Ts[(wm * 8 + g) * TSS_ + k0 + tt];
+    else x = Bs[(wm * 8 + g) * BSR + k0 + tt];
     const double xs = x.x + x.y;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const double2 y = RIGHT ? Ts[(k0 + tt) * TM_S + wn * 32 + j * 8 + g] : Bs[(k0 + tt) * (TM_W + 1) + j * 8 + g];
+      const double2 y = RIGHT ? Ts[(k0 + tt) * TSS_ + wn * 32 + j * 8 + g] : Bs[(k0 + tt) * BSL + j * 8 + g];
       dmma884(t1[j][0], t1[j][1], x.x, y.x);
       dmma884(t2[j][0], t2[j][1], x.y, y.y);
       dmma884(t3[j][0], t3[j][1], xs, y.x + y.y);
@@ -768,7 +772,7 @@ int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, b
   if (n <= 0) return PFX_OK;
   if (nb > TM_T) return fail(PFX_BADARG, "ztrmm_inplace: nb > 64");
   static bool attr = false;
-  const int smem = (TM_T * TM_S + TM_T * TM_S) * (int)sizeof(double2);
+  const int smem = (TM_T * (TM_T + 4) + TM_T * (TM_T + 4)) * (int)sizeof(double2);
   if (!attr) {
     PFX_CUDA_TRY(cudaFuncSetAttribute(ztrmm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     PFX_CUDA_TRY(cudaFuncSetAttribute(ztrmm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
