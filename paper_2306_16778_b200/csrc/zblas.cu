@@ -510,6 +510,94 @@ int ztrsm_lunn(cudaStream_t s, int batch, int nb, int n, ZMat Um, ZMat B) {
 constexpr int DI_MAX = 64;
 constexpr int DI_S = DI_MAX + 1;
 
+// Two columns per barrier: rows j and j+1 are published together (both final with respect to
+// the columns before j), every thread forms the 2 x 2 pivot block's factors itself
+// (l10 = a_{j+1,j} / u_jj, u'_11 = a_{j+1,j+1} - l10 u_{j,j+1}), and the rows below apply the
+// rank-2 update a_rc -= m1 u_jc + l2 a_{j+1,c} with l1 = a_rj / u_jj, l2 = (a_{r,j+1} - l1 u_{j,j+1}) / u'_11,
+// m1 = l1 - l2 l10 (the same factors as two rank-1 steps; rounding differs).  Half the
+// barriers and pivot reciprocals on the critical chain of the diagonal LU.
+template <int NL>
+__device__ __forceinline__ void lu_diag_phase2(int q0, cplx (&a)[16], int nb, ZMat D, int b, int row, int cg,
+                                               int lane, unsigned base, int* sing) {
+  constexpr unsigned ROW = 2 * DI_MAX * 16;  // bytes per published row (64 past the block, zero)
+  constexpr unsigned BUF = 2 * ROW;          // rows j and j+1
+#pragma unroll 1
+  for (int q = q0; q < q0 + 4; ++q) {
+    const unsigned qb = base + (unsigned)(cg + 4 * q) * 16u;  // &row0[cg + 4q]
+#pragma unroll
+    for (int jj = 0; jj < 4; jj += 2) {
+      const int j = 4 * q + jj;
+      const unsigned p0 = qb + ((jj >> 1) & 1) * BUF, p1 = p0 + ROW;  // this lane's column in rows j / j+1
+      const unsigned r0b = base + ((jj >> 1) & 1) * BUF, r1b = r0b + ROW;
+      if (row == j || row == j + 1) {
+        // entries left of j in a[0] are finished multipliers: publish only c >= j
+        const unsigned pb = row == j ? p0 : p1;
+        if (cg >= jj) sts2(pb, a[0]);
+#pragma unroll
+        for (int i = 1; i < NL; ++i) sts2(pb + 64u * i, a[i]);
+      }
+      __syncthreads();
+      const cplx u00 = lds2(r0b + (unsigned)j * 16u), u01 = lds2(r0b + (unsigned)(j + 1) * 16u);
+      const cplx a10 = lds2(r1b + (unsigned)j * 16u), a11 = lds2(r1b + (unsigned)(j + 1) * 16u);
+      const cplx r00 = crcp_fast(u00);
+      const cplx l10 = cmul(a10, r00);
+      const cplx u11 = cfms(a11, l10, u01);
+      if (row == j && cg == jj && u00.re == 0.0 && u00.im == 0.0) *sing = 1;
+      if (row == j + 1 && cg == jj + 1 && u11.re == 0.0 && u11.im == 0.0) *sing = 1;
+      // a_rj, a_{r,j+1} from the row's lanes holding columns j, j+1 (whole warp: no divergence)
+      const int src = (lane & ~3) | jj;
+      cplx aj, aj1;
+      aj.re = __shfl_sync(0xffffffffu, a[0].re, src);
+      aj.im = __shfl_sync(0xffffffffu, a[0].im, src);
+      aj1.re = __shfl_sync(0xffffffffu, a[0].re, src + 1);
+      aj1.im = __shfl_sync(0xffffffffu, a[0].im, src + 1);
+      if (row > j + 1) {
+        const cplx l1 = cmul(aj, r00);
+        const cplx l2 = cmul(cfms(aj1, l1, u01), crcp_fast(u11));
+        const cplx m1 = cfms(l1, l2, l10);
+        const cplx x0 = cfms(cfms(a[0], m1, lds2(p0)), l2, lds2(p1));
+#pragma unroll
+        for (int i = 1; i < NL; ++i) a[i] = cfms(cfms(a[i], m1, lds2(p0 + 64u * i)), l2, lds2(p1 + 64u * i));
+        a[0] = cg == jj ? l1 : (cg == jj + 1 ? l2 : (cg > jj + 1 ? x0 : a[0]));
+      } else if (row == j + 1) {
+        // row j+1: its multiplier l10 in column j, the eliminated U row from column j+1 on
+        const cplx x0 = cfms(a[0], l10, lds2(p0));
+#pragma unroll
+        for (int i = 1; i < NL; ++i) a[i] = cfms(a[i], l10, lds2(p0 + 64u * i));
+        a[0] = cg == jj ? l10 : (cg > jj ? x0 : a[0]);
+      }
+    }
+    const int c = cg + 4 * q;
+    if (row < nb && c < nb) *D.at(b, row, c) = make_double2(a[0].re, a[0].im);
+#pragma unroll
+    for (int i = 0; i < NL - 1; ++i) a[i] = a[i + 1];
+    a[NL - 1] = mk(0, 0);
+  }
+}
+
+__global__ void __launch_bounds__(256) zgetrf_diag2_kernel(int nb, ZMat D, int* sing) {
+  // two double-buffered pairs of pivot rows, each running 64 entries past the block, kept zero
+  __shared__ __align__(16) double2 prow[2][2][2 * DI_MAX];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int row = tid >> 2, cg = tid & 3;
+  (&prow[0][0][0])[tid] = make_double2(0, 0);
+  (&prow[0][0][0])[tid + 256] = make_double2(0, 0);
+  const unsigned base = (unsigned)__cvta_generic_to_shared(&prow[0][0][0]);
+  cplx a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int c = cg + 4 * i;
+    if (row < nb && c < nb) a[i] = ld(D.at(b, row, c));
+    else a[i] = mk(row == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  lu_diag_phase2<16>(0, a, nb, D, b, row, cg, lane, base, sing);
+  lu_diag_phase2<12>(4, a, nb, D, b, row, cg, lane, base, sing);
+  lu_diag_phase2<8>(8, a, nb, D, b, row, cg, lane, base, sing);
+  lu_diag_phase2<4>(12, a, nb, D, b, row, cg, lane, base, sing);
+}
+
 // Register-resident: thread (row = tid / 4, phase = tid % 4) holds A[row][phase + 4(q + i)],
 // i < 16 - q, where q is the current 4-column block: after every 4 columns the finished
 // register a[0] is stored and the window rotates, so every register index stays static
@@ -653,9 +741,11 @@ __global__ void __launch_bounds__(256) ztrtri_diag_kernel(int nb, ZMat D, ZMat L
 }
 
 int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing) {
+  static const bool getrf2 = getenv("PFX_GETRF1") == nullptr;  // PFX_GETRF1=1: one column per barrier
   if (nb > DI_MAX) return fail(PFX_BADARG, "zgetrf_diag: nb > 64");
   PFX_LAUNCH_F("zgetrf_diag", s, 8.0 / 3.0 * nb * nb * (double)nb * batch,
-               zgetrf_diag_kernel<<<batch, 256, 0, s>>>(nb, D, sing));
+               (getrf2 ? zgetrf_diag2_kernel<<<batch, 256, 0, s>>>(nb, D, sing)
+                       : zgetrf_diag_kernel<<<batch, 256, 0, s>>>(nb, D, sing)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
