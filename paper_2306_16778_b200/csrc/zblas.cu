@@ -12,16 +12,15 @@
 
 namespace pfx {
 
-constexpr int GK = 16;
+// K staged KS complex at a time (16 by default; 32 for the small-grid, K <= 64 launches of the
+// band LU's critical chain, where the number of load round trips sets the latency).
 // Row strides (in 16-byte words) for conflict-free DMMA fragment loads: a quarter-warp reads
 // A at rows g (0..1) x columns t (0..3) -> stride 4 mod 8; B at rows t x columns g -> stride
-// 2 mod 8 (GK + 1 and TN + 1 were 2-way conflicted: ncu counted half the wavefronts as excess)
-constexpr int GAS = GK + 4;
-
-template <int TM, int TN>
+// 2 mod 8 (KS + 1 and TN + 1 were 2-way conflicted: ncu counted half the wavefronts as excess)
+template <int TM, int TN, int KS>
 struct GemmSmem {
-  double2 A[2][TM][GAS];
-  double2 B[2][GK][TN + 2];
+  double2 A[2][TM][KS + 4];
+  double2 B[2][KS][TN + 2];
 };
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
@@ -37,14 +36,14 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // T1 = sum Ar Br, T2 = sum Ai Bi, T3 = sum (Ar + Ai)(Br + Bi), then Cr = T1 - T2 and
 // Ci = T3 - T1 - T2 (normwise-stable; the imaginary part's error is bounded by eps |A||B|
 // instead of componentwise).
-template <int TM, int TN, int NW, bool M3 = false>
+template <int TM, int TN, int NW, bool M3 = false, int GK = 16>
 __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                                                         int accumulate) {
   constexpr int NT = NW * 32;
   constexpr int WN = NW / 2;
   constexpr int FM = TM / 2 / 8, FN = TN / WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GemmSmem<TM, TN>& S = *reinterpret_cast<GemmSmem<TM, TN>*>(smem_raw);
+  GemmSmem<TM, TN, GK>& S = *reinterpret_cast<GemmSmem<TM, TN, GK>*>(smem_raw);
   const int b = blockIdx.z;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -162,19 +161,20 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
   }
 }
 
-template <int TM, int TN, int NW, bool M3>
+template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                         bool accumulate) {
   static bool attr = false;
-  const int smem = (int)sizeof(GemmSmem<TM, TN>);
+  const int smem = (int)sizeof(GemmSmem<TM, TN, KS>);
   if (!attr) {
     PFX_CUDA_TRY(
-        cudaFuncSetAttribute(zgemm_kernel<TM, TN, NW, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cudaFuncSetAttribute(zgemm_kernel<TM, TN, NW, M3, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch);
   PFX_LAUNCH_F("zgemm", s, 8.0 * (double)m * n * k * batch,
-               (zgemm_kernel<TM, TN, NW, M3><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0)));
+               (zgemm_kernel<TM, TN, NW, M3, KS><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C,
+                                                                       accumulate ? 1 : 0)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
@@ -189,9 +189,14 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
   }
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
   const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, 64) * (int64_t)batch;
-  if (tiles64 < 2 * sms)
+  static const bool ks32 = getenv("PFX_ZGEMM_KS16") == nullptr;
+  if (tiles64 < 2 * sms) {
+    if (k <= 64 && ks32)  // short K: two 32-deep stages instead of four 16-deep ones
+      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate)
+                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate);
     return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate)
               : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate);
+  }
   return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate)
             : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate);
 }
