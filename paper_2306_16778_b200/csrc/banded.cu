@@ -31,14 +31,14 @@ constexpr int BD_NB = 64;
 // grid (row groups, pairs): each warp writes whole rows of the padded row band (no index
 // division: the band is ~40 GB for C5, so this is a pure HBM write stream)
 __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const double* V, int nrhs, double shift_c,
-                         const double2* theta, ZMat M, ZMat X) {
+                         const double2* theta, ZMat M, ZMat X, int64_t i0, int64_t i1) {  // rows [i0, i1)
   const int k = blockIdx.y;
   const cplx th = ld(&theta[k]);
   double2* base = M.p - (kb + BD_NB) + k * M.stride;  // row-band base of pair k
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = wid; i < N; i += nw) {
+  for (int64_t i = i0 + wid; i < i1; i += nw) {
     double2* rowp = base + i * Wd;
     for (int e = lane; e < Wd; e += 32) {
       const int off = e - (kb + BD_NB);  // j - i
@@ -54,8 +54,8 @@ __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const do
       rowp[e] = z;
     }
   }
-  const int64_t nx = N * nrhs;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nx; e += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t e = i0 * nrhs + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < i1 * nrhs;
+       e += (int64_t)gridDim.x * blockDim.x)
     X.p[k * X.stride + e] = make_double2(V[e], 0.0);
 }
 
@@ -318,9 +318,12 @@ struct BdGraph {
 BdGraph g_bd_graph;
 }  // namespace
 
+// band_host / V_host (host mode): the band (diagonal-major, (kb+1) x N) and V are copied in by
+// row chunks on a copy stream, and each chunk's rows are built as soon as the band columns they
+// read (i0 - kb .. i1) have landed, so the 1 GB copy-in overlaps the build.
 int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int64_t nrhs, double shift_c,
                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
-               float* per_pair_ms) {
+               float* per_pair_ms, const double* band_host, const double* V_host) {
   const int kb = (int)kb64;
   const int nb = BD_NB;
   const int Wd = 2 * kb + 2 * nb + 1;
@@ -346,8 +349,41 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
   dim3 bg(1184, npairs);
-  PFX_LAUNCH("bd_build", stream, bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X));
-  PFX_CUDA_TRY(cudaGetLastError());
+  if (!band_host) {
+    PFX_LAUNCH("bd_build", stream,
+               bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X, 0, N));
+    PFX_CUDA_TRY(cudaGetLastError());
+  } else {
+    constexpr int NCH = 8;
+    static cudaStream_t cin = nullptr;
+    static cudaEvent_t evs[NCH + 1];
+    if (!cin) {
+      PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+      for (auto& e : evs) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    // the staging buffers are idle on entry (host-mode calls end synchronised)
+    PFX_CUDA_TRY(cudaEventRecord(evs[NCH], stream));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(cin, evs[NCH], 0));
+    double* bandd = const_cast<double*>(band);
+    double* Vd = const_cast<double*>(V);
+    int64_t done = 0;  // band columns [0, done) copied
+    for (int c = 0; c < NCH; ++c) {
+      const int64_t i0 = N * c / NCH, i1 = N * (c + 1) / NCH;
+      if (i1 > done) {
+        PFX_CUDA_TRY(cudaMemcpy2DAsync(bandd + done, (size_t)N * sizeof(double), band_host + done,
+                                       (size_t)N * sizeof(double), (size_t)(i1 - done) * sizeof(double),
+                                       (size_t)kb + 1, cudaMemcpyHostToDevice, cin));
+        done = i1;
+      }
+      PFX_CUDA_TRY(cudaMemcpyAsync(Vd + i0 * nrhs, V_host + i0 * nrhs, (size_t)(i1 - i0) * nrhs * sizeof(double),
+                                   cudaMemcpyHostToDevice, cin));
+      PFX_CUDA_TRY(cudaEventRecord(evs[c], cin));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evs[c], 0));
+      PFX_LAUNCH("bd_build", stream,
+                 bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X, i0, i1));
+      PFX_CUDA_TRY(cudaGetLastError());
+    }
+  }
   if (prof_on()) {
     // profiling wants per-kernel events: run the launches directly
     if (int rc = bd_factor_solve(stream, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing)) return rc;

@@ -30,7 +30,7 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
                 const TriShard* sh = nullptr);
 int banded_run(const double* band, int64_t N, int64_t kb, const double* V, int64_t nrhs, double shift_c,
                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
-               float* per_pair_ms);
+               float* per_pair_ms, const double* band_host = nullptr, const double* V_host = nullptr);
 int pole_table_host(int n, double* theta2, double* coef2);
 int shifted_solve_large(const double* A, int a_complex, int d, const double2* theta_d, const double* V, int nrhs,
                         double2* Y, cudaStream_t stream);
@@ -507,15 +507,22 @@ int pfx_expm_banded(int mem, const double* band, int64_t N, int64_t kb, const do
   const double2 *th = nullptr, *co = nullptr;
   if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
   const double *Bd = nullptr, *Vd = nullptr;
-  if ((rc = stage_in(mem, 3, band, (size_t)(kb + 1) * N * sizeof(double), stream, &Bd))) return rc;
-  if ((rc = stage_in(mem, 5, V, (size_t)N * nrhs * sizeof(double), stream, &Vd))) return rc;
+  if (mem == PFX_MEM_HOST) {  // copied in by row chunks inside banded_run, overlapping the build
+    Bd = static_cast<const double*>(scratch(3, (size_t)(kb + 1) * N * sizeof(double)));
+    Vd = static_cast<const double*>(scratch(5, (size_t)N * nrhs * sizeof(double)));
+    if (!Bd || !Vd) return fail(PFX_CUDA, "staging allocation failed");
+  } else {
+    Bd = band;
+    Vd = V;
+  }
   double* Out = out;
   const size_t obytes = (size_t)N * nrhs * sizeof(double);
   if (mem == PFX_MEM_HOST) {
     Out = static_cast<double*>(scratch(6, obytes));
     if (!Out) return fail(PFX_CUDA, "staging allocation failed");
   }
-  rc = banded_run(Bd, N, kb, Vd, nrhs, shift_c, th, co, npairs, Out, stream, per_pair_ms);
+  rc = banded_run(Bd, N, kb, Vd, nrhs, shift_c, th, co, npairs, Out, stream, per_pair_ms,
+                  mem == PFX_MEM_HOST ? band : nullptr, mem == PFX_MEM_HOST ? V : nullptr);
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
     PFX_CUDA_TRY(cudaMemcpyAsync(out, Out, obytes, cudaMemcpyDeviceToHost, stream));
