@@ -1226,6 +1226,8 @@ int tridiag_run(const double* diag, const double* off, int64_t N, const double* 
       if (!hflag) return fail(PFX_CUDA, "pinned status word allocation failed");
       PFX_CUDA_TRY(cudaMemcpyAsync(hflag, trunc_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
       if (int rc = sync_stream(stream)) return rc;
+      static const bool rep = getenv("PFX_TRI_REPORT") != nullptr;
+      if (rep) fprintf(stderr, "[tri host pipeline] truncation %s\n", *hflag ? "rejected: global fallback" : "accepted");
       if (*hflag) {
         // weak decay across a row group: redo the carries globally (V is on the device)
         TriArgs af = a;

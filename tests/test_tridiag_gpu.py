@@ -92,12 +92,15 @@ def test_shift_many_groups_ragged_tiles():
 
 
 @pytest.mark.parametrize("N,nrhs,scale", [(4096, 4, 25.0), (1 << 16, 16, 25.0), (1 << 18, 16, 25.0),
-                                          (1 << 16, 3, 0.05)])
+                                          (1 << 16, 3, 0.05), (4096, 4, 1e3), (8192, 3, 1e4)])
 def test_host_pipeline_matches_device(N, nrhs, scale):
     """Host-memory calls pipeline the copies by row groups with per-group carries (backward
     carries truncated at the next group, verified by tri_trunc_check, global fallback
-    otherwise).  Small groups or weak decay (scale 0.05: |l'| close to 1 over many rows) take
-    the fallback; C2-like sizes take the truncated carries.  Both must agree with the
+    otherwise).  The first four cases (C2-like scales, and scale 0.05) take the truncated
+    carries (PFX_TRI_REPORT=1 prints the verdict).  A large scale (|l'| -> 1 when the
+    off-diagonal dwarfs every pole) makes tri_trunc_check reject the truncation, so the last two
+    cases exercise the global fallback.  Rounding grows with the norm (the oracle differs from
+    both paths by as much), so the tolerance scales with it.  Both must agree with the
     device-memory call, which scans the carries globally (and uses longer chunks), to
     rounding."""
     import torch
@@ -112,4 +115,5 @@ def test_host_pipeline_matches_device(N, nrhs, scale):
     dev = torch.device("cuda:0")
     devr = _native.expm_tridiag_device(*(torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (d, o, V)), t2,
                                        c2, 0.0).cpu().numpy()
-    assert rel(host, devr) <= 1e-12, rel(host, devr)
+    tol = 5e-14 * max(scale, 20.0)
+    assert rel(host, devr) <= tol, rel(host, devr)
