@@ -804,7 +804,10 @@ __global__ void scale_rows(double* x, int64_t n, double s) {
 }
 
 namespace {
-constexpr int TR_GROUPS = 16;
+#ifndef PFX_TR_GROUPS
+#define PFX_TR_GROUPS 16  // row groups of the host pipeline (tools/ab_c2_host.sh)
+#endif
+constexpr int TR_GROUPS = PFX_TR_GROUPS;
 struct TriPipe {
   cudaStream_t in = nullptr, outs = nullptr;
   cudaStream_t cs[TR_GROUPS] = {};  // per-group fix streams: earlier groups first (D2H order)
