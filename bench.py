@@ -2,11 +2,12 @@
 """Benchmark of the partial-fraction exp(A)V hot path on B200 (BASELINE.json metric:
 "exp(A)V evals/sec at 1/2/4/8 B200; % of FP64-tensor or HBM roofline").
 
-Default workload = BASELINE configs[1] (C2): 1-D Dirichlet Laplacian, N = 2^20,
-spectrum (-100, 0), 16 seeded Gaussian RHS, n = 24 (12 conjugate pole pairs).
-One eval (= one step) = exp(tA)V for the whole 16-column block.  --workload C1/C3/C5
-selects the other configs (C4 when built).  Inputs are seeded synthetic data with
-the reference recipes (paper_2306_16778_b200/workloads.py); there is no dataset.
+Default workload = BASELINE configs[3] (C4), the largest single-GPU config and the one whose
+text carries the metric's "1/2/4/8 GPUs": one dense complex Hermitian A, d = 4096, spectrum
+U[-500, 0], the full exp(A) (V = I, 4096 RHS), n = 24 (12 conjugate pole pairs), one blocked
+LU per shift.  One eval (= one step) = the whole 4096 x 4096 result.  --workload C1/C2/C3/C5
+selects the other configs.  Inputs are seeded synthetic data with the reference recipes
+(paper_2306_16778_b200/workloads.py); there is no dataset.
 
 Multi-GPU (torchrun, one process per GPU), total work fixed as N grows ("scaling":
 "strong"), --shard selects how it is split:
@@ -17,7 +18,7 @@ Multi-GPU (torchrun, one process per GPU), total work fixed as N grows ("scaling
          (pfx_expm_tridiag_shard); the two chunk scans exchange one small all-gather each
          and every output row is final on its rank (no reduction of the 134 MB result);
   batch  C3 only: each rank solves its block of the 512 matrices (no collective);
-  auto   (default) rows for C2, batch for C3, pole otherwise.
+  auto   rows for C2, batch for C3, pole otherwise (default: pole on every config).
 
 Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA events on
 the launching stream, max over ranks; library profiling is off in the timed region (a
@@ -27,10 +28,15 @@ dominant-kernel roofline).  L2 policy per config (config.l2): C2-C5 inputs excee
 times each step with its own event pair recorded after the flush (the K step durations are
 summed; the flush sits between timed iterations).
 
-`--impl reference` runs the reference's CPU algorithm for the same workload (the
-oracle restatement: zgtsv/zgbsv/LAPACK per pole pair with the 2 Re(a y) combine and
-ascending reduction, oracle/restate.py) on all host cores, one bounded sample of
-the workload per step, and prints the same metric.
+`--impl reference` times the reference's own CPU implementation of the same workload on the
+host cores (oracle/cpu_timer.py): the unmodified reference package from baseline/_ref through
+its public API for the dense configs (matexp_action / matexp_full), the oracle restatement
+(zgtsv / zgbsv per pole pair, 2 Re(a y), ascending reduction) for the structured ones, which
+the dense-only reference cannot express.  BLAS threads are exported before numpy loads, the
+inputs are built outside the timer, every step is one bounded sample of the workload, and the
+value is the median step after the warm-up (reference bench.py:196-205).  The thread setting
+is the best of BASELINE.md §3's three, recorded on the pod by `--cpu-calibrate`
+(profiles/cpu_settings.json).  The same timer gives the GPU arm's `cpu_baseline`.
 """
 from __future__ import annotations
 
@@ -175,8 +181,6 @@ class Workload:
             self.h2d = d.nbytes + o.nbytes + V.nbytes
             self.d2h = V.nbytes
             self.evals_per_step = 1.0
-            self.desc = {"workload": "C2: tridiagonal 1-D Dirichlet Laplacian, N=2^20, spectrum (-100,0), 16 RHS, n=24",
-                         "N": 1 << 20, "nrhs": 16, "n": 24, "l2": "inputs (144 MB) + output (128 MB) exceed L2 (126 MB); no flush"}
         elif name == "C1":
             n = W.C1["n"]
             A, v, _ = W.c1_inputs()
@@ -184,8 +188,6 @@ class Workload:
             self.h2d = A.nbytes + v.nbytes
             self.d2h = v.nbytes
             self.evals_per_step = 1.0
-            self.desc = {"workload": "C1: dense real symmetric d=128, spectrum U[-50,0], exp(A)v, n=16", "d": 128, "n": 16,
-                         "l2": "256 MB L2 flush before every step, between the per-step CUDA event pairs"}
         elif name == "C3":
             n = W.C3["n"]
             A, V = W.c3_batch()
@@ -193,8 +195,6 @@ class Workload:
             self.h2d = A.nbytes + V.nbytes
             self.d2h = V.nbytes * 2
             self.evals_per_step = float(W.C3["batch"])
-            self.desc = {"workload": "C3: 512 dense complex Hermitian d=256, spectrum U[-200,0], exp(A)v, n=20",
-                         "batch": 512, "d": 256, "n": 20, "l2": "inputs 537 MB exceed L2; no flush"}
         elif name == "C4":
             n = W.C4["n"]
             A, _ = W.c4_matrix()
@@ -202,8 +202,6 @@ class Workload:
             self.h2d = A.nbytes
             self.d2h = A.nbytes
             self.evals_per_step = 1.0
-            self.desc = {"workload": "C4: dense complex Hermitian d=4096, spectrum U[-500,0], full exp(A), n=24",
-                         "d": 4096, "n": 24, "l2": "inputs 268 MB exceed L2; no flush"}
         elif name == "C5":
             n = W.C5["n"]
             band = W.c5_band()
@@ -212,8 +210,6 @@ class Workload:
             self.h2d = band.nbytes + V.nbytes
             self.d2h = V.nbytes
             self.evals_per_step = 1.0
-            self.desc = {"workload": "C5: 2-D 5-point Laplacian 512x512 (bandwidth 512), spectrum (-400,0), 8 RHS, n=16",
-                         "N": 262144, "kb": 512, "nrhs": 8, "n": 16, "l2": "inputs > L2; no flush"}
         else:
             raise SystemExit(f"unknown workload {name}")
         if batch_range is not None:  # batch sharding (C3): this rank's matrices only
@@ -266,94 +262,109 @@ class Workload:
         return _native.expm_banded_host(p["band"], p["V"], self.theta2, self.coef2, 0.0, out=o)
 
 
-# ---- CPU baseline (oracle restatement on the host cores) ----------------------------
+# ---- CPU baseline (the reference on the host cores) ---------------------------------
 
-def _cpu_task(args):
-    name, n, cols = args
-    if name != "C4":
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    from oracle import restate
-    from paper_2306_16778_b200 import workloads as W
-
-    if name == "C2":
-        d, o = W.c2_matrix()
-        V = W.c2_rhs()
-        restate.tridiag_action(d, o, V[:, cols], n)
-        return len(cols) / 16.0
-    if name == "C1":
-        A, v, _ = W.c1_inputs()
-        restate.run_tasks_dense(A, v, n)
-        return 1.0
-    if name == "C3":
-        for b in cols:
-            restate.run_tasks_dense(W.c3_matrix(b), W.c3_vector(b), n)
-        return float(len(cols))
-    if name == "C4":
-        # one pole pair of the full exp(A): zgesv with 4096 identity RHS (engine.py:208)
-        A, _ = W.c4_matrix()
-        th, co = restate.pairs(n)
-        k = cols[0]
-        X = np.linalg.solve(A + th[k] * np.eye(A.shape[0]), np.eye(A.shape[0], dtype=complex))
-        aX = co[k] * X
-        _ = aX + aX.conj().T
-        return 1.0 / len(th)
-    if name == "C5":
-        # one pole pair (zgbsv, kl=ku=512) on all 8 RHS, on the leading C5_ROWS_FRAC of the
-        # rows (the banded LU costs N kb^2: work scales linearly with the rows kept)
-        band = W.c5_band()
-        V = W.c5_rhs()
-        nk = band.shape[1] // C5_ROWS_FRAC
-        band, V = np.ascontiguousarray(band[:, :nk]), np.ascontiguousarray(V[:nk])
-        th, co = restate.pairs(n)
-        ab = restate.sym_band_to_general(band)
-        ab[2 * band.shape[0] - 2, :] += th[cols[0]]
-        import scipy.linalg.lapack as lapack
-        lapack.zgbsv(band.shape[0] - 1, band.shape[0] - 1, ab, V.astype(complex), overwrite_ab=1)
-        return 1.0 / len(th) / C5_ROWS_FRAC
-    raise ValueError(name)
+# BASELINE.md §3 thread settings: (processes, BLAS threads per process)
+def cpu_settings(cores):
+    return {"S1": (1, 1), "S2": (cores, 1), "S3": (1, cores)}
 
 
-C5_ROWS_FRAC = 8
+CPU_SETTINGS_FILE = os.path.join(ROOT, "profiles", "cpu_settings.json")
+# survey winners, used until a calibration on the pod is recorded
+CPU_DEFAULT_SETTING = {"C1": "S1", "C2": "S2", "C3": "S2", "C4": "S3", "C5": "S2"}
 
 
-def cpu_sample_plan(name, cores):
-    """Bounded sample of the workload (~10-30 s of CPU work), as (tasks, description)."""
-    if name == "C2":
-        tasks = [(name, 24, [c]) for c in range(min(cores, 16))]
-        return tasks, f"{len(tasks)} of the 16 RHS columns of C2 (all 12 pole pairs, full N=2^20), one process per column"
-    if name == "C1":
-        tasks = [(name, 16, [0])] * cores
-        return tasks, f"{cores} independent C1 evals, one per process"
-    if name == "C3":
-        per = 2
-        tasks = [(name, 20, list(range(i * per, (i + 1) * per))) for i in range(cores)]
-        return tasks, f"{cores * per} of the 512 C3 matrices ({per} per process)"
-    if name == "C4":
-        tasks = [(name, 24, [0])]
-        return tasks, "1 of the 12 pole pairs of C4 (zgesv d=4096 with identity RHS, all BLAS threads)"
-    if name == "C5":
-        tasks = [(name, 16, [k]) for k in range(min(max(cores // 2, 1), 8))]
-        return tasks, (f"{len(tasks)} of the 8 pole pairs of C5 (zgbsv kl=ku=512, 8 RHS) on the leading 1/{C5_ROWS_FRAC} "
-                       "of the rows (work linear in rows), one process each")
-    raise ValueError(name)
+def cpu_best_setting(name):
+    if os.path.exists(CPU_SETTINGS_FILE):
+        with open(CPU_SETTINGS_FILE) as fh:
+            rec = json.load(fh)
+        if name in rec and "best" in rec[name]:
+            return rec[name]["best"]
+    return CPU_DEFAULT_SETTING[name]
 
 
-def run_cpu(name, cores, steps=1, warmup=0):
-    """Returns (evals/s, description, cores used). Process pool: LAPACK releases no GIL in the f2py wrappers."""
-    from concurrent.futures import ProcessPoolExecutor
+def run_cpu(name, cores, setting, steps, warmup):
+    """One oracle.cpu_timer subprocess (BLAS threads exported before numpy loads, inputs built
+    once per process outside the timer, median of `steps` after `warmup`).  Returns its dict."""
+    procs, blas = cpu_settings(cores)[setting]
+    cmd = [sys.executable, "-m", "oracle.cpu_timer", "--workload", name, "--procs", str(procs), "--blas", str(blas),
+           "--steps", str(steps), "--warmup", str(warmup)]
+    env = dict(os.environ, OPENBLAS_NUM_THREADS=str(blas), OMP_NUM_THREADS=str(blas), MKL_NUM_THREADS=str(blas))
+    env.pop("CUDA_VISIBLE_DEVICES", None)
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"cpu_timer failed: {res.stderr[-2000:]}")
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    out["setting"] = setting
+    return out
 
-    tasks, desc = cpu_sample_plan(name, cores)
-    used = len(tasks)
-    tot_work = tot_t = 0.0
-    with ProcessPoolExecutor(max_workers=used) as pool:
-        for it in range(warmup + steps):
-            t0 = time.perf_counter()
-            work = sum(pool.map(_cpu_task, tasks))
-            dt = time.perf_counter() - t0
-            if it >= warmup:
-                tot_work += work
-                tot_t += dt
-    return tot_work / tot_t, desc, used
+
+def cpu_calibrate(name, cores, steps=5, warmup=1):
+    """Times all three settings (median of `steps` after `warmup` each) and records the best."""
+    rec = {}
+    if os.path.exists(CPU_SETTINGS_FILE):
+        with open(CPU_SETTINGS_FILE) as fh:
+            rec = json.load(fh)
+    res = {s: run_cpu(name, cores, s, steps, warmup) for s in cpu_settings(cores)}
+    best = max(res, key=lambda s: res[s]["value"])
+    rec[name] = {"best": best, "nproc": cores, "cpu": _cpu_model(),
+                 "settings": {s: {k: r[k] for k in ("value", "median_step_s", "procs", "blas_threads", "kind",
+                                                     "sample", "blas")} for s, r in res.items()}}
+    os.makedirs(os.path.dirname(CPU_SETTINGS_FILE), exist_ok=True)
+    with open(CPU_SETTINGS_FILE, "w") as fh:
+        json.dump(rec, fh, indent=1)
+    return rec[name]
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline_entry(r):
+    return {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+            "sample": r["sample"] + f"; median of {r['steps']} after {r['warmup']} warm-up (setting {r['setting']})",
+            "setting": r["setting"], "median_step_s": r["median_step_s"], "blas": r.get("blas"),
+            "nproc": r.get("nproc"), "cpu": _cpu_model()}
+
+
+def config_dict(name, world, shard):
+    """The `config` object both arms print (identical for the same workload and N)."""
+    desc = dict(WORKLOAD_DESC[name])
+    desc["parallelism"] = {
+        "pole": f"pole-shard x{world}" + (" + 1 NCCL reduce" if world > 1 else ""),
+        "rows": f"row-shard x{world} + 2 small all-gathers (scan aggregates); output rows stay on their rank",
+        "batch": f"batch-shard x{world} (no collective)"}[shard]
+    return desc
+
+
+WORKLOAD_DESC = {
+    "C1": {"workload": "C1: dense real symmetric d=128, spectrum U[-50,0], exp(A)v, n=16", "d": 128, "n": 16,
+           "l2": "256 MB L2 flush before every step, between the per-step CUDA event pairs"},
+    "C2": {"workload": "C2: tridiagonal 1-D Dirichlet Laplacian, N=2^20, spectrum (-100,0), 16 RHS, n=24",
+           "N": 1 << 20, "nrhs": 16, "n": 24,
+           "l2": "inputs (144 MB) + output (128 MB) exceed L2 (126 MB); no flush"},
+    "C3": {"workload": "C3: 512 dense complex Hermitian d=256, spectrum U[-200,0], exp(A)v, n=20",
+           "batch": 512, "d": 256, "n": 20, "l2": "inputs 537 MB exceed L2; no flush"},
+    "C4": {"workload": "C4: dense complex Hermitian d=4096, spectrum U[-500,0], full exp(A) (V=I), n=24",
+           "d": 4096, "n": 24, "l2": "input 268 MB and 12 x 268 MB of factors exceed L2; no flush"},
+    "C5": {"workload": "C5: 2-D 5-point Laplacian 512x512 (bandwidth 512), spectrum (-400,0), 8 RHS, n=16",
+           "N": 262144, "kb": 512, "nrhs": 8, "n": 16, "l2": "inputs > L2; no flush"},
+}
+
+
+def resolve_shard(shard, workload, world):
+    if shard == "auto":
+        shard = {"C2": "rows", "C3": "batch"}.get(workload, "pole")
+    if (shard == "rows" and workload != "C2") or (shard == "batch" and workload != "C3"):
+        raise SystemExit(f"--shard {shard} does not apply to {workload}")
+    return "pole" if world == 1 else shard
 
 
 # ---- main ------------------------------------------------------------------------
@@ -364,11 +375,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--cpu-calibrate", action="store_true",
+                    help="time the three BASELINE.md §3 CPU thread settings for --workload and record the best")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--prof-steps", type=int, default=3)
-    ap.add_argument("--shard", choices=["auto", "pole", "rows", "batch"], default="auto")
+    ap.add_argument("--shard", choices=["auto", "pole", "rows", "batch"], default="pole")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -377,18 +390,29 @@ def main():
     cores = os.cpu_count() or 1
     peaks = load_peaks()
 
+    shard = resolve_shard(args.shard, args.workload, world)
+    config = config_dict(args.workload, world, shard)
+
+    if args.cpu_calibrate:
+        if rank == 0:
+            print(json.dumps(cpu_calibrate(args.workload, cores)), flush=True)
+        return
+
     if args.impl == "reference":
         if rank != 0:
             return
-        # every step is one bounded sample of the workload (cpu_sample_plan), K timed after W
+        # the reference's own CPU implementation on all host cores (its recorded best thread
+        # setting); every step is one bounded sample of the workload (oracle/cpu_timer.py),
+        # median over K after W warm-up steps
         steps, warmup = max(1, args.steps), max(0, args.warmup)
-        value, desc, used = run_cpu(args.workload, cores, steps=steps, warmup=warmup)
+        r = run_cpu(args.workload, cores, cpu_best_setting(args.workload), steps, warmup)
+        value = r["value"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
-            "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "c128", "data": "synthetic (seeded reference recipes)", "impl": "reference",
-            "config": {"workload": args.workload, "parallelism": f"cpu x{used} processes"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port", "sample": desc},
+            "ms_per_step": 1e3 * r["median_step_s"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic (seeded reference recipes)",
+            "impl": "reference", "config": config,
+            "cpu_baseline": cpu_baseline_entry(r),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
@@ -434,13 +458,6 @@ def main():
 
     n = {"C1": 16, "C2": 24, "C3": 20, "C4": 24, "C5": 16}[args.workload]
     npairs = n // 2
-    shard = args.shard
-    if shard == "auto":
-        shard = {"C2": "rows", "C3": "batch"}.get(args.workload, "pole")
-    if (shard == "rows" and args.workload != "C2") or (shard == "batch" and args.workload != "C3"):
-        raise SystemExit(f"--shard {shard} does not apply to {args.workload}")
-    if world == 1:
-        shard = "pole"  # one rank: every mode is the plain call
     lo, hi = (rank * npairs // world, (rank + 1) * npairs // world) if shard == "pole" else (0, npairs)
     nbatch = W.C3["batch"]
     brange = (rank * nbatch // world, (rank + 1) * nbatch // world) if shard == "batch" else None
@@ -528,10 +545,11 @@ def main():
     ms_step = ms / args.steps
     value = wl.evals_per_step * args.steps / (ms * 1e-3)
 
-    # end-to-end through the C-ABI with host buffers (H2D + compute + D2H per step).  N > 1:
-    # every rank calls the host entry on its pole slice, the host partials meet in one
-    # reduce to rank 0 (device tensors over NCCL), and rank 0 reads the sum back; the time is
-    # the max over ranks of the wall clock between two barriers
+    # end-to-end with host buffers (H2D + compute + D2H per step).  N = 1: the C-ABI host
+    # entry (PFX_MEM_HOST, its own pipelined staging).  N > 1 pole sharding: every rank copies
+    # the inputs in, solves its pole slice on the device, the device partials meet in one NCCL
+    # reduce to rank 0, and rank 0 reads the sum back; the time is the max over ranks of the
+    # wall clock between two barriers
     e2e = None
     if args.e2e_steps > 0:
         h2d, d2h = wl.h2d, wl.d2h
@@ -559,11 +577,17 @@ def main():
                 pout[r0:r1].copy_(out[r0:r1], non_blocking=True)
                 stream.synchronize()
                 return
-            part = wl.step_host()
             if world > 1 and shard == "pole":
-                t = reduce_sum(torch.from_numpy(np.ascontiguousarray(part)).reshape(-1).to(dev))
+                # one H2D of the inputs, this rank's pairs on the device, ONE reduce of the
+                # device partials to rank 0, one D2H of the sum at the root
+                for k, v in wl.pinned.items():
+                    wl.dev_in[k].copy_(v, non_blocking=True)
+                out = compute(stream)
                 if rank == 0:
-                    t.cpu()
+                    wl.pinned_out.copy_(out.reshape(-1).view(torch.float64), non_blocking=True)
+                stream.synchronize()
+                return
+            wl.step_host()
         e2e_step()
         torch.cuda.synchronize()
         barrier()
@@ -608,8 +632,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v_cpu, desc, used = run_cpu(args.workload, cores, steps=1, warmup=0)
-            cpu = {"value": v_cpu, "unit": UNIT, "cores": used, "kind": "port", "sample": desc}
+            cpu = cpu_baseline_entry(run_cpu(args.workload, cores, cpu_best_setting(args.workload), 5, 1))
         except Exception as exc:  # pragma: no cover - reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": cores, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -618,10 +641,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic (seeded reference recipes)",
-            "config": dict(wl.desc, parallelism={
-                "pole": f"pole-shard x{world}" + (" + 1 NCCL reduce" if world > 1 else ""),
-                "rows": f"row-shard x{world} + 2 small all-gathers (scan aggregates); output rows stay on their rank",
-                "batch": f"batch-shard x{world} (no collective)"}[shard]),
+            "config": config,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches * args.steps // prof_steps,
             "kernels": {k: {"launches": v[0], "total_ms": v[1], "gflop": v[2] / 1e9} for k, v in kern.items()},

@@ -56,14 +56,35 @@ extern "C" {
 #define PFX_MEM_DEVICE 0
 #define PFX_MEM_HOST 1
 
+#define PFX_PIVOT_CHECKED 0
+#define PFX_PIVOT_ALWAYS 1
+#define PFX_PIVOT_NONE 2
+
 /* Library version (major*10000 + minor*100 + patch). */
 int pfx_version(void);
 
 /* Message of the last failed call on this thread ("" if none). */
 const char* pfx_last_error(void);
 
-/* Free the device arenas held by the library on the current device. */
+/* Free the device arenas and cached pole tables held by the library on the current device. */
 int pfx_release(void);
+
+/*
+ * Pivoting policy of the dense path (pfx_expm_dense; process-wide, default
+ * PFX_PIVOT_CHECKED; see pfx_expm_dense).  pfx_pivot_fallbacks() counts the dense calls
+ * whose checked interchange-free factorisation was redone with interchanges.
+ */
+int pfx_set_pivot_mode(int mode);
+int pfx_get_pivot_mode(void);
+long long pfx_pivot_fallbacks(void);
+
+/*
+ * Threading: one call at a time per device.  Every entry point holds its device's lock
+ * for the whole call (the device workspace is shared by all calls on that device);
+ * device-memory calls are ordered after the previous call's use of the workspace on the
+ * GPU as well (an event the next call's stream waits on), so host threads may call
+ * concurrently, on any streams and devices.
+ */
 
 /*
  * Pole/residue table of R_n(z) = 1/exp_n(-z): n even in [2, 64].
@@ -84,13 +105,21 @@ int pfx_pole_table(int n, double* theta2, double* coef2);
  *        (V = I, out is batch x d x d).
  *   out  batch x d x (nrhs or d); complex iff out_complex.  out_complex must
  *        equal !(real path) as defined above (engine.py:185), else PFX_BADARG.
- * A must be Hermitian: every pivot of A + theta I then has |Im| >= Im theta > 0,
- * so with all Im theta_k > 0 the LU runs without interchanges (d <= 512: batched
- * SMEM-panel LU; d > 512: blocked LU on DMMA); a table with some Im theta_k <= 0
- * (or PFX_DENSE_PIVOT=1 in the environment, d <= 512) selects partial pivoting
- * (LAPACK getrf semantics).  For real A in full mode and d > 512 the inverse is
- * taken as complex symmetric (lower triangle computed, mirrored in the combine).
- * An exactly zero pivot returns PFX_SINGULAR.
+ * Factorisation: LU with partial pivoting, as the reference's LAPACK zgesv / zgetrf
+ * (engine.py:200,203,208), under the pivoting policy of pfx_set_pivot_mode:
+ *   PFX_PIVOT_CHECKED (default): the factorisation runs without row interchanges and
+ *     checks, for every column, that partial pivoting (izamax: max |re|+|im| of the
+ *     updated column, first index on ties) would have kept the diagonal pivot; if any
+ *     column fails the check, the call is redone with interchanges.  The result is
+ *     therefore always a partial-pivoting LU.  For Hermitian A the check essentially never
+ *     fails (every pivot of A + theta I has |Im| >= Im theta > 0, SURVEY finding 7, and
+ *     the diagonal dominates), so the interchange-free kernels run at full speed.
+ *   PFX_PIVOT_ALWAYS: getrf-style interchanges on every column (PFX_DENSE_PIVOT=1 in the
+ *     environment forces this too).
+ *   PFX_PIVOT_NONE: interchange-free, unchecked (opt-in).
+ * (d <= 512: batched SMEM-panel LU; d > 512: blocked LU on DMMA.)  For real A in full
+ * mode and d > 512 the inverse is taken as complex symmetric (lower triangle computed,
+ * mirrored in the combine).  An exactly zero pivot returns PFX_SINGULAR.
  */
 int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t batch, const double* V,
                    int v_complex, int64_t nrhs, double shift_c, const double* theta2, const double* coef2,

@@ -30,10 +30,12 @@ def dst_exp_lap1d(N: int, s: float, V: np.ndarray) -> np.ndarray:
     return scipy.fft.dst(W, type=1, norm="ortho", axis=0)
 
 
-def dst_exp_lap2d(m: int, s: float, V: np.ndarray) -> np.ndarray:
+def dst_exp_lap2d(m: int, s: float, V: np.ndarray, ny: int | None = None) -> np.ndarray:
+    """exp(s (kron(T_ny, I_m) + kron(I_ny, T_m))) V on an m x ny grid (x = m fastest);
+    ny = None: the square m x m grid."""
+    ny = m if ny is None else ny
     nrhs = V.shape[1]
-    X = V.reshape(m, m, nrhs)
+    X = V.reshape(ny, m, nrhs)
     W = scipy.fft.dstn(X, type=1, norm="ortho", axes=(0, 1))
-    lam = _lam(m, s)
-    W = W * np.exp(lam[:, None] + lam[None, :])[:, :, None]
-    return scipy.fft.dstn(W, type=1, norm="ortho", axes=(0, 1)).reshape(m * m, nrhs)
+    W = W * np.exp(_lam(ny, s)[:, None] + _lam(m, s)[None, :])[:, :, None]
+    return scipy.fft.dstn(W, type=1, norm="ortho", axes=(0, 1)).reshape(m * ny, nrhs)

@@ -54,6 +54,9 @@ SIGNATURES = {
     ),
     "pfx_prof_enable": (_int, [_int]),
     "pfx_prof_read": (_int, [ctypes.c_char_p, _int]),
+    "pfx_set_pivot_mode": (_int, [_int]),
+    "pfx_get_pivot_mode": (_int, []),
+    "pfx_pivot_fallbacks": (ctypes.c_longlong, []),
     "pfx_shifted_solve": (
         _int,
         [_int, _vp, _int, _i64, ctypes.c_double, ctypes.c_double, _vp, _i64, _vp, _vp],
@@ -113,6 +116,28 @@ def prof_read() -> dict:
     return out
 
 
+PIVOT_MODES = {"checked": 0, "always": 1, "none": 2}
+
+
+def set_pivot_mode(mode: str) -> None:
+    """Dense pivoting policy (include/pfx.h pfx_set_pivot_mode): 'checked' (default: partial
+    pivoting semantics, interchange-free kernels verified column by column, redone with
+    interchanges when a check fails), 'always' (getrf interchanges), 'none' (unchecked)."""
+    if mode not in PIVOT_MODES:
+        raise BadSpec(f"pivot mode must be one of {sorted(PIVOT_MODES)}, got {mode!r}")
+    _check(lib().pfx_set_pivot_mode(PIVOT_MODES[mode]), "pfx_set_pivot_mode")
+
+
+def get_pivot_mode() -> str:
+    m = lib().pfx_get_pivot_mode()
+    return {v: k for k, v in PIVOT_MODES.items()}[m]
+
+
+def pivot_fallbacks() -> int:
+    """Dense calls whose checked interchange-free factorisation was redone with interchanges."""
+    return int(lib().pfx_pivot_fallbacks())
+
+
 def pole_table(n: int):
     theta2 = np.zeros(n, dtype=np.float64)
     coef2 = np.zeros(n, dtype=np.float64)
@@ -151,12 +176,32 @@ def _f64_view(t):
     """Raw float64 storage of a real or complex128 tensor (contiguous)."""
     import torch
 
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise BadSpec("expected a tensor on the CUDA device")
     t = t.contiguous()
     if t.dtype == torch.complex128:
         return t
     if t.dtype != torch.float64:
         raise BadSpec(f"expected float64/complex128 tensor, got {t.dtype}")
     return t
+
+
+def _real_dev(t, name: str, shape=None):
+    """A float64 CUDA tensor argument, contiguous.  The caller keeps the returned tensor
+    referenced until the call has returned (a temporary .contiguous() copy freed early would
+    hand the library a dangling pointer).  Wrong dtype / device / shape -> BadSpec (never an
+    out-of-bounds read of misinterpreted memory)."""
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        raise BadSpec(f"{name} must be a torch tensor on the CUDA device")
+    if t.dtype != torch.float64:
+        raise BadSpec(f"{name} must be float64, got {t.dtype}")
+    if t.device.type != "cuda":
+        raise BadSpec(f"{name} must live on a CUDA device, got {t.device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise BadSpec(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return t.contiguous()
 
 
 def _ptr(t) -> int:
@@ -169,6 +214,8 @@ def expm_dense_device(A, V, theta2, coef2, shift_c: float, out=None, per_pair_ms
     """Device-tensor entry: A (batch,d,d) or (d,d); V (batch,d,nrhs)/(d,nrhs)/(d,) or None (full)."""
     torch = _torch()
     A = _f64_view(A)
+    if A.dim() not in (2, 3) or A.shape[-1] != A.shape[-2]:
+        raise BadSpec(f"A must be (d, d) or (batch, d, d), got {tuple(A.shape)}")
     squeeze_batch = A.dim() == 2
     if squeeze_batch:
         A = A.unsqueeze(0)
@@ -194,6 +241,8 @@ def expm_dense_device(A, V, theta2, coef2, shift_c: float, out=None, per_pair_ms
     odt = torch.float64 if real_path else torch.complex128
     if out is None:
         out = torch.empty((batch, d, ncols), dtype=odt, device=A.device)
+    elif out.dtype != odt or out.numel() != batch * d * ncols or not out.is_contiguous() or out.device != A.device:
+        raise BadSpec(f"out must be a contiguous {odt} tensor with {batch * d * ncols} elements on {A.device}")
     npairs = len(theta2) // 2
     ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
     st = lib().pfx_expm_dense(
@@ -259,18 +308,33 @@ def expm_dense_host(A: np.ndarray, V, theta2, coef2, shift_c: float, per_pair_ms
 
 # ---- tridiagonal / banded ------------------------------------------------------
 
+def _out_dev(out, shape, like):
+    import torch
+
+    if out is None:
+        return torch.empty(shape, dtype=torch.float64, device=like.device)
+    if out.dtype != torch.float64 or tuple(out.shape) != tuple(shape) or not out.is_contiguous() \
+            or out.device != like.device:
+        raise BadSpec(f"out must be a contiguous float64 tensor of shape {tuple(shape)} on {like.device}")
+    return out
+
+
 def expm_tridiag_device(diag, off, V, theta2, coef2, shift_c: float, out=None, per_pair_ms=None, stream=None):
     torch = _torch()
     squeeze = V.dim() == 1
     if squeeze:
         V = V.unsqueeze(-1)
+    if V.dim() != 2:
+        raise BadSpec(f"V must be (N,) or (N, nrhs), got {tuple(V.shape)}")
     N, nrhs = V.shape
-    if out is None:
-        out = torch.empty((N, nrhs), dtype=torch.float64, device=V.device)
+    V = _real_dev(V, "V")
+    diag = _real_dev(diag, "diag", (N,))
+    off = _real_dev(off, "off", (N - 1,))
+    out = _out_dev(out, (N, nrhs), V)
     npairs = len(theta2) // 2
     ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
     st = lib().pfx_expm_tridiag(
-        PFX_MEM_DEVICE, _ptr(diag), _ptr(off) if N > 1 else None, N, _ptr(V.contiguous()), nrhs, float(shift_c),
+        PFX_MEM_DEVICE, _ptr(diag), _ptr(off) if N > 1 else None, N, _ptr(V), nrhs, float(shift_c),
         _f64p(theta2), _f64p(coef2), npairs, _ptr(out), ctypes.cast(ms, _fp) if ms is not None else None,
         _stream_ptr(stream),
     )
@@ -301,9 +365,15 @@ def expm_tridiag_shard(diag, off, V, theta2, coef2, shift_c: float, rank: int, n
     squeeze = V.dim() == 1
     if squeeze:
         V = V.unsqueeze(-1)
+    if V.dim() != 2:
+        raise BadSpec(f"V must be (N,) or (N, nrhs), got {tuple(V.shape)}")
     N, nrhs = V.shape
+    V = _real_dev(V, "V")
+    diag = _real_dev(diag, "diag", (N,))
+    off = _real_dev(off, "off", (N - 1,))
     if out is None:
         out = torch.zeros((N, nrhs), dtype=torch.float64, device=V.device)
+    out = _out_dev(out, (N, nrhs), V)
     failure = []
 
     def _cb(ctx, buf, count):
@@ -321,7 +391,7 @@ def expm_tridiag_shard(diag, off, V, theta2, coef2, shift_c: float, rank: int, n
 
     cb = ALLGATHER_FN(_cb)
     st = lib().pfx_expm_tridiag_shard(
-        _ptr(diag), _ptr(off) if N > 1 else None, N, _ptr(V.contiguous()), nrhs, float(shift_c), _f64p(theta2),
+        _ptr(diag), _ptr(off) if N > 1 else None, N, _ptr(V), nrhs, float(shift_c), _f64p(theta2),
         _f64p(coef2), len(theta2) // 2, _ptr(out), rank, nranks, ctypes.cast(cb, _vp), None, _stream_ptr(stream),
     )
     if failure:
@@ -381,14 +451,17 @@ def expm_banded_device(band, V, theta2, coef2, shift_c: float, out=None, per_pai
     squeeze = V.dim() == 1
     if squeeze:
         V = V.unsqueeze(-1)
+    if V.dim() != 2 or band.dim() != 2:
+        raise BadSpec(f"V must be (N,) or (N, nrhs) and band (kb + 1, N), got {tuple(V.shape)}, {tuple(band.shape)}")
     N, nrhs = V.shape
     kb = band.shape[0] - 1
-    if out is None:
-        out = torch.empty((N, nrhs), dtype=torch.float64, device=V.device)
+    V = _real_dev(V, "V")
+    band = _real_dev(band, "band", (kb + 1, N))
+    out = _out_dev(out, (N, nrhs), V)
     npairs = len(theta2) // 2
     ms = (ctypes.c_float * npairs)() if per_pair_ms is not None else None
     st = lib().pfx_expm_banded(
-        PFX_MEM_DEVICE, _ptr(band.contiguous()), N, kb, _ptr(V.contiguous()), nrhs, float(shift_c), _f64p(theta2),
+        PFX_MEM_DEVICE, _ptr(band), N, kb, _ptr(V), nrhs, float(shift_c), _f64p(theta2),
         _f64p(coef2), npairs, _ptr(out), ctypes.cast(ms, _fp) if ms is not None else None, _stream_ptr(stream),
     )
     _check(st, "pfx_expm_banded")

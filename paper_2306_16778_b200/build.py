@@ -32,8 +32,25 @@ def _deps():
     return _sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
 
 
+STAMP = LIB + ".flags"
+
+
+def _flags_id() -> str:
+    """Everything that changes the generated code besides the sources: the nvcc command
+    line (including PFX_NVCC_FLAGS ablations) and the compiler."""
+    return " ".join([NVCC, *ARCH, *COMMON])
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
+        return True
+    # a library built with different flags (e.g. an interrupted timing ablation that
+    # compiled a phase out) is never reused
+    try:
+        with open(STAMP) as fh:
+            if fh.read() != _flags_id():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(p) > t for p in _deps())
@@ -65,6 +82,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(_flags_id())
     if verbose:
         for o in objs:
             print(open(o + ".log").read())

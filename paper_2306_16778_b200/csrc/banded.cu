@@ -173,7 +173,10 @@ struct BdStreams {
   cudaEvent_t ev[8] = {};
 };
 static int bd_streams(BdStreams& S) {
-  static BdStreams g;
+  static BdStreams gs[kMaxDevices];
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
+  BdStreams& g = gs[dev];
   if (!g.s1) {
     // the critical chain must win the SM slots whenever a trailing-update CTA retires:
     // s1 (panel beside the critical chain) high priority, s2 / s3 (trailing work) low
@@ -295,11 +298,7 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
       PFX_CUDA_TRY(cudaGetLastError());
     }
     const int fsm = (64 * 65 + 64 * std::min(nr, 64)) * (int)sizeof(double2);
-    static int fsm_set = 0;
-    if (fsm > fsm_set) {
-      PFX_CUDA_TRY(cudaFuncSetAttribute(bd_back_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
-      fsm_set = fsm;
-    }
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(bd_back_finish), fsm)) return rc;
     dim3 gf((unsigned)npairs, (unsigned)ceil_div(nr, 64));
     PFX_LAUNCH_F("bd_back_finish", stream, 4.0 * jb * jb * (double)nr * npairs,
                  bd_back_finish<<<gf, 256, fsm, stream>>>(X, blk(Ui, j0), j0, jb, nr, nq, P));
@@ -315,7 +314,7 @@ struct BdGraph {
   int64_t N = 0;
   int kb = 0, nr = 0, np = 0;
 };
-BdGraph g_bd_graph;
+BdGraph g_bd_graph[kMaxDevices];  // per device: a graph is bound to the device it was captured on
 }  // namespace
 
 // band_host / V_host (host mode): the band (diagonal-major, (kb+1) x N) and V are copied in by
@@ -355,11 +354,18 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     PFX_CUDA_TRY(cudaGetLastError());
   } else {
     constexpr int NCH = 8;
-    static cudaStream_t cin = nullptr;
-    static cudaEvent_t evs[NCH + 1];
+    struct CopyIn {
+      cudaStream_t cin = nullptr;
+      cudaEvent_t evs[NCH + 1];
+    };
+    static CopyIn cis[kMaxDevices];
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
+    cudaStream_t& cin = cis[dev].cin;
+    cudaEvent_t* evs = cis[dev].evs;
     if (!cin) {
       PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-      for (auto& e : evs) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      for (int i = 0; i <= NCH; ++i) PFX_CUDA_TRY(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming));
     }
     // the staging buffers are idle on entry (host-mode calls end synchronised)
     PFX_CUDA_TRY(cudaEventRecord(evs[NCH], stream));
@@ -388,7 +394,9 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     // profiling wants per-kernel events: run the launches directly
     if (int rc = bd_factor_solve(stream, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing)) return rc;
   } else {
-    BdGraph& G = g_bd_graph;
+    const int gdev = current_device();
+    if (gdev < 0 || gdev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
+    BdGraph& G = g_bd_graph[gdev];
     if (!G.exec || G.ws != ws || G.N != N || G.kb != kb || G.nr != (int)nrhs || G.np != npairs) {
       if (G.exec) {
         cudaGraphExecDestroy(G.exec);
@@ -433,7 +441,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  if (*hsg) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted band factorization");
+  if (*hsg & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted band factorization");
   return PFX_OK;
 }
 

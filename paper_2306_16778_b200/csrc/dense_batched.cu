@@ -137,12 +137,16 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         if (tid == 0) {
           s_piv[jj] = jj;
           ipiv[p + jj] = p + jj;
-          if (pv.re == 0.0 && pv.im == 0.0) *sing = 1;
+          if (pv.re == 0.0 && pv.im == 0.0) atomicOr(sing, ST_SINGULAR);
         }
         const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp_fast(pv);
+        const double pabs = fabs(pv.re) + fabs(pv.im);
         for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
           double2* row = &P[r * PS];
-          const cplx l = cmul(ld(&row[jj]), rp);
+          const cplx xj = ld(&row[jj]);
+          // partial-pivoting check (izamax on the updated column): row r would displace jj
+          if (fabs(xj.re) + fabs(xj.im) > pabs) atomicOr(sing, ST_PIVOT);
+          const cplx l = cmul(xj, rp);
           const double2* prow_j = &P[jj * PS];
           // four columns per round: all loads first (this row is never the pivot row, but
           // the compiler cannot prove it), then the updates and stores
@@ -200,7 +204,7 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
       if (tid == 0) {
         s_piv[jj] = piv;
         ipiv[p + jj] = p + piv;
-        if (best == 0.0) *sing = 1;
+        if (best == 0.0) atomicOr(sing, ST_SINGULAR);
       }
       for (int c = tid; c < jb; c += DB_THREADS) {
         prow[c] = P[piv * PS + c];
@@ -547,12 +551,16 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
       if (tid == 0) {
         s_piv[jj] = jj;
         ipiv[p + jj] = p + jj;
-        if (pv.re == 0.0 && pv.im == 0.0) *sing = 1;
+        if (pv.re == 0.0 && pv.im == 0.0) atomicOr(sing, ST_SINGULAR);
       }
       const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp_fast(pv);
+      const double pabs = fabs(pv.re) + fabs(pv.im);
       for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
         double2* row = &P[r * PS];
-        const cplx l = cmul(ld(&row[jj]), rp);
+        const cplx xj = ld(&row[jj]);
+        // partial-pivoting check (izamax on the updated column): row r would displace jj
+        if (fabs(xj.re) + fabs(xj.im) > pabs) atomicOr(sing, ST_PIVOT);
+        const cplx l = cmul(xj, rp);
         const double2* prow_j = &P[jj * PS];
         for (int c = jj + 1; c < jb; c += 4) {
           cplx x[4], y[4];
@@ -998,7 +1006,7 @@ __global__ void __launch_bounds__(DB_THREADS, MINB) dense_batched_kernel(DenseBa
     __syncthreads();
     for (int i = tid; i < d; i += DB_THREADS) s_perm[i] = PIV ? reinterpret_cast<int*>(S)[i] : i;
     __syncthreads();
-    if (*s_sing && tid == 0) atomicExch(a.status, PFX_SINGULAR);
+    if (tid == 0 && *s_sing) atomicOr(a.status, *s_sing);
     // ---- K3: solves, one RHS column at a time through shared memory
     double2* Yg = a.Y + (size_t)slot * d * nc;
     double2* Ycg = a.Yc ? a.Yc + (size_t)slot * d * nc : nullptr;
@@ -1087,8 +1095,7 @@ int dense_batched_supported(int64_t d) { return d >= 1 && d <= 512; }
 
 // resident CTAs (= concurrently factored systems) of dense_batched_run for nsys systems of size d
 int dense_batched_slots(int d, int64_t nsys) {
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   const bool many = nsys > sms;
   return (d <= 256 && many) ? 2 * sms : sms;
 }
@@ -1097,12 +1104,8 @@ int dense_batched_slots(int d, int64_t nsys) {
 int dense_batched_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int ncols,
                       int full, int real_path, int solve_only, double shift_c, const double2* theta_d, const double2* coef_d,
                       int npairs, double* out, cudaStream_t stream, float* launch_ms, int pivot) {
-  int dev = 0;
-  PFX_CUDA_TRY(cudaGetDevice(&dev));
-  static int sms_of[16] = {};
-  if (dev < 16 && !sms_of[dev]) PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
-  int sms = dev < 16 ? sms_of[dev] : 148;
-  int dev_sms = sms;
+  const int sms = device_sms();
+  const int dev_sms = sms;
   const bool many = (int64_t)batch * npairs > dev_sms;
   const int nb = (d <= 256 && !many) ? 32 : 16;
   const int minb = (d <= 256 && many) ? 2 : 1;
@@ -1143,8 +1146,9 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   args.status = args.ipiv + (size_t)slots * d;
   args.stage = stage;
   args.dbg = nullptr;
-  static unsigned long long* dbg_dev = nullptr;
+  static unsigned long long* dbg_devs[kMaxDevices] = {};
   if (getenv("PFX_DENSE_PHASES")) {
+    unsigned long long*& dbg_dev = dbg_devs[current_device() & (kMaxDevices - 1)];
     if (!dbg_dev) PFX_CUDA_TRY(cudaMalloc(&dbg_dev, 8 * sizeof(unsigned long long)));
     PFX_CUDA_TRY(cudaMemsetAsync(dbg_dev, 0, 8 * sizeof(unsigned long long), stream));
     args.dbg = dbg_dev;
@@ -1157,7 +1161,7 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
     PFX_CUDA_TRY(cudaEventCreate(&e1));
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
-  auto kern = pivot ? (nb == 32 ? dense_batched_kernel<32, 1, true>
+  auto kern = pivot == 1 ? (nb == 32 ? dense_batched_kernel<32, 1, true>
                                 : (minb == 2 ? dense_batched_kernel<16, 2, true> : dense_batched_kernel<16, 1, true>))
                     : (nb == 32 ? dense_batched_kernel<32, 1, false>
                                 : (minb == 2 ? dense_batched_kernel<16, 2, false> : dense_batched_kernel<16, 1, false>));
@@ -1181,6 +1185,13 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
   PFX_CUDA_TRY(cudaMemcpyAsync(hst, args.status, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (int rc_ = sync_stream(stream)) return rc_;
   const int st = *hst;
+  if (pivot == 2 && (st & ST_PIVOT)) {
+    // checked mode: some column's diagonal pivot is not the one partial pivoting picks ->
+    // redo the whole call with interchanges
+    note_pivot_fallback();
+    return dense_batched_run(A, a_complex, d, batch, V, v_complex, ncols, full, real_path, solve_only, shift_c,
+                             theta_d, coef_d, npairs, out, stream, launch_ms, 1);
+  }
   if (args.dbg) {
     unsigned long long h[8];
     PFX_CUDA_TRY(cudaMemcpy(h, args.dbg, sizeof(h), cudaMemcpyDeviceToHost));
@@ -1189,7 +1200,7 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
             "swaps=%.1f trsm=%.1f gemm=%.1f\n",
             h[6] / 1e6, h[7] / 1e6, h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
   }
-  if (st == PFX_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
+  if (st & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
   return PFX_OK;
 }
 

@@ -12,9 +12,12 @@
 //   X_k = U_k^{-1} L_k^{-1} B                  blocked forward/backward substitution,
 //        B = I (full mode) or V (action); all DMMA (zgemm + ztrmm by the stored inverses)
 //   out = e^c sum_k S_k                          fused combine kernel, k ascending
-// No pivoting on this path: for Hermitian A and Im(theta_k) >= 0.7366 every pivot of
-// A + theta_k I has |Im| >= Im(theta_k) (SURVEY finding 7), so the factorisation cannot
-// break down; the batched small-matrix path (dense_batched.cu) keeps partial pivoting.
+// Pivoting (pfx_set_pivot_mode): by default the factorisation runs without interchanges and
+// checks every column against partial pivoting (the diagonal block LU inside the block, the
+// L21 product below it); if partial pivoting would have exchanged a row anywhere, the call is
+// redone with the pivoted blocked LU (lu_solve_piv).  For Hermitian A and Im(theta_k) >=
+// 0.7366 every pivot of A + theta_k I has |Im| >= Im(theta_k) (SURVEY finding 7), and the
+// diagonal dominates the columns of A + theta I, so the check passes on these inputs.
 // Complex action (Yc = M^{-H} V) is obtained from the conjugate shifts theta_k^* as
 // extra batch members, since (A + theta I)^H = A + conj(theta) I for Hermitian A.
 #include "zblas.cuh"
@@ -91,8 +94,11 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
 // sym_lower (with identity_rhs): M is complex symmetric, so X = M^{-1} is too and the
 // backward pass computes only the lower triangle: block row p needs columns <= p, and the
 // rows below it already hold X[>p, <=p] (a third of the full backward flops).
+// check_pivots: every column is checked against partial pivoting (zgetrf_diag inside the
+// diagonal block, the L21 product below it); a column whose diagonal pivot partial pivoting
+// would have exchanged raises ST_PIVOT in *sing.
 int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
-                   bool identity_rhs, bool sym_lower) {
+                   bool identity_rhs, bool sym_lower, bool check_pivots) {
   const int nb = DL_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -117,7 +123,10 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
     if ((rc = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return rc;
     if (rest > 0) {
       if ((rc = ztrmm_inplace(s, nsys, jb, rest, li(j0), sub(M, j0, j0 + jb), false, false))) return rc;
-      if ((rc = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true))) return rc;
+      // L21 = A21 U11^{-1}, each entry checked against partial pivoting (checked mode)
+      if ((rc = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true, sub(M, j0, j0),
+                              check_pivots ? sing : nullptr)))
+        return rc;
       if ((rc = zgemm(s, nsys, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
                       sub(M, j0 + jb, j0 + jb))))
         return rc;
@@ -146,17 +155,25 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
   return PFX_OK;
 }
 
+int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* ipiv, int* sing);
+
+// pivot: 0 = interchange-free, 1 = partial pivoting (lu_solve_piv), 2 = checked: the
+// interchange-free LU verifies every column against partial pivoting and the call is redone
+// with lu_solve_piv when a check fails (pfx_set_pivot_mode).
 int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
                     int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
-                    double* out, cudaStream_t stream, float* per_pair_ms) {
+                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot) {
   const int conj_sys = (!full && !real_path) ? 1 : 0;
   const int nsys = npairs * (1 + conj_sys);
   const size_t mbytes = (size_t)nsys * d * d * sizeof(double2);
   const size_t xbytes = (size_t)nsys * d * ncols * sizeof(double2);
   const int nblk = (d + DL_NB - 1) / DL_NB;
   const size_t libytes = (size_t)nsys * nblk * DL_NB * DL_NB * sizeof(double2);
+  // Li / Ui (no-pivot path) and ipiv (pivoted path) share the same space
+  static_assert(sizeof(int) * DL_NB <= 2 * DL_NB * DL_NB * sizeof(double2), "ipiv fits the inverse tiles");
   char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256));
   if (!ws) return fail(PFX_CUDA, "large dense workspace allocation failed");
+  int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
   ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
   ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), ncols, (int64_t)d * ncols};
@@ -174,16 +191,39 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
                                                                     theta_d, npairs, nsys, M, X));
   PFX_CUDA_TRY(cudaGetLastError());
   // real A in full mode: A + theta I is complex symmetric -> lower-triangle inverse
-  const int sym_lower = (full && !a_complex && real_path) ? 1 : 0;
-  int rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0);
-  if (rc) return rc;
+  int sym_lower = (full && !a_complex && real_path) ? 1 : 0;
+  int* hsg = pinned_word();
+  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
+  int rc;
+  bool pivoted = pivot == 1;
+  if (!pivoted) {
+    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2);
+    if (rc) return rc;
+    if (pivot == 2) {
+      PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      if (int rc_ = sync_stream(stream)) return rc_;
+      if (*hsg & ST_PIVOT) {
+        // a column whose diagonal pivot partial pivoting would have exchanged: redo the
+        // factorisations with interchanges from the original matrices
+        note_pivot_fallback();
+        pivoted = true;
+        PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+        PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full,
+                                                                          shift_c, theta_d, npairs, nsys, M, X));
+        PFX_CUDA_TRY(cudaGetLastError());
+      }
+    }
+  }
+  if (pivoted) {
+    sym_lower = 0;
+    rc = lu_solve_piv(stream, nsys, d, M, X, ncols, ipiv, sing);
+    if (rc) return rc;
+  }
   const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
   PFX_LAUNCH("dl_combine", stream,
              dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
                                                  out));
   PFX_CUDA_TRY(cudaGetLastError());
-  int* hsg = pinned_word();
-  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
   PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (per_pair_ms) {
     PFX_CUDA_TRY(cudaEventRecord(e1, stream));
@@ -196,32 +236,17 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  if (*hsg) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
+  if (*hsg & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
   return PFX_OK;
 }
 
-// Single shifted solve Y = (A + theta I)^{-1} V for d > 512 (pfx_shifted_solve; the reference
-// linalg.shifted_solve, linalg.py:92-108, has no size limit).  theta is arbitrary here (it may
-// be real), so this is getrf/getrs with partial pivoting: per 64-column panel the pivoting
-// panel kernel (izamax ties), the interchanges on the columns left and right of the panel and
-// on the right-hand sides, U12 = L11^{-1} A12, A22 -= L21 U12; then blocked forward and
-// backward substitution.
-int shifted_solve_large(const double* A, int a_complex, int d, const double2* theta_d, const double* V, int nrhs,
-                        double2* Y, cudaStream_t stream) {
+// LU with partial pivoting of nsys d x d matrices M (getrf semantics: per 64-column panel
+// the pivoting panel kernel, izamax ties to the first index), then X = U^{-1} L^{-1} P X.
+// Per panel: the interchanges on the columns left and right of the panel and on X,
+// U12 = L11^{-1} A12, A22 -= L21 U12; then blocked forward and backward substitution.
+// ipiv: (d/64 panels) x nsys x 64 ints.
+int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* ipiv, int* sing) {
   const int nb = DL_NB;
-  const size_t mbytes = (size_t)d * d * sizeof(double2);
-  const size_t xbytes = (size_t)d * nrhs * sizeof(double2);
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + (size_t)d * sizeof(int) + 256));
-  if (!ws) return fail(PFX_CUDA, "shifted-solve workspace allocation failed");
-  ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
-  ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, (int64_t)d * nrhs};
-  int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
-  int* sing = ipiv + d;
-  PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
-  dim3 bg(1184, 1);
-  PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, 1, nrhs, 0, 0.0, theta_d, 1, 1,
-                                                                    M, X));
-  PFX_CUDA_TRY(cudaGetLastError());
   auto sub = [](ZMat T, int64_t i, int64_t j) {
     ZMat r = T;
     r.p = T.p + i * T.ld + j;
@@ -231,23 +256,24 @@ int shifted_solve_large(const double* A, int a_complex, int d, const double2* th
   for (int j0 = 0; j0 < d; j0 += nb) {
     const int jb = std::min(nb, d - j0);
     const int rest = d - j0 - jb;
-    if ((rc = zgetf2_panel(stream, 1, d - j0, jb, sub(M, j0, j0), ipiv + j0, sing))) return rc;
-    if ((rc = zlaswp(stream, 1, jb, M, j0, 0, j0, ipiv + j0, +1))) return rc;
-    if ((rc = zlaswp(stream, 1, jb, M, j0, j0 + jb, d, ipiv + j0, +1))) return rc;
-    if ((rc = zlaswp(stream, 1, jb, X, j0, 0, nrhs, ipiv + j0, +1))) return rc;
+    int* ip = ipiv + (size_t)(j0 / nb) * nsys * nb;
+    if ((rc = zgetf2_panel(s, nsys, d - j0, jb, sub(M, j0, j0), ip, sing))) return rc;
+    if ((rc = zlaswp(s, nsys, jb, M, j0, 0, j0, ip, +1))) return rc;
+    if ((rc = zlaswp(s, nsys, jb, M, j0, j0 + jb, d, ip, +1))) return rc;
+    if ((rc = zlaswp(s, nsys, jb, X, j0, 0, ncols, ip, +1))) return rc;
     if (rest > 0) {
-      if ((rc = ztrsm_llnu(stream, 1, jb, rest, sub(M, j0, j0), sub(M, j0, j0 + jb)))) return rc;
-      if ((rc = zgemm(stream, 1, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
+      if ((rc = ztrsm_llnu(s, nsys, jb, rest, sub(M, j0, j0), sub(M, j0, j0 + jb)))) return rc;
+      if ((rc = zgemm(s, nsys, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
                       sub(M, j0 + jb, j0 + jb))))
         return rc;
     }
   }
-  // X = L^{-1} P V (P already applied), then U^{-1}
+  // X = L^{-1} P X (P already applied), then U^{-1}
   for (int j0 = 0; j0 < d; j0 += nb) {
     const int jb = std::min(nb, d - j0);
     const int rest = d - j0 - jb;
-    if ((rc = ztrsm_llnu(stream, 1, jb, nrhs, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
-    if (rest > 0 && (rc = zgemm(stream, 1, rest, nrhs, jb, -1.0, sub(M, j0 + jb, j0), sub(X, j0, 0),
+    if ((rc = ztrsm_llnu(s, nsys, jb, ncols, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
+    if (rest > 0 && (rc = zgemm(s, nsys, rest, ncols, jb, -1.0, sub(M, j0 + jb, j0), sub(X, j0, 0),
                                 sub(X, j0 + jb, 0))))
       return rc;
   }
@@ -256,17 +282,41 @@ int shifted_solve_large(const double* A, int a_complex, int d, const double2* th
     const int j0 = pb * nb;
     const int jb = std::min(nb, d - j0);
     const int rest = d - j0 - jb;
-    if (rest > 0 && (rc = zgemm(stream, 1, jb, nrhs, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0),
+    if (rest > 0 && (rc = zgemm(s, nsys, jb, ncols, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0),
                                 sub(X, j0, 0))))
       return rc;
-    if ((rc = ztrsm_lunn(stream, 1, jb, nrhs, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
+    if ((rc = ztrsm_lunn(s, nsys, jb, ncols, sub(M, j0, j0), sub(X, j0, 0)))) return rc;
   }
+  return PFX_OK;
+}
+
+// Single shifted solve Y = (A + theta I)^{-1} V for d > 512 (pfx_shifted_solve; the reference
+// linalg.shifted_solve, linalg.py:92-108, has no size limit).  theta is arbitrary here (it may
+// be real), so this is getrf/getrs with partial pivoting (lu_solve_piv).
+int shifted_solve_large(const double* A, int a_complex, int d, const double2* theta_d, const double* V, int nrhs,
+                        double2* Y, cudaStream_t stream) {
+  const int nb = DL_NB;
+  const size_t mbytes = (size_t)d * d * sizeof(double2);
+  const size_t xbytes = (size_t)d * nrhs * sizeof(double2);
+  const size_t pbytes = (size_t)((d + nb - 1) / nb) * nb * sizeof(int);
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + pbytes + 256));
+  if (!ws) return fail(PFX_CUDA, "shifted-solve workspace allocation failed");
+  ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
+  ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, (int64_t)d * nrhs};
+  int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
+  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + pbytes);
+  PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+  dim3 bg(1184, 1);
+  PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, 1, nrhs, 0, 0.0, theta_d, 1, 1,
+                                                                    M, X));
+  PFX_CUDA_TRY(cudaGetLastError());
+  if (int rc = lu_solve_piv(stream, 1, d, M, X, nrhs, ipiv, sing)) return rc;
   PFX_CUDA_TRY(cudaMemcpyAsync(Y, X.p, xbytes, cudaMemcpyDeviceToDevice, stream));
   int* hsg = pinned_word();
   if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
   PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (int rc_ = sync_stream(stream)) return rc_;
-  if (*hsg) return fail(PFX_SINGULAR, "exactly zero pivot in the shifted factorization");
+  if (*hsg & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in the shifted factorization");
   return PFX_OK;
 }
 

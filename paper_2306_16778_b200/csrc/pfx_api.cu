@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -23,7 +24,7 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
                       int npairs, double* out, cudaStream_t stream, float* launch_ms, int pivot);
 int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
                     int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
-                    double* out, cudaStream_t stream, float* per_pair_ms);
+                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot);
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                 float* launch_ms, const double* V_host = nullptr, double* out_host = nullptr,
@@ -110,21 +111,90 @@ int sync_stream(cudaStream_t stream) {
   return PFX_OK;
 }
 
+int current_device() {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return dev;
+}
+
+int device_sms() {
+  static int sms_of[kMaxDevices] = {};
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  if (!sms_of[dev] && cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  return sms_of[dev];
+}
+
 int raise_smem_limit(const void* kernel, size_t bytes) {
+  struct Entry {
+    const void* kernel;
+    int dev;
+    size_t bytes;
+  };
   static std::mutex mu;
-  static std::vector<std::pair<const void*, size_t>> set;
+  static std::vector<Entry> set;
+  const int dev = current_device();
   std::lock_guard<std::mutex> lk(mu);
   for (auto& e : set)
-    if (e.first == kernel) {
-      if (e.second >= bytes) return PFX_OK;
+    if (e.kernel == kernel && e.dev == dev) {
+      if (e.bytes >= bytes) return PFX_OK;
       PFX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      e.second = bytes;
+      e.bytes = bytes;
       return PFX_OK;
     }
   PFX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  set.emplace_back(kernel, bytes);
+  set.push_back(Entry{kernel, dev, bytes});
   return PFX_OK;
 }
+
+// ---- per-device call lock and pivoting policy -------------------------------------
+namespace {
+std::recursive_mutex g_dev_mu[kMaxDevices];
+std::atomic<int> g_pivot_mode{PFX_PIVOT_CHECKED};
+std::atomic<long long> g_pivot_fallbacks{0};
+}  // namespace
+
+// Device-memory calls may return before their kernels finish (stream-ordered on the caller's
+// stream), so the host lock alone does not keep two calls on different streams out of the
+// shared workspace: every call also makes its stream wait for the previous call's
+// "workspace free" event and records that event on its own stream when it returns.
+cudaEvent_t g_ws_free[kMaxDevices] = {};
+
+struct DeviceLock {
+  std::unique_lock<std::recursive_mutex> lk;
+  bool ok = false;
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  explicit DeviceLock(cudaStream_t s) : stream(s) {
+    dev = current_device();
+    if (dev < 0 || dev >= kMaxDevices) return;
+    lk = std::unique_lock<std::recursive_mutex>(g_dev_mu[dev]);
+    if (!g_ws_free[dev] && cudaEventCreateWithFlags(&g_ws_free[dev], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    if (cudaStreamWaitEvent(stream, g_ws_free[dev], 0) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    ok = true;
+  }
+  ~DeviceLock() {
+    if (ok && cudaEventRecord(g_ws_free[dev], stream) != cudaSuccess) cudaGetLastError();
+  }
+};
+#define PFX_DEVICE_LOCK(stream)                                                    \
+  ::pfx::DeviceLock _pfx_dev_lock(stream);                                         \
+  if (!_pfx_dev_lock.ok) return ::pfx::fail(PFX_CUDA, "no usable CUDA device (or device index >= 16)")
+
+int pivot_mode() { return g_pivot_mode.load(); }
+void note_pivot_fallback() { g_pivot_fallbacks.fetch_add(1); }
 
 void* scratch(int slot, size_t bytes) {
   int dev = 0;
@@ -169,15 +239,25 @@ struct PoleEntry {
   std::vector<double> host;
   double2* dev = nullptr;
 };
-std::vector<PoleEntry> g_pole_cache[16];
+std::vector<PoleEntry> g_pole_cache[kMaxDevices];
 std::mutex g_pole_mu;
+// Bounded: a caller sweeping many shifts (shifted_solve in a loop) would otherwise grow the
+// cache without limit.  Evicting is safe because every call returns synchronised under its
+// device lock, so no kernel can still be reading an evicted table.
+constexpr size_t kPoleCacheMax = 32;
 }  // namespace
+
+static void release_poles(int devid) {
+  std::lock_guard<std::mutex> lk(g_pole_mu);
+  for (PoleEntry& e : g_pole_cache[devid])
+    if (e.dev) cudaFree(e.dev);
+  g_pole_cache[devid].clear();
+}
 
 static int upload_poles(const double* theta2, const double* coef2, int npairs, cudaStream_t stream,
                         const double2** th, const double2** co) {
-  int devid = 0;
-  PFX_CUDA_TRY(cudaGetDevice(&devid));
-  if (devid >= 16) return fail(PFX_CUDA, "device index out of range");
+  const int devid = current_device();
+  if (devid < 0 || devid >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
   std::vector<double> tmp(4 * (size_t)npairs);
   std::memcpy(tmp.data(), theta2, 2 * npairs * sizeof(double));
   std::memcpy(tmp.data() + 2 * npairs, coef2, 2 * npairs * sizeof(double));
@@ -188,6 +268,10 @@ static int upload_poles(const double* theta2, const double* coef2, int npairs, c
       *co = e.dev + npairs;
       return PFX_OK;
     }
+  if (g_pole_cache[devid].size() >= kPoleCacheMax) {
+    cudaFree(g_pole_cache[devid].front().dev);
+    g_pole_cache[devid].erase(g_pole_cache[devid].begin());
+  }
   PoleEntry e;
   e.host = tmp;
   PFX_CUDA_TRY(cudaMalloc(&e.dev, tmp.size() * sizeof(double)));
@@ -209,6 +293,21 @@ static int check_poles(const double* theta2, const double* coef2, int npairs) {
     if (!(theta2[2 * k + 1] > 0.0)) return fail(PFX_BADARG, "pole representatives must have Im(theta) > 0");
   }
   return PFX_OK;
+}
+
+// Pivoting argument of the dense kernels (pfx_set_pivot_mode; PFX_DENSE_PIVOT=1 in the
+// environment forces ALWAYS, for A/B checks): 0 = interchange-free, unchecked; 1 = partial
+// pivoting (getrf interchanges); 2 = checked: the interchange-free factorisation verifies that
+// partial pivoting would have chosen every diagonal pivot, else the call refactors with
+// interchanges.
+static int dense_pivot_arg() {
+  static const bool force_piv = getenv("PFX_DENSE_PIVOT") != nullptr;
+  if (force_piv) return 1;
+  switch (pivot_mode()) {
+    case PFX_PIVOT_ALWAYS: return 1;
+    case PFX_PIVOT_NONE: return 0;
+    default: return 2;
+  }
 }
 
 // Host staging: copy host inputs into arena slots 3..5, output into slot 6.
@@ -285,9 +384,22 @@ int pfx_prof_read(char* buf, int buflen) {
 const char* pfx_last_error(void) { return g_err.c_str(); }
 
 int pfx_release(void) {
+  PFX_DEVICE_LOCK(nullptr);
   release_scratch();
+  release_poles(current_device());
   return PFX_OK;
 }
+
+int pfx_set_pivot_mode(int mode) {
+  if (mode != PFX_PIVOT_CHECKED && mode != PFX_PIVOT_ALWAYS && mode != PFX_PIVOT_NONE)
+    return fail(PFX_BADARG, "pivot mode must be PFX_PIVOT_CHECKED, PFX_PIVOT_ALWAYS or PFX_PIVOT_NONE");
+  g_pivot_mode.store(mode);
+  return PFX_OK;
+}
+
+int pfx_get_pivot_mode(void) { return g_pivot_mode.load(); }
+
+long long pfx_pivot_fallbacks(void) { return g_pivot_fallbacks.load(); }
 
 int pfx_pole_table(int n, double* theta2, double* coef2) {
   if (!theta2 || !coef2) return fail(PFX_BADARG, "null output array");
@@ -317,6 +429,7 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
   const size_t abytes = (size_t)batch * d * d * sizeof(double) * (a_complex ? 2 : 1);
   const size_t vbytes = full ? 0 : (size_t)batch * d * nrhs * sizeof(double) * (v_complex ? 2 : 1);
   const size_t obytes = (size_t)batch * d * ncols * sizeof(double) * (out_complex ? 2 : 1);
+  PFX_DEVICE_LOCK(stream);  // argument checks above need no device
   const double2 *th = nullptr, *co = nullptr;
   rc = upload_poles(theta2, coef2, npairs, stream, &th, &co);
   if (rc) return rc;
@@ -328,8 +441,11 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
     const int64_t slots = dense_batched_slots((int)d, batch * npairs);
     const int64_t per = std::max<int64_t>(1, slots * 5 / npairs);
     if (batch >= 2 * per) {
-      static cudaStream_t cin = nullptr;
-      static std::vector<cudaEvent_t> evs;
+      static cudaStream_t cins[kMaxDevices] = {};
+      static std::vector<cudaEvent_t> evss[kMaxDevices];
+      const int dev = current_device();
+      cudaStream_t& cin = cins[dev];
+      std::vector<cudaEvent_t>& evs = evss[dev];
       if (!cin) PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
       const int64_t first = batch % per ? batch % per : per;
       const int64_t nch = 1 + (batch - first + per - 1) / per;
@@ -360,10 +476,7 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
                                        cudaMemcpyHostToDevice, cin));
         PFX_CUDA_TRY(cudaEventRecord(evs[i], cin));
       }
-      static const bool force_piv = getenv("PFX_DENSE_PIVOT") != nullptr;
-      int pivot = force_piv ? 1 : 0;
-      for (int k = 0; k < npairs && !pivot; ++k)
-        if (!(theta2[2 * k + 1] > 0.0)) pivot = 1;
+      const int pivot = dense_pivot_arg();
       float tot = 0.0f;
       for (int64_t i = 0; i < nch; ++i) {
         int64_t b0, nb;
@@ -395,20 +508,14 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
   }
   float ms = 0.0f;
   if (dense_batched_supported(d)) {
-    // Hermitian A and Im(theta_k) > 0 for every pair: no pivot can vanish (|Im u_ii| >=
-    // Im theta_k), so the LU runs without interchanges; PFX_DENSE_PIVOT=1 forces getrf
-    // semantics (partial pivoting) for A/B checks
-    static const bool force_piv = getenv("PFX_DENSE_PIVOT") != nullptr;
-    int pivot = force_piv ? 1 : 0;
-    for (int k = 0; k < npairs && !pivot; ++k)
-      if (!(theta2[2 * k + 1] > 0.0)) pivot = 1;
+    const int pivot = dense_pivot_arg();
     rc = dense_batched_run(Ad, a_complex, (int)d, (int)batch, Vd, v_complex, ncols, full, real_path, 0, shift_c, th, co,
                            npairs, Od, stream, per_pair_ms ? &ms : nullptr, pivot);
     if (per_pair_ms)
       for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
   } else {
     rc = dense_large_run(Ad, a_complex, (int)d, Vd, v_complex, ncols, full, real_path, shift_c, th, co, npairs, Od,
-                         stream, per_pair_ms);
+                         stream, per_pair_ms, dense_pivot_arg());
   }
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
@@ -429,6 +536,7 @@ int pfx_expm_tridiag(int mem, const double* diag, const double* off, int64_t N, 
   if (!std::isfinite(shift_c)) return fail(PFX_BADARG, "shift must be finite");
   int rc = check_poles(theta2, coef2, npairs);
   if (rc) return rc;
+  PFX_DEVICE_LOCK(stream);  // argument checks above need no device
   const double2 *th = nullptr, *co = nullptr;
   if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
   const double *Dd = nullptr, *Od_ = nullptr, *Vd = nullptr;
@@ -487,6 +595,7 @@ int pfx_expm_tridiag_shard(const double* diag, const double* off, int64_t N, con
   int rc = check_poles(theta2, coef2, npairs);
   if (rc) return rc;
   if (npairs > 16) return fail(PFX_BADARG, "row sharding needs npairs <= 16 (n <= 32)");
+  PFX_DEVICE_LOCK(stream);  // argument checks above need no device
   const double2 *th = nullptr, *co = nullptr;
   if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
   TriShard sh{rank, nranks, allgather, ctx};
@@ -504,6 +613,7 @@ int pfx_expm_banded(int mem, const double* band, int64_t N, int64_t kb, const do
   if (!std::isfinite(shift_c)) return fail(PFX_BADARG, "shift must be finite");
   int rc = check_poles(theta2, coef2, npairs);
   if (rc) return rc;
+  PFX_DEVICE_LOCK(stream);  // argument checks above need no device
   const double2 *th = nullptr, *co = nullptr;
   if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
   const double *Bd = nullptr, *Vd = nullptr;
@@ -540,6 +650,7 @@ int pfx_shifted_solve(int mem, const double* A, int a_complex, int64_t d, double
   if (!std::isfinite(theta_re) || !std::isfinite(theta_im)) return fail(PFX_BADARG, "non-finite shift");
   // one system, residue 1: stage = Y = (A + theta I)^{-1} V (complex V, complex Y)
   double th2[2] = {theta_re, theta_im}, co2[2] = {1.0, 0.0};
+  PFX_DEVICE_LOCK(stream);  // argument checks above need no device
   const double2 *th = nullptr, *co = nullptr;
   int rc = upload_poles(th2, co2, 1, stream, &th, &co);
   if (rc) return rc;

@@ -42,8 +42,25 @@ struct TriShard {
 int tri_partition(int64_t N, int64_t nrhs, int rank, int nranks, int* L, int* P, int64_t* c0, int64_t* c1);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `bytes` exceeds what was set
 // before for this kernel (the call itself costs host time on every launch otherwise)
+// Kept per (kernel, device): the attribute is a per-device property.
 int raise_smem_limit(const void* kernel, size_t bytes);
 void release_scratch();
+// SM count of the current device (cached per device)
+int device_sms();
+// Every C-ABI entry point holds its device's lock for the whole call: the arena slots,
+// staging streams and status words of a device are shared by all calls on it, and every
+// call returns synchronised, so one call at a time per device keeps them consistent when
+// several host threads call concurrently.
+constexpr int kMaxDevices = 16;
+int current_device();
+// dense pivoting policy (pfx_set_pivot_mode) and the count of checked factorisations that
+// had to be redone with interchanges
+int pivot_mode();
+void note_pivot_fallback();
+// status word bits the dense kernels raise (atomicOr): an exactly zero pivot, and a pivot
+// that partial pivoting would have exchanged (checked mode)
+constexpr int ST_SINGULAR = 1;
+constexpr int ST_PIVOT = 2;
 
 // Kernel timing (pfx_prof_enable / pfx_prof_read).  PFX_LAUNCH brackets a launch
 // with events when profiling is on; otherwise it is just the launch.

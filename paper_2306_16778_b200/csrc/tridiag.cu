@@ -755,12 +755,8 @@ static int carry_scan(const TriArgs& a, int npairs, int64_t nrhs, cudaStream_t s
   const int64_t np_ = a.c1 - a.c0;
   if (np_ <= CS_SMEM_P) {
     const int smem = 2 * (int)(np_ + (np_ >> 4) + 1) * (int)sizeof(double2);
-    static int set = 0;
-    if (smem > set) {
-      const int mx = 2 * (CS_SMEM_P + (CS_SMEM_P >> 4) + 1) * (int)sizeof(double2);
-      PFX_CUDA_TRY(cudaFuncSetAttribute(tri_carry_scan_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      set = mx;
-    }
+    const int mx = 2 * (CS_SMEM_P + (CS_SMEM_P >> 4) + 1) * (int)sizeof(double2);
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(tri_carry_scan_smem), mx)) return rc;
     PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan_smem<<<blocks, CS_T, smem, stream>>>(a));
   } else {
     PFX_LAUNCH("tri_carry_scan", stream, tri_carry_scan<<<blocks, CS_T, 0, stream>>>(a));
@@ -782,10 +778,10 @@ static int launch_stream(const TriArgs& a, cudaStream_t stream, int which) {
   const int smem = (int)(sizeof(TriStage<KM>) * TR_SW_WARPS * 2);
   const int th = TR_SW_WARPS * 32;
   if (which == 0) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_pass<KM, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(tri_pass<KM, 0>), smem)) return rc;
     PFX_LAUNCH("tri_sweep", stream, (tri_pass<KM, 0><<<blocks, th, smem, stream>>>(a)));
   } else {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(tri_pass<KM, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(tri_pass<KM, 1>), smem)) return rc;
     PFX_LAUNCH("tri_fix", stream, (tri_pass<KM, 1><<<blocks, th, smem, stream>>>(a)));
   }
   return PFX_OK;
@@ -816,7 +812,10 @@ struct TriPipe {
   cudaEvent_t kick = nullptr;  // timing-enabled (see the group loop)
 };
 int tri_pipe(TriPipe& T) {
-  static TriPipe g;
+  static TriPipe gs[kMaxDevices];  // streams and events belong to the device they were made on
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
+  TriPipe& g = gs[dev];
   if (!g.in) {
     PFX_CUDA_TRY(cudaStreamCreateWithFlags(&g.in, cudaStreamNonBlocking));
     PFX_CUDA_TRY(cudaStreamCreateWithFlags(&g.outs, cudaStreamNonBlocking));
@@ -847,11 +846,7 @@ int tri_pipe(TriPipe& T) {
 // 256 rows left 20 SMs idle), within [32, TR_L] rows and a multiple of 32.  Row-sharded calls
 // size them for one rank's share of the rows; rank r owns chunks [P r / R, P (r + 1) / R).
 int tri_partition(int64_t N, int64_t nrhs, int rank, int nranks, int* L_, int* P_, int64_t* c0, int64_t* c1) {
-  int dev = 0;
-  PFX_CUDA_TRY(cudaGetDevice(&dev));
-  static int sms_of[16] = {};
-  if (dev < 16 && !sms_of[dev]) PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
-  const int64_t slots = (int64_t)(dev < 16 ? sms_of[dev] : 148) * 2 * LS_WARPS * 4;
+  const int64_t slots = (int64_t)device_sms() * 2 * LS_WARPS * 4;
   const int64_t per = ceil_div(ceil_div(N, nranks) * ceil_div(nrhs, 16), slots);
   const int L = (int)std::min<int64_t>(TR_L, std::max<int64_t>(nranks > 1 ? 32 : 64, ceil_div(per, 32) * 32));
   const int P = (int)ceil_div(N, L);

@@ -164,13 +164,8 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
 template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                         bool accumulate) {
-  static bool attr = false;
   const int smem = (int)sizeof(GemmSmem<TM, TN, KS>);
-  if (!attr) {
-    PFX_CUDA_TRY(
-        cudaFuncSetAttribute(zgemm_kernel<TM, TN, NW, M3, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgemm_kernel<TM, TN, NW, M3, KS>), smem)) return rc;
   dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch);
   PFX_LAUNCH_F("zgemm", s, 8.0 * (double)m * n * k * batch,
                (zgemm_kernel<TM, TN, NW, M3, KS><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C,
@@ -181,12 +176,7 @@ static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double a
 
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate) {
   if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    PFX_CUDA_TRY(cudaGetDevice(&dev));
-    PFX_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  const int sms = device_sms();
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
   const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, 64) * (int64_t)batch;
   static const bool ks32 = getenv("PFX_ZGEMM_KS16") == nullptr;
@@ -267,7 +257,7 @@ __global__ void __launch_bounds__(P_THREADS) zgetf2_kernel(int m, int nb, ZMat P
     __syncthreads();
     cplx pv = ld(&prow[j]);
     if (pv.re == 0.0 && pv.im == 0.0) {
-      if (tid == 0) *sing = 1;
+      if (tid == 0) atomicOr(sing, ST_SINGULAR);
       continue;
     }
     cplx rp = crcp(pv);
@@ -351,7 +341,7 @@ __global__ void __launch_bounds__(P_THREADS) zgetf2_smem_kernel(int m, int nb, Z
     }
     const cplx pv = ld(&Ps[j * ps + j]);
     if (pv.re == 0.0 && pv.im == 0.0) {
-      if (tid == 0) *sing = 1;
+      if (tid == 0) atomicOr(sing, ST_SINGULAR);
       __syncthreads();
       continue;
     }
@@ -378,11 +368,7 @@ int zgetf2_panel(cudaStream_t s, int batch, int m, int nb, ZMat P, int* ipiv, in
   if (nb > 64) return fail(PFX_BADARG, "zgetf2_panel: nb > 64");
   if ((int64_t)m * (nb + 1) <= PS_MAXEL) {
     const int smem = (int)((int64_t)m * (nb + 1) * sizeof(double2));
-    static bool attr = false;
-    if (!attr) {
-      PFX_CUDA_TRY(cudaFuncSetAttribute(zgetf2_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_MAXEL * 16 + 64));
-      attr = true;
-    }
+    if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgetf2_smem_kernel), PS_MAXEL * 16 + 64)) return rc;
     PFX_LAUNCH_F("zgetf2", s, 8.0 / 3.0 * nb * nb * (double)m * batch,
                  zgetf2_smem_kernel<<<batch, P_THREADS, smem, s>>>(m, nb, P, ipiv, sing));
     PFX_CUDA_TRY(cudaGetLastError());
@@ -480,13 +466,8 @@ __global__ void __launch_bounds__(T_THREADS) ztrsm_left_kernel(int nb, int n, ZM
 static int trsm_smem(int nb) { return (int)((size_t)nb * (nb + 1) + (size_t)nb * (T_COLS + 1)) * (int)sizeof(double2); }
 static const int kTrsmSmemMax = (64 * 65 + 64 * 33) * (int)sizeof(double2);
 static int trsm_attrs() {
-  static bool done = false;
-  if (!done) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_left_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
-    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrsm_left_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmemMax));
-    done = true;
-  }
-  return PFX_OK;
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(ztrsm_left_kernel<0>), kTrsmSmemMax)) return rc;
+  return raise_smem_limit(reinterpret_cast<const void*>(ztrsm_left_kernel<1>), kTrsmSmemMax);
 }
 
 int ztrsm_llnu(cudaStream_t s, int batch, int nb, int n, ZMat Lm, ZMat B) {
@@ -547,8 +528,12 @@ __device__ __forceinline__ void lu_diag_phase2(int q0, cplx (&a)[16], int nb, ZM
       const cplx r00 = crcp_fast(u00);
       const cplx l10 = cmul(a10, r00);
       const cplx u11 = cfms(a11, l10, u01);
-      if (row == j && cg == jj && u00.re == 0.0 && u00.im == 0.0) *sing = 1;
-      if (row == j + 1 && cg == jj + 1 && u11.re == 0.0 && u11.im == 0.0) *sing = 1;
+      if (row == j && cg == jj && u00.re == 0.0 && u00.im == 0.0) atomicOr(sing, ST_SINGULAR);
+      if (row == j + 1 && cg == jj + 1 && u11.re == 0.0 && u11.im == 0.0) atomicOr(sing, ST_SINGULAR);
+      // partial-pivoting check (izamax, first index on ties): column j's updated entries
+      // below the diagonal (a10 for row j+1, a_rj below) against u00; column j+1's against u11
+      const double pa0 = cabs1(u00), pa1 = cabs1(u11);
+      if (row == j + 1 && cg == 0 && cabs1(a10) > pa0) atomicOr(sing, ST_PIVOT);
       // a_rj, a_{r,j+1} from the row's lanes holding columns j, j+1 (whole warp: no divergence)
       const int src = (lane & ~3) | jj;
       cplx aj, aj1;
@@ -558,7 +543,9 @@ __device__ __forceinline__ void lu_diag_phase2(int q0, cplx (&a)[16], int nb, ZM
       aj1.im = __shfl_sync(0xffffffffu, a[0].im, src + 1);
       if (row > j + 1) {
         const cplx l1 = cmul(aj, r00);
-        const cplx l2 = cmul(cfms(aj1, l1, u01), crcp_fast(u11));
+        const cplx a1 = cfms(aj1, l1, u01);
+        if (cg == 0 && row < nb && (cabs1(aj) > pa0 || cabs1(a1) > pa1)) atomicOr(sing, ST_PIVOT);
+        const cplx l2 = cmul(a1, crcp_fast(u11));
         const cplx m1 = cfms(l1, l2, l10);
         const cplx x0 = cfms(cfms(a[0], m1, lds2(p0)), l2, lds2(p1));
 #pragma unroll
@@ -628,7 +615,7 @@ __device__ __forceinline__ void lu_diag_phase(int q0, cplx (&a)[16], int nb, ZMa
         if (cg >= jj) sts2(pb, a[0]);
 #pragma unroll
         for (int i = 1; i < NL; ++i) sts2(pb + 64u * i, a[i]);
-        if (cg == jj && a[0].re == 0.0 && a[0].im == 0.0) *sing = 1;
+        if (cg == jj && a[0].re == 0.0 && a[0].im == 0.0) atomicOr(sing, ST_SINGULAR);
       }
       __syncthreads();
       const int src = (lane & ~3) | jj;
@@ -636,7 +623,9 @@ __device__ __forceinline__ void lu_diag_phase(int q0, cplx (&a)[16], int nb, ZMa
       aj.re = __shfl_sync(0xffffffffu, a[0].re, src);
       aj.im = __shfl_sync(0xffffffffu, a[0].im, src);
       if (row > j) {
-        const cplx l = cmul(aj, crcp_fast(lds2(base + (jj & 1) * BUF + (unsigned)j * 16u)));
+        const cplx pv = lds2(base + (jj & 1) * BUF + (unsigned)j * 16u);
+        if (cg == 0 && row < nb && cabs1(aj) > cabs1(pv)) atomicOr(sing, ST_PIVOT);  // partial-pivoting check
+        const cplx l = cmul(aj, crcp_fast(pv));
         const cplx a0 = cfms(a[0], l, lds2(pb));
 #pragma unroll
         for (int i = 1; i < NL; ++i) a[i] = cfms(a[i], l, lds2(pb + 64u * i));
@@ -757,12 +746,8 @@ int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing) {
 
 int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui) {
   if (nb > DI_MAX) return fail(PFX_BADARG, "ztrtri_diag: nb > 64");
-  static bool attr = false;
   const int smem = (DI_MAX * DI_S + DI_MAX) * (int)sizeof(double2);
-  if (!attr) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrtri_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(ztrtri_diag_kernel), smem)) return rc;
   dim3 grid((unsigned)ceil_div(nb, 8), 2, (unsigned)batch);
   PFX_LAUNCH_F("ztrtri_diag", s, 8.0 / 3.0 * nb * nb * (double)nb * batch,
                ztrtri_diag_kernel<<<grid, 256, smem, s>>>(nb, D, Li, Ui));
@@ -778,7 +763,7 @@ constexpr int TM_T = 64;
 constexpr int TM_W = 32;
 
 template <bool RIGHT>
-__global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper) {
+__global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper, ZMat Dg, int* flag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // row strides (16-byte words) for conflict-free DMMA fragment loads: an A-operand array
   // (read at rows g x columns tt of a quarter-warp) 4 mod 8, a B-operand array (rows tt x
@@ -858,27 +843,34 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
       if (!RIGHT) {
         if (r < nb && t0 + c < n) *B.at(b, r, t0 + c) = v;
       } else {
-        if (t0 + r < n && c < nb) *B.at(b, t0 + r, c) = v;
+        if (t0 + r < n && c < nb) {
+          *B.at(b, t0 + r, c) = v;
+          if (flag) {
+            // L21 = A21 U11^{-1}: the updated column entry l u_cc of a row below the block
+            // must not exceed the pivot u_cc (partial-pivoting check, izamax order)
+            const cplx u = ld(Dg.at(b, c, c));
+            if (cabs1(cmul(mk(v.x, v.y), u)) > cabs1(u)) atomicOr(flag, ST_PIVOT);
+          }
+        }
       }
     }
 }
 
-int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper) {
+int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper, ZMat Dg,
+                  int* pivot_flag) {
   if (n <= 0) return PFX_OK;
   if (nb > TM_T) return fail(PFX_BADARG, "ztrmm_inplace: nb > 64");
-  static bool attr = false;
   const int smem = (TM_T * (TM_T + 4) + TM_T * (TM_T + 4)) * (int)sizeof(double2);
-  if (!attr) {
-    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrmm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PFX_CUDA_TRY(cudaFuncSetAttribute(ztrmm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(ztrmm_kernel<false>), smem)) return rc;
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(ztrmm_kernel<true>), smem)) return rc;
   dim3 grid((unsigned)ceil_div(n, TM_W), (unsigned)batch);
   const double fl = 4.0 * nb * nb * (double)n * batch;  // triangular: half the square product
   if (right)
-    PFX_LAUNCH_F("ztrmm", s, fl, ztrmm_kernel<true><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0));
+    PFX_LAUNCH_F("ztrmm", s, fl,
+                 ztrmm_kernel<true><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, pivot_flag));
   else
-    PFX_LAUNCH_F("ztrmm", s, fl, ztrmm_kernel<false><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0));
+    PFX_LAUNCH_F("ztrmm", s, fl,
+                 ztrmm_kernel<false><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, nullptr));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }

@@ -22,13 +22,19 @@ struct ZMat {
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
           bool accumulate = true);
 
-// No-pivot LU of the nb x nb diagonal block D (nb <= 64) in shared memory, in place.
+// No-pivot LU of the nb x nb diagonal block D (nb <= 64) in registers, in place.  Raises
+// ST_SINGULAR in *sing on an exactly zero pivot and ST_PIVOT where partial pivoting inside the
+// block would have exchanged rows (the rows below the block are checked by ztrmm_inplace).
 int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing);
 // Triangular inverses of a factored diagonal block: Li = L^{-1} (unit lower), Ui = U^{-1}.
 int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui);
 // In place: B = Tinv * B (left, B nb x n) or B = B * Tinv (right, B n x nb), Tinv nb x nb
 // (nb <= 64) triangular (upper or lower), on DMMA; one CTA per 32-wide strip of B.
-int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper);
+// pivot_flag (right products only): B = L21 = A21 U11^{-1} of a no-pivot LU step whose
+// diagonal block (factored in place) is Dg; every entry is checked against partial pivoting
+// (|l u_cc|_1 > |u_cc|_1 means row interchanges were due) and ST_PIVOT is or-ed into *pivot_flag.
+int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper,
+                  ZMat Dg = ZMat{nullptr, 0, 0}, int* pivot_flag = nullptr);
 
 // Unblocked LU of the m x nb panel at P (in place).  ipiv (optional, batch x nb, 0-based
 // rows relative to the panel) -> partial pivoting with row swaps inside the panel only.

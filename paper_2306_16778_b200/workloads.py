@@ -115,6 +115,21 @@ def c4_matrix(d: int = C4["d"]):
     return A, (lo, hi)
 
 
+def c4_eigen(d: int = C4["d"]):
+    """(A, Q, lam) of the C4 recipe: A = Q diag(lam) Q^H (symmetrised), so exp(A) is known
+    by construction (Q e^lam Q^H), the eigen-oracle of SURVEY §8d P2 without an eigh."""
+    rng = np.random.default_rng([0, 0])
+    lam = np.sort(rng.uniform(C4["lo"], C4["hi"], d))
+    Gr = rng.standard_normal((d, d))
+    Gi = rng.standard_normal((d, d))
+    Q, R = np.linalg.qr(Gr + 1j * Gi)
+    dr = np.diag(R)
+    Q = Q * (dr / np.abs(dr))
+    A = (Q * lam) @ Q.conj().T
+    A = (A + A.conj().T) / 2.0
+    return A, Q, lam
+
+
 # -- C5 ----------------------------------------------------------------------
 
 def c5_band(m: int = C5["m"], scale: float = C5["scale"]):
@@ -122,12 +137,19 @@ def c5_band(m: int = C5["m"], scale: float = C5["scale"]):
 
     Returned in symmetric lower band storage: band[r, j] = A[j + r, j] for
     r = 0..m (kb = m), zero where j + r >= N.  Spectrum inside (-8*scale, 0)."""
-    N = m * m
-    band = np.zeros((m + 1, N))
+    return c5_band_rect(m, m, scale)
+
+
+def c5_band_rect(nx: int, ny: int, scale: float = C5["scale"]):
+    """5-point Dirichlet Laplacian on an nx x ny grid (x fastest, natural ordering):
+    A = scale*(kron(T_ny, I_nx) + kron(I_ny, T_nx)), bandwidth kb = nx, N = nx*ny, in the
+    lower band storage of c5_band.  The C5 recipe at a reduced row count (full bandwidth)."""
+    N = nx * ny
+    band = np.zeros((nx + 1, N))
     band[0, :] = -4.0 * scale
     j = np.arange(N - 1)
-    band[1, : N - 1] = np.where((j % m) != m - 1, scale, 0.0)
-    band[m, : N - m] = scale
+    band[1, : N - 1] = np.where((j % nx) != nx - 1, scale, 0.0)
+    band[nx, : N - nx] = scale
     return band
 
 
