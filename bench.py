@@ -602,7 +602,12 @@ def main():
 
     launches = sum(v[0] for v in kern.values())
     dom = DOMINANT[args.workload]
-    dom_cnt, dom_ms, dom_fl = kern.get(dom, (0, 0.0, 0.0))
+    # profile names carry a phase / variant tag ("zgemm@lu", "dense_batched_kernel@nb16x2"):
+    # the dominant kernel is every launch of that kernel
+    dom_cnt, dom_ms, dom_fl = 0, 0.0, 0.0
+    for kname, (c_, t_, f_) in kern.items():
+        if kname.split("@")[0] == dom:
+            dom_cnt, dom_ms, dom_fl = dom_cnt + c_, dom_ms + t_, dom_fl + f_
     roofline = None
     if dom_cnt:
         t_launch = dom_ms / dom_cnt * 1e-3

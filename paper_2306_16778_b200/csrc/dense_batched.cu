@@ -1166,7 +1166,12 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
                     : (nb == 32 ? dense_batched_kernel<32, 1, false>
                                 : (minb == 2 ? dense_batched_kernel<16, 2, false> : dense_batched_kernel<16, 1, false>));
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(kern), smem)) return rc;
-  PFX_LAUNCH("dense_batched_kernel", stream, kern<<<slots, DB_THREADS, smem, stream>>>(args));
+  {
+    // the variant in the profile name: NB, resident CTAs per SM, interchanges
+    ProfTag tag(pivot == 1 ? (nb == 32 ? "nb32piv" : (minb == 2 ? "nb16x2piv" : "nb16piv"))
+                           : (nb == 32 ? "nb32" : (minb == 2 ? "nb16x2" : "nb16")));
+    PFX_LAUNCH("dense_batched_kernel", stream, kern<<<slots, DB_THREADS, smem, stream>>>(args));
+  }
   PFX_CUDA_TRY(cudaGetLastError());
   const size_t per_out = per_sys * (real_path ? 1 : 2);
   const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);

@@ -116,6 +116,7 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
     return r;
   };
   int rc;
+  ProfTag tag_lu("lu");
   for (int j0 = 0; j0 < d; j0 += nb) {
     const int jb = std::min(nb, d - j0);
     const int rest = d - j0 - jb;
@@ -133,14 +134,20 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
     }
   }
   // forward: X_p -= L[p, :p] X[:p]; X_p = L_pp^{-1} X_p
+  ProfTag tag_fwd("fwd");
   for (int j0 = 0; j0 < d; j0 += nb) {
     const int jb = std::min(nb, d - j0);
     const int nc = identity_rhs ? j0 : ncols;            // columns the update can touch
     const int ns = identity_rhs ? std::min(ncols, j0 + jb) : ncols;  // columns the solve touches
-    if (j0 > 0 && (rc = zgemm(s, nsys, jb, nc, j0, -1.0, sub(M, j0, 0), sub(X, 0, 0), sub(X, j0, 0)))) return rc;
+    // identity RHS: X[:j0, :j0] = L^{-1} so far is unit lower triangular, and each column
+    // tile's product starts at its own diagonal (half the products of a full GEMM)
+    if (j0 > 0 && (rc = zgemm(s, nsys, jb, nc, j0, -1.0, sub(M, j0, 0), sub(X, 0, 0), sub(X, j0, 0), true,
+                              identity_rhs)))
+      return rc;
     if ((rc = ztrmm_inplace(s, nsys, jb, ns, li(j0), sub(X, j0, 0), false, false))) return rc;
   }
   // backward: X_p -= U[p, p+1:] X[p+1:]; X_p = U_pp^{-1} X_p
+  ProfTag tag_bwd("bwd");
   const int nblk = (d + nb - 1) / nb;
   for (int pb = nblk - 1; pb >= 0; --pb) {
     const int j0 = pb * nb;

@@ -59,7 +59,12 @@ bool g_prof_on = false;
 
 bool prof_on() { return g_prof_on; }
 
-void prof_mark(const char* name, cudaStream_t stream, bool begin, double flops) {
+static thread_local const char* g_prof_tag = nullptr;
+void prof_set_tag(const char* tag) { g_prof_tag = tag; }
+const char* prof_get_tag() { return g_prof_tag; }
+
+void prof_mark(const char* name_, cudaStream_t stream, bool begin, double flops) {
+  const std::string name = g_prof_tag ? std::string(name_) + "@" + g_prof_tag : std::string(name_);
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (begin) {
     ProfRec r;

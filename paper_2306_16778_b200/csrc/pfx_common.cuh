@@ -67,6 +67,15 @@ constexpr int ST_PIVOT = 2;
 // PFX_LAUNCH_F also records the launch's algorithmic flop count.
 bool prof_on();
 void prof_mark(const char* name, cudaStream_t stream, bool begin, double flops = 0.0);
+// Phase tag (this thread): while a ProfTag is alive, profiled launches are recorded as
+// "name@tag" (e.g. zgemm@lu, zgemm@fwd), so the kernel breakdown separates the phases.
+void prof_set_tag(const char* tag);
+const char* prof_get_tag();
+struct ProfTag {
+  const char* prev;
+  explicit ProfTag(const char* tag) : prev(prof_get_tag()) { prof_set_tag(tag); }
+  ~ProfTag() { prof_set_tag(prev); }
+};
 #define PFX_LAUNCH_F(name, stream, flops, ...)                          \
   do {                                                                  \
     if (::pfx::prof_on()) ::pfx::prof_mark(name, stream, true, flops);  \

@@ -38,7 +38,7 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // instead of componentwise).
 template <int TM, int TN, int NW, bool M3 = false, int GK = 16>
 __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                                                        int accumulate) {
+                                                        int accumulate, int b_lower) {
   constexpr int NT = NW * 32;
   constexpr int WN = NW / 2;
   constexpr int FM = TM / 2 / 8, FN = TN / WN / 8;
@@ -62,6 +62,10 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
     }
 
   const int ktiles = (k + GK - 1) / GK;
+  // b_lower: B is lower triangular (B[r][c] = 0 for r < c), so this column tile's products
+  // start at row n0 of B; a tile entirely right of the triangle adds nothing
+  const int kt0 = b_lower ? n0 / GK : 0;
+  if (b_lower && accumulate && kt0 >= ktiles) return;
   auto load = [&](int buf, int kt) {
     const int k0 = kt * GK;
 #pragma unroll
@@ -81,9 +85,9 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
       cp_async16_zfill(&S.B[buf][r][c], src, v);
     }
   };
-  if (ktiles > 0) load(0, 0);
+  if (kt0 < ktiles) load(kt0 & 1, kt0);
   cp_async_commit();
-  for (int kt = 0; kt < ktiles; ++kt) {
+  for (int kt = kt0; kt < ktiles; ++kt) {
     const int buf = kt & 1;
     if (kt + 1 < ktiles) load(buf ^ 1, kt + 1);
     cp_async_commit();
@@ -163,18 +167,23 @@ __global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, dou
 
 template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                        bool accumulate) {
+                        bool accumulate, bool b_lower) {
   const int smem = (int)sizeof(GemmSmem<TM, TN, KS>);
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgemm_kernel<TM, TN, NW, M3, KS>), smem)) return rc;
   dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch);
-  PFX_LAUNCH_F("zgemm", s, 8.0 * (double)m * n * k * batch,
+  // algorithmic flops: 8 per complex multiply-add actually required (b_lower: the products
+  // with the zero triangle of B are not counted)
+  double fl = 8.0 * (double)m * n * k * batch;
+  if (b_lower) fl = 8.0 * (double)m * batch * ((double)n * k - 0.5 * (double)std::min(n, k) * std::min(n, k));
+  PFX_LAUNCH_F("zgemm", s, fl,
                (zgemm_kernel<TM, TN, NW, M3, KS><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C,
-                                                                       accumulate ? 1 : 0)));
+                                                                       accumulate ? 1 : 0, b_lower ? 1 : 0)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
 
-int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate) {
+int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate,
+          bool b_lower) {
   if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
   const int sms = device_sms();
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
@@ -182,13 +191,13 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
   static const bool ks32 = getenv("PFX_ZGEMM_KS16") == nullptr;
   if (tiles64 < 2 * sms) {
     if (k <= 64 && ks32)  // short K: two 32-deep stages instead of four 16-deep ones
-      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate)
-                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate);
-    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate)
-              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate);
+      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower)
+                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower);
+    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower)
+              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower);
   }
-  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate)
-            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate);
+  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower)
+            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower);
 }
 
 // ---------------------------------------------------------------------------

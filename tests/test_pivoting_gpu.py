@@ -87,7 +87,7 @@ def test_weak_diagonal_batched_two_cta_variant(pivot_mode):
 
 def test_weak_diagonal_full_mode_large(pivot_mode):
     d = 576
-    A = weak_diagonal_hermitian(d, seed=11, scale=5.0)
+    A = weak_diagonal_hermitian(d, seed=11, scale=20.0)
     pivot_mode("checked")
     before = _native.pivot_fallbacks()
     t2, c2 = default_table(12).interleaved()
