@@ -36,8 +36,10 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // T1 = sum Ar Br, T2 = sum Ai Bi, T3 = sum (Ar + Ai)(Br + Bi), then Cr = T1 - T2 and
 // Ci = T3 - T1 - T2 (normwise-stable; the imaginary part's error is bounded by eps |A||B|
 // instead of componentwise).
+// Two CTAs per SM for the 64x64 tile (<= 128 registers): one CTA's epilogue and K-stage loads
+// overlap the other's DMMA stream (at 156 registers a single CTA per SM ran 15% slower).
 template <int TM, int TN, int NW, bool M3 = false, int GK = 16>
-__global__ void __launch_bounds__(NW * 32) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                                                         int accumulate, int b_lower) {
   constexpr int NT = NW * 32;
   constexpr int WN = NW / 2;
