@@ -117,133 +117,89 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
   };
   int rc;
   ProfTag tag_lu("lu");
-  for (int j0 = 0; j0 < d; j0 += nb) {
+  // one 64-column panel: diagonal LU, both triangular inverses, U12 = L11^{-1} A12 over the
+  // whole row block, L21 = A21 U11^{-1} over the whole column block (checked against partial
+  // pivoting in checked mode)
+  auto factor = [&](int j0, int jb, int rest) -> int {
+    int r;
+    if ((r = zgetrf_diag(s, nsys, jb, sub(M, j0, j0), sing))) return r;
+    if ((r = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return r;
+    if (rest > 0) {
+      if ((r = ztrmm_inplace(s, nsys, jb, rest, li(j0), sub(M, j0, j0 + jb), false, false))) return r;
+      if ((r = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true, sub(M, j0, j0),
+                             check_pivots ? sing : nullptr)))
+        return r;
+    }
+    return PFX_OK;
+  };
+  // Two-panel delayed update: panel a = [j0, j1) is factored, panel b = [j1, j1 + 64) takes
+  // only panel a's update (its column block and its row block), panel b is factored, and the
+  // trailing matrix takes both panels' updates in ONE K = 128 GEMM.  The trailing matrix (up
+  // to 12 x 268 MB, far beyond L2) is read and written once per 128 columns instead of once
+  // per 64, and every trailing tile does twice the DMMA work per epilogue.
+  for (int j0 = 0; j0 < d; j0 += 2 * nb) {
     const int jb = std::min(nb, d - j0);
     const int rest = d - j0 - jb;
-    if ((rc = zgetrf_diag(s, nsys, jb, sub(M, j0, j0), sing))) return rc;
-    if ((rc = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return rc;
-    if (rest > 0) {
-      if ((rc = ztrmm_inplace(s, nsys, jb, rest, li(j0), sub(M, j0, j0 + jb), false, false))) return rc;
-      // L21 = A21 U11^{-1}, each entry checked against partial pivoting (checked mode)
-      if ((rc = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true, sub(M, j0, j0),
-                              check_pivots ? sing : nullptr)))
-        return rc;
-      if ((rc = zgemm(s, nsys, rest, rest, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
-                      sub(M, j0 + jb, j0 + jb))))
-        return rc;
-    }
+    if ((rc = factor(j0, jb, rest))) return rc;
+    if (rest == 0) break;
+    const int j1 = j0 + jb;
+    const int jb1 = std::min(nb, d - j1);
+    const int rest1 = d - j1 - jb1;
+    if ((rc = zgemm(s, nsys, d - j1, jb1, jb, -1.0, sub(M, j1, j0), sub(M, j0, j1), sub(M, j1, j1)))) return rc;
+    if (rest1 > 0 &&
+        (rc = zgemm(s, nsys, jb1, rest1, jb, -1.0, sub(M, j1, j0), sub(M, j0, j1 + jb1), sub(M, j1, j1 + jb1))))
+      return rc;
+    if ((rc = factor(j1, jb1, rest1))) return rc;
+    if (rest1 > 0 && (rc = zgemm(s, nsys, rest1, rest1, jb + jb1, -1.0, sub(M, j1 + jb1, j0), sub(M, j0, j1 + jb1),
+                                 sub(M, j1 + jb1, j1 + jb1))))
+      return rc;
   }
+  // Both substitutions run in super-blocks of SB = 8 block rows: one GEMM with m = 512 rows
+  // applies everything already final outside the super-block (its column strips of X stream
+  // from HBM once per super-block instead of once per block row, shared by the 8 row tiles
+  // through L2), then the block rows inside take only the super-block's own couplings.
+  constexpr int SB = 8 * DL_NB;
   // forward: X_p -= L[p, :p] X[:p]; X_p = L_pp^{-1} X_p
   ProfTag tag_fwd("fwd");
-  for (int j0 = 0; j0 < d; j0 += nb) {
-    const int jb = std::min(nb, d - j0);
-    const int nc = identity_rhs ? j0 : ncols;            // columns the update can touch
-    const int ns = identity_rhs ? std::min(ncols, j0 + jb) : ncols;  // columns the solve touches
-    // identity RHS: X[:j0, :j0] = L^{-1} so far is unit lower triangular, and each column
+  for (int J0 = 0; J0 < d; J0 += SB) {
+    const int J1 = std::min(d, J0 + SB);
+    // identity RHS: X[:J0, :J0] = L^{-1} so far is unit lower triangular, and each column
     // tile's product starts at its own diagonal (half the products of a full GEMM)
-    if (j0 > 0 && (rc = zgemm(s, nsys, jb, nc, j0, -1.0, sub(M, j0, 0), sub(X, 0, 0), sub(X, j0, 0), true,
-                              identity_rhs)))
+    if (J0 > 0 && (rc = zgemm(s, nsys, J1 - J0, identity_rhs ? J0 : ncols, J0, -1.0, sub(M, J0, 0), sub(X, 0, 0),
+                              sub(X, J0, 0), true, identity_rhs ? 0 : -1)))
       return rc;
-    if ((rc = ztrmm_inplace(s, nsys, jb, ns, li(j0), sub(X, j0, 0), false, false))) return rc;
+    for (int j0 = J0; j0 < J1; j0 += nb) {
+      const int jb = std::min(nb, d - j0);
+      const int nc = identity_rhs ? j0 : ncols;                        // columns the update can touch
+      const int ns = identity_rhs ? std::min(ncols, j0 + jb) : ncols;  // columns the solve touches
+      // rows [J0, j0) of X are lower triangular from column J0 on: B[r][c] = 0 for r + J0 < c
+      if (j0 > J0 && (rc = zgemm(s, nsys, jb, nc, j0 - J0, -1.0, sub(M, j0, J0), sub(X, J0, 0), sub(X, j0, 0),
+                                 true, identity_rhs ? J0 : -1)))
+        return rc;
+      if ((rc = ztrmm_inplace(s, nsys, jb, ns, li(j0), sub(X, j0, 0), false, false))) return rc;
+    }
   }
   // backward: X_p -= U[p, p+1:] X[p+1:]; X_p = U_pp^{-1} X_p
   ProfTag tag_bwd("bwd");
-  const int nblk = (d + nb - 1) / nb;
-  for (int pb = nblk - 1; pb >= 0; --pb) {
-    const int j0 = pb * nb;
-    const int jb = std::min(nb, d - j0);
-    const int rest = d - j0 - jb;
-    const int nc = sym_lower ? std::min(ncols, j0 + jb) : ncols;
-    if (rest > 0 &&
-        (rc = zgemm(s, nsys, jb, nc, rest, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0))))
+  const int nsb = (d + SB - 1) / SB;
+  for (int q = nsb - 1; q >= 0; --q) {
+    const int J0 = q * SB, J1 = std::min(d, J0 + SB);
+    // sym_lower: only columns below the super-block's end are needed (rows of X below J1 hold
+    // only their lower triangle, which is all these columns read)
+    const int ncs = sym_lower ? std::min(ncols, J1) : ncols;
+    if (J1 < d &&
+        (rc = zgemm(s, nsys, J1 - J0, ncs, d - J1, -1.0, sub(M, J0, J1), sub(X, J1, 0), sub(X, J0, 0))))
       return rc;
-    if ((rc = ztrmm_inplace(s, nsys, jb, nc, ui(j0), sub(X, j0, 0), false, true))) return rc;
-  }
-  return PFX_OK;
-}
-
-int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* ipiv, int* sing);
-
-// pivot: 0 = interchange-free, 1 = partial pivoting (lu_solve_piv), 2 = checked: the
-// interchange-free LU verifies every column against partial pivoting and the call is redone
-// with lu_solve_piv when a check fails (pfx_set_pivot_mode).
-int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
-                    int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
-                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot) {
-  const int conj_sys = (!full && !real_path) ? 1 : 0;
-  const int nsys = npairs * (1 + conj_sys);
-  const size_t mbytes = (size_t)nsys * d * d * sizeof(double2);
-  const size_t xbytes = (size_t)nsys * d * ncols * sizeof(double2);
-  const int nblk = (d + DL_NB - 1) / DL_NB;
-  const size_t libytes = (size_t)nsys * nblk * DL_NB * DL_NB * sizeof(double2);
-  // Li / Ui (no-pivot path) and ipiv (pivoted path) share the same space
-  static_assert(sizeof(int) * DL_NB <= 2 * DL_NB * DL_NB * sizeof(double2), "ipiv fits the inverse tiles");
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256));
-  if (!ws) return fail(PFX_CUDA, "large dense workspace allocation failed");
-  int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
-  ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
-  ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
-  ZMat X{reinterpret_cast<double2*>(ws + mbytes), ncols, (int64_t)d * ncols};
-  ZMat Ui{reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
-  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + 2 * libytes);
-  PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (per_pair_ms) {
-    PFX_CUDA_TRY(cudaEventCreate(&e0));
-    PFX_CUDA_TRY(cudaEventCreate(&e1));
-    PFX_CUDA_TRY(cudaEventRecord(e0, stream));
-  }
-  dim3 bg(1184, nsys);
-  PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full, shift_c,
-                                                                    theta_d, npairs, nsys, M, X));
-  PFX_CUDA_TRY(cudaGetLastError());
-  // real A in full mode: A + theta I is complex symmetric -> lower-triangle inverse
-  int sym_lower = (full && !a_complex && real_path) ? 1 : 0;
-  int* hsg = pinned_word();
-  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
-  int rc;
-  bool pivoted = pivot == 1;
-  if (!pivoted) {
-    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2);
-    if (rc) return rc;
-    if (pivot == 2) {
-      PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
-      if (int rc_ = sync_stream(stream)) return rc_;
-      if (*hsg & ST_PIVOT) {
-        // a column whose diagonal pivot partial pivoting would have exchanged: redo the
-        // factorisations with interchanges from the original matrices
-        note_pivot_fallback();
-        pivoted = true;
-        PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
-        PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full,
-                                                                          shift_c, theta_d, npairs, nsys, M, X));
-        PFX_CUDA_TRY(cudaGetLastError());
-      }
+    for (int j0 = J1 - nb >= J0 ? ((J1 - J0 - 1) / nb) * nb + J0 : J0; j0 >= J0; j0 -= nb) {
+      const int jb = std::min(nb, d - j0);
+      const int inner = J1 - j0 - jb;  // couplings inside the super-block
+      const int nc = sym_lower ? std::min(ncols, j0 + jb) : ncols;
+      if (inner > 0 &&
+          (rc = zgemm(s, nsys, jb, nc, inner, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0))))
+        return rc;
+      if ((rc = ztrmm_inplace(s, nsys, jb, nc, ui(j0), sub(X, j0, 0), false, true))) return rc;
     }
   }
-  if (pivoted) {
-    sym_lower = 0;
-    rc = lu_solve_piv(stream, nsys, d, M, X, ncols, ipiv, sing);
-    if (rc) return rc;
-  }
-  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
-  PFX_LAUNCH("dl_combine", stream,
-             dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
-                                                 out));
-  PFX_CUDA_TRY(cudaGetLastError());
-  PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  if (per_pair_ms) {
-    PFX_CUDA_TRY(cudaEventRecord(e1, stream));
-  }
-  if (int rc_ = sync_stream(stream)) return rc_;
-  if (per_pair_ms) {
-    float ms = 0.0f;
-    PFX_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
-    for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-  }
-  if (*hsg & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
   return PFX_OK;
 }
 

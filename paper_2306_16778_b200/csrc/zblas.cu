@@ -40,7 +40,7 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // overlap the other's DMMA stream (at 156 registers a single CTA per SM ran 15% slower).
 template <int TM, int TN, int NW, bool M3 = false, int GK = 16>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                                                        int accumulate, int b_lower) {
+                                                        int accumulate, int b_lower_off) {
   constexpr int NT = NW * 32;
   constexpr int WN = NW / 2;
   constexpr int FM = TM / 2 / 8, FN = TN / WN / 8;
@@ -64,10 +64,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) zgemm_kernel(int m, 
     }
 
   const int ktiles = (k + GK - 1) / GK;
-  // b_lower: B is lower triangular (B[r][c] = 0 for r < c), so this column tile's products
-  // start at row n0 of B; a tile entirely right of the triangle adds nothing
-  const int kt0 = b_lower ? n0 / GK : 0;
-  if (b_lower && accumulate && kt0 >= ktiles) return;
+  // b_lower_off >= 0: B is lower triangular with offset (B[r][c] = 0 for r + off < c), so
+  // this column tile's products start at row n0 - off of B; a tile entirely right of the
+  // triangle adds nothing
+  const int kt0 = b_lower_off >= 0 ? max(0, n0 - b_lower_off) / GK : 0;
+  if (b_lower_off >= 0 && accumulate && kt0 >= ktiles) return;
   auto load = [&](int buf, int kt) {
     const int k0 = kt * GK;
 #pragma unroll
@@ -101,8 +102,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) zgemm_kernel(int m, 
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
         double2 x = S.A[buf][wm * (TM / 2) + i * 8 + g][kk + t];
-        ar[i] = alpha * x.x;
-        ai[i] = alpha * x.y;
+        ar[i] = x.x;  // alpha is applied once, in the epilogue
+        ai[i] = x.y;
       }
 #pragma unroll
       for (int j = 0; j < FN; ++j) {
@@ -145,22 +146,42 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) zgemm_kernel(int m, 
           ci[i][j][h] = t3[M3 ? i : 0][M3 ? j : 0][h] - t1 - t2;
         }
   }
+  // epilogue C = C + alpha * acc: every C load of the thread is issued before the first add
+  // (one round trip to L2/HBM per thread instead of one per element)
+  // (two fragment rows per round keeps the loaded values within the register budget)
   double2* Cb = C.p + b * C.stride;
+  constexpr int EH = FM >= 2 ? 2 : 1;
 #pragma unroll
-  for (int i = 0; i < FM; ++i) {
-    const int row = m0 + wm * (TM / 2) + i * 8 + g;
-    if (row >= m) continue;
+  for (int i0 = 0; i0 < FM; i0 += EH) {
+    double2 cv[EH][FN][2];
 #pragma unroll
-    for (int j = 0; j < FN; ++j) {
+    for (int u = 0; u < EH; ++u) {
+      const int row = m0 + wm * (TM / 2) + (i0 + u) * 8 + g;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = n0 + wn * FN * 8 + j * 8 + 2 * t + h;
-        if (col < n) {
-          double2* p = Cb + (int64_t)row * C.ld + col;
-          double2 v = accumulate ? *p : make_double2(0.0, 0.0);
-          v.x += cr[i][j][h];
-          v.y += ci[i][j][h];
-          *p = v;
+      for (int j = 0; j < FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = n0 + wn * FN * 8 + j * 8 + 2 * t + h;
+          cv[u][j][h] = (accumulate && row < m && col < n) ? __ldcg(Cb + (int64_t)row * C.ld + col)
+                                                           : make_double2(0.0, 0.0);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < EH; ++u) {
+      const int i = i0 + u;
+      const int row = m0 + wm * (TM / 2) + i * 8 + g;
+      if (row >= m) continue;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = n0 + wn * FN * 8 + j * 8 + 2 * t + h;
+          if (col < n) {
+            double2 v = cv[u][j][h];
+            v.x = fma(alpha, cr[i][j][h], v.x);
+            v.y = fma(alpha, ci[i][j][h], v.y);
+            Cb[(int64_t)row * C.ld + col] = v;
+          }
         }
       }
     }
@@ -169,23 +190,27 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) zgemm_kernel(int m, 
 
 template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                        bool accumulate, bool b_lower) {
+                        bool accumulate, int b_lower_off) {
   const int smem = (int)sizeof(GemmSmem<TM, TN, KS>);
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgemm_kernel<TM, TN, NW, M3, KS>), smem)) return rc;
   dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch);
   // algorithmic flops: 8 per complex multiply-add actually required (b_lower: the products
   // with the zero triangle of B are not counted)
   double fl = 8.0 * (double)m * n * k * batch;
-  if (b_lower) fl = 8.0 * (double)m * batch * ((double)n * k - 0.5 * (double)std::min(n, k) * std::min(n, k));
+  if (b_lower_off >= 0) {
+    double nz = 0.0;  // nonzero rows of B summed over its columns
+    for (int c = 0; c < n; ++c) nz += (double)std::max(0, k - std::max(0, c - b_lower_off));
+    fl = 8.0 * (double)m * batch * nz;
+  }
   PFX_LAUNCH_F("zgemm", s, fl,
                (zgemm_kernel<TM, TN, NW, M3, KS><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C,
-                                                                       accumulate ? 1 : 0, b_lower ? 1 : 0)));
+                                                                       accumulate ? 1 : 0, b_lower_off)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
 
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate,
-          bool b_lower) {
+          int b_lower_off) {
   if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
   const int sms = device_sms();
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
@@ -193,13 +218,13 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
   static const bool ks32 = getenv("PFX_ZGEMM_KS16") == nullptr;
   if (tiles64 < 2 * sms) {
     if (k <= 64 && ks32)  // short K: two 32-deep stages instead of four 16-deep ones
-      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower)
-                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower);
-    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower)
-              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower);
+      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
+                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
+    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
+              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
   }
-  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower)
-            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower);
+  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
+            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
 }
 
 // ---------------------------------------------------------------------------

@@ -19,10 +19,11 @@ struct ZMat {
 
 // C[b] += alpha * A[b] (m x k) * B[b] (k x n) (accumulate = true) or C[b] = alpha * A B.
 // DMMA m8n8k4, 64x64x16 tiles.
-// b_lower: B (k x n) is lower triangular, B[r][c] = 0 for r < c; each column tile skips
-// the zero rows (the forward substitution of the identity right-hand side).
+// b_lower_off >= 0: B (k x n) is lower triangular with that row offset, B[r][c] = 0 for
+// r + b_lower_off < c; each column tile skips the zero rows (the forward substitution of the
+// identity right-hand side).  -1: B dense.
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-          bool accumulate = true, bool b_lower = false);
+          bool accumulate = true, int b_lower_off = -1);
 
 // No-pivot LU of the nb x nb diagonal block D (nb <= 64) in registers, in place.  Raises
 // ST_SINGULAR in *sing on an exactly zero pivot and ST_PIVOT where partial pivoting inside the
