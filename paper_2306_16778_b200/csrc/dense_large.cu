@@ -203,6 +203,91 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
   return PFX_OK;
 }
 
+int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* ipiv, int* sing);
+
+// pivot: 0 = interchange-free, 1 = partial pivoting (lu_solve_piv), 2 = checked: the
+// interchange-free LU verifies every column against partial pivoting and the call is redone
+// with lu_solve_piv when a check fails (pfx_set_pivot_mode).
+int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
+                    int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
+                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot) {
+  const int conj_sys = (!full && !real_path) ? 1 : 0;
+  const int nsys = npairs * (1 + conj_sys);
+  const size_t mbytes = (size_t)nsys * d * d * sizeof(double2);
+  const size_t xbytes = (size_t)nsys * d * ncols * sizeof(double2);
+  const int nblk = (d + DL_NB - 1) / DL_NB;
+  const size_t libytes = (size_t)nsys * nblk * DL_NB * DL_NB * sizeof(double2);
+  // Li / Ui (no-pivot path) and ipiv (pivoted path) share the same space
+  static_assert(sizeof(int) * DL_NB <= 2 * DL_NB * DL_NB * sizeof(double2), "ipiv fits the inverse tiles");
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256));
+  if (!ws) return fail(PFX_CUDA, "large dense workspace allocation failed");
+  int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
+  ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
+  ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
+  ZMat X{reinterpret_cast<double2*>(ws + mbytes), ncols, (int64_t)d * ncols};
+  ZMat Ui{reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
+  int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + 2 * libytes);
+  PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (per_pair_ms) {
+    PFX_CUDA_TRY(cudaEventCreate(&e0));
+    PFX_CUDA_TRY(cudaEventCreate(&e1));
+    PFX_CUDA_TRY(cudaEventRecord(e0, stream));
+  }
+  dim3 bg(1184, nsys);
+  PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full, shift_c,
+                                                                    theta_d, npairs, nsys, M, X));
+  PFX_CUDA_TRY(cudaGetLastError());
+  // real A in full mode: A + theta I is complex symmetric -> lower-triangle inverse
+  int sym_lower = (full && !a_complex && real_path) ? 1 : 0;
+  int* hsg = pinned_word();
+  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
+  int rc;
+  bool pivoted = pivot == 1;
+  if (!pivoted) {
+    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2);
+    if (rc) return rc;
+    if (pivot == 2) {
+      PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      if (int rc_ = sync_stream(stream)) return rc_;
+      if (*hsg & ST_PIVOT) {
+        // a column whose diagonal pivot partial pivoting would have exchanged: redo the
+        // factorisations with interchanges from the original matrices
+        note_pivot_fallback();
+        pivoted = true;
+        PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+        PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full,
+                                                                          shift_c, theta_d, npairs, nsys, M, X));
+        PFX_CUDA_TRY(cudaGetLastError());
+      }
+    }
+  }
+  if (pivoted) {
+    sym_lower = 0;
+    rc = lu_solve_piv(stream, nsys, d, M, X, ncols, ipiv, sing);
+    if (rc) return rc;
+  }
+  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
+  PFX_LAUNCH("dl_combine", stream,
+             dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
+                                                 out));
+  PFX_CUDA_TRY(cudaGetLastError());
+  PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (per_pair_ms) {
+    PFX_CUDA_TRY(cudaEventRecord(e1, stream));
+  }
+  if (int rc_ = sync_stream(stream)) return rc_;
+  if (per_pair_ms) {
+    float ms = 0.0f;
+    PFX_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (*hsg & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
+  return PFX_OK;
+}
+
 // LU with partial pivoting of nsys d x d matrices M (getrf semantics: per 64-column panel
 // the pivoting panel kernel, izamax ties to the first index), then X = U^{-1} L^{-1} P X.
 // Per panel: the interchanges on the columns left and right of the panel and on X,
