@@ -39,7 +39,7 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // Two CTAs per SM for the 64x64 tile (<= 128 registers): one CTA's epilogue and K-stage loads
 // overlap the other's DMMA stream (at 156 registers a single CTA per SM ran 15% slower).
 template <int TM, int TN, int NW, bool M3 = false, int GK = 16>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
+__global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 : 1) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                                                         int accumulate, int b_lower_off) {
   constexpr int NT = NW * 32;
   constexpr int WN = NW / 2;
@@ -223,6 +223,12 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
     return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
               : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
   }
+  // 64x64 tiles on 4 warps of 32x32 (248 registers, two CTAs per SM): per 4-deep K step a
+  // warp issues 8 fragment loads and 8 operand sums for 48 DMMAs (3M), where the 8-warp
+  // 32x16 layout issued 6 + 6 for 24; 5-8% faster on every C4 shape (tools/zgemm_probe.cu).
+  // PFX_ZGEMM_W8=1 keeps the 8-warp layout for A/B checks.
+  static const bool w8 = getenv("PFX_ZGEMM_W8") != nullptr;
+  if (m3 && !w8) return zgemm_launch<64, 64, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
   return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
             : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
 }
