@@ -59,18 +59,6 @@ __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const do
     X.p[k * X.stride + e] = make_double2(V[e], 0.0);
 }
 
-__global__ void bd_combine(ZMat X, int64_t n, int npairs, const double2* coef, double scale, double* out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int k = 0; k < npairs; ++k) {
-      cplx a = ld(&coef[k]);
-      cplx x = ld(&X.p[k * X.stride + e]);
-      double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
-      acc = k == 0 ? sk : acc + sk;
-    }
-    out[e] = scale == 1.0 ? acc : scale * acc;
-  }
-}
 
 // The factorisation + solves touch only the workspace, so the ~8 launches per 64-row
 // block step are captured once into a CUDA graph per (shape, workspace) and replayed:
@@ -122,8 +110,19 @@ __global__ void __launch_bounds__(256) bd_back_partial(ZMat M, ZMat X, int64_t j
   }
 }
 
+// Fused residue combine (engine.py:201,226-228): the last pair to finish a (block, column
+// chunk) of the back substitution sums all pairs' rows in ascending pair order into `out`, so
+// no separate pass re-reads the n/2 solutions.  The parameters live in device memory (the
+// back substitution is replayed from a captured graph; `out` and the residues change per call).
+struct BdCombine {
+  const double2* coef;
+  double scale;
+  double* out;
+  int* cnt;  // one counter per (block, column chunk), zero on entry, left zero
+};
+
 __global__ void __launch_bounds__(256) bd_back_finish(ZMat X, ZMat Ui, int64_t j0, int jb, int nr, int nq,
-                                                      const double2* P) {
+                                                      const double2* P, const BdCombine* cmb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* us = reinterpret_cast<double2*>(smem_raw);  // 64 x 65 (upper triangle of U11^{-1})
   double2* ts = us + 64 * 65;                          // 64 x ncl (this CTA's column chunk)
@@ -161,6 +160,33 @@ __global__ void __launch_bounds__(256) bd_back_finish(ZMat X, ZMat Ui, int64_t j
     if (k < jb) a0 = cfma(ld(&us[r * 65 + k]), ld(&ts[k * ncl + c]), a0);
     *X.at(b, j0 + r, cc + c) = make_double2(a0.re + a1.re, a0.im + a1.im);
   }
+  if (!cmb) return;
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  const int npairs = gridDim.x;
+  int* cnt = cmb->cnt + (j0 / 64) * gridDim.y + blockIdx.y;
+  if (tid == 0) {
+    const int prev = atomicAdd(cnt, 1);
+    s_last = prev == npairs - 1;
+    if (s_last) *cnt = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double2* coef = cmb->coef;
+  const double sc = cmb->scale;
+  for (int e = tid; e < jb * ncl; e += 256) {
+    const int r = e / ncl, c = e - r * ncl;
+    double acc = 0.0;
+    for (int k = 0; k < npairs; ++k) {
+      const cplx a = ld(&coef[k]);
+      const double2 x = __ldcg(X.at(k, j0 + r, cc + c));
+      const double sk = 2.0 * fma(a.re, x.x, -a.im * x.y);
+      acc = k == 0 ? sk : acc + sk;
+    }
+    cmb->out[(j0 + r) * (int64_t)nr + cc + c] = sc == 1.0 ? acc : sc * acc;
+  }
 }
 
 // Three streams inside one captured graph: the critical chain (diagonal LU -> inverses ->
@@ -193,7 +219,7 @@ static int bd_streams(BdStreams& S) {
 }
 
 static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui, double2* P, int64_t N, int kb,
-                           int nr, int npairs, int* sing) {
+                           int nr, int npairs, int* sing, const BdCombine* cmb) {
   const int nb = BD_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -301,7 +327,7 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
     if (int rc = raise_smem_limit(reinterpret_cast<const void*>(bd_back_finish), fsm)) return rc;
     dim3 gf((unsigned)npairs, (unsigned)ceil_div(nr, 64));
     PFX_LAUNCH_F("bd_back_finish", stream, 4.0 * jb * jb * (double)nr * npairs,
-                 bd_back_finish<<<gf, 256, fsm, stream>>>(X, blk(Ui, j0), j0, jb, nr, nq, P));
+                 bd_back_finish<<<gf, 256, fsm, stream>>>(X, blk(Ui, j0), j0, jb, nr, nq, P, cmb));
     PFX_CUDA_TRY(cudaGetLastError());
   }
   return PFX_OK;
@@ -332,7 +358,8 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   const size_t libytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
   const size_t uibytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
   const size_t pbytes = (size_t)npairs * ceil_div(kb, BK_C) * nb * nrhs * sizeof(double2);
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + libytes + uibytes + pbytes + 256));
+  const size_t cbytes = (size_t)nblk * ceil_div(nrhs, 64) * sizeof(int);
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64 + cbytes));
   if (!ws) return fail(PFX_CUDA, "banded workspace allocation failed (needs " + std::to_string((mbytes + xbytes) >> 20) + " MiB)");
   ZMat M{reinterpret_cast<double2*>(ws) + kb + nb, Wd - 1, (int64_t)N * Wd};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, N * nrhs};
@@ -341,6 +368,16 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   double2* P = reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes + uibytes);
   int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + libytes + uibytes + pbytes);
   PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+  // combine parameters (device copy read by the graph-captured back substitution) + counters
+  BdCombine* cmb_d = reinterpret_cast<BdCombine*>(ws + mbytes + xbytes + libytes + uibytes + pbytes + 256);
+  int* cnt = reinterpret_cast<int*>(ws + mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64);
+  {
+    static_assert(sizeof(BdCombine) <= 64, "combine parameters fit their slot");
+    const BdCombine h{coef_d, shift_c == 0.0 ? 1.0 : exp(shift_c), out, cnt};
+    // pageable source: the runtime stages it before returning, so a stack value is safe
+    PFX_CUDA_TRY(cudaMemcpyAsync(cmb_d, &h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    PFX_CUDA_TRY(cudaMemsetAsync(cnt, 0, cbytes, stream));
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (per_pair_ms) {
     PFX_CUDA_TRY(cudaEventCreate(&e0));
@@ -392,7 +429,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   }
   if (prof_on()) {
     // profiling wants per-kernel events: run the launches directly
-    if (int rc = bd_factor_solve(stream, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing)) return rc;
+    if (int rc = bd_factor_solve(stream, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing, cmb_d)) return rc;
   } else {
     const int gdev = current_device();
     if (gdev < 0 || gdev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
@@ -410,7 +447,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
       PFX_CUDA_TRY(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
       cudaGraph_t graph;
       PFX_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int rc = bd_factor_solve(cs, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing);
+      int rc = bd_factor_solve(cs, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing, cmb_d);
       cudaError_t ce = cudaStreamEndCapture(cs, &graph);
       if (rc) return rc;
       if (ce != cudaSuccess) return fail(PFX_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -426,9 +463,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     }
     PFX_CUDA_TRY(cudaGraphLaunch(G.exec, stream));
   }
-  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
-  PFX_LAUNCH("bd_combine", stream, bd_combine<<<1184, 256, 0, stream>>>(X, N * nrhs, npairs, coef_d, scale, out));
-  PFX_CUDA_TRY(cudaGetLastError());
+  // (the residue combine ran fused into the back substitution: bd_back_finish)
   int* hsg = pinned_word();
   if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
   PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));

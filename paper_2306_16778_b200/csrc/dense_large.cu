@@ -97,8 +97,10 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
 // check_pivots: every column is checked against partial pivoting (zgetrf_diag inside the
 // diagonal block, the L21 product below it); a column whose diagonal pivot partial pivoting
 // would have exchanged raises ST_PIVOT in *sing.
+// cmb (optional): the residue combine is fused into the last product of each block row of the
+// backward substitution (ZCombine; cmb->cnt holds nblk x cmb->nstrips zeroed counters).
 int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
-                   bool identity_rhs, bool sym_lower, bool check_pivots) {
+                   bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb) {
   const int nb = DL_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -197,7 +199,15 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
       if (inner > 0 &&
           (rc = zgemm(s, nsys, jb, nc, inner, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0))))
         return rc;
-      if ((rc = ztrmm_inplace(s, nsys, jb, nc, ui(j0), sub(X, j0, 0), false, true))) return rc;
+      ZCombine cm;
+      if (cmb) {
+        cm = *cmb;
+        cm.row0 = j0;
+        cm.cnt = cmb->cnt + (int64_t)(j0 / nb) * cmb->nstrips;
+      }
+      if ((rc = ztrmm_inplace(s, nsys, jb, nc, ui(j0), sub(X, j0, 0), false, true, ZMat{nullptr, 0, 0}, nullptr,
+                              cmb ? &cm : nullptr)))
+        return rc;
     }
   }
   return PFX_OK;
@@ -219,9 +229,12 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   const size_t libytes = (size_t)nsys * nblk * DL_NB * DL_NB * sizeof(double2);
   // Li / Ui (no-pivot path) and ipiv (pivoted path) share the same space
   static_assert(sizeof(int) * DL_NB <= 2 * DL_NB * DL_NB * sizeof(double2), "ipiv fits the inverse tiles");
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256));
+  const int nstrips = (ncols + 31) / 32;
+  const size_t cbytes = (size_t)nblk * nstrips * sizeof(int);
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256 + cbytes));
   if (!ws) return fail(PFX_CUDA, "large dense workspace allocation failed");
   int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
+  int* cnt = reinterpret_cast<int*>(ws + mbytes + xbytes + 2 * libytes + 256);
   ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
   ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), ncols, (int64_t)d * ncols};
@@ -244,8 +257,21 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
   int rc;
   bool pivoted = pivot == 1;
+  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
+  // the combine runs fused into the backward substitution (no separate pass over the n/2
+  // solutions); the pivoted path below keeps the standalone combine kernel
+  ZCombine cm;
+  cm.mode = full ? (real_path ? 2 : 1) : (real_path ? 3 : 4);
+  cm.npairs = npairs;
+  cm.coef = coef_d;
+  cm.scale = scale;
+  cm.out = out;
+  cm.ldo = ncols;
+  cm.cnt = cnt;
+  cm.nstrips = nstrips;
   if (!pivoted) {
-    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2);
+    PFX_CUDA_TRY(cudaMemsetAsync(cnt, 0, cbytes, stream));
+    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2, &cm);
     if (rc) return rc;
     if (pivot == 2) {
       PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -267,11 +293,12 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     rc = lu_solve_piv(stream, nsys, d, M, X, ncols, ipiv, sing);
     if (rc) return rc;
   }
-  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
-  PFX_LAUNCH("dl_combine", stream,
-             dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
-                                                 out));
-  PFX_CUDA_TRY(cudaGetLastError());
+  if (pivoted) {
+    PFX_LAUNCH("dl_combine", stream,
+               dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
+                                                   out));
+    PFX_CUDA_TRY(cudaGetLastError());
+  }
   PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (per_pair_ms) {
     PFX_CUDA_TRY(cudaEventRecord(e1, stream));

@@ -804,8 +804,73 @@ int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui) {
 constexpr int TM_T = 64;
 constexpr int TM_W = 32;
 
+// load bypassing L1 (values other CTAs wrote during this kernel)
+__device__ __forceinline__ cplx ldcg(const double2* p) {
+  const double2 v = __ldcg(p);
+  return cplx{v.x, v.y};
+}
+
+// The fused combine epilogue of ztrmm_kernel (see ZCombine): called by the last CTA of a strip
+// group; B is the X slab (batch stride, rows from block row r0), cols [c0, c1) of the group.
+__device__ void combine_block(const ZCombine& cm, ZMat X, int nb, int c0, int c1) {
+  const int tid = threadIdx.x;
+  const int64_t r0 = cm.row0;
+  const double sc = cm.scale;
+  const int w = c1 - c0;
+  // X rows are relative to the block row (X.at(k, r, c) = element (r0 + r, c)); the mirrored
+  // reads X_k[c, r0 + r] are rows c of the full matrix: offset -r0
+  for (int e = tid; e < nb * w; e += 256) {
+    const int r = e / w, c = c0 + (e - (e / w) * w);
+    const int64_t gr = r0 + r;  // global row of this element
+    if (cm.mode == 1) {
+      cplx acc = mk(0, 0);
+      for (int k = 0; k < cm.npairs; ++k) {
+        const cplx a = ld(&cm.coef[k]);
+        const cplx x = ldcg(X.at(k, r, c));
+        const cplx y = ldcg(X.at(k, c - r0, gr));  // X_k[c, gr]
+        const cplx sk = cadd(cmul(a, x), cconj(cmul(a, y)));
+        acc = k == 0 ? sk : cadd(acc, sk);
+      }
+      if (sc != 1.0) acc = cscale(acc, sc);
+      reinterpret_cast<double2*>(cm.out)[gr * cm.ldo + c] = make_double2(acc.re, acc.im);
+      if (c != gr) reinterpret_cast<double2*>(cm.out)[(int64_t)c * cm.ldo + gr] = make_double2(acc.re, -acc.im);
+    } else if (cm.mode == 2) {
+      if (c > gr) continue;  // lower triangle of the block row (the diagonal block's upper half mirrors)
+      double acc = 0.0;
+      for (int k = 0; k < cm.npairs; ++k) {
+        const cplx a = ld(&cm.coef[k]);
+        const cplx x = ldcg(X.at(k, r, c));
+        const double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
+        acc = k == 0 ? sk : acc + sk;
+      }
+      if (sc != 1.0) acc *= sc;
+      cm.out[gr * cm.ldo + c] = acc;
+      if (c != gr) cm.out[(int64_t)c * cm.ldo + gr] = acc;
+    } else if (cm.mode == 3) {
+      double acc = 0.0;
+      for (int k = 0; k < cm.npairs; ++k) {
+        const cplx a = ld(&cm.coef[k]);
+        const cplx x = ldcg(X.at(k, r, c));
+        const double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
+        acc = k == 0 ? sk : acc + sk;
+      }
+      cm.out[gr * cm.ldo + c] = sc == 1.0 ? acc : sc * acc;
+    } else {
+      cplx acc = mk(0, 0);
+      for (int k = 0; k < cm.npairs; ++k) {
+        const cplx a = ld(&cm.coef[k]);
+        const cplx sk = cadd(cmul(a, ldcg(X.at(k, r, c))), cmul(cconj(a), ldcg(X.at(cm.npairs + k, r, c))));
+        acc = k == 0 ? sk : cadd(acc, sk);
+      }
+      if (sc != 1.0) acc = cscale(acc, sc);
+      reinterpret_cast<double2*>(cm.out)[gr * cm.ldo + c] = make_double2(acc.re, acc.im);
+    }
+  }
+}
+
 template <bool RIGHT>
-__global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper, ZMat Dg, int* flag) {
+__global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper, ZMat Dg, int* flag,
+                                                    ZCombine cm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // row strides (16-byte words) for conflict-free DMMA fragment loads: an A-operand array
   // (read at rows g x columns tt of a quarter-warp) 4 mod 8, a B-operand array (rows tt x
@@ -896,10 +961,41 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
         }
       }
     }
+  if (RIGHT || cm.mode == 0) return;
+  // ---- fused residue combine (left products of the backward substitution only)
+  const int64_t r0 = cm.row0;
+  const int c0 = t0, c1 = min(n, t0 + TM_W);
+  // full modes: strips meeting the diagonal block's columns (action modes: columns are RHS)
+  const bool diag = cm.mode <= 2 && c0 < r0 + nb && c1 > r0;
+  if (cm.mode == 1 && !diag && c1 <= r0) return;       // left of the diagonal: a later block row
+  if (cm.mode == 2 && !diag && c0 >= r0 + nb) return;  // right of the diagonal: an earlier block row
+  // diagonal strips form one group (their mirrored reads cross each other's rows)
+  const int g0 = diag ? (int)(r0 / TM_W) : blockIdx.x;
+  const int g1 = diag ? (int)((r0 + nb - 1) / TM_W) : blockIdx.x;
+  const int expect = (g1 - g0 + 1) * (int)gridDim.y;
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(&cm.cnt[g0], 1);
+    s_last = prev == expect - 1;
+    if (s_last) cm.cnt[g0] = 0;  // ready for the next call
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  ZMat X = B;
+  X.p = B.p;  // batch stride = B.stride, rows relative to the block row
+  if (diag)
+    combine_block(cm, X, nb, g0 * TM_W, min(n, (g1 + 1) * TM_W));
+  else
+    combine_block(cm, X, nb, c0, c1);
 }
 
 int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper, ZMat Dg,
-                  int* pivot_flag) {
+                  int* pivot_flag, const ZCombine* cmb) {
+  ZCombine cm;
+  if (cmb && !right) cm = *cmb;
   if (n <= 0) return PFX_OK;
   if (nb > TM_T) return fail(PFX_BADARG, "ztrmm_inplace: nb > 64");
   const int smem = (TM_T * (TM_T + 4) + TM_T * (TM_T + 4)) * (int)sizeof(double2);
@@ -909,10 +1005,10 @@ int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, b
   const double fl = 4.0 * nb * nb * (double)n * batch;  // triangular: half the square product
   if (right)
     PFX_LAUNCH_F("ztrmm", s, fl,
-                 ztrmm_kernel<true><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, pivot_flag));
+                 ztrmm_kernel<true><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, pivot_flag, cm));
   else
     PFX_LAUNCH_F("ztrmm", s, fl,
-                 ztrmm_kernel<false><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, nullptr));
+                 ztrmm_kernel<false><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, nullptr, cm));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }

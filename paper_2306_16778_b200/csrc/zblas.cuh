@@ -33,11 +33,34 @@ int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing);
 int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui);
 // In place: B = Tinv * B (left, B nb x n) or B = B * Tinv (right, B n x nb), Tinv nb x nb
 // (nb <= 64) triangular (upper or lower), on DMMA; one CTA per 32-wide strip of B.
+// Fused residue combine (K5/K6 of the dense path, engine.py:199-213,225-228) as the epilogue of
+// the last backward-substitution product of each block row: once all systems' CTAs of a
+// strip have written their final rows X_k[r0 .. r0+nb, strip], the last one to arrive (a
+// per-(block row, strip) counter) sums the systems in ascending k and writes `out`.
+//   mode 1  complex full:   out = sum_k a_k X_k + (a_k X_k)^H  (Hermitian; the block row's
+//           entries right of its diagonal and their mirror images, X_k[strip, block] rows
+//           being final already: every (i, j) is written by block row min(i, j))
+//   mode 2  real full, X_k complex symmetric stored as its lower triangle:
+//           out = sum_k 2 Re(a_k X_k)  (entries left of the diagonal and their mirrors)
+//   mode 3  real action:    out = sum_k 2 Re(a_k Y_k)
+//   mode 4  complex action: out = sum_k a_k Y_k + conj(a_k) Yc_k  (Yc_k = system npairs + k)
+struct ZCombine {
+  int mode = 0;          // 0: no combine
+  int npairs = 0;
+  const double2* coef = nullptr;
+  double scale = 1.0;    // e^c of the shift method
+  double* out = nullptr; // d x ncols, real (modes 2, 3) or complex (1, 4), row-major
+  int64_t ldo = 0;       // row stride of out (elements)
+  int* cnt = nullptr;    // counters, zero on entry, left zero
+  int64_t row0 = 0;      // first row of the block row (= its column for the diagonal)
+  int nstrips = 0;       // counters per block row
+};
+
 // pivot_flag (right products only): B = L21 = A21 U11^{-1} of a no-pivot LU step whose
 // diagonal block (factored in place) is Dg; every entry is checked against partial pivoting
 // (|l u_cc|_1 > |u_cc|_1 means row interchanges were due) and ST_PIVOT is or-ed into *pivot_flag.
 int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper,
-                  ZMat Dg = ZMat{nullptr, 0, 0}, int* pivot_flag = nullptr);
+                  ZMat Dg = ZMat{nullptr, 0, 0}, int* pivot_flag = nullptr, const ZCombine* cmb = nullptr);
 
 // Unblocked LU of the m x nb panel at P (in place).  ipiv (optional, batch x nb, 0-based
 // rows relative to the panel) -> partial pivoting with row swaps inside the panel only.
