@@ -72,9 +72,15 @@ ALG_BYTES = {
     "C4": 5.37e8,
     "C5": 8.0 * 2 * 513 * 262144 * 16,
 }
-# dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, from the
-# round's `ncu --set full` capture (profiles/r01_c2_tri_ls_ncu_details.csv); None = not captured
-DOM_TRAFFIC = {"C2": 1.288e9, "C3": 4.566e10}
+# Per-launch hardware counters of the dominant kernel from the round's ncu pass over the same
+# bench command (tools/ncu_summary.py -> profiles/ncu_summary.json): mean dram__bytes_read.sum +
+# dram__bytes_write.sum per launch, duration-weighted DMMA / FP64 pipe utilisation.
+def load_ncu_summary():
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
 DOMINANT = {"C1": "dense_batched_kernel", "C2": "tri_sweep", "C3": "dense_batched_kernel", "C4": "zgemm", "C5": "zgemm"}
 
 
@@ -602,6 +608,7 @@ def main():
 
     launches = sum(v[0] for v in kern.values())
     dom = DOMINANT[args.workload]
+    ncu = load_ncu_summary().get(args.workload, {})
     # profile names carry a phase / variant tag ("zgemm@lu", "dense_batched_kernel@nb16x2"):
     # the dominant kernel is every launch of that kernel
     dom_cnt, dom_ms, dom_fl = 0, 0.0, 0.0
@@ -621,7 +628,8 @@ def main():
         achieved = flops_per_launch / t_launch / 1e12
         roofline = {"bound": "tensor", "pipe": "fp64 (DMMA m8n8k4 peak, measured)", "achieved": achieved,
                     "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                    "frac": achieved / peaks["fp64_tflops"], "traffic": DOM_TRAFFIC.get(args.workload), "kernel": dom,
+                    "frac": achieved / peaks["fp64_tflops"], "traffic": ncu.get("dram_bytes_per_launch"),
+                    "kernel": dom,
                     "kernel_ms": dom_ms / dom_cnt, "peak_source": peaks["fp64_source"],
                     "share_of_step": (dom_ms / prof_steps) / ms_step,
                     "path_frac": ALG_FLOPS[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e12
@@ -631,8 +639,17 @@ def main():
         # whole step and the dominant kernel's measured DRAM traffic (ncu) over its live time
         roofline["hbm_peak_gbs"] = peaks["hbm_gbs"]
         roofline["hbm_frac_alg"] = roofline["hbm_gbs_alg"] / peaks["hbm_gbs"]
-        tr = DOM_TRAFFIC.get(args.workload)
+        tr = ncu.get("dram_bytes_per_launch")
         roofline["dram_gbs"] = tr / t_launch / 1e9 if tr else None
+        # the tensor pipe's own utilisation (ncu) beside the algorithmic fraction: the 3M complex
+        # product does 6 real flops per complex multiply-add where the algorithmic count is 8
+        roofline["dmma_pipe_ncu"] = ncu.get("dmma_pipe_pct", None) and ncu["dmma_pipe_pct"] / 100.0
+        roofline["fp64_pipe_ncu"] = ncu.get("fp64_pipe_pct", None) and ncu["fp64_pipe_pct"] / 100.0
+        roofline["ncu_source"] = ncu.get("source")
+        if args.workload == "C5":
+            roofline["note"] = ("C5 runs its block steps as a graph on 5 concurrent streams: the per-launch "
+                                "durations overlap, so share_of_step counts overlapping time and path_frac is "
+                                "the step-level figure")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

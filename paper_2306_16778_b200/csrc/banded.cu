@@ -69,11 +69,51 @@ __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const do
 // ascending order (deterministic), subtracts, and applies the stored U11^{-1}.
 constexpr int BK_C = 32;
 
+// Fused residue combine (engine.py:201,226-228): out[rows of block j] = e^c sum_k 2 Re(a_k X_k)
+// in ascending pair order.  It rides along in the back substitution: the partial-product
+// launch of block j - 1 carries one extra CTA that combines block j, whose rows every pair
+// finished in the previous launch (L2-hot), so the combine adds no step to the serial chain
+// and no pass re-reads the n/2 solutions; block 0 is combined by one last small launch.
+// The parameters live in device memory (the back substitution is replayed from a captured
+// graph; `out` and the residues change per call).
+struct BdCombine {
+  const double2* coef;
+  double scale;
+  double* out;
+};
+
+__device__ void bd_combine_rows(const ZMat& X, int64_t j0, int jb, int nr, int npairs, const BdCombine* cmb) {
+  const double2* coef = cmb->coef;
+  const double sc = cmb->scale;
+  for (int e = threadIdx.x; e < jb * nr; e += blockDim.x) {
+    const int64_t i = (j0 + e / nr) * nr + e % nr;  // element of the N x nr block
+    double acc = 0.0;
+    for (int k = 0; k < npairs; ++k) {
+      const cplx a = ld(&coef[k]);
+      const double2 x = X.p[k * X.stride + i];
+      const double sk = 2.0 * fma(a.re, x.x, -a.im * x.y);
+      acc = k == 0 ? sk : acc + sk;
+    }
+    cmb->out[i] = sc == 1.0 ? acc : sc * acc;
+  }
+}
+
+__global__ void bd_combine_block(ZMat X, int64_t j0, int jb, int nr, int npairs, const BdCombine* cmb) {
+  bd_combine_rows(X, j0, jb, nr, npairs, cmb);
+}
+
+// grid (nq + 1, npairs): CTA x = nq (pair 0 only) is the ride-along combine of the block
+// below (rows [cj0, cj0 + cjb), final for every pair).
 __global__ void __launch_bounds__(256) bd_back_partial(ZMat M, ZMat X, int64_t j0, int jb, int rest, int nr,
-                                                       double2* P) {
+                                                       double2* P, int nq, const BdCombine* cmb, int64_t cj0,
+                                                       int cjb) {
   __shared__ __align__(16) double2 us[64][BK_C + 1];
   __shared__ __align__(16) double2 xs[BK_C][9];
-  const int q = blockIdx.x, b = blockIdx.y, nq = gridDim.x;
+  const int q = blockIdx.x, b = blockIdx.y;
+  if (q == nq) {
+    if (b == 0) bd_combine_rows(X, cj0, cjb, nr, gridDim.y, cmb);
+    return;
+  }
   const int tid = threadIdx.x;
   const int t0 = q * BK_C, tn = min(BK_C, rest - t0);
   const int64_t col0 = j0 + jb + t0;
@@ -110,19 +150,8 @@ __global__ void __launch_bounds__(256) bd_back_partial(ZMat M, ZMat X, int64_t j
   }
 }
 
-// Fused residue combine (engine.py:201,226-228): the last pair to finish a (block, column
-// chunk) of the back substitution sums all pairs' rows in ascending pair order into `out`, so
-// no separate pass re-reads the n/2 solutions.  The parameters live in device memory (the
-// back substitution is replayed from a captured graph; `out` and the residues change per call).
-struct BdCombine {
-  const double2* coef;
-  double scale;
-  double* out;
-  int* cnt;  // one counter per (block, column chunk), zero on entry, left zero
-};
-
 __global__ void __launch_bounds__(256) bd_back_finish(ZMat X, ZMat Ui, int64_t j0, int jb, int nr, int nq,
-                                                      const double2* P, const BdCombine* cmb) {
+                                                      const double2* P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* us = reinterpret_cast<double2*>(smem_raw);  // 64 x 65 (upper triangle of U11^{-1})
   double2* ts = us + 64 * 65;                          // 64 x ncl (this CTA's column chunk)
@@ -159,33 +188,6 @@ __global__ void __launch_bounds__(256) bd_back_finish(ZMat X, ZMat Ui, int64_t j
     }
     if (k < jb) a0 = cfma(ld(&us[r * 65 + k]), ld(&ts[k * ncl + c]), a0);
     *X.at(b, j0 + r, cc + c) = make_double2(a0.re + a1.re, a0.im + a1.im);
-  }
-  if (!cmb) return;
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  const int npairs = gridDim.x;
-  int* cnt = cmb->cnt + (j0 / 64) * gridDim.y + blockIdx.y;
-  if (tid == 0) {
-    const int prev = atomicAdd(cnt, 1);
-    s_last = prev == npairs - 1;
-    if (s_last) *cnt = 0;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const double2* coef = cmb->coef;
-  const double sc = cmb->scale;
-  for (int e = tid; e < jb * ncl; e += 256) {
-    const int r = e / ncl, c = e - r * ncl;
-    double acc = 0.0;
-    for (int k = 0; k < npairs; ++k) {
-      const cplx a = ld(&coef[k]);
-      const double2 x = __ldcg(X.at(k, j0 + r, cc + c));
-      const double sk = 2.0 * fma(a.re, x.x, -a.im * x.y);
-      acc = k == 0 ? sk : acc + sk;
-    }
-    cmb->out[(j0 + r) * (int64_t)nr + cc + c] = sc == 1.0 ? acc : sc * acc;
   }
 }
 
@@ -318,16 +320,25 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
     const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);
     const int nq = (int)ceil_div(rest, BK_C);
     if (nq > 0) {
-      dim3 g((unsigned)nq, (unsigned)npairs);
+      // + one CTA combining block pb + 1 (finished by the previous launch)
+      dim3 g((unsigned)nq + 1, (unsigned)npairs);
+      const int64_t cj0 = j0 + nb;
+      const int cjb = (int)std::min<int64_t>(nb, N - cj0);
       PFX_LAUNCH_F("bd_back_partial", stream, 8.0 * jb * rest * (double)nr * npairs,
-                   bd_back_partial<<<g, 256, 0, stream>>>(M, X, j0, jb, rest, nr, P));
+                   bd_back_partial<<<g, 256, 0, stream>>>(M, X, j0, jb, rest, nr, P, nq, cmb, cj0, cjb));
       PFX_CUDA_TRY(cudaGetLastError());
     }
     const int fsm = (64 * 65 + 64 * std::min(nr, 64)) * (int)sizeof(double2);
     if (int rc = raise_smem_limit(reinterpret_cast<const void*>(bd_back_finish), fsm)) return rc;
     dim3 gf((unsigned)npairs, (unsigned)ceil_div(nr, 64));
     PFX_LAUNCH_F("bd_back_finish", stream, 4.0 * jb * jb * (double)nr * npairs,
-                 bd_back_finish<<<gf, 256, fsm, stream>>>(X, blk(Ui, j0), j0, jb, nr, nq, P, cmb));
+                 bd_back_finish<<<gf, 256, fsm, stream>>>(X, blk(Ui, j0), j0, jb, nr, nq, P));
+    PFX_CUDA_TRY(cudaGetLastError());
+  }
+  if (!(skip & 1)) {
+    // block 0 (the last one the back substitution finishes)
+    PFX_LAUNCH("bd_combine_block", stream,
+               bd_combine_block<<<1, 256, 0, stream>>>(X, 0, (int)std::min<int64_t>(nb, N), nr, npairs, cmb));
     PFX_CUDA_TRY(cudaGetLastError());
   }
   return PFX_OK;
@@ -358,8 +369,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   const size_t libytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
   const size_t uibytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
   const size_t pbytes = (size_t)npairs * ceil_div(kb, BK_C) * nb * nrhs * sizeof(double2);
-  const size_t cbytes = (size_t)nblk * ceil_div(nrhs, 64) * sizeof(int);
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64 + cbytes));
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64));
   if (!ws) return fail(PFX_CUDA, "banded workspace allocation failed (needs " + std::to_string((mbytes + xbytes) >> 20) + " MiB)");
   ZMat M{reinterpret_cast<double2*>(ws) + kb + nb, Wd - 1, (int64_t)N * Wd};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, N * nrhs};
@@ -368,15 +378,13 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   double2* P = reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes + uibytes);
   int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + libytes + uibytes + pbytes);
   PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
-  // combine parameters (device copy read by the graph-captured back substitution) + counters
+  // combine parameters (device copy read by the graph-captured back substitution)
   BdCombine* cmb_d = reinterpret_cast<BdCombine*>(ws + mbytes + xbytes + libytes + uibytes + pbytes + 256);
-  int* cnt = reinterpret_cast<int*>(ws + mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64);
   {
     static_assert(sizeof(BdCombine) <= 64, "combine parameters fit their slot");
-    const BdCombine h{coef_d, shift_c == 0.0 ? 1.0 : exp(shift_c), out, cnt};
+    const BdCombine h{coef_d, shift_c == 0.0 ? 1.0 : exp(shift_c), out};
     // pageable source: the runtime stages it before returning, so a stack value is safe
     PFX_CUDA_TRY(cudaMemcpyAsync(cmb_d, &h, sizeof(h), cudaMemcpyHostToDevice, stream));
-    PFX_CUDA_TRY(cudaMemsetAsync(cnt, 0, cbytes, stream));
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (per_pair_ms) {

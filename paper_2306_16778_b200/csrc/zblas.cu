@@ -812,6 +812,58 @@ __device__ __forceinline__ cplx ldcg(const double2* p) {
 
 // The fused combine epilogue of ztrmm_kernel (see ZCombine): called by the last CTA of a strip
 // group; B is the X slab (batch stride, rows from block row r0), cols [c0, c1) of the group.
+// Mode 1 (complex full, Hermitian): the mirrored reads X_k[c, r0 + r] and the mirrored writes
+// out[c, r0 + r] go through shared memory (sm: >= 64 x 65 double2) so that every global access
+// runs along a row; each thread keeps its elements' sums in registers across the pairs.
+__device__ void combine_hermitian(const ZCombine& cm, ZMat X, int nb, int c0, int c1, double2* sm) {
+  constexpr int MAXE = (64 * 64) / 256;
+  const int tid = threadIdx.x;
+  const int64_t r0 = cm.row0;
+  const int w = c1 - c0;
+  const int SP = nb + 1;  // sm row stride: sm[c * SP + r]
+  cplx acc[MAXE];
+#pragma unroll
+  for (int i = 0; i < MAXE; ++i) acc[i] = mk(0, 0);
+  for (int k = 0; k < cm.npairs; ++k) {
+    __syncthreads();
+    for (int e = tid; e < w * nb; e += 256) {  // X_k[c0 + cc, r0 + r], coalesced along r
+      const int cc = e / nb, r = e - (e / nb) * nb;
+      sm[cc * SP + r] = __ldcg(X.at(k, c0 + cc - r0, r0 + r));
+    }
+    __syncthreads();
+    const cplx a = ld(&cm.coef[k]);
+#pragma unroll
+    for (int i = 0; i < MAXE; ++i) {
+      const int e = tid + 256 * i;
+      if (e < nb * w) {
+        const int r = e / w, c = e - (e / w) * w;  // coalesced along c
+        const cplx x = ldcg(X.at(k, r, c0 + c));
+        const cplx y = ld(&sm[c * SP + r]);
+        const cplx sk = cadd(cmul(a, x), cconj(cmul(a, y)));
+        acc[i] = k == 0 ? sk : cadd(acc[i], sk);
+      }
+    }
+  }
+  __syncthreads();
+  double2* out = reinterpret_cast<double2*>(cm.out);
+#pragma unroll
+  for (int i = 0; i < MAXE; ++i) {
+    const int e = tid + 256 * i;
+    if (e < nb * w) {
+      const int r = e / w, c = e - (e / w) * w;
+      cplx v = acc[i];
+      if (cm.scale != 1.0) v = cscale(v, cm.scale);
+      out[(r0 + r) * cm.ldo + c0 + c] = make_double2(v.re, v.im);
+      sm[c * SP + r] = make_double2(v.re, -v.im);  // mirror image, written back row-wise below
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < w * nb; e += 256) {
+    const int cc = e / nb, r = e - (e / nb) * nb;
+    if (c0 + cc != r0 + r) out[(int64_t)(c0 + cc) * cm.ldo + r0 + r] = sm[cc * SP + r];
+  }
+}
+
 __device__ void combine_block(const ZCombine& cm, ZMat X, int nb, int c0, int c1) {
   const int tid = threadIdx.x;
   const int64_t r0 = cm.row0;
@@ -984,12 +1036,12 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  ZMat X = B;
-  X.p = B.p;  // batch stride = B.stride, rows relative to the block row
-  if (diag)
-    combine_block(cm, X, nb, g0 * TM_W, min(n, (g1 + 1) * TM_W));
+  // batch stride = B.stride, rows relative to the block row; the product's shared memory is idle
+  const int gc0 = diag ? g0 * TM_W : c0, gc1 = diag ? min(n, (g1 + 1) * TM_W) : c1;
+  if (cm.mode == 1)
+    combine_hermitian(cm, B, nb, gc0, gc1, reinterpret_cast<double2*>(smem_raw));
   else
-    combine_block(cm, X, nb, c0, c1);
+    combine_block(cm, B, nb, gc0, gc1);
 }
 
 int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper, ZMat Dg,
