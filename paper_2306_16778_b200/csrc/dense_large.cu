@@ -97,8 +97,9 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
 // check_pivots: every column is checked against partial pivoting (zgetrf_diag inside the
 // diagonal block, the L21 product below it); a column whose diagonal pivot partial pivoting
 // would have exchanged raises ST_PIVOT in *sing.
-// cmb (optional): the residue combine is fused into the last product of each block row of the
-// backward substitution (ZCombine; cmb->cnt holds nblk x cmb->nstrips zeroed counters).
+// cmb (optional): the residue combine rides along the backward substitution (ZCombine): the
+// entries block row p decides are summed by an extra slice of CTAs in the GEMM launch that
+// follows its last product, and the last block row's by one final combine launch.
 int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
                    bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb) {
   const int nb = DL_NB;
@@ -184,32 +185,41 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
   // backward: X_p -= U[p, p+1:] X[p+1:]; X_p = U_pp^{-1} X_p
   ProfTag tag_bwd("bwd");
   const int nsb = (d + SB - 1) / SB;
+  ZCombine pend;  // the combine of the block row finished last, carried by the next GEMM
+  auto ride = [&]() -> const ZCombine* { return pend.mode ? &pend : nullptr; };
   for (int q = nsb - 1; q >= 0; --q) {
     const int J0 = q * SB, J1 = std::min(d, J0 + SB);
     // sym_lower: only columns below the super-block's end are needed (rows of X below J1 hold
     // only their lower triangle, which is all these columns read)
     const int ncs = sym_lower ? std::min(ncols, J1) : ncols;
-    if (J1 < d &&
-        (rc = zgemm(s, nsys, J1 - J0, ncs, d - J1, -1.0, sub(M, J0, J1), sub(X, J1, 0), sub(X, J0, 0))))
-      return rc;
-    for (int j0 = J1 - nb >= J0 ? ((J1 - J0 - 1) / nb) * nb + J0 : J0; j0 >= J0; j0 -= nb) {
+    if (J1 < d) {
+      if ((rc = zgemm(s, nsys, J1 - J0, ncs, d - J1, -1.0, sub(M, J0, J1), sub(X, J1, 0), sub(X, J0, 0), true, -1,
+                      ride())))
+        return rc;
+      pend = ZCombine();
+    }
+    for (int j0 = ((J1 - J0 - 1) / nb) * nb + J0; j0 >= J0; j0 -= nb) {
       const int jb = std::min(nb, d - j0);
       const int inner = J1 - j0 - jb;  // couplings inside the super-block
       const int nc = sym_lower ? std::min(ncols, j0 + jb) : ncols;
-      if (inner > 0 &&
-          (rc = zgemm(s, nsys, jb, nc, inner, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0))))
-        return rc;
-      ZCombine cm;
-      if (cmb) {
-        cm = *cmb;
-        cm.row0 = j0;
-        cm.cnt = cmb->cnt + (int64_t)(j0 / nb) * cmb->nstrips;
+      if (inner > 0) {
+        if ((rc = zgemm(s, nsys, jb, nc, inner, -1.0, sub(M, j0, j0 + jb), sub(X, j0 + jb, 0), sub(X, j0, 0), true,
+                        -1, ride())))
+          return rc;
+        pend = ZCombine();
       }
-      if ((rc = ztrmm_inplace(s, nsys, jb, nc, ui(j0), sub(X, j0, 0), false, true, ZMat{nullptr, 0, 0}, nullptr,
-                              cmb ? &cm : nullptr)))
-        return rc;
+      if (pend.mode && (rc = zcombine(s, pend))) return rc;  // nothing carried it (not expected)
+      if ((rc = ztrmm_inplace(s, nsys, jb, nc, ui(j0), sub(X, j0, 0), false, true))) return rc;
+      if (cmb) {
+        pend = *cmb;
+        pend.X = sub(X, j0, 0);
+        pend.row0 = j0;
+        pend.nb = jb;
+        pend.ncols = ncols;
+      }
     }
   }
+  if (pend.mode && (rc = zcombine(s, pend))) return rc;  // block row 0
   return PFX_OK;
 }
 
@@ -229,12 +239,9 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   const size_t libytes = (size_t)nsys * nblk * DL_NB * DL_NB * sizeof(double2);
   // Li / Ui (no-pivot path) and ipiv (pivoted path) share the same space
   static_assert(sizeof(int) * DL_NB <= 2 * DL_NB * DL_NB * sizeof(double2), "ipiv fits the inverse tiles");
-  const int nstrips = (ncols + 31) / 32;
-  const size_t cbytes = (size_t)nblk * nstrips * sizeof(int);
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256 + cbytes));
+  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + 2 * libytes + 256));
   if (!ws) return fail(PFX_CUDA, "large dense workspace allocation failed");
   int* ipiv = reinterpret_cast<int*>(ws + mbytes + xbytes);
-  int* cnt = reinterpret_cast<int*>(ws + mbytes + xbytes + 2 * libytes + 256);
   ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
   ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), ncols, (int64_t)d * ncols};
@@ -267,10 +274,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   cm.scale = scale;
   cm.out = out;
   cm.ldo = ncols;
-  cm.cnt = cnt;
-  cm.nstrips = nstrips;
   if (!pivoted) {
-    PFX_CUDA_TRY(cudaMemsetAsync(cnt, 0, cbytes, stream));
     rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2, &cm);
     if (rc) return rc;
     if (pivot == 2) {

@@ -29,6 +29,156 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
 }
 
+// ---------------------------------------------------------------------------
+// Residue combine riding along in a later launch (see ZCombine in zblas.cuh).  All loads of
+// the solutions bypass L1 (other CTAs of earlier launches wrote them).
+__device__ __forceinline__ cplx ldcg(const double2* p) {
+  const double2 v = __ldcg(p);
+  return cplx{v.x, v.y};
+}
+
+// Mode 1 (complex full, Hermitian) for the block row's columns [c0, c1): the mirrored reads
+// X_k[c, r0 + r] and the mirrored writes out[c, r0 + r] go through shared memory (sm: >= 64 x 65
+// double2) so that every global access runs along a row; each thread keeps its elements' sums
+// in registers across the systems.
+__device__ void combine_hermitian(const ZCombine& cm, int c0, int c1, double2* sm) {
+  constexpr int MAXE = (64 * 64) / 128;  // >= 128 threads per CTA
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t r0 = cm.row0;
+  const int nb = cm.nb, w = c1 - c0;
+  const int SP = nb + 1;  // sm[c * SP + r]
+  const ZMat& X = cm.X;
+  cplx acc[MAXE];
+#pragma unroll
+  for (int i = 0; i < MAXE; ++i) acc[i] = mk(0, 0);
+  for (int k = 0; k < cm.npairs; ++k) {
+    __syncthreads();
+    for (int e = tid; e < w * nb; e += nt) {  // X_k[c0 + cc, r0 + r], coalesced along r
+      const int cc = e / nb, r = e - cc * nb;
+      sm[cc * SP + r] = __ldcg(X.at(k, c0 + cc - r0, r0 + r));
+    }
+    __syncthreads();
+    const cplx a = ld(&cm.coef[k]);
+#pragma unroll
+    for (int i = 0; i < MAXE; ++i) {
+      const int e = tid + nt * i;
+      if (e < nb * w) {
+        const int r = e / w, c = e - r * w;  // coalesced along c
+        const cplx x = ldcg(X.at(k, r, c0 + c));
+        const cplx y = ld(&sm[c * SP + r]);
+        const cplx sk = cadd(cmul(a, x), cconj(cmul(a, y)));
+        acc[i] = k == 0 ? sk : cadd(acc[i], sk);
+      }
+    }
+  }
+  __syncthreads();
+  double2* out = reinterpret_cast<double2*>(cm.out);
+#pragma unroll
+  for (int i = 0; i < MAXE; ++i) {
+    const int e = tid + nt * i;
+    if (e < nb * w) {
+      const int r = e / w, c = e - r * w;
+      cplx v = acc[i];
+      if (cm.scale != 1.0) v = cscale(v, cm.scale);
+      out[(r0 + r) * cm.ldo + c0 + c] = make_double2(v.re, v.im);
+      sm[c * SP + r] = make_double2(v.re, -v.im);  // the mirror image, written row-wise below
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < w * nb; e += nt) {
+    const int cc = e / nb, r = e - cc * nb;
+    if (c0 + cc != r0 + r) out[(int64_t)(c0 + cc) * cm.ldo + r0 + r] = sm[cc * SP + r];
+  }
+}
+
+// Modes 2-4 for the block row's columns [c0, c1) (no transposed reads).
+__device__ void combine_plain(const ZCombine& cm, int c0, int c1) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t r0 = cm.row0;
+  const int nb = cm.nb, w = c1 - c0;
+  const double sc = cm.scale;
+  const ZMat& X = cm.X;
+  for (int e = tid; e < nb * w; e += nt) {
+    const int r = e / w, c = c0 + (e - r * w);
+    const int64_t gr = r0 + r;
+    if (cm.mode == 4) {
+      cplx acc = mk(0, 0);
+      for (int k = 0; k < cm.npairs; ++k) {
+        const cplx a = ld(&cm.coef[k]);
+        const cplx sk = cadd(cmul(a, ldcg(X.at(k, r, c))), cmul(cconj(a), ldcg(X.at(cm.npairs + k, r, c))));
+        acc = k == 0 ? sk : cadd(acc, sk);
+      }
+      if (sc != 1.0) acc = cscale(acc, sc);
+      reinterpret_cast<double2*>(cm.out)[gr * cm.ldo + c] = make_double2(acc.re, acc.im);
+      continue;
+    }
+    if (cm.mode == 2 && c > gr) continue;  // lower triangle (the diagonal block's upper half mirrors)
+    double acc = 0.0;
+    for (int k = 0; k < cm.npairs; ++k) {
+      const cplx a = ld(&cm.coef[k]);
+      const cplx x = ldcg(X.at(k, r, c));
+      const double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
+      acc = k == 0 ? sk : acc + sk;
+    }
+    if (sc != 1.0) acc *= sc;
+    cm.out[gr * cm.ldo + c] = acc;
+    if (cm.mode == 2 && c != gr) cm.out[(int64_t)c * cm.ldo + gr] = acc;
+  }
+}
+
+// The column groups one finished block row decides: mode 1 its diagonal block (one group: the
+// mirrored reads cross its own rows) and the 32-wide strips right of it; mode 2 the diagonal
+// block and the strips left of it; modes 3/4 every column.  Group g -> [c0, c1).
+__device__ __forceinline__ int combine_groups(const ZCombine& cm) {
+  const int64_t r0 = cm.row0;
+  if (cm.mode == 1) return 1 + (int)((cm.ncols - (r0 + cm.nb) + 31) / 32);
+  if (cm.mode == 2) return 1 + (int)((r0 + 31) / 32);
+  return (cm.ncols + 31) / 32;
+}
+__device__ __forceinline__ void combine_group_cols(const ZCombine& cm, int g, int& c0, int& c1) {
+  const int r0 = (int)cm.row0;
+  if (cm.mode == 3 || cm.mode == 4) {
+    c0 = g * 32;
+    c1 = min(cm.ncols, c0 + 32);
+  } else if (g == 0) {
+    c0 = r0;
+    c1 = r0 + cm.nb;
+  } else if (cm.mode == 1) {
+    c0 = r0 + cm.nb + (g - 1) * 32;
+    c1 = min(cm.ncols, c0 + 32);
+  } else {
+    c0 = (g - 1) * 32;
+    c1 = min(r0, c0 + 32);
+  }
+}
+
+// Every CTA of the carrying slice takes groups cta, cta + nctas, ...
+__device__ void ride_combine(const ZCombine& cm, int cta, int nctas, double2* sm) {
+  const int ng = combine_groups(cm);
+  for (int g = cta; g < ng; g += nctas) {
+    int c0, c1;
+    combine_group_cols(cm, g, c0, c1);
+    if (c1 <= c0) continue;
+    if (cm.mode == 1) combine_hermitian(cm, c0, c1, sm);
+    else combine_plain(cm, c0, c1);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) zcombine_kernel(ZCombine cm) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ride_combine(cm, blockIdx.x, gridDim.x, reinterpret_cast<double2*>(smem_raw));
+}
+
+int zcombine(cudaStream_t s, const ZCombine& cm) {
+  if (cm.mode == 0) return PFX_OK;
+  const int smem = 64 * 65 * (int)sizeof(double2);
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zcombine_kernel), smem)) return rc;
+  PFX_LAUNCH("zcombine", s, zcombine_kernel<<<148, 256, smem, s>>>(cm));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
 // TM x TN output tile, NW warps in a 2 x (NW/2) grid, each warp FM x FN DMMA 8x8 tiles.
 // 64x64/8 warps for large problems; 32x32/4 warps when the 64-tile grid would leave SMs
 // idle (one 64x64x64 complex tile is ~16K DMMA cycles of a single SM).
@@ -40,8 +190,16 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // overlap the other's DMMA stream (at 156 registers a single CTA per SM ran 15% slower).
 template <int TM, int TN, int NW, bool M3 = false, int GK = 16>
 __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 : 1) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                                                        int accumulate, int b_lower_off) {
+                                                        int accumulate, int b_lower_off, ZCombine ride) {
   constexpr int NT = NW * 32;
+  if constexpr (TM == 64 && NW == 4) {  // only this layout carries a combine (register budget)
+    if (ride.mode != 0 && blockIdx.z == gridDim.z - 1) {  // the carried residue combine slice
+      extern __shared__ __align__(16) unsigned char smem_raw[];
+      ride_combine(ride, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y,
+                   reinterpret_cast<double2*>(smem_raw));
+      return;
+    }
+  }
   constexpr int WN = NW / 2;
   constexpr int FM = TM / 2 / 8, FN = TN / WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -190,10 +348,19 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
 
 template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                        bool accumulate, int b_lower_off) {
+                        bool accumulate, int b_lower_off, const ZCombine* ride) {
   const int smem = (int)sizeof(GemmSmem<TM, TN, KS>);
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgemm_kernel<TM, TN, NW, M3, KS>), smem)) return rc;
-  dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch);
+  ZCombine rd;
+  if (ride) rd = *ride;
+  // the combine's shared-memory staging (64 x 65) must fit the GEMM's allocation
+  static_assert(sizeof(GemmSmem<TM, TN, KS>) >= 64 * 65 * sizeof(double2) || TM < 64, "combine staging fits");
+  constexpr bool carries = TM == 64 && NW == 4;
+  dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch + (ride && carries ? 1 : 0));
+  if (ride && !carries) {  // other layouts: the combine goes on its own launch
+    if (int rc = zcombine(s, rd)) return rc;
+    rd = ZCombine();
+  }
   // algorithmic flops: 8 per complex multiply-add actually required (b_lower: the products
   // with the zero triangle of B are not counted)
   double fl = 8.0 * (double)m * n * k * batch;
@@ -204,33 +371,33 @@ static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double a
   }
   PFX_LAUNCH_F("zgemm", s, fl,
                (zgemm_kernel<TM, TN, NW, M3, KS><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C,
-                                                                       accumulate ? 1 : 0, b_lower_off)));
+                                                                       accumulate ? 1 : 0, b_lower_off, rd)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
 
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate,
-          int b_lower_off) {
-  if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return PFX_OK;
+          int b_lower_off, const ZCombine* ride) {
+  if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return ride ? zcombine(s, *ride) : PFX_OK;
   const int sms = device_sms();
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
   const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, 64) * (int64_t)batch;
   static const bool ks32 = getenv("PFX_ZGEMM_KS16") == nullptr;
   if (tiles64 < 2 * sms) {
     if (k <= 64 && ks32)  // short K: two 32-deep stages instead of four 16-deep ones
-      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
-                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
-    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
-              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
+      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)
+                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
+    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)
+              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
   }
   // 64x64 tiles on 4 warps of 32x32 (248 registers, two CTAs per SM): per 4-deep K step a
   // warp issues 8 fragment loads and 8 operand sums for 48 DMMAs (3M), where the 8-warp
   // 32x16 layout issued 6 + 6 for 24; 5-8% faster on every C4 shape (tools/zgemm_probe.cu).
   // PFX_ZGEMM_W8=1 keeps the 8-warp layout for A/B checks.
   static const bool w8 = getenv("PFX_ZGEMM_W8") != nullptr;
-  if (m3 && !w8) return zgemm_launch<64, 64, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
-  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off)
-            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off);
+  if (m3 && !w8) return zgemm_launch<64, 64, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
+  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)
+            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
 }
 
 // ---------------------------------------------------------------------------
@@ -804,125 +971,8 @@ int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui) {
 constexpr int TM_T = 64;
 constexpr int TM_W = 32;
 
-// load bypassing L1 (values other CTAs wrote during this kernel)
-__device__ __forceinline__ cplx ldcg(const double2* p) {
-  const double2 v = __ldcg(p);
-  return cplx{v.x, v.y};
-}
-
-// The fused combine epilogue of ztrmm_kernel (see ZCombine): called by the last CTA of a strip
-// group; B is the X slab (batch stride, rows from block row r0), cols [c0, c1) of the group.
-// Mode 1 (complex full, Hermitian): the mirrored reads X_k[c, r0 + r] and the mirrored writes
-// out[c, r0 + r] go through shared memory (sm: >= 64 x 65 double2) so that every global access
-// runs along a row; each thread keeps its elements' sums in registers across the pairs.
-__device__ void combine_hermitian(const ZCombine& cm, ZMat X, int nb, int c0, int c1, double2* sm) {
-  constexpr int MAXE = (64 * 64) / 256;
-  const int tid = threadIdx.x;
-  const int64_t r0 = cm.row0;
-  const int w = c1 - c0;
-  const int SP = nb + 1;  // sm row stride: sm[c * SP + r]
-  cplx acc[MAXE];
-#pragma unroll
-  for (int i = 0; i < MAXE; ++i) acc[i] = mk(0, 0);
-  for (int k = 0; k < cm.npairs; ++k) {
-    __syncthreads();
-    for (int e = tid; e < w * nb; e += 256) {  // X_k[c0 + cc, r0 + r], coalesced along r
-      const int cc = e / nb, r = e - (e / nb) * nb;
-      sm[cc * SP + r] = __ldcg(X.at(k, c0 + cc - r0, r0 + r));
-    }
-    __syncthreads();
-    const cplx a = ld(&cm.coef[k]);
-#pragma unroll
-    for (int i = 0; i < MAXE; ++i) {
-      const int e = tid + 256 * i;
-      if (e < nb * w) {
-        const int r = e / w, c = e - (e / w) * w;  // coalesced along c
-        const cplx x = ldcg(X.at(k, r, c0 + c));
-        const cplx y = ld(&sm[c * SP + r]);
-        const cplx sk = cadd(cmul(a, x), cconj(cmul(a, y)));
-        acc[i] = k == 0 ? sk : cadd(acc[i], sk);
-      }
-    }
-  }
-  __syncthreads();
-  double2* out = reinterpret_cast<double2*>(cm.out);
-#pragma unroll
-  for (int i = 0; i < MAXE; ++i) {
-    const int e = tid + 256 * i;
-    if (e < nb * w) {
-      const int r = e / w, c = e - (e / w) * w;
-      cplx v = acc[i];
-      if (cm.scale != 1.0) v = cscale(v, cm.scale);
-      out[(r0 + r) * cm.ldo + c0 + c] = make_double2(v.re, v.im);
-      sm[c * SP + r] = make_double2(v.re, -v.im);  // mirror image, written back row-wise below
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < w * nb; e += 256) {
-    const int cc = e / nb, r = e - (e / nb) * nb;
-    if (c0 + cc != r0 + r) out[(int64_t)(c0 + cc) * cm.ldo + r0 + r] = sm[cc * SP + r];
-  }
-}
-
-__device__ void combine_block(const ZCombine& cm, ZMat X, int nb, int c0, int c1) {
-  const int tid = threadIdx.x;
-  const int64_t r0 = cm.row0;
-  const double sc = cm.scale;
-  const int w = c1 - c0;
-  // X rows are relative to the block row (X.at(k, r, c) = element (r0 + r, c)); the mirrored
-  // reads X_k[c, r0 + r] are rows c of the full matrix: offset -r0
-  for (int e = tid; e < nb * w; e += 256) {
-    const int r = e / w, c = c0 + (e - (e / w) * w);
-    const int64_t gr = r0 + r;  // global row of this element
-    if (cm.mode == 1) {
-      cplx acc = mk(0, 0);
-      for (int k = 0; k < cm.npairs; ++k) {
-        const cplx a = ld(&cm.coef[k]);
-        const cplx x = ldcg(X.at(k, r, c));
-        const cplx y = ldcg(X.at(k, c - r0, gr));  // X_k[c, gr]
-        const cplx sk = cadd(cmul(a, x), cconj(cmul(a, y)));
-        acc = k == 0 ? sk : cadd(acc, sk);
-      }
-      if (sc != 1.0) acc = cscale(acc, sc);
-      reinterpret_cast<double2*>(cm.out)[gr * cm.ldo + c] = make_double2(acc.re, acc.im);
-      if (c != gr) reinterpret_cast<double2*>(cm.out)[(int64_t)c * cm.ldo + gr] = make_double2(acc.re, -acc.im);
-    } else if (cm.mode == 2) {
-      if (c > gr) continue;  // lower triangle of the block row (the diagonal block's upper half mirrors)
-      double acc = 0.0;
-      for (int k = 0; k < cm.npairs; ++k) {
-        const cplx a = ld(&cm.coef[k]);
-        const cplx x = ldcg(X.at(k, r, c));
-        const double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
-        acc = k == 0 ? sk : acc + sk;
-      }
-      if (sc != 1.0) acc *= sc;
-      cm.out[gr * cm.ldo + c] = acc;
-      if (c != gr) cm.out[(int64_t)c * cm.ldo + gr] = acc;
-    } else if (cm.mode == 3) {
-      double acc = 0.0;
-      for (int k = 0; k < cm.npairs; ++k) {
-        const cplx a = ld(&cm.coef[k]);
-        const cplx x = ldcg(X.at(k, r, c));
-        const double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
-        acc = k == 0 ? sk : acc + sk;
-      }
-      cm.out[gr * cm.ldo + c] = sc == 1.0 ? acc : sc * acc;
-    } else {
-      cplx acc = mk(0, 0);
-      for (int k = 0; k < cm.npairs; ++k) {
-        const cplx a = ld(&cm.coef[k]);
-        const cplx sk = cadd(cmul(a, ldcg(X.at(k, r, c))), cmul(cconj(a), ldcg(X.at(cm.npairs + k, r, c))));
-        acc = k == 0 ? sk : cadd(acc, sk);
-      }
-      if (sc != 1.0) acc = cscale(acc, sc);
-      reinterpret_cast<double2*>(cm.out)[gr * cm.ldo + c] = make_double2(acc.re, acc.im);
-    }
-  }
-}
-
 template <bool RIGHT>
-__global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper, ZMat Dg, int* flag,
-                                                    ZCombine cm) {
+__global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper, ZMat Dg, int* flag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // row strides (16-byte words) for conflict-free DMMA fragment loads: an A-operand array
   // (read at rows g x columns tt of a quarter-warp) 4 mod 8, a B-operand array (rows tt x
@@ -1013,41 +1063,10 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
         }
       }
     }
-  if (RIGHT || cm.mode == 0) return;
-  // ---- fused residue combine (left products of the backward substitution only)
-  const int64_t r0 = cm.row0;
-  const int c0 = t0, c1 = min(n, t0 + TM_W);
-  // full modes: strips meeting the diagonal block's columns (action modes: columns are RHS)
-  const bool diag = cm.mode <= 2 && c0 < r0 + nb && c1 > r0;
-  if (cm.mode == 1 && !diag && c1 <= r0) return;       // left of the diagonal: a later block row
-  if (cm.mode == 2 && !diag && c0 >= r0 + nb) return;  // right of the diagonal: an earlier block row
-  // diagonal strips form one group (their mirrored reads cross each other's rows)
-  const int g0 = diag ? (int)(r0 / TM_W) : blockIdx.x;
-  const int g1 = diag ? (int)((r0 + nb - 1) / TM_W) : blockIdx.x;
-  const int expect = (g1 - g0 + 1) * (int)gridDim.y;
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int prev = atomicAdd(&cm.cnt[g0], 1);
-    s_last = prev == expect - 1;
-    if (s_last) cm.cnt[g0] = 0;  // ready for the next call
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // batch stride = B.stride, rows relative to the block row; the product's shared memory is idle
-  const int gc0 = diag ? g0 * TM_W : c0, gc1 = diag ? min(n, (g1 + 1) * TM_W) : c1;
-  if (cm.mode == 1)
-    combine_hermitian(cm, B, nb, gc0, gc1, reinterpret_cast<double2*>(smem_raw));
-  else
-    combine_block(cm, B, nb, gc0, gc1);
 }
 
 int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper, ZMat Dg,
-                  int* pivot_flag, const ZCombine* cmb) {
-  ZCombine cm;
-  if (cmb && !right) cm = *cmb;
+                  int* pivot_flag) {
   if (n <= 0) return PFX_OK;
   if (nb > TM_T) return fail(PFX_BADARG, "ztrmm_inplace: nb > 64");
   const int smem = (TM_T * (TM_T + 4) + TM_T * (TM_T + 4)) * (int)sizeof(double2);
@@ -1057,10 +1076,10 @@ int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, b
   const double fl = 4.0 * nb * nb * (double)n * batch;  // triangular: half the square product
   if (right)
     PFX_LAUNCH_F("ztrmm", s, fl,
-                 ztrmm_kernel<true><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, pivot_flag, cm));
+                 ztrmm_kernel<true><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, pivot_flag));
   else
     PFX_LAUNCH_F("ztrmm", s, fl,
-                 ztrmm_kernel<false><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, nullptr, cm));
+                 ztrmm_kernel<false><<<grid, 256, smem, s>>>(nb, n, Tinv, B, upper ? 1 : 0, Dg, nullptr));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }

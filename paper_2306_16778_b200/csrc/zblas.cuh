@@ -17,26 +17,12 @@ struct ZMat {
   __host__ __device__ double2* at(int b, int64_t i, int64_t j) const { return p + b * stride + i * ld + j; }
 };
 
-// C[b] += alpha * A[b] (m x k) * B[b] (k x n) (accumulate = true) or C[b] = alpha * A B.
-// DMMA m8n8k4, 64x64x16 tiles.
-// b_lower_off >= 0: B (k x n) is lower triangular with that row offset, B[r][c] = 0 for
-// r + b_lower_off < c; each column tile skips the zero rows (the forward substitution of the
-// identity right-hand side).  -1: B dense.
-int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-          bool accumulate = true, int b_lower_off = -1);
-
-// No-pivot LU of the nb x nb diagonal block D (nb <= 64) in registers, in place.  Raises
-// ST_SINGULAR in *sing on an exactly zero pivot and ST_PIVOT where partial pivoting inside the
-// block would have exchanged rows (the rows below the block are checked by ztrmm_inplace).
-int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing);
-// Triangular inverses of a factored diagonal block: Li = L^{-1} (unit lower), Ui = U^{-1}.
-int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui);
-// In place: B = Tinv * B (left, B nb x n) or B = B * Tinv (right, B n x nb), Tinv nb x nb
-// (nb <= 64) triangular (upper or lower), on DMMA; one CTA per 32-wide strip of B.
-// Fused residue combine (K5/K6 of the dense path, engine.py:199-213,225-228) as the epilogue of
-// the last backward-substitution product of each block row: once all systems' CTAs of a
-// strip have written their final rows X_k[r0 .. r0+nb, strip], the last one to arrive (a
-// per-(block row, strip) counter) sums the systems in ascending k and writes `out`.
+// Fused residue combine (K5/K6 of the dense path, engine.py:199-213,225-228), riding along in the
+// substitution's next GEMM launch: when the backward substitution has finished block row r0
+// (rows [r0, r0 + nb) of every system's X_k are final), the next zgemm launch carries one extra
+// z-slice of CTAs that sums the systems in ascending k for the entries that block row decides
+// and writes them to `out` -- in parallel with that GEMM's tiles, reading rows just written
+// (L2-hot), so no separate pass over the n/2 solutions and no step on the serial chain.
 //   mode 1  complex full:   out = sum_k a_k X_k + (a_k X_k)^H  (Hermitian; the block row's
 //           entries right of its diagonal and their mirror images, X_k[strip, block] rows
 //           being final already: every (i, j) is written by block row min(i, j))
@@ -51,16 +37,37 @@ struct ZCombine {
   double scale = 1.0;    // e^c of the shift method
   double* out = nullptr; // d x ncols, real (modes 2, 3) or complex (1, 4), row-major
   int64_t ldo = 0;       // row stride of out (elements)
-  int* cnt = nullptr;    // counters, zero on entry, left zero
-  int64_t row0 = 0;      // first row of the block row (= its column for the diagonal)
-  int nstrips = 0;       // counters per block row
+  ZMat X{nullptr, 0, 0}; // the systems' solutions, rows relative to row0
+  int64_t row0 = 0;      // first row of the finished block row (= its column for the diagonal)
+  int nb = 0;            // rows in the block row
+  int ncols = 0;         // columns of out / X
 };
+// Launch a combine on its own (the last block row, which no later GEMM follows).
+int zcombine(cudaStream_t s, const ZCombine& cm);
+
+// C[b] += alpha * A[b] (m x k) * B[b] (k x n) (accumulate = true) or C[b] = alpha * A B.
+// DMMA m8n8k4, 64x64x16 tiles.
+// b_lower_off >= 0: B (k x n) is lower triangular with that row offset, B[r][c] = 0 for
+// r + b_lower_off < c; each column tile skips the zero rows (the forward substitution of the
+// identity right-hand side).  -1: B dense.
+// ride (optional): a residue combine carried by this launch (one extra z-slice of CTAs).
+int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
+          bool accumulate = true, int b_lower_off = -1, const ZCombine* ride = nullptr);
+
+// No-pivot LU of the nb x nb diagonal block D (nb <= 64) in registers, in place.  Raises
+// ST_SINGULAR in *sing on an exactly zero pivot and ST_PIVOT where partial pivoting inside the
+// block would have exchanged rows (the rows below the block are checked by ztrmm_inplace).
+int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing);
+// Triangular inverses of a factored diagonal block: Li = L^{-1} (unit lower), Ui = U^{-1}.
+int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui);
+// In place: B = Tinv * B (left, B nb x n) or B = B * Tinv (right, B n x nb), Tinv nb x nb
+// (nb <= 64) triangular (upper or lower), on DMMA; one CTA per 32-wide strip of B.
 
 // pivot_flag (right products only): B = L21 = A21 U11^{-1} of a no-pivot LU step whose
 // diagonal block (factored in place) is Dg; every entry is checked against partial pivoting
 // (|l u_cc|_1 > |u_cc|_1 means row interchanges were due) and ST_PIVOT is or-ed into *pivot_flag.
 int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper,
-                  ZMat Dg = ZMat{nullptr, 0, 0}, int* pivot_flag = nullptr, const ZCombine* cmb = nullptr);
+                  ZMat Dg = ZMat{nullptr, 0, 0}, int* pivot_flag = nullptr);
 
 // Unblocked LU of the m x nb panel at P (in place).  ipiv (optional, batch x nb, 0-based
 // rows relative to the panel) -> partial pivoting with row swaps inside the panel only.
