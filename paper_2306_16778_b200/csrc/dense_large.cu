@@ -274,8 +274,15 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   cm.scale = scale;
   cm.out = out;
   cm.ldo = ncols;
+  // PFX_FUSED_COMBINE=1: the combine rides along the backward substitution (ZCombine) instead of
+  // the standalone pass below.  Measured on C4 (12 x 4096^2): standalone 1.56 ms of a 180 ms
+  // step; riding along, the latency-bound combine CTAs take SM slots from the DMMA-bound GEMM
+  // tiles and the step grew to 187-192 ms (profiles/r02_c4_combine_ab.txt), so it is opt-in.
+  static const bool fuse = getenv("PFX_FUSED_COMBINE") != nullptr;
+  const bool fused = fuse && !pivoted;
   if (!pivoted) {
-    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2, &cm);
+    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2,
+                        fused ? &cm : nullptr);
     if (rc) return rc;
     if (pivot == 2) {
       PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -297,7 +304,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     rc = lu_solve_piv(stream, nsys, d, M, X, ncols, ipiv, sing);
     if (rc) return rc;
   }
-  if (pivoted) {
+  if (!fused) {
     PFX_LAUNCH("dl_combine", stream,
                dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
                                                    out));

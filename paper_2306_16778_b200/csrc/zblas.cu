@@ -53,9 +53,21 @@ __device__ void combine_hermitian(const ZCombine& cm, int c0, int c1, double2* s
   for (int i = 0; i < MAXE; ++i) acc[i] = mk(0, 0);
   for (int k = 0; k < cm.npairs; ++k) {
     __syncthreads();
-    for (int e = tid; e < w * nb; e += nt) {  // X_k[c0 + cc, r0 + r], coalesced along r
-      const int cc = e / nb, r = e - cc * nb;
-      sm[cc * SP + r] = __ldcg(X.at(k, c0 + cc - r0, r0 + r));
+    // X_k[c0 + cc, r0 + r], coalesced along r; eight loads in flight per thread
+    for (int e0 = tid; e0 < w * nb; e0 += 8 * nt) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * nt;
+        const int cc = e / nb, r = e - cc * nb;
+        v[u] = e < w * nb ? __ldcg(X.at(k, c0 + cc - r0, r0 + r)) : make_double2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * nt;
+        const int cc = e / nb, r = e - cc * nb;
+        if (e < w * nb) sm[cc * SP + r] = v[u];
+      }
     }
     __syncthreads();
     const cplx a = ld(&cm.coef[k]);
@@ -193,7 +205,8 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
                                                         int accumulate, int b_lower_off, ZCombine ride) {
   constexpr int NT = NW * 32;
   if constexpr (TM == 64 && NW == 4) {  // only this layout carries a combine (register budget)
-    if (ride.mode != 0 && blockIdx.z == gridDim.z - 1) {  // the carried residue combine slice
+    // the carried residue combine is slice z = 0: dispatched first, it runs beside the tiles
+    if (ride.mode != 0 && blockIdx.z == 0) {
       extern __shared__ __align__(16) unsigned char smem_raw[];
       ride_combine(ride, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y,
                    reinterpret_cast<double2*>(smem_raw));
@@ -204,7 +217,7 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
   constexpr int FM = TM / 2 / 8, FN = TN / WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GemmSmem<TM, TN, GK>& S = *reinterpret_cast<GemmSmem<TM, TN, GK>*>(smem_raw);
-  const int b = blockIdx.z;
+  const int b = blockIdx.z - ((TM == 64 && NW == 4 && ride.mode != 0) ? 1 : 0);
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
