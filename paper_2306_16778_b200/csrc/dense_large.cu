@@ -25,6 +25,7 @@
 namespace pfx {
 
 constexpr int DL_NB = 64;
+constexpr int DL_GROUP = 2;  // panels per delayed trailing update (K = 64 G)
 
 __global__ void dl_build(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
                          double shift_c, const double2* theta, int npairs, int nsys, ZMat M, ZMat X) {
@@ -135,26 +136,34 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
     }
     return PFX_OK;
   };
-  // Two-panel delayed update: panel a = [j0, j1) is factored, panel b = [j1, j1 + 64) takes
-  // only panel a's update (its column block and its row block), panel b is factored, and the
-  // trailing matrix takes both panels' updates in ONE K = 128 GEMM.  The trailing matrix (up
-  // to 12 x 268 MB, far beyond L2) is read and written once per 128 columns instead of once
-  // per 64, and every trailing tile does twice the DMMA work per epilogue.
-  for (int j0 = 0; j0 < d; j0 += 2 * nb) {
-    const int jb = std::min(nb, d - j0);
-    const int rest = d - j0 - jb;
-    if ((rc = factor(j0, jb, rest))) return rc;
-    if (rest == 0) break;
-    const int j1 = j0 + jb;
-    const int jb1 = std::min(nb, d - j1);
-    const int rest1 = d - j1 - jb1;
-    if ((rc = zgemm(s, nsys, d - j1, jb1, jb, -1.0, sub(M, j1, j0), sub(M, j0, j1), sub(M, j1, j1)))) return rc;
-    if (rest1 > 0 &&
-        (rc = zgemm(s, nsys, jb1, rest1, jb, -1.0, sub(M, j1, j0), sub(M, j0, j1 + jb1), sub(M, j1, j1 + jb1))))
-      return rc;
-    if ((rc = factor(j1, jb1, rest1))) return rc;
-    if (rest1 > 0 && (rc = zgemm(s, nsys, rest1, rest1, jb + jb1, -1.0, sub(M, j1 + jb1, j0), sub(M, j0, j1 + jb1),
-                                 sub(M, j1 + jb1, j1 + jb1))))
+  // Delayed update over groups of G panels (left-looking inside the group, right-looking
+  // across groups): panel p of a group first takes the updates of the group's earlier panels
+  // (its column block and its row block, K = 64 (p - g0) / 64), is factored, and after the
+  // group the trailing matrix takes all G panels' updates in ONE K = 64 G GEMM.  The trailing
+  // matrix (up to 12 x 268 MB, far beyond L2) is read and written once per 64 G columns
+  // instead of once per 64, and every trailing tile does G times the DMMA work per epilogue.
+  // PFX_LU_GROUP=<G> overrides the default group (A/B experiments).
+  static const int G = [] {
+    const char* e = getenv("PFX_LU_GROUP");
+    const int g = e ? atoi(e) : DL_GROUP;
+    return g < 1 ? 1 : (g > 8 ? 8 : g);
+  }();
+  for (int g0 = 0; g0 < d; g0 += G * nb) {
+    const int gend = std::min(d, g0 + G * nb);
+    for (int jp = g0; jp < gend; jp += nb) {
+      const int jb = std::min(nb, d - jp);
+      const int rest = d - jp - jb;
+      if (jp > g0) {
+        if ((rc = zgemm(s, nsys, d - jp, jb, jp - g0, -1.0, sub(M, jp, g0), sub(M, g0, jp), sub(M, jp, jp))))
+          return rc;
+        if (rest > 0 && (rc = zgemm(s, nsys, jb, rest, jp - g0, -1.0, sub(M, jp, g0), sub(M, g0, jp + jb),
+                                    sub(M, jp, jp + jb))))
+          return rc;
+      }
+      if ((rc = factor(jp, jb, rest))) return rc;
+    }
+    if (gend < d && (rc = zgemm(s, nsys, d - gend, d - gend, gend - g0, -1.0, sub(M, gend, g0), sub(M, g0, gend),
+                                sub(M, gend, gend))))
       return rc;
   }
   // Both substitutions run in super-blocks of SB = 8 block rows: one GEMM with m = 512 rows

@@ -984,6 +984,9 @@ int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui) {
 constexpr int TM_T = 64;
 constexpr int TM_W = 32;
 
+// Persistent over the strips of one system: grid (CTAs per system, batch); each CTA loads T
+// once and walks strips blockIdx.x, blockIdx.x + gridDim.x, ..., the next strip's cp.async
+// load in flight while the current one is multiplied (two strip buffers).
 template <bool RIGHT>
 __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat B, int upper, ZMat Dg, int* flag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -993,31 +996,34 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
   constexpr int TSS_ = RIGHT ? TM_T + 2 : TM_T + 4;  // Ts
   constexpr int BSL = TM_W + 2;                      // Bs, left: [k][col] (B operand)
   constexpr int BSR = TM_T + 4;                      // Bs, right: [row][k] (A operand)
+  constexpr int BSZ = (TM_T * BSL > TM_W * BSR) ? TM_T * BSL : TM_W * BSR;
   double2* Ts = reinterpret_cast<double2*>(smem_raw);  // 64 x TSS_
-  double2* Bs = Ts + TM_T * (TM_T + 4);                // left: [k 64][col BSL]; right: [row TM_W][k BSR]
+  double2* Bs0 = Ts + TM_T * (TM_T + 4);               // left: [k 64][col BSL]; right: [row TM_W][k BSR]
   const int b = blockIdx.y;
-  const int t0 = blockIdx.x * TM_W;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tt = lane & 3;
+  const int nstrips = (n + TM_W - 1) / TM_W;
   for (int e = tid; e < TM_T * TM_T; e += 256) {
     const int r = e >> 6, c = e & 63;
     if (r < nb && c < nb) cp_async16(&Ts[r * TSS_ + c], T.at(b, r, c));
     else Ts[r * TSS_ + c] = make_double2(0, 0);
   }
-  for (int e = tid; e < TM_T * TM_W; e += 256) {
-    if (!RIGHT) {  // Bs[k][col] = B[k][t0 + col]
-      const int r = e / TM_W, c = e - r * TM_W;
-      if (r < nb && t0 + c < n) cp_async16(&Bs[r * BSL + c], B.at(b, r, t0 + c));
-      else Bs[r * BSL + c] = make_double2(0, 0);
-    } else {  // Bs[row][k] = B[t0 + row][k]
-      const int r = e >> 6, c = e & 63;
-      if (t0 + r < n && c < nb) cp_async16(&Bs[r * BSR + c], B.at(b, t0 + r, c));
-      else Bs[r * BSR + c] = make_double2(0, 0);
+  auto load_strip = [&](int st, double2* Bs) {
+    const int t0 = st * TM_W;
+    for (int e = tid; e < TM_T * TM_W; e += 256) {
+      if (!RIGHT) {  // Bs[k][col] = B[k][t0 + col]
+        const int r = e / TM_W, c = e - r * TM_W;
+        if (r < nb && t0 + c < n) cp_async16(&Bs[r * BSL + c], B.at(b, r, t0 + c));
+        else Bs[r * BSL + c] = make_double2(0, 0);
+      } else {  // Bs[row][k] = B[t0 + row][k]
+        const int r = e >> 6, c = e & 63;
+        if (t0 + r < n && c < nb) cp_async16(&Bs[r * BSR + c], B.at(b, t0 + r, c));
+        else Bs[r * BSR + c] = make_double2(0, 0);
+      }
     }
-  }
+  };
+  if ((int)blockIdx.x < nstrips) load_strip(blockIdx.x, Bs0);
   cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
   // left: R (64 x 32) = T Bs, warp = 8-row slab, 4 column fragments
   // right: R (32 x 64) = Bs T, warp = (8-row slab wm = warp >> 1, 32-column half wn = warp & 1)
   const int wm = RIGHT ? (warp >> 1) : warp;
@@ -1030,62 +1036,70 @@ __global__ void __launch_bounds__(256) ztrmm_kernel(int nb, int n, ZMat T, ZMat 
     if (upper) khi = wn * 32 + 32;    // T upper: T[k][c] = 0 for k > c
     else klo = wn * 32;               // T lower: T[k][c] = 0 for k < c
   }
-  // 3M complex product: T1 = sum Xr Yr, T2 = sum Xi Yi, T3 = sum (Xr + Xi)(Yr + Yi)
-  double t1[4][2], t2[4][2], t3[4][2];
+  int it = 0;
+  for (int st = blockIdx.x; st < nstrips; st += gridDim.x, ++it) {
+    double2* Bs = Bs0 + (it & 1) * BSZ;
+    const int nxt = st + gridDim.x;
+    if (nxt < nstrips) load_strip(nxt, Bs0 + ((it + 1) & 1) * BSZ);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const int t0 = st * TM_W;
+    // 3M complex product: T1 = sum Xr Yr, T2 = sum Xi Yi, T3 = sum (Xr + Xi)(Yr + Yi)
+    double t1[4][2], t2[4][2], t3[4][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) t1[j][0] = t1[j][1] = t2[j][0] = t2[j][1] = t3[j][0] = t3[j][1] = 0.0;
-  for (int k0 = klo; k0 < khi; k0 += 4) {
-    double2 x;
-    if (!RIGHT) x = Ts[(wm * 8 + g) * TSS_ + k0 + tt];
-    else x = Bs[(wm * 8 + g) * BSR + k0 + tt];
-    const double xs = x.x + x.y;
+    for (int j = 0; j < 4; ++j) t1[j][0] = t1[j][1] = t2[j][0] = t2[j][1] = t3[j][0] = t3[j][1] = 0.0;
+    for (int k0 = klo; k0 < khi; k0 += 4) {
+      double2 x;
+      if (!RIGHT) x = Ts[(wm * 8 + g) * TSS_ + k0 + tt];
+      else x = Bs[(wm * 8 + g) * BSR + k0 + tt];
+      const double xs = x.x + x.y;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double2 y = RIGHT ? Ts[(k0 + tt) * TSS_ + wn * 32 + j * 8 + g] : Bs[(k0 + tt) * BSL + j * 8 + g];
-      dmma884(t1[j][0], t1[j][1], x.x, y.x);
-      dmma884(t2[j][0], t2[j][1], x.y, y.y);
-      dmma884(t3[j][0], t3[j][1], xs, y.x + y.y);
+      for (int j = 0; j < 4; ++j) {
+        const double2 y = RIGHT ? Ts[(k0 + tt) * TSS_ + wn * 32 + j * 8 + g] : Bs[(k0 + tt) * BSL + j * 8 + g];
+        dmma884(t1[j][0], t1[j][1], x.x, y.x);
+        dmma884(t2[j][0], t2[j][1], x.y, y.y);
+        dmma884(t3[j][0], t3[j][1], xs, y.x + y.y);
+      }
     }
-  }
-  double cr[4][2], ci[4][2];
+    const int r = wm * 8 + g;
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      cr[j][h] = t1[j][h] - t2[j][h];
-      ci[j][h] = t3[j][h] - t1[j][h] - t2[j][h];
-    }
-  const int r = wm * 8 + g;
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = wn * 32 + j * 8 + 2 * tt + h;
-      const double2 v = make_double2(cr[j][h], ci[j][h]);
-      if (!RIGHT) {
-        if (r < nb && t0 + c < n) *B.at(b, r, t0 + c) = v;
-      } else {
-        if (t0 + r < n && c < nb) {
-          *B.at(b, t0 + r, c) = v;
-          if (flag) {
-            // L21 = A21 U11^{-1}: the updated column entry l u_cc of a row below the block
-            // must not exceed the pivot u_cc (partial-pivoting check, izamax order)
-            const cplx u = ld(Dg.at(b, c, c));
-            if (cabs1(cmul(mk(v.x, v.y), u)) > cabs1(u)) atomicOr(flag, ST_PIVOT);
+      for (int h = 0; h < 2; ++h) {
+        const int c = wn * 32 + j * 8 + 2 * tt + h;
+        const double2 v = make_double2(t1[j][h] - t2[j][h], t3[j][h] - t1[j][h] - t2[j][h]);
+        if (!RIGHT) {
+          if (r < nb && t0 + c < n) *B.at(b, r, t0 + c) = v;
+        } else {
+          if (t0 + r < n && c < nb) {
+            *B.at(b, t0 + r, c) = v;
+            if (flag) {
+              // L21 = A21 U11^{-1}: the updated column entry l u_cc of a row below the block
+              // must not exceed the pivot u_cc (partial-pivoting check, izamax order)
+              const cplx u = ld(Dg.at(b, c, c));
+              if (cabs1(cmul(mk(v.x, v.y), u)) > cabs1(u)) atomicOr(flag, ST_PIVOT);
+            }
           }
         }
       }
-    }
+    __syncthreads();  // this strip buffer is refilled two iterations on
+  }
 }
 
 int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, bool right, bool upper, ZMat Dg,
                   int* pivot_flag) {
   if (n <= 0) return PFX_OK;
   if (nb > TM_T) return fail(PFX_BADARG, "ztrmm_inplace: nb > 64");
-  const int smem = (TM_T * (TM_T + 4) + TM_T * (TM_T + 4)) * (int)sizeof(double2);
+  // T + two strip buffers (64 x 34 left / 32 x 68 right)
+  const int smem = (TM_T * (TM_T + 4) + 2 * TM_T * (TM_W + 2)) * (int)sizeof(double2);
+  static_assert(TM_T * (TM_W + 2) >= TM_W * (TM_T + 4), "strip buffer size");
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(ztrmm_kernel<false>), smem)) return rc;
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(ztrmm_kernel<true>), smem)) return rc;
-  dim3 grid((unsigned)ceil_div(n, TM_W), (unsigned)batch);
+  // about one CTA per SM in all (two strip buffers + T: 139 KB of shared memory per CTA)
+  const int nstrips = (int)ceil_div(n, TM_W);
+  const int per_sys = std::max(1, std::min(nstrips, device_sms() / batch));
+  dim3 grid((unsigned)per_sys, (unsigned)batch);
   const double fl = 4.0 * nb * nb * (double)n * batch;  // triangular: half the square product
   if (right)
     PFX_LAUNCH_F("ztrmm", s, fl,
