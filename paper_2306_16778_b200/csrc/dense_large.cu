@@ -25,7 +25,7 @@
 namespace pfx {
 
 constexpr int DL_NB = 64;
-constexpr int DL_GROUP = 2;  // panels per delayed trailing update (K = 64 G)
+constexpr int DL_GROUP = 4;  // panels per delayed trailing update (K = 64 G)
 
 __global__ void dl_build(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
                          double shift_c, const double2* theta, int npairs, int nsys, ZMat M, ZMat X) {
