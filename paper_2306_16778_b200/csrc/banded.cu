@@ -28,24 +28,49 @@ namespace pfx {
 
 constexpr int BD_NB = 64;
 
-// grid (row groups, pairs): each warp writes whole rows of the padded row band (no index
-// division: the band is ~40 GB for C5, so this is a pure HBM write stream)
+// grid (row groups, systems): each warp writes whole rows of the padded row band (no index
+// division: the band is ~40 GB for C5, so this is a pure HBM write stream).
+// Partitioned solve (nparts = 2, SPIKE): system s = part * npairs + k holds the rows of
+// partition `part` (Np = N / 2 rows each), the second partition REVERSED (local row i <->
+// global row N - 1 - i), so both factorisations run top-down in one batch and each
+// partition's interface rows are its last ones.  Couplings across the partition boundary are
+// left out here (bd_spike_*).  Global rows [g0, g1) of every system are built.
+__device__ __forceinline__ double band_at(const double* band, int64_t N, int kb, int64_t gi, int64_t gj) {
+  const int64_t d = gj - gi;
+  const int64_t ad = d < 0 ? -d : d;
+  if (ad > kb || gi < 0 || gj < 0 || gi >= N || gj >= N) return 0.0;
+  return band[ad * N + (gi < gj ? gi : gj)];
+}
+
 __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const double* V, int nrhs, double shift_c,
-                         const double2* theta, ZMat M, ZMat X, int64_t i0, int64_t i1) {  // rows [i0, i1)
-  const int k = blockIdx.y;
+                         const double2* theta, ZMat M, ZMat X, int64_t g0, int64_t g1, int npairs, int nparts,
+                         int64_t Np) {
+  const int s = blockIdx.y;
+  const int part = s / npairs, k = s - part * npairs;
   const cplx th = ld(&theta[k]);
-  double2* base = M.p - (kb + BD_NB) + k * M.stride;  // row-band base of pair k
+  double2* base = M.p - (kb + BD_NB) + s * M.stride;  // row-band base of system s
+  // local rows of this system whose global row lies in [g0, g1)
+  int64_t i0, i1;
+  if (part == 0) {
+    i0 = g0 < Np ? g0 : Np;
+    i1 = g1 < Np ? g1 : Np;
+  } else {
+    const int64_t a = (N - g1) > 0 ? N - g1 : 0, b = N - g0;  // local = N - 1 - global
+    i0 = a;
+    i1 = b < Np ? b : Np;
+  }
+  if (i1 <= i0) return;
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = i0 + wid; i < i1; i += nw) {
     double2* rowp = base + i * Wd;
+    const int64_t gi = part ? N - 1 - i : i;
     for (int e = lane; e < Wd; e += 32) {
-      const int off = e - (kb + BD_NB);  // j - i
+      const int off = e - (kb + BD_NB);  // local j - i
       const int64_t j = i + off;
-      const int ao = off < 0 ? -off : off;
       double v = 0.0;
-      if (ao <= kb && j >= 0 && j < N) v = ao == 0 ? band[i] : band[(int64_t)ao * N + (off < 0 ? j : i)];
+      if (j >= 0 && j < Np) v = band_at(band, N, kb, gi, part ? N - 1 - j : j);
       double2 z = make_double2(v, 0.0);
       if (off == 0) {
         z.x = (v - shift_c) + th.re;
@@ -55,17 +80,19 @@ __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const do
     }
   }
   for (int64_t e = i0 * nrhs + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < i1 * nrhs;
-       e += (int64_t)gridDim.x * blockDim.x)
-    X.p[k * X.stride + e] = make_double2(V[e], 0.0);
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / nrhs, c = e - i * nrhs;
+    const int64_t gi = part ? N - 1 - i : i;
+    X.p[s * X.stride + e] = make_double2(V[gi * nrhs + c], 0.0);
+  }
 }
-
 
 // The factorisation + solves touch only the workspace, so the ~8 launches per 64-row
 // block step are captured once into a CUDA graph per (shape, workspace) and replayed:
 // the per-launch host overhead was the bound of this path (N/64 = 4096 block steps).
-// Block back substitution y1 = U11^{-1} (y1 - U12 y2) for one 64-row block, all pairs:
+// Block back substitution y1 = U11^{-1} (y1 - U12 y2) for one 64-row block, all systems:
 // bd_back_partial splits the kb-long inner dimension into 32-wide chunks (one CTA per chunk
-// and pair: P[q] = U12[:, chunk q] y2[chunk q]), bd_back_finish sums the chunks in
+// and system: P[q] = U12[:, chunk q] y2[chunk q]), bd_back_finish sums the chunks in
 // ascending order (deterministic), subtracts, and applies the stored U11^{-1}.
 constexpr int BK_C = 32;
 
@@ -80,26 +107,32 @@ struct BdCombine {
   const double2* coef;
   double scale;
   double* out;
+  int npairs, nparts;  // systems = nparts x npairs (partition 1 reversed)
+  int64_t Np, N;       // rows per system, global rows
 };
 
-__device__ void bd_combine_rows(const ZMat& X, int64_t j0, int jb, int nr, int npairs, const BdCombine* cmb) {
+__device__ void bd_combine_rows(const ZMat& X, int64_t j0, int jb, int nr, const BdCombine* cmb) {
   const double2* coef = cmb->coef;
   const double sc = cmb->scale;
-  for (int e = threadIdx.x; e < jb * nr; e += blockDim.x) {
-    const int64_t i = (j0 + e / nr) * nr + e % nr;  // element of the N x nr block
-    double acc = 0.0;
-    for (int k = 0; k < npairs; ++k) {
-      const cplx a = ld(&coef[k]);
-      const double2 x = X.p[k * X.stride + i];
-      const double sk = 2.0 * fma(a.re, x.x, -a.im * x.y);
-      acc = k == 0 ? sk : acc + sk;
+  const int npairs = cmb->npairs;
+  for (int part = 0; part < cmb->nparts; ++part)
+    for (int e = threadIdx.x; e < jb * nr; e += blockDim.x) {
+      const int64_t li = j0 + e / nr, c = e % nr;
+      const int64_t i = li * nr + c;  // element of the system's Np x nr block
+      double acc = 0.0;
+      for (int k = 0; k < npairs; ++k) {
+        const cplx a = ld(&coef[k]);
+        const double2 x = X.p[(part * npairs + k) * X.stride + i];
+        const double sk = 2.0 * fma(a.re, x.x, -a.im * x.y);
+        acc = k == 0 ? sk : acc + sk;
+      }
+      const int64_t gi = part ? cmb->N - 1 - li : li;
+      cmb->out[gi * nr + c] = sc == 1.0 ? acc : sc * acc;
     }
-    cmb->out[i] = sc == 1.0 ? acc : sc * acc;
-  }
 }
 
-__global__ void bd_combine_block(ZMat X, int64_t j0, int jb, int nr, int npairs, const BdCombine* cmb) {
-  bd_combine_rows(X, j0, jb, nr, npairs, cmb);
+__global__ void bd_combine_block(ZMat X, int64_t j0, int jb, int nr, const BdCombine* cmb) {
+  bd_combine_rows(X, j0, jb, nr, cmb);
 }
 
 // grid (nq + 1, npairs): CTA x = nq (pair 0 only) is the ride-along combine of the block
@@ -111,7 +144,7 @@ __global__ void __launch_bounds__(256) bd_back_partial(ZMat M, ZMat X, int64_t j
   __shared__ __align__(16) double2 xs[BK_C][9];
   const int q = blockIdx.x, b = blockIdx.y;
   if (q == nq) {
-    if (b == 0) bd_combine_rows(X, cj0, cjb, nr, gridDim.y, cmb);
+    if (b == 0) bd_combine_rows(X, cj0, cjb, nr, cmb);
     return;
   }
   const int tid = threadIdx.x;
@@ -191,6 +224,165 @@ __global__ void __launch_bounds__(256) bd_back_finish(ZMat X, ZMat Ui, int64_t j
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two-partition SPIKE interface (nparts = 2).  With M0 (rows [0, Np)) and the reversed M1
+// (rows [Np, N) read backwards) factored side by side, the bottom KB rows of each system are the
+// interface (KB >= kb, rounded so the region starts on a 64-row block).  E0 (KB x KB) couples
+// partition 0's interface rows to partition 1's interface unknowns (its local order), and
+// E1 = E0^T the other way (A symmetric).  With y = L^{-1} f from the forward elimination:
+//   V_p = U_bb^{-1} L_bb^{-1} E_p,  g_p = U_bb^{-1} y_bb        (bottom-block products only:
+//        a right-hand side zero above the interface stays zero under L^{-1}, and the bottom
+//        rows of U^{-1} z involve only z's bottom rows)
+//   [I V0; V1 I] [a; b] = [g0; g1]  ->  (I - V0 V1) a = g0 - V0 g1,  b = g1 - V1 a
+//   y0_bb -= L0_bb^{-1} (E0 b),  y1_bb -= L1_bb^{-1} (E1 a)           (the coupling moved to
+//        the right-hand side; only the interface rows of y change)
+// then the ordinary back substitution of both partitions gives the exact solution: the
+// chain of dependent block steps is half as long (N / 2 / 64 instead of N / 64).
+struct BdSpike {
+  int KB = 0;               // interface rows per system
+  int64_t R0 = 0;           // first interface row (local), a multiple of 64
+  ZMat W{nullptr, 0, 0};    // nsys x KB x (KB + nr): [coupling | y_bb] -> [V | g]
+  ZMat E{nullptr, 0, 0};    // KB x KB (E0), batch stride 0
+  ZMat Et{nullptr, 0, 0};   // KB x KB (E0^T), batch stride 0
+  ZMat S{nullptr, 0, 0};    // npairs x KB x KB
+  ZMat AB{nullptr, 0, 0};   // nsys x KB x nr: interface unknowns a (part 0), b (part 1)
+  ZMat T{nullptr, 0, 0};    // nsys x KB x nr: corrections
+  ZMat LiS{nullptr, 0, 0}, UiS{nullptr, 0, 0};  // npairs x (KB / 64) x 64 x 64
+  const double* band = nullptr;
+  int64_t N = 0;
+  int kb = 0;
+};
+
+__global__ void bd_spike_coupling(const double* band, int64_t N, int kb, int64_t Np, int KB, ZMat E, ZMat Et) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)KB * KB;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / KB), t = (int)(e - (e / KB) * KB);
+    const int64_t g0 = Np - KB + r;           // partition 0 interface row r (global)
+    const int64_t g1 = N - 1 - (Np - KB + t);  // partition 1 interface row t (global)
+    const double v = band_at(band, N, kb, g0, g1);
+    E.p[(int64_t)r * E.ld + t] = make_double2(v, 0.0);
+    Et.p[(int64_t)t * Et.ld + r] = make_double2(v, 0.0);
+  }
+}
+
+// W[s] = [E_s | y_s(interface rows)]
+__global__ void bd_spike_setup(ZMat W, ZMat E, ZMat Et, ZMat X, int64_t R0, int KB, int nr, int npairs) {
+  const int s = blockIdx.y;
+  const ZMat& C = s < npairs ? E : Et;
+  const int w = KB + nr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)KB * w;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / w), c = (int)(e - (e / w) * w);
+    W.p[s * W.stride + (int64_t)r * W.ld + c] = c < KB ? C.p[(int64_t)r * C.ld + c] : *X.at(s, R0 + r, c - KB);
+  }
+}
+
+// S[k] = I;  AB[k] = g0 (R, the right-hand side of S a = g0 - V0 g1);  AB[npairs + k] = g1
+__global__ void bd_spike_init(ZMat S, ZMat AB, ZMat W, int KB, int nr, int npairs) {
+  const int k = blockIdx.y;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)KB * KB;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / KB), c = (int)(e - (e / KB) * KB);
+    S.p[k * S.stride + e] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)KB * nr;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / nr), c = (int)(e - (e / nr) * nr);
+    AB.p[k * AB.stride + e] = W.p[k * W.stride + (int64_t)r * W.ld + KB + c];
+    AB.p[(npairs + k) * AB.stride + e] = W.p[(npairs + k) * W.stride + (int64_t)r * W.ld + KB + c];
+  }
+}
+
+// X[s](interface rows) -= T[s]
+__global__ void bd_spike_correct(ZMat X, ZMat T, int64_t R0, int KB, int nr) {
+  const int s = blockIdx.y;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)KB * nr;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / nr), c = (int)(e - (e / nr) * nr);
+    double2* x = X.at(s, R0 + r, c);
+    const double2 t = T.p[s * T.stride + e];
+    *x = make_double2(x->x - t.x, x->y - t.y);
+  }
+}
+
+int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
+                   bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb);
+
+// B = L_bb^{-1} B (lower = true) or U_bb^{-1} B, over the interface rows [R0, R0 + KB) of every
+// system's band factors; B: KB x ncols dense per system.  Blocked by the band LU's own 64-row
+// blocks and their stored diagonal inverses.
+static int bd_region_solve(cudaStream_t st, int nsys, ZMat M, ZMat Li, ZMat Ui, int64_t R0, int KB, ZMat B, int ncols,
+                           bool lower) {
+  const int nb = BD_NB;
+  const int nbk = (KB + nb - 1) / nb;  // the last block may be partial (Np not a multiple of 64)
+  auto sub = [](ZMat A, int64_t i, int64_t j) {
+    ZMat r = A;
+    r.p = A.p + i * A.ld + j;
+    return r;
+  };
+  auto blk = [&](ZMat T, int64_t j0) {
+    ZMat r = T;
+    r.p = T.p + (j0 / nb) * nb * nb;
+    return r;
+  };
+  int rc;
+  for (int q = 0; q < nbk; ++q) {
+    const int p = lower ? q : nbk - 1 - q;
+    const int64_t j0 = R0 + (int64_t)p * nb;
+    const int jb = std::min(nb, KB - p * nb);
+    if (lower) {
+      if (p > 0 && (rc = zgemm(st, nsys, jb, ncols, p * nb, -1.0, sub(M, j0, R0), sub(B, 0, 0), sub(B, p * nb, 0))))
+        return rc;
+      if ((rc = ztrmm_inplace(st, nsys, jb, ncols, blk(Li, j0), sub(B, p * nb, 0), false, false))) return rc;
+    } else {
+      const int below = KB - p * nb - jb;
+      if (below > 0 && (rc = zgemm(st, nsys, jb, ncols, below, -1.0, sub(M, j0, j0 + jb), sub(B, p * nb + jb, 0),
+                                   sub(B, p * nb, 0))))
+        return rc;
+      if ((rc = ztrmm_inplace(st, nsys, jb, ncols, blk(Ui, j0), sub(B, p * nb, 0), false, true))) return rc;
+    }
+  }
+  return PFX_OK;
+}
+
+static int bd_spike_interface(cudaStream_t st, const BdSpike& sp, ZMat M, ZMat X, ZMat Li, ZMat Ui, int64_t Np,
+                              int nr, int npairs, int* sing) {
+  const int KB = sp.KB, nsys = 2 * npairs;
+  int rc;
+  ZMat Wv = sp.W;  // V columns [0, KB) of W
+  ZMat Wg = sp.W;  // g columns [KB, KB + nr)
+  Wg.p = sp.W.p + KB;
+  PFX_LAUNCH("bd_spike", st, bd_spike_coupling<<<296, 256, 0, st>>>(sp.band, sp.N, sp.kb, Np, KB, sp.E, sp.Et));
+  PFX_CUDA_TRY(cudaGetLastError());
+  PFX_LAUNCH("bd_spike", st, bd_spike_setup<<<dim3(64, nsys), 256, 0, st>>>(sp.W, sp.E, sp.Et, X, sp.R0, KB, nr, npairs));
+  PFX_CUDA_TRY(cudaGetLastError());
+  // V = U_bb^{-1} L_bb^{-1} E (coupling columns), g = U_bb^{-1} y_bb (right-hand-side columns)
+  if ((rc = bd_region_solve(st, nsys, M, Li, Ui, sp.R0, KB, Wv, KB, true))) return rc;
+  if ((rc = bd_region_solve(st, nsys, M, Li, Ui, sp.R0, KB, Wv, KB + nr, false))) return rc;
+  PFX_LAUNCH("bd_spike", st, bd_spike_init<<<dim3(64, npairs), 256, 0, st>>>(sp.S, sp.AB, sp.W, KB, nr, npairs));
+  PFX_CUDA_TRY(cudaGetLastError());
+  ZMat V0 = Wv, V1 = Wv, g1 = Wg;
+  V1.p = Wv.p + npairs * Wv.stride;
+  g1.p = Wg.p + npairs * Wg.stride;
+  ZMat A0 = sp.AB, A1 = sp.AB;  // a (part 0), b (part 1) slots
+  A1.p = sp.AB.p + npairs * sp.AB.stride;
+  // S = I - V0 V1,  a-slot = g0 - V0 g1,  a = S^{-1} (a-slot)
+  if ((rc = zgemm(st, npairs, KB, KB, KB, -1.0, V0, V1, sp.S))) return rc;
+  if ((rc = zgemm(st, npairs, KB, nr, KB, -1.0, V0, g1, A0))) return rc;
+  if ((rc = lu_solve_nopiv(st, npairs, KB, sp.S, A0, sp.LiS, sp.UiS, nr, sing, false, false, false, nullptr))) return rc;
+  // b = g1 - V1 a
+  if ((rc = zgemm(st, npairs, KB, nr, KB, -1.0, V1, A0, A1))) return rc;
+  // corrections T0 = L0_bb^{-1} (E0 b), T1 = L1_bb^{-1} (E1 a), applied to the interface rows of y
+  ZMat T0 = sp.T, T1 = sp.T;
+  T1.p = sp.T.p + npairs * sp.T.stride;
+  if ((rc = zgemm(st, npairs, KB, nr, KB, 1.0, sp.E, A1, T0, false))) return rc;
+  if ((rc = zgemm(st, npairs, KB, nr, KB, 1.0, sp.Et, A0, T1, false))) return rc;
+  if ((rc = bd_region_solve(st, nsys, M, Li, Ui, sp.R0, KB, sp.T, nr, true))) return rc;
+  PFX_LAUNCH("bd_spike", st, bd_spike_correct<<<dim3(8, nsys), 256, 0, st>>>(X, sp.T, sp.R0, KB, nr));
+  PFX_CUDA_TRY(cudaGetLastError());
+  return PFX_OK;
+}
+
 // Three streams inside one captured graph: the critical chain (diagonal LU -> inverses ->
 // L21 -> A22 update -> next LU) stays on `main`; U12 = L11^{-1} M12 runs beside L21 on
 // `s1`; the right-hand-side elimination (y1 = L11^{-1} y1, y2 -= L21 y1) trails on `s2`,
@@ -220,8 +412,9 @@ static int bd_streams(BdStreams& S) {
   return PFX_OK;
 }
 
+// N, npairs: rows per system and systems in the batch (SPIKE: Np and 2 npairs; sp the interface)
 static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui, double2* P, int64_t N, int kb,
-                           int nr, int npairs, int* sing, const BdCombine* cmb) {
+                           int nr, int npairs, int* sing, const BdCombine* cmb, const BdSpike* sp) {
   const int nb = BD_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -313,6 +506,7 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
   if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));
   PFX_CUDA_TRY(cudaEventRecord(evR, S.s2));
   PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evR, 0));
+  if (sp && (rc = bd_spike_interface(stream, *sp, M, X, Li, Ui, N, nr, npairs / 2, sing))) return rc;
   const int64_t nblk = (N + nb - 1) / nb;
   for (int64_t pb = nblk - 1; pb >= 0 && !(skip & 1); --pb) {
     const int64_t j0 = pb * nb;
@@ -338,7 +532,7 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
   if (!(skip & 1)) {
     // block 0 (the last one the back substitution finishes)
     PFX_LAUNCH("bd_combine_block", stream,
-               bd_combine_block<<<1, 256, 0, stream>>>(X, 0, (int)std::min<int64_t>(nb, N), nr, npairs, cmb));
+               bd_combine_block<<<1, 256, 0, stream>>>(X, 0, (int)std::min<int64_t>(nb, N), nr, cmb));
     PFX_CUDA_TRY(cudaGetLastError());
   }
   return PFX_OK;
@@ -350,6 +544,7 @@ struct BdGraph {
   void* ws = nullptr;
   int64_t N = 0;
   int kb = 0, nr = 0, np = 0;
+  const double* band = nullptr;
 };
 BdGraph g_bd_graph[kMaxDevices];  // per device: a graph is bound to the device it was captured on
 }  // namespace
@@ -363,26 +558,71 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   const int kb = (int)kb64;
   const int nb = BD_NB;
   const int Wd = 2 * kb + 2 * nb + 1;
-  const size_t mbytes = (size_t)npairs * N * Wd * sizeof(double2);
-  const size_t xbytes = (size_t)npairs * N * nrhs * sizeof(double2);
-  const int64_t nblk = (N + nb - 1) / nb;
-  const size_t libytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
-  const size_t uibytes = (size_t)npairs * nblk * nb * nb * sizeof(double2);
-  const size_t pbytes = (size_t)npairs * ceil_div(kb, BK_C) * nb * nrhs * sizeof(double2);
-  char* ws = static_cast<char*>(scratch(1, mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64));
+  // Two-partition SPIKE (BdSpike) when the halves are long against the band: the serial chain of
+  // block steps halves.  PFX_BD_SPIKE=0 keeps the single-partition factorisation.
+  static const bool spike_on = [] {
+    const char* e = getenv("PFX_BD_SPIKE");
+    return !(e && atoi(e) == 0);
+  }();
+  const int64_t Nh = N / 2;
+  const int KB = kb > 0 ? (int)(Nh - ((Nh - kb) / nb) * nb) : 0;  // interface rows, from a block start
+  const bool spike = spike_on && kb > 0 && N % 2 == 0 && Nh >= 8 * (int64_t)kb && Nh >= 4 * nb && KB <= 1024 &&
+                     (Nh - KB) % nb == 0;
+  const int nparts = spike ? 2 : 1;
+  const int64_t Np = spike ? Nh : N;  // rows per system
+  const int nsys = nparts * npairs;
+  const size_t mbytes = (size_t)nsys * Np * Wd * sizeof(double2);
+  const size_t xbytes = (size_t)nsys * Np * nrhs * sizeof(double2);
+  const int64_t nblk = (Np + nb - 1) / nb;
+  const size_t libytes = (size_t)nsys * nblk * nb * nb * sizeof(double2);
+  const size_t uibytes = (size_t)nsys * nblk * nb * nb * sizeof(double2);
+  const size_t pbytes = (size_t)nsys * ceil_div(kb, BK_C) * nb * nrhs * sizeof(double2);
+  // SPIKE interface buffers
+  const size_t wbytes = spike ? (size_t)nsys * KB * (KB + nrhs) * sizeof(double2) : 0;
+  const size_t ebytes = spike ? (size_t)2 * KB * KB * sizeof(double2) : 0;
+  const size_t sbytes = spike ? (size_t)npairs * KB * KB * sizeof(double2) : 0;
+  const size_t abbytes = spike ? (size_t)2 * nsys * KB * nrhs * sizeof(double2) : 0;
+  const int kbb = (KB + nb - 1) / nb;  // 64-row blocks of the interface
+  const size_t lsbytes = spike ? (size_t)2 * npairs * kbb * nb * nb * sizeof(double2) : 0;
+  const size_t base_bytes = mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64;
+  char* ws = static_cast<char*>(scratch(1, base_bytes + wbytes + ebytes + sbytes + abbytes + lsbytes + 256));
   if (!ws) return fail(PFX_CUDA, "banded workspace allocation failed (needs " + std::to_string((mbytes + xbytes) >> 20) + " MiB)");
-  ZMat M{reinterpret_cast<double2*>(ws) + kb + nb, Wd - 1, (int64_t)N * Wd};
-  ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, N * nrhs};
+  ZMat M{reinterpret_cast<double2*>(ws) + kb + nb, Wd - 1, (int64_t)Np * Wd};
+  ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, Np * nrhs};
   ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), nb, nblk * nb * nb};
   ZMat Ui{reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes), nb, nblk * nb * nb};
   double2* P = reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes + uibytes);
   int* sing = reinterpret_cast<int*>(ws + mbytes + xbytes + libytes + uibytes + pbytes);
   PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+  BdSpike sp;
+  if (spike) {
+    double2* q = reinterpret_cast<double2*>(ws + base_bytes);
+    sp.KB = KB;
+    sp.R0 = Np - KB;
+    sp.W = ZMat{q, KB + nrhs, (int64_t)KB * (KB + nrhs)};
+    q += (size_t)nsys * KB * (KB + nrhs);
+    sp.E = ZMat{q, KB, 0};
+    q += (size_t)KB * KB;
+    sp.Et = ZMat{q, KB, 0};
+    q += (size_t)KB * KB;
+    sp.S = ZMat{q, KB, (int64_t)KB * KB};
+    q += (size_t)npairs * KB * KB;
+    sp.AB = ZMat{q, nrhs, (int64_t)KB * nrhs};
+    q += (size_t)nsys * KB * nrhs;
+    sp.T = ZMat{q, nrhs, (int64_t)KB * nrhs};
+    q += (size_t)nsys * KB * nrhs;
+    sp.LiS = ZMat{q, nb, (int64_t)kbb * nb * nb};
+    q += (size_t)npairs * kbb * nb * nb;
+    sp.UiS = ZMat{q, nb, (int64_t)kbb * nb * nb};
+    sp.band = band;
+    sp.N = N;
+    sp.kb = kb;
+  }
   // combine parameters (device copy read by the graph-captured back substitution)
   BdCombine* cmb_d = reinterpret_cast<BdCombine*>(ws + mbytes + xbytes + libytes + uibytes + pbytes + 256);
   {
     static_assert(sizeof(BdCombine) <= 64, "combine parameters fit their slot");
-    const BdCombine h{coef_d, shift_c == 0.0 ? 1.0 : exp(shift_c), out};
+    const BdCombine h{coef_d, shift_c == 0.0 ? 1.0 : exp(shift_c), out, npairs, nparts, Np, N};
     // pageable source: the runtime stages it before returning, so a stack value is safe
     PFX_CUDA_TRY(cudaMemcpyAsync(cmb_d, &h, sizeof(h), cudaMemcpyHostToDevice, stream));
   }
@@ -392,10 +632,11 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
     PFX_CUDA_TRY(cudaEventCreate(&e1));
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
-  dim3 bg(1184, npairs);
+  dim3 bg((unsigned)(nsys > 8 ? 592 : 1184), nsys);
   if (!band_host) {
     PFX_LAUNCH("bd_build", stream,
-               bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X, 0, N));
+               bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X, 0, N, npairs,
+                                                nparts, Np));
     PFX_CUDA_TRY(cudaGetLastError());
   } else {
     constexpr int NCH = 8;
@@ -431,18 +672,20 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
       PFX_CUDA_TRY(cudaEventRecord(evs[c], cin));
       PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evs[c], 0));
       PFX_LAUNCH("bd_build", stream,
-                 bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X, i0, i1));
+                 bd_build<<<bg, 256, 0, stream>>>(band, N, kb, Wd, V, (int)nrhs, shift_c, theta_d, M, X, i0, i1, npairs,
+                                                  nparts, Np));
       PFX_CUDA_TRY(cudaGetLastError());
     }
   }
   if (prof_on()) {
     // profiling wants per-kernel events: run the launches directly
-    if (int rc = bd_factor_solve(stream, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing, cmb_d)) return rc;
+    if (int rc = bd_factor_solve(stream, M, X, Li, Ui, P, Np, kb, (int)nrhs, nsys, sing, cmb_d, spike ? &sp : nullptr))
+      return rc;
   } else {
     const int gdev = current_device();
     if (gdev < 0 || gdev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
     BdGraph& G = g_bd_graph[gdev];
-    if (!G.exec || G.ws != ws || G.N != N || G.kb != kb || G.nr != (int)nrhs || G.np != npairs) {
+    if (!G.exec || G.ws != ws || G.N != N || G.kb != kb || G.nr != (int)nrhs || G.np != npairs || G.band != band) {
       if (G.exec) {
         cudaGraphExecDestroy(G.exec);
         G.exec = nullptr;
@@ -455,7 +698,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
       PFX_CUDA_TRY(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
       cudaGraph_t graph;
       PFX_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int rc = bd_factor_solve(cs, M, X, Li, Ui, P, N, kb, (int)nrhs, npairs, sing, cmb_d);
+      int rc = bd_factor_solve(cs, M, X, Li, Ui, P, Np, kb, (int)nrhs, nsys, sing, cmb_d, spike ? &sp : nullptr);
       cudaError_t ce = cudaStreamEndCapture(cs, &graph);
       if (rc) return rc;
       if (ce != cudaSuccess) return fail(PFX_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -468,6 +711,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
       G.kb = kb;
       G.nr = (int)nrhs;
       G.np = npairs;
+      G.band = band;  // the SPIKE coupling kernel reads the band
     }
     PFX_CUDA_TRY(cudaGraphLaunch(G.exec, stream));
   }

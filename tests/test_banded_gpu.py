@@ -68,3 +68,26 @@ def test_wide_band_many_rhs(N, kb, nrhs):
     got = matexp_action(BandedHermitian(band), V, ExpOptions(n=16, mode="action")).value
     want = restate.banded_action(band, V, 16)
     assert rel(got, want) <= TOL, rel(got, want)
+
+
+@pytest.mark.parametrize("nx,ny,nrhs", [(32, 24, 3), (48, 40, 1), (64, 20, 9), (100, 26, 2)])
+def test_two_partition_spike_grids(nx, ny, nrhs):
+    """Even N with halves >= 8 kb: the band solve runs as two partitions (SPIKE, the second
+    reversed) coupled through their interface rows; the result must match zgbsv on the whole
+    band, including grids whose interface region is rounded up to a 64-row block."""
+    band = workloads.c5_band_rect(nx, ny, scale=3.0)
+    V = np.random.default_rng(nx * 7 + ny).standard_normal((nx * ny, nrhs))
+    got = matexp_action(BandedHermitian(band), V, ExpOptions(n=16, mode="action")).value
+    want = restate.banded_action(band, V, 16)
+    assert rel(got, want) <= TOL, rel(got, want)
+
+
+def test_two_partition_spike_random_band():
+    rng = np.random.default_rng(77)
+    N, kb = 3000, 90
+    band = rng.uniform(-1, 1, (kb + 1, N)) * (0.5 / np.sqrt(kb + 1))
+    band[0] = -rng.uniform(0.5, 3.0, N)
+    V = rng.standard_normal((N, 4))
+    got = matexp_action(BandedHermitian(band), V, ExpOptions(n=20, mode="action")).value
+    want = restate.banded_action(band, V, 20)
+    assert rel(got, want) <= TOL, rel(got, want)
