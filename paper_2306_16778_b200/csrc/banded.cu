@@ -389,8 +389,8 @@ static int bd_spike_interface(cudaStream_t st, const BdSpike& sp, ZMat M, ZMat X
 // where it overlaps the next block steps (its inputs, L11^{-1} per block and the L21
 // columns, are never written again).
 struct BdStreams {
-  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr, s4 = nullptr, s5 = nullptr;
+  cudaEvent_t ev[10] = {};
 };
 static int bd_streams(BdStreams& S) {
   static BdStreams gs[kMaxDevices];
@@ -404,6 +404,7 @@ static int bd_streams(BdStreams& S) {
     PFX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s1, cudaStreamNonBlocking, hi));
     PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s4, cudaStreamNonBlocking, hi));
+    PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s5, cudaStreamNonBlocking, hi));
     PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s2, cudaStreamNonBlocking, lo));
     PFX_CUDA_TRY(cudaStreamCreateWithPriority(&g.s3, cudaStreamNonBlocking, lo));
     for (auto& e : g.ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -436,7 +437,8 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
     return e ? atoi(e) : 0;
   }();
   cudaEvent_t evT = S.ev[0], evU = S.ev[1], evL = S.ev[2], evR = S.ev[3], evP = S.ev[4], evB = S.ev[5];
-  cudaEvent_t evS = S.ev[6], evA = S.ev[7];
+  cudaEvent_t evS = S.ev[6], evA = S.ev[7], evT2 = S.ev[8];
+  bool pending_t2 = false;  // a t2 (far trailing update) is queued on s3
   bool pending_s = false;  // strips of the previous step queued on s4
   // s2 / s3 start after everything already queued on main (the build kernel)
   PFX_CUDA_TRY(cudaEventRecord(evT, stream));
@@ -464,14 +466,18 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
                                 sub(X, j0 + jb, 0))))
       return rc;
     if (rest > 0) {
-      // look-ahead: only the next diagonal block (ra x ra) is updated on main before the next
-      // LU; the rest of the next row / column strips (needed by the next panel products)
-      // go to s4, and the trailing (rest - ra)^2 part to s3, both overlapping the next LU /
-      // inverses.  Everything here lies inside the previous step's trailing region, so main
-      // waits for it (evB) first.
+      // Depth-two look-ahead.  Step j's update A -= L[:, j] U[j, :] of the coupled region
+      // [j + 1, j + 1 + kb)^2 is split by how soon it is needed:
+      //   main  the next diagonal block (ra x ra), before the next LU;
+      //   s4    the rest of the next row / column strips (the next panel products read them);
+      //   s5    t1: the row / column strips of block j + 2 (needed by the NEXT step's diagonal
+      //         update and strips) -- waits for t2 of the previous step, which covered them;
+      //   s3    t2: everything from block j + 3 on, needed only two steps later.
+      // So the critical chain waits for a 64-wide L-shaped strip, not for the whole trailing
+      // update (which, with 2 x npairs systems per launch under SPIKE, outlasted the chain).
       const int ra = std::min(nb, rest);
       PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
-      if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));
+      if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));  // t1 of the previous step
       PFX_CUDA_TRY(cudaEventRecord(evP, stream));  // panels of this step are final
       if ((rc = zgemm(stream, npairs, ra, ra, jb, -1.0, sub(M, j0 + jb, j0), sub(M, j0, j0 + jb),
                       sub(M, j0 + jb, j0 + jb))))
@@ -489,21 +495,35 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
         PFX_CUDA_TRY(cudaEventRecord(evS, S.s4));
         pending_s = true;
         if (!(skip & 4)) {
-          // the trailing update becomes ready together with the next block's LU (both after
-          // the diagonal-block update), so the higher-priority LU is dispatched first
+          const int64_t k0 = j0 + jb + ra;     // first row / column of block j + 2
+          const int r2 = rest - ra;            // coupled rows / cols from block j + 2 on
+          const int rb = std::min(nb, r2);     // block j + 2
+          // t1: block j + 2's row strip (rb x r2) and column strip ((r2 - rb) x rb)
           PFX_CUDA_TRY(cudaEventRecord(evA, stream));
-          PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evA, 0));
-          if ((rc = zgemm(S.s3, npairs, rest - ra, rest - ra, jb, -1.0, sub(M, j0 + jb + ra, j0),
-                          sub(M, j0, j0 + jb + ra), sub(M, j0 + jb + ra, j0 + jb + ra))))
+          PFX_CUDA_TRY(cudaStreamWaitEvent(S.s5, evA, 0));
+          if (pending_t2) PFX_CUDA_TRY(cudaStreamWaitEvent(S.s5, evT2, 0));
+          if ((rc = zgemm(S.s5, npairs, rb, r2, jb, -1.0, sub(M, k0, j0), sub(M, j0, k0), sub(M, k0, k0)))) return rc;
+          if (r2 > rb && (rc = zgemm(S.s5, npairs, r2 - rb, rb, jb, -1.0, sub(M, k0 + rb, j0), sub(M, j0, k0),
+                                     sub(M, k0 + rb, k0))))
             return rc;
-          PFX_CUDA_TRY(cudaEventRecord(evB, S.s3));
+          PFX_CUDA_TRY(cudaEventRecord(evB, S.s5));
           pending_b = true;
+          // t2: the rest, two steps of slack (s3 keeps the steps' t2 in order)
+          if (r2 > rb) {
+            PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evA, 0));
+            if ((rc = zgemm(S.s3, npairs, r2 - rb, r2 - rb, jb, -1.0, sub(M, k0 + rb, j0), sub(M, j0, k0 + rb),
+                            sub(M, k0 + rb, k0 + rb))))
+              return rc;
+            PFX_CUDA_TRY(cudaEventRecord(evT2, S.s3));
+            pending_t2 = true;
+          }
         }
       }
     }
   }
   if (pending_s) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evS, 0));
   if (pending_b) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evB, 0));
+  if (pending_t2) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evT2, 0));
   PFX_CUDA_TRY(cudaEventRecord(evR, S.s2));
   PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evR, 0));
   if (sp && (rc = bd_spike_interface(stream, *sp, M, X, Li, Ui, N, nr, npairs / 2, sing))) return rc;

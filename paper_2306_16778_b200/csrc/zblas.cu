@@ -1098,7 +1098,10 @@ int ztrmm_inplace(cudaStream_t s, int batch, int nb, int n, ZMat Tinv, ZMat B, b
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(ztrmm_kernel<true>), smem)) return rc;
   // about one CTA per SM in all (two strip buffers + T: 139 KB of shared memory per CTA)
   const int nstrips = (int)ceil_div(n, TM_W);
-  const int per_sys = std::max(1, std::min(nstrips, device_sms() / batch));
+  // latency-critical small launches (all strips fit about two CTAs per SM) keep one strip per
+  // CTA; large ones go persistent, one CTA per SM in all
+  const int sms = device_sms();
+  const int per_sys = (int64_t)nstrips * batch <= 2 * sms ? nstrips : std::max(1, std::min(nstrips, sms / batch));
   dim3 grid((unsigned)per_sys, (unsigned)batch);
   const double fl = 4.0 * nb * nb * (double)n * batch;  // triangular: half the square product
   if (right)
