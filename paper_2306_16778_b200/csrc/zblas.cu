@@ -17,11 +17,14 @@ namespace pfx {
 // Row strides (in 16-byte words) for conflict-free DMMA fragment loads: a quarter-warp reads
 // A at rows g (0..1) x columns t (0..3) -> stride 4 mod 8; B at rows t x columns g -> stride
 // 2 mod 8 (KS + 1 and TN + 1 were 2-way conflicted: ncu counted half the wavefronts as excess)
-template <int TM, int TN, int KS>
+// NS-stage cp.async ring (double buffering)
+template <int TM, int TN, int KS, int NS = 2>
 struct GemmSmem {
-  double2 A[2][TM][KS + 4];
-  double2 B[2][KS][TN + 2];
+  double2 A[NS][TM][KS + 4];
+  double2 B[NS][KS][TN + 2];
 };
+template <int TM, int NW>
+__host__ __device__ constexpr int gemm_stages() { return 2; }  // 3 stages on the 4-warp layout: no gain on long K, -14% on K = 128 (tools/zgemm_probe.cu)
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
   unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -216,7 +219,8 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
   constexpr int WN = NW / 2;
   constexpr int FM = TM / 2 / 8, FN = TN / WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GemmSmem<TM, TN, GK>& S = *reinterpret_cast<GemmSmem<TM, TN, GK>*>(smem_raw);
+  constexpr int NS = gemm_stages<TM, NW>();
+  GemmSmem<TM, TN, GK, NS>& S = *reinterpret_cast<GemmSmem<TM, TN, GK, NS>*>(smem_raw);
   const int b = blockIdx.z - ((TM == 64 && NW == 4 && ride.mode != 0) ? 1 : 0);
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -259,13 +263,16 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
       cp_async16_zfill(&S.B[buf][r][c], src, v);
     }
   };
-  if (kt0 < ktiles) load(kt0 & 1, kt0);
-  cp_async_commit();
-  for (int kt = kt0; kt < ktiles; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < ktiles) load(buf ^ 1, kt + 1);
+#pragma unroll
+  for (int st = 0; st < NS - 1; ++st) {
+    if (kt0 + st < ktiles) load(st, kt0 + st);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int kt = kt0; kt < ktiles; ++kt) {
+    const int buf = (kt - kt0) % NS;
+    if (kt + NS - 1 < ktiles) load((kt - kt0 + NS - 1) % NS, kt + NS - 1);
+    cp_async_commit();
+    cp_async_wait<NS - 1>();
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < GK; kk += 4) {
@@ -362,12 +369,13 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
 template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                         bool accumulate, int b_lower_off, const ZCombine* ride) {
-  const int smem = (int)sizeof(GemmSmem<TM, TN, KS>);
+  const int smem = (int)sizeof(GemmSmem<TM, TN, KS, gemm_stages<TM, NW>()>);
   if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgemm_kernel<TM, TN, NW, M3, KS>), smem)) return rc;
   ZCombine rd;
   if (ride) rd = *ride;
   // the combine's shared-memory staging (64 x 65) must fit the GEMM's allocation
-  static_assert(sizeof(GemmSmem<TM, TN, KS>) >= 64 * 65 * sizeof(double2) || TM < 64, "combine staging fits");
+  static_assert(sizeof(GemmSmem<TM, TN, KS, gemm_stages<TM, NW>()>) >= 64 * 65 * sizeof(double2) || TM < 64,
+                "combine staging fits");
   constexpr bool carries = TM == 64 && NW == 4;
   dim3 grid((unsigned)ceil_div(n, TN), (unsigned)ceil_div(m, TM), (unsigned)batch + (ride && carries ? 1 : 0));
   if (ride && !carries) {  // other layouts: the combine goes on its own launch
