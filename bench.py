@@ -388,6 +388,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--prof-steps", type=int, default=3)
     ap.add_argument("--shard", choices=["auto", "pole", "rows", "batch"], default="pole")
+    ap.add_argument("--check", action="store_true",
+                    help="after timing, compare rank 0's sharded result with an unsharded call (check_rel)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -606,6 +608,28 @@ def main():
         e2e = {"value": wl.evals_per_step * args.e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
+    # --check: rank 0's part of the sharded result against the same computation unsharded
+    check_rel = None
+    if args.check:
+        out_sh = compute(stream)
+        torch.cuda.synchronize()
+        if rank == 0:
+            full = Workload(args.workload, torch, dev, 0, npairs)
+            ref = full.step(stream)
+            torch.cuda.synchronize()
+            a = out_sh.reshape(ref.shape[0], -1) if shard != "batch" else out_sh.reshape(out_sh.shape[0], -1)
+            b = ref.reshape(ref.shape[0], -1)
+            if shard == "rows":
+                r0, r1 = rows
+                a, b = a[r0:r1], b[r0:r1]
+            elif shard == "batch":
+                b0, b1 = brange
+                b = b[b0:b1]
+            check_rel = float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+            del full, ref
+        if world > 1:
+            barrier()
+
     launches = sum(v[0] for v in kern.values())
     dom = DOMINANT[args.workload]
     ncu = load_ncu_summary().get(args.workload, {})
@@ -666,6 +690,7 @@ def main():
             "config": config,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches * args.steps // prof_steps,
+            **({"check_rel": check_rel} if args.check else {}),
             "kernels": {k: {"launches": v[0], "total_ms": v[1], "gflop": v[2] / 1e9} for k, v in kern.items()},
         }
         print(json.dumps(line), flush=True)
