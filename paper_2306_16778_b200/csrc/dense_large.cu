@@ -88,6 +88,78 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
   }
 }
 
+// LU (no interchanges, checked against partial pivoting when check_pivots) of nsys d x d
+// matrices M in place; naug extra columns right of each matrix (M is d x (d + naug), the
+// right-hand sides) take every row operation, so they leave as L^{-1} B.  Li / Ui receive the
+// diagonal blocks' triangular inverses.
+int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, ZMat Ui, int* sing,
+                    bool check_pivots) {
+  const int nb = DL_NB;
+  auto sub = [](ZMat A, int64_t i, int64_t j) {
+    ZMat r = A;
+    r.p = A.p + i * A.ld + j;
+    return r;
+  };
+  auto li = [&](int j0) {
+    ZMat r = Li;
+    r.p = Li.p + (int64_t)(j0 / nb) * nb * nb;
+    return r;
+  };
+  auto ui = [&](int j0) {
+    ZMat r = Ui;
+    r.p = Ui.p + (int64_t)(j0 / nb) * nb * nb;
+    return r;
+  };
+  int rc;
+  ProfTag tag_lu("lu");
+  // one 64-column panel: diagonal LU, both triangular inverses, U12 = L11^{-1} A12 over the
+  // whole row block, L21 = A21 U11^{-1} over the whole column block (checked against partial
+  // pivoting in checked mode)
+  auto factor = [&](int j0, int jb, int rest) -> int {
+    int r;
+    if ((r = zgetrf_diag(s, nsys, jb, sub(M, j0, j0), sing))) return r;
+    if ((r = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return r;
+    if (rest + naug > 0 &&
+        (r = ztrmm_inplace(s, nsys, jb, rest + naug, li(j0), sub(M, j0, j0 + jb), false, false)))
+      return r;
+    if (rest > 0 && (r = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true, sub(M, j0, j0),
+                                       check_pivots ? sing : nullptr)))
+      return r;
+    return PFX_OK;
+  };
+  // Delayed update over groups of G panels (left-looking inside the group, right-looking
+  // across groups): panel p of a group first takes the updates of the group's earlier panels
+  // (its column block and its row block, K = 64 (p - g0) / 64), is factored, and after the
+  // group the trailing matrix takes all G panels' updates in ONE K = 64 G GEMM.  The trailing
+  // matrix (up to 12 x 268 MB, far beyond L2) is read and written once per 64 G columns
+  // instead of once per 64, and every trailing tile does G times the DMMA work per epilogue.
+  // PFX_LU_GROUP=<G> overrides the default group (A/B experiments).
+  static const int G = [] {
+    const char* e = getenv("PFX_LU_GROUP");
+    const int g = e ? atoi(e) : DL_GROUP;
+    return g < 1 ? 1 : (g > 8 ? 8 : g);
+  }();
+  for (int g0 = 0; g0 < d; g0 += G * nb) {
+    const int gend = std::min(d, g0 + G * nb);
+    for (int jp = g0; jp < gend; jp += nb) {
+      const int jb = std::min(nb, d - jp);
+      const int rest = d - jp - jb;
+      if (jp > g0) {
+        if ((rc = zgemm(s, nsys, d - jp, jb, jp - g0, -1.0, sub(M, jp, g0), sub(M, g0, jp), sub(M, jp, jp))))
+          return rc;
+        if (rest + naug > 0 && (rc = zgemm(s, nsys, jb, rest + naug, jp - g0, -1.0, sub(M, jp, g0),
+                                           sub(M, g0, jp + jb), sub(M, jp, jp + jb))))
+          return rc;
+      }
+      if ((rc = factor(jp, jb, rest))) return rc;
+    }
+    if (gend < d && (rc = zgemm(s, nsys, d - gend, d - gend + naug, gend - g0, -1.0, sub(M, gend, g0),
+                                sub(M, g0, gend), sub(M, gend, gend))))
+      return rc;
+  }
+  return PFX_OK;
+}
+
 // LU (no pivoting) of nsys d x d matrices M, then X = U^{-1} L^{-1} X.  identity_rhs: X
 // starts as I, so L^{-1} X is unit lower triangular and the forward substitution of block
 // row p only touches columns < (p+1) nb (one third of the full-RHS work instead of half).
@@ -120,52 +192,7 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
     return r;
   };
   int rc;
-  ProfTag tag_lu("lu");
-  // one 64-column panel: diagonal LU, both triangular inverses, U12 = L11^{-1} A12 over the
-  // whole row block, L21 = A21 U11^{-1} over the whole column block (checked against partial
-  // pivoting in checked mode)
-  auto factor = [&](int j0, int jb, int rest) -> int {
-    int r;
-    if ((r = zgetrf_diag(s, nsys, jb, sub(M, j0, j0), sing))) return r;
-    if ((r = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return r;
-    if (rest > 0) {
-      if ((r = ztrmm_inplace(s, nsys, jb, rest, li(j0), sub(M, j0, j0 + jb), false, false))) return r;
-      if ((r = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true, sub(M, j0, j0),
-                             check_pivots ? sing : nullptr)))
-        return r;
-    }
-    return PFX_OK;
-  };
-  // Delayed update over groups of G panels (left-looking inside the group, right-looking
-  // across groups): panel p of a group first takes the updates of the group's earlier panels
-  // (its column block and its row block, K = 64 (p - g0) / 64), is factored, and after the
-  // group the trailing matrix takes all G panels' updates in ONE K = 64 G GEMM.  The trailing
-  // matrix (up to 12 x 268 MB, far beyond L2) is read and written once per 64 G columns
-  // instead of once per 64, and every trailing tile does G times the DMMA work per epilogue.
-  // PFX_LU_GROUP=<G> overrides the default group (A/B experiments).
-  static const int G = [] {
-    const char* e = getenv("PFX_LU_GROUP");
-    const int g = e ? atoi(e) : DL_GROUP;
-    return g < 1 ? 1 : (g > 8 ? 8 : g);
-  }();
-  for (int g0 = 0; g0 < d; g0 += G * nb) {
-    const int gend = std::min(d, g0 + G * nb);
-    for (int jp = g0; jp < gend; jp += nb) {
-      const int jb = std::min(nb, d - jp);
-      const int rest = d - jp - jb;
-      if (jp > g0) {
-        if ((rc = zgemm(s, nsys, d - jp, jb, jp - g0, -1.0, sub(M, jp, g0), sub(M, g0, jp), sub(M, jp, jp))))
-          return rc;
-        if (rest > 0 && (rc = zgemm(s, nsys, jb, rest, jp - g0, -1.0, sub(M, jp, g0), sub(M, g0, jp + jb),
-                                    sub(M, jp, jp + jb))))
-          return rc;
-      }
-      if ((rc = factor(jp, jb, rest))) return rc;
-    }
-    if (gend < d && (rc = zgemm(s, nsys, d - gend, d - gend, gend - g0, -1.0, sub(M, gend, g0), sub(M, g0, gend),
-                                sub(M, gend, gend))))
-      return rc;
-  }
+  if ((rc = lu_factor_nopiv(s, nsys, d, 0, M, Li, Ui, sing, check_pivots))) return rc;
   // Both substitutions run in super-blocks of SB = 8 block rows: one GEMM with m = 512 rows
   // applies everything already final outside the super-block (its column strips of X stream
   // from HBM once per super-block instead of once per block row, shared by the 8 row tiles

@@ -33,6 +33,22 @@ int banded_run(const double* band, int64_t N, int64_t kb, const double* V, int64
                const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                float* per_pair_ms, const double* band_host = nullptr, const double* V_host = nullptr);
 int pole_table_host(int n, double* theta2, double* coef2);
+int dense_blocked_eligible(int64_t d, int64_t batch, int npairs, int full, int64_t ncols);
+int dense_blocked_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int nr,
+                      int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
+                      double* out, cudaStream_t stream, float* launch_ms, int pivot);
+
+// d <= 512: many systems with few right-hand sides go to the batched blocked path (block
+// toolkit, dense_blocked.cu), the rest to the one-CTA-per-system kernel (dense_batched.cu)
+static int dense_small_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex,
+                           int ncols, int full, int real_path, double shift_c, const double2* th, const double2* co,
+                           int npairs, double* out, cudaStream_t stream, float* ms, int pivot) {
+  if (pivot != 1 && dense_blocked_eligible(d, batch, npairs, full, ncols))
+    return dense_blocked_run(A, a_complex, d, batch, V, v_complex, ncols, real_path, shift_c, th, co, npairs, out,
+                             stream, ms, pivot);
+  return dense_batched_run(A, a_complex, d, batch, V, v_complex, ncols, full, real_path, 0, shift_c, th, co, npairs,
+                           out, stream, ms, pivot);
+}
 int shifted_solve_large(const double* A, int a_complex, int d, const double2* theta_d, const double* V, int nrhs,
                         double2* Y, cudaStream_t stream);
 
@@ -489,10 +505,10 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
         PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evs[i], 0));
         float ms = 0.0f;
         // returns synchronised (status word); the next chunk's copy is already in flight
-        rc = dense_batched_run(reinterpret_cast<const double*>(Ad + b0 * am), a_complex, (int)d, (int)nb,
-                               vbytes ? reinterpret_cast<const double*>(Vd + b0 * vm) : nullptr, v_complex, ncols, full,
-                               real_path, 0, shift_c, th, co, npairs, reinterpret_cast<double*>(Od + b0 * om), stream,
-                               per_pair_ms ? &ms : nullptr, pivot);
+        rc = dense_small_run(reinterpret_cast<const double*>(Ad + b0 * am), a_complex, (int)d, (int)nb,
+                             vbytes ? reinterpret_cast<const double*>(Vd + b0 * vm) : nullptr, v_complex, ncols, full,
+                             real_path, shift_c, th, co, npairs, reinterpret_cast<double*>(Od + b0 * om), stream,
+                             per_pair_ms ? &ms : nullptr, pivot);
         if (rc) return rc;
         tot += ms;
         PFX_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(out) + b0 * om, Od + b0 * om, nb * om,
@@ -514,8 +530,8 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
   float ms = 0.0f;
   if (dense_batched_supported(d)) {
     const int pivot = dense_pivot_arg();
-    rc = dense_batched_run(Ad, a_complex, (int)d, (int)batch, Vd, v_complex, ncols, full, real_path, 0, shift_c, th, co,
-                           npairs, Od, stream, per_pair_ms ? &ms : nullptr, pivot);
+    rc = dense_small_run(Ad, a_complex, (int)d, (int)batch, Vd, v_complex, ncols, full, real_path, shift_c, th, co,
+                         npairs, Od, stream, per_pair_ms ? &ms : nullptr, pivot);
     if (per_pair_ms)
       for (int k = 0; k < npairs; ++k) per_pair_ms[k] = ms;
   } else {

@@ -212,3 +212,33 @@ def test_host_batch_pipeline_matches_device(batch, d):
     want = restate.run_tasks_dense(A[-1], V[-1, :, 0], 20)
     got = np.asarray(host).reshape(batch, d)[-1]
     assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-10
+
+
+@pytest.mark.parametrize("d,batch,nr,cplx_a,cplx_v", [(256, 32, 1, True, False), (256, 30, 3, True, True),
+                                                      (192, 40, 1, False, False), (320, 32, 2, True, False),
+                                                      (512, 32, 4, False, True), (200, 36, 1, True, False)])
+def test_blocked_batched_path(d, batch, nr, cplx_a, cplx_v):
+    """Many systems with few right-hand sides (batch x pairs >= 2 x SMs, 192 <= d <= 512): the
+    batched blocked path (dense_blocked.cu) against the restatement, including a partial last
+    64-block (d = 200, 320), real A (real and complex right-hand sides) and up to 4 columns."""
+    from paper_2306_16778_b200 import _native
+
+    rng = np.random.default_rng(d * 100 + batch)
+    n = 20
+    if cplx_a:
+        As = np.stack([workloads.random_complex_hermitian(d, -30.0, 0.0, seed=11, trial=i)[0] for i in range(batch)])
+    else:
+        As = np.stack([workloads.random_real_symmetric(d, -30.0, 0.0, seed=12, trial=i)[0] for i in range(batch)])
+    V = rng.standard_normal((batch, d, nr))
+    if cplx_v:
+        V = V + 1j * rng.standard_normal((batch, d, nr))
+    t2, c2 = default_table(n).interleaved()
+    _native.prof_enable(True)
+    _native.prof_read()
+    got = _native.expm_dense_host(As, V, t2, c2, 0.0)
+    kern = _native.prof_read()
+    _native.prof_enable(False)
+    assert "db_build" in kern, kern
+    for i in [0, batch // 2, batch - 1]:
+        want = restate.run_tasks_dense(As[i], V[i], n)
+        assert rel(got[i], want) <= TOL, (i, rel(got[i], want))
