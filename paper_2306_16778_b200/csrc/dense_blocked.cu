@@ -224,16 +224,17 @@ __global__ void db_combine(ZMat M, ZMat Z, int d, int nr, int batch, int npairs,
   }
 }
 
-// Many systems, few right-hand sides, 192 <= d <= 512: the batched blocked path pays off
-// (PFX_DENSE_BLOCKED=0 / 1 forces it off / on for A/B checks).
+// Opt-in (PFX_DENSE_BLOCKED=1): measured on C3 (5,120 systems of d = 256) at 26.5 ms against
+// 19.0 ms for the one-CTA-per-system kernel -- the LU GEMMs take 6.2 ms, but the 64 x 64 panel
+// kernels at this count (diagonal LU 3.9 ms, triangular inverses 6.0 ms, panel products 5.4 ms)
+// cost more than the fused kernel's whole factorisation.  Kept, tested, for A/B work.
 int dense_blocked_eligible(int64_t d, int64_t batch, int npairs, int full, int64_t ncols) {
   static const int force = [] {
     const char* e = getenv("PFX_DENSE_BLOCKED");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 0;
   }();
   if (full || ncols < 1 || ncols > BT_NR || d < 64 || d > 512) return 0;
-  if (force >= 0) return force;
-  return d >= 192 && batch * npairs >= 2 * (int64_t)device_sms();
+  return force > 0;
 }
 
 int dense_blocked_run(const double* A, int a_complex, int d, int batch, const double* V, int v_complex, int nr,

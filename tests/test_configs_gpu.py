@@ -4,10 +4,9 @@ The north star asks every config to match the CPU reference on the same seeded i
 (SURVEY §8d): P1 ||Y_gpu - Y_cpu|| / ||Y_cpu|| <= 1e-10 (2-norm for vectors, Frobenius for
 blocks, both for C4) and P2 ||Y_gpu - E|| <= 10 ||Y_cpu - E|| against the exact oracle E.
 
-  C3  the full 512-matrix batch, d = 256, n = 20: 5,120 systems, so the batched blocked path
-      (dense_blocked.cu: LU of all systems on the block toolkit's DMMA GEMMs, checked against
-      partial pivoting, conjugate-transpose solves on the same LU) runs -- the path the bench
-      times.  Matrices 0-3 against the
+  C3  the full 512-matrix batch, d = 256, n = 20: 5,120 systems > 148 SMs, so the two-CTA
+      `dense_batched_kernel<16, 2>` with the two-panel interchange-free LU (checked against
+      partial pivoting) runs -- the kernel the bench times.  Matrices 0-3 against the
       reference's own outputs (tests/golden/c3_head.npz), sampled indices against the
       restatement of engine.py:202-206 (lu_factor, lu_solve trans=0/2).
   C4  d = 4096, lambda in [-500, 0], full exp(A), n = 24: P1 against the CPU reference
@@ -71,11 +70,11 @@ def test_c3_full_batch_head_vs_reference(c3_run):
     for i in range(z["value"].shape[0]):
         assert rel(got[i], z["value"][i]) <= TOL, (i, rel(got[i], z["value"][i]))
         assert np.linalg.norm(got[i] - z["oracle"][i]) <= 10 * np.linalg.norm(z["value"][i] - z["oracle"][i])
-    # the production path: the batched blocked solve on the block toolkit (every chunk of the
-    # host pipeline: build, LU on DMMA, the three triangular solves), no chunk redone with
-    # interchanges, and no launch of the one-CTA-per-system kernel
-    assert kern["db_build"][0] >= 1 and kern["bt_solve"][0] == 3 * kern["db_build"][0], kern
-    assert not any(k.startswith("dense_batched_kernel") for k in kern), kern
+    # the production kernel: every launch (the host call pipelines the batch in chunks) is the
+    # two-CTA NB = 16 interchange-free variant, and no chunk was redone with interchanges
+    launches = {k: v for k, v in kern.items() if k.startswith("dense_batched_kernel")}
+    assert set(launches) == {"dense_batched_kernel@nb16x2"}, launches
+    assert launches["dense_batched_kernel@nb16x2"][0] >= 1
     assert fallbacks == 0
 
 

@@ -214,31 +214,42 @@ def test_host_batch_pipeline_matches_device(batch, d):
     assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-10
 
 
-@pytest.mark.parametrize("d,batch,nr,cplx_a,cplx_v", [(256, 32, 1, True, False), (256, 30, 3, True, True),
-                                                      (192, 40, 1, False, False), (320, 32, 2, True, False),
-                                                      (512, 32, 4, False, True), (200, 36, 1, True, False)])
-def test_blocked_batched_path(d, batch, nr, cplx_a, cplx_v):
-    """Many systems with few right-hand sides (batch x pairs >= 2 x SMs, 192 <= d <= 512): the
-    batched blocked path (dense_blocked.cu) against the restatement, including a partial last
-    64-block (d = 200, 320), real A (real and complex right-hand sides) and up to 4 columns."""
-    from paper_2306_16778_b200 import _native
-
+_BLOCKED_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import restate
+from paper_2306_16778_b200 import _native, workloads
+from paper_2306_16778_b200.roots import default_table
+worst = 0.0
+for d, batch, nr, ca, cv in [(256, 32, 1, 1, 0), (256, 30, 3, 1, 1), (192, 40, 1, 0, 0), (320, 32, 2, 1, 0),
+                              (512, 32, 4, 0, 1), (200, 36, 1, 1, 0)]:
     rng = np.random.default_rng(d * 100 + batch)
-    n = 20
-    if cplx_a:
-        As = np.stack([workloads.random_complex_hermitian(d, -30.0, 0.0, seed=11, trial=i)[0] for i in range(batch)])
-    else:
-        As = np.stack([workloads.random_real_symmetric(d, -30.0, 0.0, seed=12, trial=i)[0] for i in range(batch)])
-    V = rng.standard_normal((batch, d, nr))
-    if cplx_v:
-        V = V + 1j * rng.standard_normal((batch, d, nr))
-    t2, c2 = default_table(n).interleaved()
-    _native.prof_enable(True)
-    _native.prof_read()
+    mk = workloads.random_complex_hermitian if ca else workloads.random_real_symmetric
+    As = np.stack([mk(d, -30.0, 0.0, seed=11, trial=i)[0] for i in range(batch)])
+    V = rng.standard_normal((batch, d, nr)) + (1j * rng.standard_normal((batch, d, nr)) if cv else 0)
+    t2, c2 = default_table(20).interleaved()
+    _native.prof_enable(True); _native.prof_read()
     got = _native.expm_dense_host(As, V, t2, c2, 0.0)
-    kern = _native.prof_read()
-    _native.prof_enable(False)
-    assert "db_build" in kern, kern
+    kern = _native.prof_read(); _native.prof_enable(False)
+    assert "db_build" in kern and "bt_solve" in kern, kern
     for i in [0, batch // 2, batch - 1]:
-        want = restate.run_tasks_dense(As[i], V[i], n)
-        assert rel(got[i], want) <= TOL, (i, rel(got[i], want))
+        want = restate.run_tasks_dense(As[i], V[i], 20)
+        worst = max(worst, float(np.linalg.norm(got[i] - want) / np.linalg.norm(want)))
+print("WORST", worst)
+"""
+
+
+def test_blocked_batched_path_opt_in():
+    """The opt-in batched blocked path (PFX_DENSE_BLOCKED=1, dense_blocked.cu) against the
+    restatement in a subprocess (the switch is read once per process): complex and real A, real
+    and complex right-hand sides, up to 4 columns, partial last 64-blocks (d = 200, 320)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PFX_DENSE_BLOCKED="1")
+    res = subprocess.run([sys.executable, "-c", _BLOCKED_SCRIPT, root], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    worst = float(res.stdout.split("WORST")[-1])
+    assert worst <= TOL, worst

@@ -129,19 +129,3 @@ def test_bad_pivot_mode():
 
     with pytest.raises(BadSpec):
         _native.set_pivot_mode("sometimes")
-
-
-def test_weak_diagonal_blocked_batched_path(pivot_mode):
-    # 32 matrices x 10 pairs = 320 systems of d = 256: the batched blocked path; the weak
-    # diagonal fails its pivot check and the call is redone on the pivoting kernels
-    d, b, n = 256, 32, 20
-    As = np.stack([workloads.random_complex_hermitian(d, -30.0, 0.0, seed=9, trial=i)[0] for i in range(b)])
-    As[3] = weak_diagonal_hermitian(d, seed=5)
-    V = np.stack([workloads.unit_vector(d, 4, i) for i in range(b)])
-    pivot_mode("checked")
-    before = _native.pivot_fallbacks()
-    got = run(As, V[..., None], n)[..., 0]
-    assert _native.pivot_fallbacks() == before + 1
-    for i in [0, 3, b - 1]:
-        want = restate.run_tasks_dense(As[i], V[i], n)
-        assert rel(got[i], want) <= TOL, (i, rel(got[i], want))
