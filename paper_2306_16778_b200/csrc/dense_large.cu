@@ -27,12 +27,16 @@ namespace pfx {
 constexpr int DL_NB = 64;
 constexpr int DL_GROUP = 4;  // panels per delayed trailing update (K = 64 G)
 
+// rows [r0, r1) of every system (the host pipeline builds row chunks as they land)
 __global__ void dl_build(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
-                         double shift_c, const double2* theta, int npairs, int nsys, ZMat M, ZMat X) {
+                         double shift_c, const double2* theta, int npairs, int nsys, ZMat M, ZMat X, int r0 = 0,
+                         int r1 = 1 << 30) {
   const int k = blockIdx.y;
   const cplx th = k < npairs ? ld(&theta[k]) : cconj(ld(&theta[k - npairs]));
-  const int64_t dd = (int64_t)d * d;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dd; e += (int64_t)gridDim.x * blockDim.x) {
+  r1 = r1 < d ? r1 : d;
+  const int64_t dd = (int64_t)r1 * d;
+  for (int64_t e = (int64_t)r0 * d + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dd;
+       e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = e / d, j = e - i * d;
     double2 v = a_complex ? reinterpret_cast<const double2*>(A)[e] : make_double2(A[e], 0.0);
     if (i == j) {
@@ -41,8 +45,9 @@ __global__ void dl_build(const double* A, int a_complex, int d, const double* V,
     }
     *M.at(k, i, j) = v;
   }
-  const int64_t nx = (int64_t)d * ncols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nx; e += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t nx = (int64_t)r1 * ncols;
+  for (int64_t e = (int64_t)r0 * ncols + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nx;
+       e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = e / ncols, j = e - i * ncols;
     double2 v;
     if (full)
@@ -55,10 +60,13 @@ __global__ void dl_build(const double* A, int a_complex, int d, const double* V,
 
 // out = scale * sum_k S_k (k ascending).  sym_lower: X_k holds only its lower triangle
 // (complex symmetric inverse, real-A full mode), read as X(max(i,j), min(i,j)).
+// rows [r0, r1) (the host pipeline copies finished row chunks back while the next are combined)
 __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* coef, int full, int real_path,
-                           int sym_lower, double scale, double* out) {
-  const int64_t n = (int64_t)d * ncols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+                           int sym_lower, double scale, double* out, int r0 = 0, int r1 = 1 << 30) {
+  r1 = r1 < d ? r1 : d;
+  const int64_t n = (int64_t)r1 * ncols;
+  for (int64_t e = (int64_t)r0 * ncols + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = e / ncols, j = e - i * ncols;
     if (real_path) {
       const int64_t xi = sym_lower && j > i ? j : i, xj = sym_lower && j > i ? i : j;
@@ -266,7 +274,8 @@ int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int
 // with lu_solve_piv when a check fails (pfx_set_pivot_mode).
 int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
                     int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
-                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot) {
+                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot, const double* A_host,
+                    const double* V_host, double* out_host) {
   const int conj_sys = (!full && !real_path) ? 1 : 0;
   const int nsys = npairs * (1 + conj_sys);
   const size_t mbytes = (size_t)nsys * d * d * sizeof(double2);
@@ -291,9 +300,51 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     PFX_CUDA_TRY(cudaEventRecord(e0, stream));
   }
   dim3 bg(1184, nsys);
-  PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full, shift_c,
-                                                                    theta_d, npairs, nsys, M, X));
-  PFX_CUDA_TRY(cudaGetLastError());
+  // host mode: A goes in by row chunks on a copy stream and each chunk's rows are built as soon
+  // as they land; the result comes back by row chunks while the next ones are combined
+  constexpr int NCH = 8;
+  struct CopyIn {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[2 * NCH + 1];
+  };
+  static CopyIn cis[kMaxDevices];
+  cudaStream_t cin = nullptr;
+  cudaEvent_t* evs = nullptr;
+  if (A_host || out_host) {
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
+    if (!cis[dev].cs) {
+      PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cis[dev].cs, cudaStreamNonBlocking));
+      for (auto& e : cis[dev].ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cin = cis[dev].cs;
+    evs = cis[dev].ev;
+  }
+  const size_t arow = (size_t)d * sizeof(double) * (a_complex ? 2 : 1);
+  if (A_host) {
+    // the staging buffers are idle on entry (host-mode calls end synchronised)
+    PFX_CUDA_TRY(cudaEventRecord(evs[2 * NCH], stream));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(cin, evs[2 * NCH], 0));
+    if (V_host && V)
+      PFX_CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(V), V_host,
+                                   (size_t)d * ncols * sizeof(double) * (v_complex ? 2 : 1),
+                                   cudaMemcpyHostToDevice, cin));
+    for (int c = 0; c < NCH; ++c) {
+      const int r0 = (int)((int64_t)d * c / NCH), r1 = (int)((int64_t)d * (c + 1) / NCH);
+      PFX_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(const_cast<double*>(A)) + r0 * arow,
+                                   reinterpret_cast<const char*>(A_host) + r0 * arow, (size_t)(r1 - r0) * arow,
+                                   cudaMemcpyHostToDevice, cin));
+      PFX_CUDA_TRY(cudaEventRecord(evs[c], cin));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evs[c], 0));
+      PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full,
+                                                                        shift_c, theta_d, npairs, nsys, M, X, r0, r1));
+      PFX_CUDA_TRY(cudaGetLastError());
+    }
+  } else {
+    PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full,
+                                                                      shift_c, theta_d, npairs, nsys, M, X));
+    PFX_CUDA_TRY(cudaGetLastError());
+  }
   // real A in full mode: A + theta I is complex symmetric -> lower-triangle inverse
   int sym_lower = (full && !a_complex && real_path) ? 1 : 0;
   int* hsg = pinned_word();
@@ -340,11 +391,30 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     rc = lu_solve_piv(stream, nsys, d, M, X, ncols, ipiv, sing);
     if (rc) return rc;
   }
-  if (!fused) {
-    PFX_LAUNCH("dl_combine", stream,
-               dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
-                                                   out));
-    PFX_CUDA_TRY(cudaGetLastError());
+  const size_t orow = (size_t)ncols * sizeof(double) * (real_path ? 1 : 2);
+  if (!fused && out_host) {
+    for (int c = 0; c < NCH; ++c) {
+      const int r0 = (int)((int64_t)d * c / NCH), r1 = (int)((int64_t)d * (c + 1) / NCH);
+      PFX_LAUNCH("dl_combine", stream,
+                 dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
+                                                     out, r0, r1));
+      PFX_CUDA_TRY(cudaGetLastError());
+      PFX_CUDA_TRY(cudaEventRecord(evs[NCH + c], stream));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(cin, evs[NCH + c], 0));
+      PFX_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(out_host) + r0 * orow, reinterpret_cast<char*>(out) + r0 * orow,
+                                   (size_t)(r1 - r0) * orow, cudaMemcpyDeviceToHost, cin));
+    }
+    PFX_CUDA_TRY(cudaEventRecord(evs[2 * NCH], cin));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evs[2 * NCH], 0));
+  } else {
+    if (!fused) {
+      PFX_LAUNCH("dl_combine", stream,
+                 dl_combine<<<2368, 256, 0, stream>>>(X, d, ncols, npairs, coef_d, full, real_path, sym_lower, scale,
+                                                     out));
+      PFX_CUDA_TRY(cudaGetLastError());
+    }
+    if (out_host)
+      PFX_CUDA_TRY(cudaMemcpyAsync(out_host, out, (size_t)d * orow, cudaMemcpyDeviceToHost, stream));
   }
   PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (per_pair_ms) {

@@ -24,7 +24,8 @@ int dense_batched_run(const double* A, int a_complex, int d, int batch, const do
                       int npairs, double* out, cudaStream_t stream, float* launch_ms, int pivot);
 int dense_large_run(const double* A, int a_complex, int d, const double* V, int v_complex, int ncols, int full,
                     int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
-                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot);
+                    double* out, cudaStream_t stream, float* per_pair_ms, int pivot, const double* A_host = nullptr,
+                    const double* V_host = nullptr, double* out_host = nullptr);
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                 float* launch_ms, const double* V_host = nullptr, double* out_host = nullptr,
@@ -518,6 +519,16 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
         for (int k = 0; k < npairs; ++k) per_pair_ms[k] = tot;
       return sync_stream(stream);
     }
+  }
+  if (mem == PFX_MEM_HOST && !dense_batched_supported(d)) {
+    // large matrices: dense_large_run pipelines the copies (row chunks in, row chunks out)
+    double* Ad = static_cast<double*>(scratch(3, abytes));
+    double* Vd = vbytes ? static_cast<double*>(scratch(4, vbytes)) : nullptr;
+    double* Od = static_cast<double*>(scratch(6, obytes));
+    if (!Ad || (vbytes && !Vd) || !Od) return fail(PFX_CUDA, "staging allocation failed");
+    rc = dense_large_run(Ad, a_complex, (int)d, Vd, v_complex, ncols, full, real_path, shift_c, th, co, npairs, Od,
+                         stream, per_pair_ms, dense_pivot_arg(), A, V, out);
+    return rc;
   }
   const double *Ad = nullptr, *Vd = nullptr;
   if ((rc = stage_in(mem, 3, A, abytes, stream, &Ad))) return rc;
