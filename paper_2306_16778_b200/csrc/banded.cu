@@ -439,13 +439,11 @@ static int bd_factor_pairs(cudaStream_t stream, const BdStreams& S, ZMat M, ZMat
     return r;
   };
   cudaEvent_t evT = S.ev[0], evU = S.ev[1], evL = S.ev[2], evS = S.ev[6], evA = S.ev[7], evT2 = S.ev[8];
-  cudaEvent_t evG1 = S.ev[3], evG2 = S.ev[5];  // (ev[4] = evP of the one-block loop stays unused here)
-  bool pend_t2 = false, pend_s = false, pend_g = false, have_u = false;
+  bool pend_t2 = false, pend_s = false;
   int rc;
   // one block: LU + inverses (main), U12 over `ucols` (s1, after `wait_s4` strips), L21 over
   // `lrows` (main), the block's RHS elimination (s2)
-  // first_of_pair: the block's row strip / column below come from the previous pair's G1 / G2
-  auto factor = [&](int64_t j0, int jb, int lrows, int ucols, bool wait_s4, bool first_of_pair) -> int {
+  auto factor = [&](int64_t j0, int jb, int lrows, int ucols, bool wait_s4) -> int {
     int r;
     if ((r = zgetrf_diag(stream, npairs, jb, sub(M, j0, j0), sing))) return r;
     if ((r = ztrtri_diag(stream, npairs, jb, sub(M, j0, j0), blk(Li, j0), blk(Ui, j0)))) return r;
@@ -453,12 +451,9 @@ static int bd_factor_pairs(cudaStream_t stream, const BdStreams& S, ZMat M, ZMat
     if (ucols > 0) {
       PFX_CUDA_TRY(cudaStreamWaitEvent(S.s1, evT, 0));
       if (wait_s4) PFX_CUDA_TRY(cudaStreamWaitEvent(S.s1, evS, 0));
-      if (first_of_pair && pend_g) PFX_CUDA_TRY(cudaStreamWaitEvent(S.s1, evG1, 0));
       if ((r = ztrmm_inplace(S.s1, npairs, jb, ucols, blk(Li, j0), sub(M, j0, j0 + jb), false, false))) return r;
       PFX_CUDA_TRY(cudaEventRecord(evU, S.s1));
-      have_u = true;
     }
-    if (first_of_pair && pend_g) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evG2, 0));
     if (lrows > 0 &&
         (r = ztrmm_inplace(stream, npairs, jb, lrows, blk(Ui, j0), sub(M, j0 + jb, j0), true, true)))
       return r;
@@ -473,20 +468,17 @@ static int bd_factor_pairs(cudaStream_t stream, const BdStreams& S, ZMat M, ZMat
   for (int64_t j0 = 0; j0 < N; j0 += 2 * nb) {
     const int jb0 = (int)std::min<int64_t>(nb, N - j0);
     const int rest0 = (int)std::min<int64_t>(kb, N - j0 - jb0);
-    if ((rc = factor(j0, jb0, rest0, rest0, false, true))) return rc;
+    if ((rc = factor(j0, jb0, rest0, rest0, false))) return rc;
     if (rest0 == 0) break;
     const int64_t j1 = j0 + jb0;
     const int jb1 = (int)std::min<int64_t>(nb, N - j1);
     const int rest1 = (int)std::min<int64_t>(kb, N - j1 - jb1);
     // panel a's update of block b: column block (rows [j1, j1 + rest0), main) and row block
-    // (cols [j1 + jb1, j1 + rest0), s4, read by b's U12; it also waits for the previous pair's
-    // G3, which covered b's row strip)
-    if (have_u) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
+    // (cols [j1 + jb1, j1 + rest0), s4, read by b's U12)
+    PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
     if ((rc = zgemm(stream, npairs, rest0, jb1, jb0, -1.0, sub(M, j1, j0), sub(M, j0, j1), sub(M, j1, j1)))) return rc;
-    const bool g3 = pend_g;  // the previous pair's G3 (recorded as evS on s5)
     pend_s = rest0 > jb1;
     if (pend_s) {
-      if (g3) PFX_CUDA_TRY(cudaStreamWaitEvent(S.s4, evS, 0));
       PFX_CUDA_TRY(cudaStreamWaitEvent(S.s4, evL, 0));
       PFX_CUDA_TRY(cudaStreamWaitEvent(S.s4, evU, 0));
       if ((rc = zgemm(S.s4, npairs, jb1, rest0 - jb1, jb0, -1.0, sub(M, j1, j0), sub(M, j0, j1 + jb1),
@@ -494,39 +486,20 @@ static int bd_factor_pairs(cudaStream_t stream, const BdStreams& S, ZMat M, ZMat
         return rc;
       PFX_CUDA_TRY(cudaEventRecord(evS, S.s4));
     }
-    if ((rc = factor(j1, jb1, rest1, rest1, pend_s, false))) return rc;
+    if ((rc = factor(j1, jb1, rest1, rest1, pend_s))) return rc;
     if (rest1 == 0) break;
-    // both panels' update of rows / cols [j2, j2 + rest1), K = jb0 + jb1, split by how soon the
-    // next pair (blocks c = j2, d = j2 + 64) needs it:
-    //   main  t1a: block c's diagonal block, before c's LU;
-    //   s5    G1: c's row strip (c's U12 waits for it), G2: rows below c of the columns of c and
-    //         d (c's L21 and d's column update wait for it), G3: d's row strip (d's row update);
-    //   s3    t2: everything from block d + 1 on (the next pair's K = 128 update waits for it).
+    // both panels' update of rows / cols [j2, j2 + rest1), K = jb0 + jb1
     const int64_t j2 = j1 + jb1;
     const int K = jb0 + jb1;
-    const int rc1 = std::min(nb, rest1);       // block c
-    const int rb = std::min(2 * nb, rest1);    // blocks c and d
-    if (have_u) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
+    const int rb = std::min(2 * nb, rest1);
+    PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
     if (pend_t2) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evT2, 0));
-    PFX_CUDA_TRY(cudaEventRecord(evA, stream));  // both panels final, far region free
-    if ((rc = zgemm(stream, npairs, rc1, rc1, K, -1.0, sub(M, j2, j0), sub(M, j0, j2), sub(M, j2, j2)))) return rc;
-    PFX_CUDA_TRY(cudaStreamWaitEvent(S.s5, evA, 0));
-    if (rest1 > rc1 &&
-        (rc = zgemm(S.s5, npairs, rc1, rest1 - rc1, K, -1.0, sub(M, j2, j0), sub(M, j0, j2 + rc1),
-                    sub(M, j2, j2 + rc1))))
-      return rc;
-    PFX_CUDA_TRY(cudaEventRecord(evG1, S.s5));
-    if (rest1 > rc1 &&
-        (rc = zgemm(S.s5, npairs, rest1 - rc1, rb, K, -1.0, sub(M, j2 + rc1, j0), sub(M, j0, j2), sub(M, j2 + rc1, j2))))
-      return rc;
-    PFX_CUDA_TRY(cudaEventRecord(evG2, S.s5));
-    if (rb > rc1 && rest1 > rb &&
-        (rc = zgemm(S.s5, npairs, rb - rc1, rest1 - rb, K, -1.0, sub(M, j2 + rc1, j0), sub(M, j0, j2 + rb),
-                    sub(M, j2 + rc1, j2 + rb))))
-      return rc;
-    PFX_CUDA_TRY(cudaEventRecord(evS, S.s5));  // the next pair's row update of d waits for G3
-    pend_g = true;
+    if ((rc = zgemm(stream, npairs, rest1, rb, K, -1.0, sub(M, j2, j0), sub(M, j0, j2), sub(M, j2, j2)))) return rc;
     if (rest1 > rb) {
+      if ((rc = zgemm(stream, npairs, rb, rest1 - rb, K, -1.0, sub(M, j2, j0), sub(M, j0, j2 + rb),
+                      sub(M, j2, j2 + rb))))
+        return rc;
+      PFX_CUDA_TRY(cudaEventRecord(evA, stream));
       PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evA, 0));
       if ((rc = zgemm(S.s3, npairs, rest1 - rb, rest1 - rb, K, -1.0, sub(M, j2 + rb, j0), sub(M, j0, j2 + rb),
                       sub(M, j2 + rb, j2 + rb))))
@@ -536,8 +509,7 @@ static int bd_factor_pairs(cudaStream_t stream, const BdStreams& S, ZMat M, ZMat
     }
   }
   if (pend_t2) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evT2, 0));
-  if (pend_g) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evS, 0));
-  if (have_u) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
+  PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
   return PFX_OK;
 }
 
