@@ -27,9 +27,6 @@
 namespace pfx {
 
 constexpr int BD_NB = 64;
-// zero diagonals of storage padding on each side of the band: two blocks, so the paired-block
-// trailing update (K = 128) reads the first block's L21 / U12 a block past its band as zeros
-constexpr int BD_PAD = 2 * BD_NB;
 
 // grid (row groups, systems): each warp writes whole rows of the padded row band (no index
 // division: the band is ~40 GB for C5, so this is a pure HBM write stream).
@@ -51,7 +48,7 @@ __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const do
   const int s = blockIdx.y;
   const int part = s / npairs, k = s - part * npairs;
   const cplx th = ld(&theta[k]);
-  double2* base = M.p - (kb + BD_PAD) + s * M.stride;  // row-band base of system s
+  double2* base = M.p - (kb + BD_NB) + s * M.stride;  // row-band base of system s
   // local rows of this system whose global row lies in [g0, g1)
   int64_t i0, i1;
   if (part == 0) {
@@ -70,7 +67,7 @@ __global__ void bd_build(const double* band, int64_t N, int kb, int Wd, const do
     double2* rowp = base + i * Wd;
     const int64_t gi = part ? N - 1 - i : i;
     for (int e = lane; e < Wd; e += 32) {
-      const int off = e - (kb + BD_PAD);  // local j - i
+      const int off = e - (kb + BD_NB);  // local j - i
       const int64_t j = i + off;
       double v = 0.0;
       if (j >= 0 && j < Np) v = band_at(band, N, kb, gi, part ? N - 1 - j : j);
@@ -416,103 +413,6 @@ static int bd_streams(BdStreams& S) {
   return PFX_OK;
 }
 
-// Block steps in pairs (a, b): block a is factored (diagonal LU, inverses, U12 on s1, L21 on
-// main, its RHS elimination on s2); block b's column block (main) and row block (s4) take panel
-// a's update; block b is factored; then ONE trailing update with K = 128 applies both panels:
-//   t1 (main)  the next pair's L-shaped strips (rows / cols of its two blocks), which the next
-//              pair's factorisation reads first;
-//   t2 (s3)    everything beyond, needed only by the pair after (its t1 waits for it).
-// Panel a's L21 / U12 reach one block past its band into the zero padding (BD_PAD = 128), so
-// the K = 128 products are plain rectangles.  Against one block per step: half the trailing
-// launches, each tile doing twice the DMMA work per epilogue.
-static int bd_factor_pairs(cudaStream_t stream, const BdStreams& S, ZMat M, ZMat X, ZMat Li, ZMat Ui, int64_t N,
-                           int kb, int nr, int npairs, int* sing) {
-  const int nb = BD_NB;
-  auto sub = [](ZMat A, int64_t i, int64_t j) {
-    ZMat r = A;
-    r.p = A.p + i * A.ld + j;
-    return r;
-  };
-  auto blk = [&](ZMat T, int64_t j0) {
-    ZMat r = T;
-    r.p = T.p + (j0 / nb) * nb * nb;
-    return r;
-  };
-  cudaEvent_t evT = S.ev[0], evU = S.ev[1], evL = S.ev[2], evS = S.ev[6], evA = S.ev[7], evT2 = S.ev[8];
-  bool pend_t2 = false, pend_s = false;
-  int rc;
-  // one block: LU + inverses (main), U12 over `ucols` (s1, after `wait_s4` strips), L21 over
-  // `lrows` (main), the block's RHS elimination (s2)
-  auto factor = [&](int64_t j0, int jb, int lrows, int ucols, bool wait_s4) -> int {
-    int r;
-    if ((r = zgetrf_diag(stream, npairs, jb, sub(M, j0, j0), sing))) return r;
-    if ((r = ztrtri_diag(stream, npairs, jb, sub(M, j0, j0), blk(Li, j0), blk(Ui, j0)))) return r;
-    PFX_CUDA_TRY(cudaEventRecord(evT, stream));
-    if (ucols > 0) {
-      PFX_CUDA_TRY(cudaStreamWaitEvent(S.s1, evT, 0));
-      if (wait_s4) PFX_CUDA_TRY(cudaStreamWaitEvent(S.s1, evS, 0));
-      if ((r = ztrmm_inplace(S.s1, npairs, jb, ucols, blk(Li, j0), sub(M, j0, j0 + jb), false, false))) return r;
-      PFX_CUDA_TRY(cudaEventRecord(evU, S.s1));
-    }
-    if (lrows > 0 &&
-        (r = ztrmm_inplace(stream, npairs, jb, lrows, blk(Ui, j0), sub(M, j0 + jb, j0), true, true)))
-      return r;
-    PFX_CUDA_TRY(cudaEventRecord(evL, stream));
-    PFX_CUDA_TRY(cudaStreamWaitEvent(S.s2, evL, 0));
-    if ((r = ztrmm_inplace(S.s2, npairs, jb, nr, blk(Li, j0), sub(X, j0, 0), false, false))) return r;
-    if (lrows > 0 &&
-        (r = zgemm(S.s2, npairs, lrows, nr, jb, -1.0, sub(M, j0 + jb, j0), sub(X, j0, 0), sub(X, j0 + jb, 0))))
-      return r;
-    return PFX_OK;
-  };
-  for (int64_t j0 = 0; j0 < N; j0 += 2 * nb) {
-    const int jb0 = (int)std::min<int64_t>(nb, N - j0);
-    const int rest0 = (int)std::min<int64_t>(kb, N - j0 - jb0);
-    if ((rc = factor(j0, jb0, rest0, rest0, false))) return rc;
-    if (rest0 == 0) break;
-    const int64_t j1 = j0 + jb0;
-    const int jb1 = (int)std::min<int64_t>(nb, N - j1);
-    const int rest1 = (int)std::min<int64_t>(kb, N - j1 - jb1);
-    // panel a's update of block b: column block (rows [j1, j1 + rest0), main) and row block
-    // (cols [j1 + jb1, j1 + rest0), s4, read by b's U12)
-    PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
-    if ((rc = zgemm(stream, npairs, rest0, jb1, jb0, -1.0, sub(M, j1, j0), sub(M, j0, j1), sub(M, j1, j1)))) return rc;
-    pend_s = rest0 > jb1;
-    if (pend_s) {
-      PFX_CUDA_TRY(cudaStreamWaitEvent(S.s4, evL, 0));
-      PFX_CUDA_TRY(cudaStreamWaitEvent(S.s4, evU, 0));
-      if ((rc = zgemm(S.s4, npairs, jb1, rest0 - jb1, jb0, -1.0, sub(M, j1, j0), sub(M, j0, j1 + jb1),
-                      sub(M, j1, j1 + jb1))))
-        return rc;
-      PFX_CUDA_TRY(cudaEventRecord(evS, S.s4));
-    }
-    if ((rc = factor(j1, jb1, rest1, rest1, pend_s))) return rc;
-    if (rest1 == 0) break;
-    // both panels' update of rows / cols [j2, j2 + rest1), K = jb0 + jb1
-    const int64_t j2 = j1 + jb1;
-    const int K = jb0 + jb1;
-    const int rb = std::min(2 * nb, rest1);
-    PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
-    if (pend_t2) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evT2, 0));
-    if ((rc = zgemm(stream, npairs, rest1, rb, K, -1.0, sub(M, j2, j0), sub(M, j0, j2), sub(M, j2, j2)))) return rc;
-    if (rest1 > rb) {
-      if ((rc = zgemm(stream, npairs, rb, rest1 - rb, K, -1.0, sub(M, j2, j0), sub(M, j0, j2 + rb),
-                      sub(M, j2, j2 + rb))))
-        return rc;
-      PFX_CUDA_TRY(cudaEventRecord(evA, stream));
-      PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evA, 0));
-      if ((rc = zgemm(S.s3, npairs, rest1 - rb, rest1 - rb, K, -1.0, sub(M, j2 + rb, j0), sub(M, j0, j2 + rb),
-                      sub(M, j2 + rb, j2 + rb))))
-        return rc;
-      PFX_CUDA_TRY(cudaEventRecord(evT2, S.s3));
-      pend_t2 = true;
-    }
-  }
-  if (pend_t2) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evT2, 0));
-  PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evU, 0));
-  return PFX_OK;
-}
-
 // N, npairs: rows per system and systems in the batch (SPIKE: Np and 2 npairs; sp the interface)
 static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui, double2* P, int64_t N, int kb,
                            int nr, int npairs, int* sing, const BdCombine* cmb, const BdSpike* sp) {
@@ -545,14 +445,6 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
   PFX_CUDA_TRY(cudaStreamWaitEvent(S.s2, evT, 0));
   PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evT, 0));
   bool pending_b = false;  // a trailing update of the previous step is queued on s3
-  // PFX_BD_GROUP=1: one block per step (below); default: blocks in pairs (bd_factor_pairs)
-  static const int group = [] {
-    const char* e = getenv("PFX_BD_GROUP");
-    return e ? atoi(e) : 2;
-  }();
-  if (group == 2 && !skip) {
-    if ((rc = bd_factor_pairs(stream, S, M, X, Li, Ui, N, kb, nr, npairs, sing))) return rc;
-  } else
   for (int64_t j0 = 0; j0 < N; j0 += nb) {
     const int jb = (int)std::min<int64_t>(nb, N - j0);
     const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);  // rows/cols coupled below/right
@@ -685,7 +577,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
                float* per_pair_ms, const double* band_host, const double* V_host) {
   const int kb = (int)kb64;
   const int nb = BD_NB;
-  const int Wd = 2 * kb + 2 * BD_PAD + 1;
+  const int Wd = 2 * kb + 2 * nb + 1;
   // Two-partition SPIKE (BdSpike) when the halves are long against the band: the serial chain of
   // block steps halves.  PFX_BD_SPIKE=0 keeps the single-partition factorisation.
   static const bool spike_on = [] {
@@ -715,7 +607,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   const size_t base_bytes = mbytes + xbytes + libytes + uibytes + pbytes + 256 + 64;
   char* ws = static_cast<char*>(scratch(1, base_bytes + wbytes + ebytes + sbytes + abbytes + lsbytes + 256));
   if (!ws) return fail(PFX_CUDA, "banded workspace allocation failed (needs " + std::to_string((mbytes + xbytes) >> 20) + " MiB)");
-  ZMat M{reinterpret_cast<double2*>(ws) + kb + BD_PAD, Wd - 1, (int64_t)Np * Wd};
+  ZMat M{reinterpret_cast<double2*>(ws) + kb + nb, Wd - 1, (int64_t)Np * Wd};
   ZMat X{reinterpret_cast<double2*>(ws + mbytes), nrhs, Np * nrhs};
   ZMat Li{reinterpret_cast<double2*>(ws + mbytes + xbytes), nb, nblk * nb * nb};
   ZMat Ui{reinterpret_cast<double2*>(ws + mbytes + xbytes + libytes), nb, nblk * nb * nb};
