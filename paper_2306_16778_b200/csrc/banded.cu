@@ -448,8 +448,8 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
   for (int64_t j0 = 0; j0 < N; j0 += nb) {
     const int jb = (int)std::min<int64_t>(nb, N - j0);
     const int rest = (int)std::min<int64_t>(kb, N - j0 - jb);  // rows/cols coupled below/right
-    if (!(skip & 8) && (rc = zgetri_diag(stream, npairs, jb, sub(M, j0, j0), blk(Li, j0), blk(Ui, j0), sing)))
-      return rc;
+    if (!(skip & 8) && (rc = zgetrf_diag(stream, npairs, jb, sub(M, j0, j0), sing))) return rc;
+    if (!(skip & 8) && (rc = ztrtri_diag(stream, npairs, jb, sub(M, j0, j0), blk(Li, j0), blk(Ui, j0)))) return rc;
     // this block's panels are the previous step's strips (s4)
     if (pending_s) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evS, 0));
     if (rest > 0 && !(skip & 16)) {

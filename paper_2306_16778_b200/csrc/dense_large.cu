@@ -125,7 +125,8 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
   // pivoting in checked mode)
   auto factor = [&](int j0, int jb, int rest) -> int {
     int r;
-    if ((r = zgetri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0), sing))) return r;
+    if ((r = zgetrf_diag(s, nsys, jb, sub(M, j0, j0), sing))) return r;
+    if ((r = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return r;
     if (rest + naug > 0 &&
         (r = ztrmm_inplace(s, nsys, jb, rest + naug, li(j0), sub(M, j0, j0 + jb), false, false)))
       return r;

@@ -964,129 +964,6 @@ __global__ void __launch_bounds__(256) ztrtri_diag_kernel(int nb, ZMat D, ZMat L
   }
 }
 
-// Fused diagonal-block LU + both triangular inverses (the chain of every block step of the
-// band LU and of the large dense LU): the register-resident two-column LU of
-// zgetrf_diag2_kernel, then, in the same CTA, L^{-1} and U^{-1} from the factors staged in
-// shared memory.  Warp w owns columns w, w + 8, ..., w + 56 of both inverses and advances FOUR
-// columns per substitution sweep (lanes = rows lane and lane + 32, the finished entry broadcast
-// by shuffle), so each column solve overlaps three others.  One launch and one load
-// of the block instead of two launches and a reload.
-template <bool UPPER>
-__device__ __forceinline__ void tri_inv4(const double2* A, const double2* rdiag, int nb, int c0, int lane, ZMat Out,
-                                         int b) {
-  // columns c0 + 8 u, u < 4
-  const int r0 = lane, r1 = lane + 32;
-  cplx x0[4], x1[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int c = c0 + 8 * u;
-    x0[u] = mk(r0 == c ? 1.0 : 0.0, 0.0);
-    x1[u] = mk(r1 == c ? 1.0 : 0.0, 0.0);
-  }
-  if (!UPPER) {
-    // X = L^{-1} e_c: step k (>= the column) broadcasts x_k and updates the rows below
-    for (int k = c0; k < nb - 1; ++k) {
-      const cplx l0 = ld(&A[r0 * DI_S + k]), l1 = ld(&A[r1 * DI_S + k]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const cplx src = k < 32 ? x0[u] : x1[u];
-        cplx xk;
-        xk.re = __shfl_sync(0xffffffffu, src.re, k & 31);
-        xk.im = __shfl_sync(0xffffffffu, src.im, k & 31);
-        // rows at or above k see L[r][k] = 0 (strict lower part only), columns right of
-        // k are still e_c there: unconditional updates
-        x0[u] = cfms(x0[u], l0, xk);
-        x1[u] = cfms(x1[u], l1, xk);
-      }
-    }
-  } else {
-    // X = U^{-1} e_c: step k finalises row k (times 1/U_kk) and eliminates it from the rows above
-    for (int k = c0 + 24; k >= 0; --k) {
-      const cplx rd = ld(&rdiag[k]);
-      const cplx u0 = r0 < k ? ld(&A[r0 * DI_S + k]) : mk(0, 0);
-      const cplx u1 = r1 < k ? ld(&A[r1 * DI_S + k]) : mk(0, 0);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (k > c0 + 8 * u) continue;  // column c0 + 8u has nothing below its diagonal
-        const cplx src = k < 32 ? x0[u] : x1[u];
-        cplx xk;
-        xk.re = __shfl_sync(0xffffffffu, src.re, k & 31);
-        xk.im = __shfl_sync(0xffffffffu, src.im, k & 31);
-        xk = cmul(xk, rd);
-        x0[u] = r0 == k ? xk : cfms(x0[u], u0, xk);
-        x1[u] = r1 == k ? xk : cfms(x1[u], u1, xk);
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int c = c0 + 8 * u;
-    if (c < nb) {
-      if (r0 < nb) *Out.at(b, r0, c) = make_double2(x0[u].re, x0[u].im);
-      if (r1 < nb) *Out.at(b, r1, c) = make_double2(x1[u].re, x1[u].im);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) zgetri_diag_kernel(int nb, ZMat D, ZMat Li, ZMat Ui, int* sing) {
-  __shared__ __align__(16) double2 prow[2][2][2 * DI_MAX];
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* A = reinterpret_cast<double2*>(smem_raw);  // 64 x DI_S: the factored block
-  double2* rdiag = A + DI_MAX * DI_S;                  // 1 / U_kk
-  const int b = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int row = tid >> 2, cg = tid & 3;
-  (&prow[0][0][0])[tid] = make_double2(0, 0);
-  (&prow[0][0][0])[tid + 256] = make_double2(0, 0);
-  const unsigned base = (unsigned)__cvta_generic_to_shared(&prow[0][0][0]);
-  cplx a[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int c = cg + 4 * i;
-    if (row < nb && c < nb) a[i] = ld(D.at(b, row, c));
-    else a[i] = mk(row == c ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-  lu_diag_phase2<16>(0, a, nb, D, b, row, cg, lane, base, sing);
-  lu_diag_phase2<12>(4, a, nb, D, b, row, cg, lane, base, sing);
-  lu_diag_phase2<8>(8, a, nb, D, b, row, cg, lane, base, sing);
-  lu_diag_phase2<4>(12, a, nb, D, b, row, cg, lane, base, sing);
-  __syncthreads();  // the factors are in D (written by this CTA): stage them, padded with I
-  for (int e = tid; e < DI_MAX * DI_MAX; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    A[r * DI_S + c] = (r < nb && c < nb) ? *D.at(b, r, c) : make_double2(r == c ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-  if (tid < DI_MAX) {
-    const cplx r = crcp(ld(&A[tid * DI_S + tid]));
-    rdiag[tid] = make_double2(r.re, r.im);
-  }
-  __syncthreads();
-  tri_inv4<true>(A, rdiag, nb, warp, lane, Ui, b);       // columns w, w + 8, w + 16, w + 24
-  tri_inv4<true>(A, rdiag, nb, warp + 32, lane, Ui, b);  // columns w + 32, ..., w + 56
-  __syncthreads();
-  // L^{-1}: the sweep reads A[r][k] for every row; rows r <= k must read 0 -> clear the upper
-  // triangle (incl. the diagonal) of the staged copy now that U^{-1} is done
-  for (int e = tid; e < DI_MAX * DI_MAX; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    if (c >= r) A[r * DI_S + c] = make_double2(0, 0);
-  }
-  __syncthreads();
-  tri_inv4<false>(A, rdiag, nb, warp, lane, Li, b);
-  tri_inv4<false>(A, rdiag, nb, warp + 32, lane, Li, b);
-}
-
-// D = L U in place and Li = L^{-1}, Ui = U^{-1} (one launch; see zgetri_diag_kernel)
-int zgetri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui, int* sing) {
-  if (nb > DI_MAX) return fail(PFX_BADARG, "zgetri_diag: nb > 64");
-  const int smem = (DI_MAX * DI_S + DI_MAX) * (int)sizeof(double2);
-  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgetri_diag_kernel), smem)) return rc;
-  PFX_LAUNCH_F("zgetri_diag", s, 16.0 / 3.0 * nb * nb * (double)nb * batch,
-               zgetri_diag_kernel<<<batch, 256, smem, s>>>(nb, D, Li, Ui, sing));
-  PFX_CUDA_TRY(cudaGetLastError());
-  return PFX_OK;
-}
-
 int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing) {
   static const bool getrf2 = getenv("PFX_GETRF1") == nullptr;  // PFX_GETRF1=1: one column per barrier
   if (nb > DI_MAX) return fail(PFX_BADARG, "zgetrf_diag: nb > 64");

@@ -58,8 +58,6 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
 // ST_SINGULAR in *sing on an exactly zero pivot and ST_PIVOT where partial pivoting inside the
 // block would have exchanged rows (the rows below the block are checked by ztrmm_inplace).
 int zgetrf_diag(cudaStream_t s, int batch, int nb, ZMat D, int* sing);
-// zgetrf_diag + ztrtri_diag in one launch (the chain of every block step).
-int zgetri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui, int* sing);
 // Triangular inverses of a factored diagonal block: Li = L^{-1} (unit lower), Ui = U^{-1}.
 int ztrtri_diag(cudaStream_t s, int batch, int nb, ZMat D, ZMat Li, ZMat Ui);
 // In place: B = Tinv * B (left, B nb x n) or B = B * Tinv (right, B n x nb), Tinv nb x nb
