@@ -68,6 +68,7 @@ struct ProfRec {
   std::string name;
   cudaEvent_t e0, e1;
   double flops;
+  cudaStream_t stream;
 };
 std::mutex g_prof_mu;
 std::vector<ProfRec> g_prof;
@@ -87,6 +88,7 @@ void prof_mark(const char* name_, cudaStream_t stream, bool begin, double flops)
     ProfRec r;
     r.name = name;
     r.flops = flops;
+    r.stream = stream;
     cudaEventCreate(&r.e0);
     cudaEventCreate(&r.e1);
     cudaEventRecord(r.e0, stream);
@@ -369,8 +371,22 @@ int pfx_prof_read(char* buf, int buflen) {
   std::vector<int> counts;
   std::vector<double> totals;
   std::vector<double> fl;
+  // PFX_PROF_TIMELINE=<file>: every launch's (name, stream, start, end) in ms from the first
+  // launch appended to <file> (critical-path analysis of the multi-stream band steps)
+  static const char* tl_path = getenv("PFX_PROF_TIMELINE");
+  FILE* tl = (tl_path && !g_prof.empty()) ? fopen(tl_path, "a") : nullptr;
+  if (tl) {
+    cudaEventSynchronize(g_prof.back().e1);
+    fprintf(tl, "# timeline %zu launches\n", g_prof.size());
+  }
   for (auto& r : g_prof) {
     cudaEventSynchronize(r.e1);
+    if (tl) {
+      float a = 0.0f, b = 0.0f;
+      cudaEventElapsedTime(&a, g_prof.front().e0, r.e0);
+      cudaEventElapsedTime(&b, g_prof.front().e0, r.e1);
+      fprintf(tl, "%s %p %.4f %.4f\n", r.name.c_str(), (void*)r.stream, a * 1e3, b * 1e3);
+    }
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, r.e0, r.e1);
     cudaEventDestroy(r.e0);
@@ -388,6 +404,7 @@ int pfx_prof_read(char* buf, int buflen) {
     totals[i] += ms;
     fl[i] += r.flops;
   }
+  if (tl) fclose(tl);
   g_prof.clear();
   std::string out;
   char line[256];

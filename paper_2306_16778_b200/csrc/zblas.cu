@@ -10,6 +10,8 @@
 // 512-byte warp request, the minimum).
 #include "zblas.cuh"
 
+#include <cuda.h>  // CUtensorMap (the encoder is fetched from the driver at run time, no -lcuda)
+
 namespace pfx {
 
 // K staged KS complex at a time (16 by default; 32 for the small-grid, K <= 64 launches of the
@@ -25,6 +27,75 @@ struct GemmSmem {
 };
 template <int TM, int NW>
 __host__ __device__ constexpr int gemm_stages() { return 2; }  // 3 stages on the 4-warp layout: no gain on long K, -14% on K = 128 (tools/zgemm_probe.cu)
+
+// ---------------------------------------------------------------------------
+// TMA staging of the zgemm tiles (cp.async.bulk.tensor, completion on an mbarrier).  The row
+// padding of GemmSmem (A rows KS + 4, B rows TN + 2 complex) is produced by widening the box:
+// the A box is KS + 4 complex wide and the B box TN + 2, so the copy lands in exactly the
+// padded, bank-conflict-free layout the fragment loads expect (the extra columns are never
+// read; columns past the matrix edge are zero-filled like every out-of-range element).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static const EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (EncodeTiledFn) nullptr;
+    }
+    return (EncodeTiledFn)f;
+  }();
+  return fn;
+}
+
+// Tensor map of a batch of rows x cols complex matrices (row stride ld, batch stride `stride`,
+// elements) as float64 [batch][rows][2 cols]; box = box_rows x box_cols complex.  False when
+// the driver has no encoder or the layout is not expressible (the caller then stages with
+// cp.async).
+static bool zmat_tensor_map(CUtensorMap* map, const ZMat& M, int rows, int cols, int batch, int box_rows,
+                            int box_cols) {
+  const EncodeTiledFn enc = encode_tiled();
+  if (!enc || batch < 1 || rows < 1 || cols < 1) return false;
+  if (batch > 1 && M.stride <= 0) return false;  // broadcast operand
+  if ((reinterpret_cast<uintptr_t>(M.p) & 15) != 0) return false;
+  const int64_t bstride = batch > 1 ? M.stride : M.ld * rows;
+  const cuuint64_t dims[3] = {2 * (cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)M.ld * 16, (cuuint64_t)bstride * 16};
+  const cuuint32_t box[3] = {2 * (cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)M.p, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
   unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -203,9 +274,12 @@ int zcombine(cudaStream_t s, const ZCombine& cm) {
 // instead of componentwise).
 // Two CTAs per SM for the 64x64 tile (<= 128 registers): one CTA's epilogue and K-stage loads
 // overlap the other's DMMA stream (at 156 registers a single CTA per SM ran 15% slower).
-template <int TM, int TN, int NW, bool M3 = false, int GK = 16>
-__global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 : 1) zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                                                        int accumulate, int b_lower_off, ZCombine ride) {
+// TMA: tiles staged by the tensor-memory accelerator (one elected thread issues both boxes of a
+// stage, every thread waits on the stage's mbarrier) instead of 16-byte cp.async by all threads.
+template <int TM, int TN, int NW, bool M3 = false, int GK = 16, bool TMA = false>
+__global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 : 1)
+    zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, int accumulate, int b_lower_off,
+                 ZCombine ride, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
   constexpr int NT = NW * 32;
   if constexpr (TM == 64 && NW == 4) {  // only this layout carries a combine (register budget)
     // the carried residue combine is slice z = 0: dispatched first, it runs beside the tiles
@@ -244,8 +318,26 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
   // triangle adds nothing
   const int kt0 = b_lower_off >= 0 ? max(0, n0 - b_lower_off) / GK : 0;
   if (b_lower_off >= 0 && accumulate && kt0 >= ktiles) return;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(GemmSmem<TM, TN, GK, NS>));
+  if constexpr (TMA) {
+    if (tid == 0) {
+#pragma unroll
+      for (int st = 0; st < NS; ++st) mbar_init(&bars[st], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
   auto load = [&](int buf, int kt) {
     const int k0 = kt * GK;
+    if constexpr (TMA) {
+      if (tid == 0) {
+        constexpr unsigned bytes = (unsigned)sizeof(S.A[0]) + (unsigned)sizeof(S.B[0]);
+        mbar_expect_tx(&bars[buf], bytes);
+        tma_load_3d(&S.A[buf][0][0], &tmA, 2 * k0, m0, b, &bars[buf]);
+        tma_load_3d(&S.B[buf][0][0], &tmB, 2 * n0, k0, b, &bars[buf]);
+      }
+      return;
+    }
 #pragma unroll
     for (int u = 0; u < (TM * GK) / NT; ++u) {
       int e = tid + u * NT;
@@ -266,14 +358,18 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
 #pragma unroll
   for (int st = 0; st < NS - 1; ++st) {
     if (kt0 + st < ktiles) load(st, kt0 + st);
-    cp_async_commit();
+    if constexpr (!TMA) cp_async_commit();
   }
   for (int kt = kt0; kt < ktiles; ++kt) {
     const int buf = (kt - kt0) % NS;
     if (kt + NS - 1 < ktiles) load((kt - kt0 + NS - 1) % NS, kt + NS - 1);
-    cp_async_commit();
-    cp_async_wait<NS - 1>();
-    __syncthreads();
+    if constexpr (TMA) {
+      mbar_wait(&bars[buf], (unsigned)((kt - kt0) / NS) & 1u);
+    } else {
+      cp_async_commit();
+      cp_async_wait<NS - 1>();
+      __syncthreads();
+    }
 #pragma unroll
     for (int kk = 0; kk < GK; kk += 4) {
       double ar[FM], ai[FM], br[FN], bi[FN];
@@ -366,11 +462,24 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
   }
 }
 
+// PFX_ZGEMM_CPASYNC=1 stages the tiles with cp.async (the round-1 loader) for A/B checks.
+static bool zgemm_use_tma() {
+  static const bool on = getenv("PFX_ZGEMM_CPASYNC") == nullptr;
+  return on;
+}
+
 template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
                         bool accumulate, int b_lower_off, const ZCombine* ride) {
-  const int smem = (int)sizeof(GemmSmem<TM, TN, KS, gemm_stages<TM, NW>()>);
-  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(zgemm_kernel<TM, TN, NW, M3, KS>), smem)) return rc;
+  constexpr int NS = gemm_stages<TM, NW>();
+  CUtensorMap tmA, tmB;
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  const bool tma = zgemm_use_tma() && zmat_tensor_map(&tmA, A, m, k, batch, TM, KS + 4) &&
+                   zmat_tensor_map(&tmB, B, k, n, batch, KS, TN + 2);
+  auto kfn = tma ? zgemm_kernel<TM, TN, NW, M3, KS, true> : zgemm_kernel<TM, TN, NW, M3, KS, false>;
+  const int smem = (int)sizeof(GemmSmem<TM, TN, KS, NS>) + (tma ? NS * 8 : 0);
+  if (int rc = raise_smem_limit(reinterpret_cast<const void*>(kfn), smem)) return rc;
   ZCombine rd;
   if (ride) rd = *ride;
   // the combine's shared-memory staging (64 x 65) must fit the GEMM's allocation
@@ -391,8 +500,8 @@ static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double a
     fl = 8.0 * (double)m * batch * nz;
   }
   PFX_LAUNCH_F("zgemm", s, fl,
-               (zgemm_kernel<TM, TN, NW, M3, KS><<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C,
-                                                                       accumulate ? 1 : 0, b_lower_off, rd)));
+               (kfn<<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0, b_lower_off, rd,
+                                                 tmA, tmB)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }

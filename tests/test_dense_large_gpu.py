@@ -53,3 +53,42 @@ def test_full_real_symmetric_inverse(d):
     assert got.dtype == np.float64
     assert rel(got, restate.run_tasks_dense(A, None, 20, threads=8)) <= TOL
     assert np.array_equal(got, got.T)
+
+
+_LOADER_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2306_16778_b200 import (BandedHermitian, ExpOptions, HermitianMatrix, matexp_action, matexp_full,
+                                   workloads)
+A, _, _ = workloads.random_complex_hermitian(1000, -80.0, 0.0, seed=21)
+full = matexp_full(HermitianMatrix(A), ExpOptions(n=12)).value
+band = workloads.c5_band_rect(96, 40, scale=300.0)
+V = np.random.default_rng(4).standard_normal((96 * 40, 3))
+act = matexp_action(BandedHermitian(band), V, ExpOptions(n=16, mode="action")).value
+np.savez(sys.argv[2], full=full, act=act)
+"""
+
+
+def test_zgemm_tma_matches_cp_async(tmp_path):
+    """The zgemm tiles are staged by TMA (cp.async.bulk.tensor into the padded layout) by
+    default; PFX_ZGEMM_CPASYNC=1 stages them with cp.async.  Same arithmetic in the same order,
+    so the large dense path (every 64x64 and 32x32 zgemm shape of the LU and substitutions) and
+    the band path (the short-K 32-deep variant) give bitwise identical results."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for tag, extra in (("tma", {}), ("cpasync", {"PFX_ZGEMM_CPASYNC": "1"})):
+        env = {k: v for k, v in os.environ.items() if k != "PFX_ZGEMM_CPASYNC"}
+        env.update(extra)
+        path = str(tmp_path / f"{tag}.npz")
+        res = subprocess.run([sys.executable, "-c", _LOADER_SCRIPT, root, path], cwd=root, env=env,
+                             capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs[tag] = np.load(path)
+    assert np.array_equal(outs["tma"]["full"], outs["cpasync"]["full"])
+    assert np.array_equal(outs["tma"]["act"], outs["cpasync"]["act"])
+    A, _, _ = workloads.random_complex_hermitian(1000, -80.0, 0.0, seed=21)
+    assert rel(outs["tma"]["full"], restate.run_tasks_dense(A, None, 12, threads=8)) <= TOL
