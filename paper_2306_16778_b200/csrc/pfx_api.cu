@@ -379,14 +379,19 @@ int pfx_prof_read(char* buf, int buflen) {
     cudaEventSynchronize(g_prof.back().e1);
     fprintf(tl, "# timeline %zu launches\n", g_prof.size());
   }
-  for (auto& r : g_prof) {
-    cudaEventSynchronize(r.e1);
-    if (tl) {
+  // the timeline pass runs before any event is destroyed (every record is timed against the
+  // first launch's start event)
+  if (tl) {
+    for (auto& r : g_prof) {
+      cudaEventSynchronize(r.e1);
       float a = 0.0f, b = 0.0f;
       cudaEventElapsedTime(&a, g_prof.front().e0, r.e0);
       cudaEventElapsedTime(&b, g_prof.front().e0, r.e1);
       fprintf(tl, "%s %p %.4f %.4f\n", r.name.c_str(), (void*)r.stream, a * 1e3, b * 1e3);
     }
+  }
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.e1);
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, r.e0, r.e1);
     cudaEventDestroy(r.e0);
