@@ -172,7 +172,7 @@ class ClockSampler:
 class Workload:
     """Inputs resident on the device + a step function calling the native library."""
 
-    def __init__(self, name, torch, dev, pairs_lo, pairs_hi, batch_range=None):
+    def __init__(self, name, torch, dev, pairs_lo, pairs_hi, batch_range=None, col_tasks=None):
         from paper_2306_16778_b200 import workloads as W
         from paper_2306_16778_b200.roots import default_table
 
@@ -225,6 +225,13 @@ class Workload:
         t2, c2 = default_table(n).interleaved()
         self.theta2 = np.ascontiguousarray(t2[2 * pairs_lo: 2 * pairs_hi])
         self.coef2 = np.ascontiguousarray(c2[2 * pairs_lo: 2 * pairs_hi])
+        # C4 at N > 1 with leftover pairs: this rank's (pair, c0, c1) tasks (sharding.colsplit_plan)
+        self.col_ranges = None
+        if col_tasks is not None:
+            idx = [k for k, _, _ in col_tasks]
+            self.theta2 = np.ascontiguousarray(np.concatenate([t2[2 * k: 2 * k + 2] for k in idx]))
+            self.coef2 = np.ascontiguousarray(np.concatenate([c2[2 * k: 2 * k + 2] for k in idx]))
+            self.col_ranges = np.array([[a, b] for _, a, b in col_tasks], dtype=np.int64)
         self.dev_in = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in self.host.items()}
         self.out = None
         self.flush = None
@@ -244,6 +251,9 @@ class Workload:
                                                    out=self.out, stream=stream)
         elif self.name in ("C1", "C3"):
             self.out = _native.expm_dense_device(di["A"], di["V"], self.theta2, self.coef2, 0.0, stream=stream)
+        elif self.name == "C4" and self.col_ranges is not None:
+            self.out = _native.expm_dense_cols_device(di["A"], self.theta2, self.coef2, self.col_ranges, 0.0,
+                                                      out=self.out, stream=stream)
         elif self.name == "C4":
             self.out = _native.expm_dense_device(di["A"], None, self.theta2, self.coef2, 0.0, out=self.out,
                                                  stream=stream)
@@ -388,6 +398,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--prof-steps", type=int, default=3)
     ap.add_argument("--shard", choices=["auto", "pole", "rows", "batch"], default="pole")
+    ap.add_argument("--no-colsplit", action="store_true",
+                    help="C4 at N > 1: plain contiguous pole blocks (no column split of the leftover pairs)")
     ap.add_argument("--check", action="store_true",
                     help="after timing, compare rank 0's sharded result with an unsharded call (check_rel)")
     args = ap.parse_args()
@@ -469,7 +481,14 @@ def main():
     lo, hi = (rank * npairs // world, (rank + 1) * npairs // world) if shard == "pole" else (0, npairs)
     nbatch = W.C3["batch"]
     brange = (rank * nbatch // world, (rank + 1) * nbatch // world) if shard == "batch" else None
-    wl = Workload(args.workload, torch, dev, lo, hi, batch_range=brange)
+    # C4 (dense full mode) with pairs that do not divide over the ranks: whole pairs per rank,
+    # the leftover pairs split by inverse columns (sharding.colsplit_plan)
+    col_tasks = None
+    if args.workload == "C4" and shard == "pole" and world > 1 and npairs % world and not args.no_colsplit:
+        from paper_2306_16778_b200.sharding import colsplit_plan
+        col_tasks = colsplit_plan(npairs, W.C4["d"], rank, world)
+        config["parallelism"] += "; leftover pairs split by inverse columns (cost-balanced)"
+    wl = Workload(args.workload, torch, dev, lo, hi, batch_range=brange, col_tasks=col_tasks)
     stream = torch.cuda.current_stream()
 
     def allgather(mine):
@@ -648,6 +667,8 @@ def main():
         else:
             # one launch of the dominant kernel carries the path's whole algorithmic work per step
             share = {"pole": (hi - lo) / npairs, "rows": 1.0 / world, "batch": 1.0 / world}[shard]
+            if col_tasks is not None:
+                share = 1.0 / world
             flops_per_launch = ALG_FLOPS[args.workload] * wl.evals_per_step * share / (dom_cnt / prof_steps)
         achieved = flops_per_launch / t_launch / 1e12
         roofline = {"bound": "tensor", "pipe": "fp64 (DMMA m8n8k4 peak, measured)", "achieved": achieved,

@@ -126,6 +126,24 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
                    int npairs, double* out, int out_complex, float* per_pair_ms, void* stream);
 
 /*
+ * Column split of the dense full mode for d > 512 (multi-GPU balance: "pole-shard
+ * the factorisations, then split each pair's inverse/solve columns across GPUs").  Pair k
+ * contributes only the columns [col_ranges[2k], col_ranges[2k+1]) of its inverse X_k
+ * (host array of 2*npairs values; each start a multiple of 64):
+ *   complex A:  out (+)= e^c sum_k (P_k + P_k^H),  P_k = a_k X_k restricted to its columns
+ *   real A:     out (+)= e^c sum_k 2 Re(P_k)
+ * so the outputs of calls whose ranges partition [0, d) for every pair add up to
+ * pfx_expm_dense's full-mode result (one NCCL reduce across the ranks, as for pole sharding).
+ * Every pair is factored whole (one batched LU); its forward substitution starts at its first
+ * column (rows above it of L^{-1}E are zero) and only its columns are solved.  accumulate != 0
+ * adds to `out` instead of overwriting it.  Replaces the same reference lines as
+ * pfx_expm_dense's full mode (engine.py:207-213).
+ */
+int pfx_expm_dense_cols(int mem, const double* A, int a_complex, int64_t d, double shift_c, const double* theta2,
+                        const double* coef2, int npairs, const int64_t* col_ranges, double* out, int out_complex,
+                        int accumulate, void* stream);
+
+/*
  * Real symmetric tridiagonal path.
  *   diag (N), off (N-1): T[i][i] = diag[i], T[i+1][i] = T[i][i+1] = off[i].
  *   V, out: N x nrhs real.  Real path only (2 Re(a_k Y_k)).

@@ -39,6 +39,10 @@ SIGNATURES = {
         _int,
         [_int, _vp, _int, _i64, _i64, _vp, _int, _i64, ctypes.c_double, _dp, _dp, _int, _vp, _int, _fp, _vp],
     ),
+    "pfx_expm_dense_cols": (
+        _int,
+        [_int, _vp, _int, _i64, ctypes.c_double, _dp, _dp, _int, ctypes.POINTER(_i64), _vp, _int, _int, _vp],
+    ),
     "pfx_expm_tridiag": (
         _int,
         [_int, _vp, _vp, _i64, _vp, _i64, ctypes.c_double, _dp, _dp, _int, _vp, _fp, _vp],
@@ -303,6 +307,64 @@ def expm_dense_host(A: np.ndarray, V, theta2, coef2, shift_c: float, per_pair_ms
         out = out[..., 0]
     if squeeze_batch:
         out = out[0]
+    return out
+
+
+def expm_dense_cols_device(A, theta2, coef2, col_ranges, shift_c: float = 0.0, out=None, accumulate=False,
+                           stream=None):
+    """Column split of the full mode (include/pfx.h pfx_expm_dense_cols): pair k contributes the
+    columns [col_ranges[k][0], col_ranges[k][1]) of its inverse.  A (d, d) device tensor, d > 512;
+    returns / updates the (d, d) partial whose sum over a partition of the columns is exp(A)."""
+    torch = _torch()
+    A = _f64_view(A)
+    if A.dim() != 2 or A.shape[0] != A.shape[1]:
+        raise BadSpec(f"A must be (d, d), got {tuple(A.shape)}")
+    d = A.shape[0]
+    a_complex = A.dtype == torch.complex128
+    odt = torch.complex128 if a_complex else torch.float64
+    npairs = len(theta2) // 2
+    rg = np.ascontiguousarray(np.asarray(col_ranges, dtype=np.int64).reshape(-1))
+    if rg.size != 2 * npairs:
+        raise BadSpec(f"col_ranges needs one (c0, c1) per pair: {npairs} pairs, got {rg.size // 2} ranges")
+    if out is None:
+        if accumulate:
+            raise BadSpec("accumulate needs an out tensor")
+        out = torch.empty((d, d), dtype=odt, device=A.device)
+    elif out.dtype != odt or tuple(out.shape) != (d, d) or not out.is_contiguous() or out.device != A.device:
+        raise BadSpec(f"out must be a contiguous ({d}, {d}) {odt} tensor on {A.device}")
+    st = lib().pfx_expm_dense_cols(
+        PFX_MEM_DEVICE, _ptr(A), int(a_complex), d, float(shift_c), _f64p(theta2), _f64p(coef2), npairs,
+        rg.ctypes.data_as(ctypes.POINTER(_i64)), _ptr(out), int(a_complex), int(bool(accumulate)), _stream_ptr(stream),
+    )
+    _check(st, "pfx_expm_dense_cols")
+    return out
+
+
+def expm_dense_cols_host(A: np.ndarray, theta2, coef2, col_ranges, shift_c: float = 0.0, out=None, accumulate=False):
+    """Host-array form of expm_dense_cols_device (PFX_MEM_HOST)."""
+    _torch()
+    A = np.ascontiguousarray(A)
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise BadSpec(f"A must be (d, d), got {A.shape}")
+    d = A.shape[0]
+    a_complex = np.iscomplexobj(A)
+    A = A.astype(np.complex128 if a_complex else np.float64, copy=False)
+    odt = np.complex128 if a_complex else np.float64
+    npairs = len(theta2) // 2
+    rg = np.ascontiguousarray(np.asarray(col_ranges, dtype=np.int64).reshape(-1))
+    if rg.size != 2 * npairs:
+        raise BadSpec(f"col_ranges needs one (c0, c1) per pair: {npairs} pairs, got {rg.size // 2} ranges")
+    if out is None:
+        if accumulate:
+            raise BadSpec("accumulate needs an out array")
+        out = np.empty((d, d), dtype=odt)
+    elif out.dtype != odt or out.shape != (d, d) or not out.flags.c_contiguous:
+        raise BadSpec(f"out must be a C-contiguous ({d}, {d}) {odt} array")
+    st = lib().pfx_expm_dense_cols(
+        PFX_MEM_HOST, A.ctypes.data, int(a_complex), d, float(shift_c), _f64p(theta2), _f64p(coef2), npairs,
+        rg.ctypes.data_as(ctypes.POINTER(_i64)), out.ctypes.data, int(a_complex), int(bool(accumulate)), None,
+    )
+    _check(st, "pfx_expm_dense_cols")
     return out
 
 

@@ -20,6 +20,9 @@
 // diagonal dominates the columns of A + theta I, so the check passes on these inputs.
 // Complex action (Yc = M^{-H} V) is obtained from the conjugate shifts theta_k^* as
 // extra batch members, since (A + theta I)^H = A + conj(theta) I for Hermitian A.
+#include <algorithm>
+#include <vector>
+
 #include "zblas.cuh"
 
 namespace pfx {
@@ -181,8 +184,12 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
 // cmb (optional): the residue combine rides along the backward substitution (ZCombine): the
 // entries block row p decides are summed by an extra slice of CTAs in the GEMM launch that
 // follows its last product, and the last block row's by one final combine launch.
-int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
-                   bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb) {
+// c0 (with identity_rhs; a multiple of 64): X holds columns [c0, c0 + ncols) of the identity
+// (the column split of one pair's inverse across GPUs).  Rows above c0 of L^{-1} X
+// are zero, and the trailing block of L^{-1} is the inverse of L's trailing block, so the forward
+// substitution runs on rows >= c0 only; the backward substitution covers every row.
+int lu_subst_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int c0, int ncols,
+                   bool identity_rhs, bool sym_lower, const ZCombine* cmb) {
   const int nb = DL_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -200,7 +207,7 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
     return r;
   };
   int rc;
-  if ((rc = lu_factor_nopiv(s, nsys, d, 0, M, Li, Ui, sing, check_pivots))) return rc;
+  if (!identity_rhs) c0 = 0;
   // Both substitutions run in super-blocks of SB = 8 block rows: one GEMM with m = 512 rows
   // applies everything already final outside the super-block (its column strips of X stream
   // from HBM once per super-block instead of once per block row, shared by the 8 row tiles
@@ -208,20 +215,21 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
   constexpr int SB = 8 * DL_NB;
   // forward: X_p -= L[p, :p] X[:p]; X_p = L_pp^{-1} X_p
   ProfTag tag_fwd("fwd");
-  for (int J0 = 0; J0 < d; J0 += SB) {
+  for (int J0 = c0; J0 < d; J0 += SB) {
     const int J1 = std::min(d, J0 + SB);
-    // identity RHS: X[:J0, :J0] = L^{-1} so far is unit lower triangular, and each column
+    // identity RHS: X[c0:J0, :J0 - c0] = L^{-1} so far is unit lower triangular, and each column
     // tile's product starts at its own diagonal (half the products of a full GEMM)
-    if (J0 > 0 && (rc = zgemm(s, nsys, J1 - J0, identity_rhs ? J0 : ncols, J0, -1.0, sub(M, J0, 0), sub(X, 0, 0),
-                              sub(X, J0, 0), true, identity_rhs ? 0 : -1)))
+    if (J0 > c0 && (rc = zgemm(s, nsys, J1 - J0, identity_rhs ? std::min(ncols, J0 - c0) : ncols, J0 - c0, -1.0,
+                               sub(M, J0, c0), sub(X, c0, 0), sub(X, J0, 0), true, identity_rhs ? 0 : -1)))
       return rc;
     for (int j0 = J0; j0 < J1; j0 += nb) {
       const int jb = std::min(nb, d - j0);
-      const int nc = identity_rhs ? j0 : ncols;                        // columns the update can touch
-      const int ns = identity_rhs ? std::min(ncols, j0 + jb) : ncols;  // columns the solve touches
-      // rows [J0, j0) of X are lower triangular from column J0 on: B[r][c] = 0 for r + J0 < c
-      if (j0 > J0 && (rc = zgemm(s, nsys, jb, nc, j0 - J0, -1.0, sub(M, j0, J0), sub(X, J0, 0), sub(X, j0, 0),
-                                 true, identity_rhs ? J0 : -1)))
+      const int nc = identity_rhs ? std::min(ncols, j0 - c0) : ncols;       // columns the update can touch
+      const int ns = identity_rhs ? std::min(ncols, j0 + jb - c0) : ncols;  // columns the solve touches
+      // rows [J0, j0) of X are lower triangular from column J0 - c0 on: B[r][c] = 0 for r + J0 - c0 < c
+      if (j0 > J0 && nc > 0 &&
+          (rc = zgemm(s, nsys, jb, nc, j0 - J0, -1.0, sub(M, j0, J0), sub(X, J0, 0), sub(X, j0, 0), true,
+                      identity_rhs ? J0 - c0 : -1)))
         return rc;
       if ((rc = ztrmm_inplace(s, nsys, jb, ns, li(j0), sub(X, j0, 0), false, false))) return rc;
     }
@@ -265,6 +273,12 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
   }
   if (pend.mode && (rc = zcombine(s, pend))) return rc;  // block row 0
   return PFX_OK;
+}
+
+int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
+                   bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb) {
+  if (int rc = lu_factor_nopiv(s, nsys, d, 0, M, Li, Ui, sing, check_pivots)) return rc;
+  return lu_subst_nopiv(s, nsys, d, M, X, Li, Ui, 0, ncols, identity_rhs, sym_lower, cmb);
 }
 
 int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* ipiv, int* sing);
@@ -428,6 +442,147 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
+  if (*hsg & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
+  return PFX_OK;
+}
+
+// ---- column split of the full mode (multi-GPU balance) ---------------------
+// X_k = columns [c0, c0 + nc) of the identity (one range per group of systems)
+__global__ void dl_ident_cols(ZMat X, int d, int c0, int nc) {
+  const int k = blockIdx.y;
+  const int64_t n = (int64_t)d * nc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / nc, j = e - i * nc;
+    *X.at(k, i, j) = make_double2(i == j + c0 ? 1.0 : 0.0, 0.0);
+  }
+}
+
+// out (+)= scale * sum_k S_k restricted to the inverse columns [c0, c0 + nc) (k ascending):
+//   real path     out[i][c0 + j] = sum_k 2 Re(a_k X_k[i][j])                     (other columns 0)
+//   complex path  out = P + P^H,  P[i][c0 + j] = sum_k a_k X_k[i][j]             (P zero elsewhere)
+// so the outputs of a partition of [0, d) add up to the unsplit full-mode result.
+__global__ void dl_combine_cols(ZMat X, int d, int c0, int nc, int nk, const double2* coef, int real_path,
+                                double scale, double* out, int accumulate) {
+  const int64_t n = (int64_t)d * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d, j = e - i * d;
+    const bool cj = j >= c0 && j < c0 + nc, ci = i >= c0 && i < c0 + nc;
+    if (real_path) {
+      double acc = 0.0;
+      if (cj)
+        for (int k = 0; k < nk; ++k) {
+          cplx a = ld(&coef[k]);
+          cplx x = ld(X.at(k, i, j - c0));
+          double sk = 2.0 * fma(a.re, x.re, -a.im * x.im);
+          acc = k == 0 ? sk : acc + sk;
+        }
+      if (scale != 1.0) acc *= scale;
+      out[e] = accumulate ? out[e] + acc : acc;
+    } else {
+      cplx acc = mk(0, 0);
+      if (cj || ci)
+        for (int k = 0; k < nk; ++k) {
+          cplx a = ld(&coef[k]);
+          cplx sk = mk(0, 0);
+          if (cj) sk = cmul(a, ld(X.at(k, i, j - c0)));
+          if (ci) sk = cadd(sk, cconj(cmul(a, ld(X.at(k, j, i - c0)))));
+          acc = k == 0 ? sk : cadd(acc, sk);
+        }
+      if (scale != 1.0) acc = cscale(acc, scale);
+      double2* o = reinterpret_cast<double2*>(out) + e;
+      if (accumulate) {
+        const double2 p = *o;
+        acc.re += p.x;
+        acc.im += p.y;
+      }
+      *o = make_double2(acc.re, acc.im);
+    }
+  }
+}
+
+// Full mode with a column range per pair: pair k contributes the columns
+// [ranges[2k], ranges[2k + 1]) of its inverse (host array; starts multiples of 64; pairs with
+// equal ranges must be adjacent to share their launches).  All pairs are factored in one
+// batched LU, then each group of equal ranges runs its substitutions and its combine.
+int dense_large_cols_run(const double* A, int a_complex, int d, double shift_c, const double2* theta_d,
+                         const double2* coef_d, int npairs, const int64_t* ranges, double* out, int accumulate,
+                         cudaStream_t stream, int pivot) {
+  const int real_path = !a_complex;
+  const int nsys = npairs;
+  const size_t mbytes = (size_t)nsys * d * d * sizeof(double2);
+  const int nblk = (d + DL_NB - 1) / DL_NB;
+  const size_t libytes = (size_t)nsys * nblk * DL_NB * DL_NB * sizeof(double2);
+  char* ws = static_cast<char*>(scratch(1, 2 * mbytes + 2 * libytes + 256));
+  if (!ws) return fail(PFX_CUDA, "large dense workspace allocation failed");
+  int* ipiv = reinterpret_cast<int*>(ws + 2 * mbytes);
+  ZMat M{reinterpret_cast<double2*>(ws), d, (int64_t)d * d};
+  ZMat X{reinterpret_cast<double2*>(ws + mbytes), d, (int64_t)d * d};
+  ZMat Li{reinterpret_cast<double2*>(ws + 2 * mbytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
+  ZMat Ui{reinterpret_cast<double2*>(ws + 2 * mbytes + libytes), DL_NB, (int64_t)nblk * DL_NB * DL_NB};
+  int* sing = reinterpret_cast<int*>(ws + 2 * mbytes + 2 * libytes);
+  auto sys = [](ZMat T, int k) {
+    T.p += (int64_t)k * T.stride;
+    return T;
+  };
+  struct Group {
+    int k0, nk, c0, nc;
+  };
+  std::vector<Group> groups;
+  for (int k = 0; k < npairs; ++k) {
+    const int c0 = (int)ranges[2 * k], nc = (int)(ranges[2 * k + 1] - ranges[2 * k]);
+    if (!groups.empty() && groups.back().c0 == c0 && groups.back().nc == nc)
+      ++groups.back().nk;
+    else
+      groups.push_back({k, 1, c0, nc});
+  }
+  int* hsg = pinned_word();
+  if (!hsg) return fail(PFX_CUDA, "pinned status word allocation failed");
+  const double scale = shift_c == 0.0 ? 1.0 : exp(shift_c);
+  auto build = [&](bool with_x) -> int {
+    PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
+    PFX_LAUNCH("dl_build", stream, dl_build<<<dim3(1184, nsys), 256, 0, stream>>>(A, a_complex, d, nullptr, 0, 0, 1,
+                                                                                    shift_c, theta_d, npairs, nsys, M, X));
+    PFX_CUDA_TRY(cudaGetLastError());
+    if (with_x)
+      for (const Group& g : groups) {
+        PFX_LAUNCH("dl_build", stream,
+                   dl_ident_cols<<<dim3(592, g.nk), 256, 0, stream>>>(sys(X, g.k0), d, g.c0, g.nc));
+        PFX_CUDA_TRY(cudaGetLastError());
+      }
+    return PFX_OK;
+  };
+  int rc;
+  bool pivoted = pivot == 1;
+  if ((rc = build(true))) return rc;
+  if (!pivoted) {
+    if ((rc = lu_factor_nopiv(stream, nsys, d, 0, M, Li, Ui, sing, pivot == 2))) return rc;
+    for (const Group& g : groups)
+      if ((rc = lu_subst_nopiv(stream, g.nk, d, sys(M, g.k0), sys(X, g.k0), sys(Li, g.k0), sys(Ui, g.k0), g.c0, g.nc,
+                               true, false, nullptr)))
+        return rc;
+    if (pivot == 2) {
+      PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      if (int rc_ = sync_stream(stream)) return rc_;
+      if (*hsg & ST_PIVOT) {
+        note_pivot_fallback();
+        pivoted = true;
+        if ((rc = build(true))) return rc;
+      }
+    }
+  }
+  if (pivoted)
+    for (const Group& g : groups)
+      if ((rc = lu_solve_piv(stream, g.nk, d, sys(M, g.k0), sys(X, g.k0), g.nc, ipiv, sing))) return rc;
+  bool first = true;
+  for (const Group& g : groups) {
+    PFX_LAUNCH("dl_combine", stream,
+               dl_combine_cols<<<2368, 256, 0, stream>>>(sys(X, g.k0), d, g.c0, g.nc, g.nk, coef_d + g.k0, real_path,
+                                                         scale, out, (accumulate || !first) ? 1 : 0));
+    PFX_CUDA_TRY(cudaGetLastError());
+    first = false;
+  }
+  PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (int rc_ = sync_stream(stream)) return rc_;
   if (*hsg & ST_SINGULAR) return fail(PFX_SINGULAR, "exactly zero pivot in a shifted factorization");
   return PFX_OK;
 }

@@ -26,6 +26,9 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
                     int real_path, double shift_c, const double2* theta_d, const double2* coef_d, int npairs,
                     double* out, cudaStream_t stream, float* per_pair_ms, int pivot, const double* A_host = nullptr,
                     const double* V_host = nullptr, double* out_host = nullptr);
+int dense_large_cols_run(const double* A, int a_complex, int d, double shift_c, const double2* theta_d,
+                         const double2* coef_d, int npairs, const int64_t* ranges, double* out, int accumulate,
+                         cudaStream_t stream, int pivot);
 int tridiag_run(const double* diag, const double* off, int64_t N, const double* V, int64_t nrhs, double shift_c,
                 const double2* theta_d, const double2* coef_d, int npairs, double* out, cudaStream_t stream,
                 float* launch_ms, const double* V_host = nullptr, double* out_host = nullptr,
@@ -571,6 +574,48 @@ int pfx_expm_dense(int mem, const double* A, int a_complex, int64_t d, int64_t b
     rc = dense_large_run(Ad, a_complex, (int)d, Vd, v_complex, ncols, full, real_path, shift_c, th, co, npairs, Od,
                          stream, per_pair_ms, dense_pivot_arg());
   }
+  if (rc) return rc;
+  if (mem == PFX_MEM_HOST) {
+    PFX_CUDA_TRY(cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, stream));
+    if (int rc_ = sync_stream(stream)) return rc_;
+  }
+  return PFX_OK;
+}
+
+int pfx_expm_dense_cols(int mem, const double* A, int a_complex, int64_t d, double shift_c, const double* theta2,
+                        const double* coef2, int npairs, const int64_t* col_ranges, double* out, int out_complex,
+                        int accumulate, void* stream_) {
+  g_err.clear();
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (mem != PFX_MEM_DEVICE && mem != PFX_MEM_HOST) return fail(PFX_BADARG, "mem must be PFX_MEM_DEVICE or PFX_MEM_HOST");
+  if (!A || !out || !col_ranges) return fail(PFX_BADARG, "A, out and col_ranges must be non-null");
+  if (dense_batched_supported(d) || d > (1 << 20))
+    return fail(PFX_BADARG, "the column split applies to the blocked large path (d > 512)");
+  if (!std::isfinite(shift_c)) return fail(PFX_BADARG, "shift must be finite");
+  int rc = check_poles(theta2, coef2, npairs);
+  if (rc) return rc;
+  if (out_complex != (a_complex ? 1 : 0))
+    return fail(PFX_BADARG, "out_complex must be 1 exactly when A is complex (engine.py:185)");
+  for (int k = 0; k < npairs; ++k) {
+    const int64_t c0 = col_ranges[2 * k], c1 = col_ranges[2 * k + 1];
+    if (c0 < 0 || c1 <= c0 || c1 > d || c0 % 64 != 0)
+      return fail(PFX_BADARG, "column ranges need 0 <= c0 < c1 <= d with c0 a multiple of 64");
+  }
+  const size_t abytes = (size_t)d * d * sizeof(double) * (a_complex ? 2 : 1);
+  const size_t obytes = (size_t)d * d * sizeof(double) * (out_complex ? 2 : 1);
+  PFX_DEVICE_LOCK(stream);
+  const double2 *th = nullptr, *co = nullptr;
+  if ((rc = upload_poles(theta2, coef2, npairs, stream, &th, &co))) return rc;
+  const double* Ad = nullptr;
+  if ((rc = stage_in(mem, 3, A, abytes, stream, &Ad))) return rc;
+  double* Od = out;
+  if (mem == PFX_MEM_HOST) {
+    Od = static_cast<double*>(scratch(6, obytes));
+    if (!Od) return fail(PFX_CUDA, "staging allocation failed");
+    if (accumulate) PFX_CUDA_TRY(cudaMemcpyAsync(Od, out, obytes, cudaMemcpyHostToDevice, stream));
+  }
+  rc = dense_large_cols_run(Ad, a_complex, (int)d, shift_c, th, co, npairs, col_ranges, Od, accumulate, stream,
+                            dense_pivot_arg());
   if (rc) return rc;
   if (mem == PFX_MEM_HOST) {
     PFX_CUDA_TRY(cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, stream));

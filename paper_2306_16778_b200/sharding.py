@@ -24,6 +24,56 @@ def slice_poles(theta2: np.ndarray, coef2: np.ndarray, lo: int, hi: int):
     return np.ascontiguousarray(theta2[2 * lo: 2 * hi]), np.ascontiguousarray(coef2[2 * lo: 2 * hi])
 
 
+def _col_cost(u: float) -> float:
+    """Cost of the inverse columns [0, u d) of one pair in units of d^3 (complex full mode):
+    a column at c takes a forward substitution over the rows below it, (1 - c/d)^2, and a
+    backward substitution over every row, 1."""
+    return (1.0 - (1.0 - u) ** 3) / 3.0 + u
+
+
+def colsplit_plan(npairs: int, d: int, rank: int, world: int, align: int = 64):
+    """Pole sharding with the leftover pairs split by columns (dense full mode).
+
+    Each rank takes npairs // world whole pairs (contiguous, ascending).  The npairs % world
+    leftover pairs are cut into `world` pieces of equal substitution cost along their inverse
+    columns (cut points rounded to `align`); a piece that crosses a pair boundary becomes two
+    ranges.  Returns this rank's [(pair, c0, c1), ...] in ascending pair order, whole pairs as
+    (k, 0, d).  Every pair's ranges over all ranks partition [0, d) exactly."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    base, rem = divmod(npairs, world)
+    tasks = [(k, 0, d) for k in range(rank * base, (rank + 1) * base)]
+    if rem == 0:
+        return tasks
+    total = _col_cost(1.0)
+
+    def cut(t: float) -> tuple[int, int]:
+        """Position t in [0, rem] of the cost line -> (leftover pair index, column)."""
+        t = min(max(t, 0.0), float(rem))
+        p = min(int(t), rem - 1)
+        target = (t - p) * total
+        lo, hi = 0.0, 1.0
+        for _ in range(60):
+            mid = 0.5 * (lo + hi)
+            if _col_cost(mid) < target:
+                lo = mid
+            else:
+                hi = mid
+        c = int(round(hi * d / align)) * align
+        return p, min(max(c, 0), d)
+
+    cuts = [cut(rem * r / world) for r in range(world + 1)]
+    cuts[0], cuts[-1] = (0, 0), (rem - 1, d)
+    (p0, c0), (p1, c1) = cuts[rank], cuts[rank + 1]
+    first = world * base
+    for p in range(p0, p1 + 1):
+        a = c0 if p == p0 else 0
+        b = c1 if p == p1 else d
+        if b > a:
+            tasks.append((first + p, a, b))
+    return tasks
+
+
 def reduce_partials(local, group=None, dst: int = 0):
     """Sum the ranks' partial results onto `dst` with ONE collective (torch.distributed.reduce).
 

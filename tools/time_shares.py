@@ -47,10 +47,26 @@ if "C4" in which:
     A, _ = W.c4_matrix()
     t2, c2 = default_table(24).interleaved()
     Ad = torch.from_numpy(A).to(dev)
-    for R in (1, 2, 4, 8):
+    for R in (1, 2, 4, 8, 5):
         npr = largest_block(12, R)
         ms = timeit(lambda: _native.expm_dense_device(Ad, None, t2[:2 * npr], c2[:2 * npr], 0.0), 1)
-        print(f"C4 ranks={R} pole-shard ({npr} pairs) {ms:.1f} ms", flush=True)
+        line = f"C4 ranks={R} pole-shard ({npr} pairs) {ms:.1f} ms"
+        if 12 % R:
+            # leftover pairs split by inverse columns (sharding.colsplit_plan): every rank's share
+            from paper_2306_16778_b200.sharding import colsplit_plan
+
+            worst = 0.0
+            for r in range(R):
+                tasks = colsplit_plan(12, A.shape[0], r, R)
+                idx = [k for k, _, _ in tasks]
+                th = np.concatenate([t2[2 * k: 2 * k + 2] for k in idx])
+                co = np.concatenate([c2[2 * k: 2 * k + 2] for k in idx])
+                rg = [(a, b) for _, a, b in tasks]
+                t = timeit(lambda: _native.expm_dense_cols_device(Ad, th, co, rg), 1)
+                worst = max(worst, t)
+                line += f"\n   colsplit rank {r}: {tasks} {t:.1f} ms"
+            line += f"\n   colsplit worst rank {worst:.1f} ms"
+        print(line, flush=True)
 if "C5" in which:
     band, V = W.c5_band(), W.c5_rhs()
     t2, c2 = default_table(16).interleaved()
