@@ -126,14 +126,14 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
   // one 64-column panel: diagonal LU, both triangular inverses, U12 = L11^{-1} A12 over the
   // whole row block, L21 = A21 U11^{-1} over the whole column block (checked against partial
   // pivoting in checked mode)
-  auto factor = [&](int j0, int jb, int rest) -> int {
+  auto factor = [&](cudaStream_t st, int j0, int jb, int rest) -> int {
     int r;
-    if ((r = zgetrf_diag(s, nsys, jb, sub(M, j0, j0), sing))) return r;
-    if ((r = ztrtri_diag(s, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return r;
+    if ((r = zgetrf_diag(st, nsys, jb, sub(M, j0, j0), sing))) return r;
+    if ((r = ztrtri_diag(st, nsys, jb, sub(M, j0, j0), li(j0), ui(j0)))) return r;
     if (rest + naug > 0 &&
-        (r = ztrmm_inplace(s, nsys, jb, rest + naug, li(j0), sub(M, j0, j0 + jb), false, false)))
+        (r = ztrmm_inplace(st, nsys, jb, rest + naug, li(j0), sub(M, j0, j0 + jb), false, false)))
       return r;
-    if (rest > 0 && (r = ztrmm_inplace(s, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true, sub(M, j0, j0),
+    if (rest > 0 && (r = ztrmm_inplace(st, nsys, jb, rest, ui(j0), sub(M, j0 + jb, j0), true, true, sub(M, j0, j0),
                                        check_pivots ? sing : nullptr)))
       return r;
     return PFX_OK;
@@ -150,23 +150,83 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
     const int g = e ? atoi(e) : DL_GROUP;
     return g < 1 ? 1 : (g > 8 ? 8 : g);
   }();
+  // Look-ahead (d >= 2048): the group's trailing update is split into the NEXT group's
+  // L-shaped strip (its 64 G columns below and its 64 G rows to the right) and the remainder
+  // beyond it.  The strip and the next group's panels (the latency-bound chain: diagonal LU,
+  // inverses, narrow products) run on a high-priority stream, the remainder -- the bulk of the
+  // DMMA work -- on the caller's stream beside them; the next strip update waits for it.
+  // PFX_LU_LOOKAHEAD=0 keeps everything on one stream.
+  static const bool la_on = [] {
+    const char* e = getenv("PFX_LU_LOOKAHEAD");
+    return !(e && atoi(e) == 0);
+  }();
+  struct LookAhead {
+    cudaStream_t hp = nullptr;
+    cudaEvent_t panels = nullptr, rest = nullptr, done = nullptr;
+  };
+  static LookAhead las[kMaxDevices];
+  LookAhead* la = nullptr;
+  if (la_on && d >= 2048 && d > 2 * G * nb) {
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
+    la = &las[dev];
+    if (!la->hp) {
+      int lo = 0, hi = 0;
+      PFX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      PFX_CUDA_TRY(cudaStreamCreateWithPriority(&la->hp, cudaStreamNonBlocking, hi));
+      PFX_CUDA_TRY(cudaEventCreateWithFlags(&la->panels, cudaEventDisableTiming));
+      PFX_CUDA_TRY(cudaEventCreateWithFlags(&la->rest, cudaEventDisableTiming));
+      PFX_CUDA_TRY(cudaEventCreateWithFlags(&la->done, cudaEventDisableTiming));
+    }
+    PFX_CUDA_TRY(cudaEventRecord(la->done, s));  // everything before (the build) precedes the chain
+    PFX_CUDA_TRY(cudaStreamWaitEvent(la->hp, la->done, 0));
+  }
+  cudaStream_t const cs = la ? la->hp : s;  // the stream of the panel chain
+  bool rest_pending = false;  // a remainder update on `s` the next strip update must wait for
   for (int g0 = 0; g0 < d; g0 += G * nb) {
     const int gend = std::min(d, g0 + G * nb);
     for (int jp = g0; jp < gend; jp += nb) {
       const int jb = std::min(nb, d - jp);
       const int rest = d - jp - jb;
       if (jp > g0) {
-        if ((rc = zgemm(s, nsys, d - jp, jb, jp - g0, -1.0, sub(M, jp, g0), sub(M, g0, jp), sub(M, jp, jp))))
+        if ((rc = zgemm(cs, nsys, d - jp, jb, jp - g0, -1.0, sub(M, jp, g0), sub(M, g0, jp), sub(M, jp, jp))))
           return rc;
-        if (rest + naug > 0 && (rc = zgemm(s, nsys, jb, rest + naug, jp - g0, -1.0, sub(M, jp, g0),
+        if (rest + naug > 0 && (rc = zgemm(cs, nsys, jb, rest + naug, jp - g0, -1.0, sub(M, jp, g0),
                                            sub(M, g0, jp + jb), sub(M, jp, jp + jb))))
           return rc;
       }
-      if ((rc = factor(jp, jb, rest))) return rc;
+      if ((rc = factor(cs, jp, jb, rest))) return rc;
     }
-    if (gend < d && (rc = zgemm(s, nsys, d - gend, d - gend + naug, gend - g0, -1.0, sub(M, gend, g0),
-                                sub(M, g0, gend), sub(M, gend, gend))))
+    if (gend >= d) break;
+    const int K = gend - g0;
+    if (!la) {
+      if ((rc = zgemm(s, nsys, d - gend, d - gend + naug, K, -1.0, sub(M, gend, g0), sub(M, g0, gend),
+                      sub(M, gend, gend))))
+        return rc;
+      continue;
+    }
+    const int gend2 = std::min(d, gend + G * nb);
+    PFX_CUDA_TRY(cudaEventRecord(la->panels, cs));
+    // the strip takes the previous remainder update first
+    if (rest_pending) PFX_CUDA_TRY(cudaStreamWaitEvent(cs, la->rest, 0));
+    if ((rc = zgemm(cs, nsys, d - gend, gend2 - gend, K, -1.0, sub(M, gend, g0), sub(M, g0, gend), sub(M, gend, gend))))
       return rc;
+    if (d - gend2 + naug > 0 && (rc = zgemm(cs, nsys, gend2 - gend, d - gend2 + naug, K, -1.0, sub(M, gend, g0),
+                                            sub(M, g0, gend2), sub(M, gend, gend2))))
+      return rc;
+    rest_pending = false;
+    if (gend2 < d) {
+      PFX_CUDA_TRY(cudaStreamWaitEvent(s, la->panels, 0));
+      if ((rc = zgemm(s, nsys, d - gend2, d - gend2 + naug, K, -1.0, sub(M, gend2, g0), sub(M, g0, gend2),
+                      sub(M, gend2, gend2))))
+        return rc;
+      PFX_CUDA_TRY(cudaEventRecord(la->rest, s));
+      rest_pending = true;
+    }
+  }
+  if (la) {
+    PFX_CUDA_TRY(cudaEventRecord(la->done, cs));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(s, la->done, 0));
   }
   return PFX_OK;
 }
@@ -556,10 +616,38 @@ int dense_large_cols_run(const double* A, int a_complex, int d, double shift_c, 
   if ((rc = build(true))) return rc;
   if (!pivoted) {
     if ((rc = lu_factor_nopiv(stream, nsys, d, 0, M, Li, Ui, sing, pivot == 2))) return rc;
-    for (const Group& g : groups)
-      if ((rc = lu_subst_nopiv(stream, g.nk, d, sys(M, g.k0), sys(X, g.k0), sys(Li, g.k0), sys(Ui, g.k0), g.c0, g.nc,
+    // groups are independent after the factorisation: every other group's substitution chain
+    // runs on a side stream, so the narrow launches of a few systems (block-row products and
+    // triangular solves inside a super-block) overlap with the other group's
+    struct Side {
+      cudaStream_t st = nullptr;
+      cudaEvent_t fork = nullptr, join = nullptr;
+    };
+    static Side sides[kMaxDevices];
+    Side* sd = nullptr;
+    if (groups.size() > 1) {
+      const int dev = current_device();
+      if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
+      sd = &sides[dev];
+      if (!sd->st) {
+        PFX_CUDA_TRY(cudaStreamCreateWithFlags(&sd->st, cudaStreamNonBlocking));
+        PFX_CUDA_TRY(cudaEventCreateWithFlags(&sd->fork, cudaEventDisableTiming));
+        PFX_CUDA_TRY(cudaEventCreateWithFlags(&sd->join, cudaEventDisableTiming));
+      }
+      PFX_CUDA_TRY(cudaEventRecord(sd->fork, stream));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(sd->st, sd->fork, 0));
+    }
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const Group& g = groups[gi];
+      cudaStream_t gs = (sd && (gi & 1)) ? sd->st : stream;
+      if ((rc = lu_subst_nopiv(gs, g.nk, d, sys(M, g.k0), sys(X, g.k0), sys(Li, g.k0), sys(Ui, g.k0), g.c0, g.nc,
                                true, false, nullptr)))
         return rc;
+    }
+    if (sd) {
+      PFX_CUDA_TRY(cudaEventRecord(sd->join, sd->st));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(stream, sd->join, 0));
+    }
     if (pivot == 2) {
       PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
       if (int rc_ = sync_stream(stream)) return rc_;
