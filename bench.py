@@ -172,7 +172,7 @@ class ClockSampler:
 class Workload:
     """Inputs resident on the device + a step function calling the native library."""
 
-    def __init__(self, name, torch, dev, pairs_lo, pairs_hi, batch_range=None, col_tasks=None):
+    def __init__(self, name, torch, dev, pairs_lo, pairs_hi, batch_range=None, col_tasks=None, c1_batch=1):
         from paper_2306_16778_b200 import workloads as W
         from paper_2306_16778_b200.roots import default_table
 
@@ -190,10 +190,16 @@ class Workload:
         elif name == "C1":
             n = W.C1["n"]
             A, v, _ = W.c1_inputs()
+            if c1_batch > 1:
+                # throughput mode: c1_batch independent C1 problems (trials 0..B-1 of the same
+                # recipe) in one call, as the CPU arm runs one problem per process at a time
+                A = np.stack([W.random_real_symmetric(W.C1["d"], W.C1["lo"], W.C1["hi"], 0, t)[0]
+                              for t in range(c1_batch)])
+                v = np.stack([W.unit_vector(W.C1["d"], 0, t) for t in range(c1_batch)])
             self.host = dict(A=A, V=v)
             self.h2d = A.nbytes + v.nbytes
             self.d2h = v.nbytes
-            self.evals_per_step = 1.0
+            self.evals_per_step = float(c1_batch)
         elif name == "C3":
             n = W.C3["n"]
             A, V = W.c3_batch()
@@ -239,7 +245,7 @@ class Workload:
             self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         # pinned host copies (inputs and result) for the end-to-end number
         self.pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in self.host.items()}
-        out_elems = {"C2": 16 << 20, "C1": 128, "C3": 512 * 256 * 2, "C4": 4096 * 4096 * 2, "C5": 262144 * 8}[name]
+        out_elems = {"C2": 16 << 20, "C1": 128 * c1_batch, "C3": 512 * 256 * 2, "C4": 4096 * 4096 * 2, "C5": 262144 * 8}[name]
         self.pinned_out = torch.empty(out_elems, dtype=torch.float64).pin_memory()
 
     def step(self, stream):
@@ -398,6 +404,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--prof-steps", type=int, default=3)
     ap.add_argument("--shard", choices=["auto", "pole", "rows", "batch"], default="pole")
+    ap.add_argument("--c1-batch", type=int, default=1,
+                    help="C1 only: this many independent C1 problems per step in one call (throughput mode)")
     ap.add_argument("--no-colsplit", action="store_true",
                     help="C4 at N > 1: plain contiguous pole blocks (no column split of the leftover pairs)")
     ap.add_argument("--check", action="store_true",
@@ -488,7 +496,13 @@ def main():
         from paper_2306_16778_b200.sharding import colsplit_plan
         col_tasks = colsplit_plan(npairs, W.C4["d"], rank, world)
         config["parallelism"] += "; leftover pairs split by inverse columns (cost-balanced)"
-    wl = Workload(args.workload, torch, dev, lo, hi, batch_range=brange, col_tasks=col_tasks)
+    if args.c1_batch > 1:
+        if args.workload != "C1":
+            raise SystemExit("--c1-batch applies to --workload C1")
+        config["batch"] = args.c1_batch
+        config["workload"] += f" x {args.c1_batch} independent problems per step (throughput mode)"
+    wl = Workload(args.workload, torch, dev, lo, hi, batch_range=brange, col_tasks=col_tasks,
+                  c1_batch=args.c1_batch)
     stream = torch.cuda.current_stream()
 
     def allgather(mine):
@@ -633,7 +647,7 @@ def main():
         out_sh = compute(stream)
         torch.cuda.synchronize()
         if rank == 0:
-            full = Workload(args.workload, torch, dev, 0, npairs)
+            full = Workload(args.workload, torch, dev, 0, npairs, c1_batch=args.c1_batch)
             ref = full.step(stream)
             torch.cuda.synchronize()
             a = out_sh.reshape(ref.shape[0], -1) if shard != "batch" else out_sh.reshape(out_sh.shape[0], -1)

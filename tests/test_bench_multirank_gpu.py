@@ -41,3 +41,21 @@ def test_two_rank_bench_line(workload, shard, tag):
     # parity: rank 0's part of the sharded result equals the unsharded computation (the pole
     # shards' partial sums meet in a different order, so to rounding, not bitwise)
     assert d["check_rel"] is not None and d["check_rel"] <= 1e-12, d["check_rel"]
+
+
+def test_c4_colsplit_five_ranks():
+    # 12 pairs on 5 ranks: two whole pairs per rank, the two leftover pairs split by inverse
+    # columns (sharding.colsplit_plan); rank 0's reduced result equals the unsharded exp(A)
+    env = dict(os.environ, PFX_BENCH_GLOO="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "5",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "5", "--workload", "C4", "--steps", "1", "--warmup", "3", "--e2e-steps", "1",
+           "--prof-steps", "1", "--check"]
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 5 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "split by inverse columns" in d["config"]["parallelism"]
+    assert d["check_rel"] is not None and d["check_rel"] <= 1e-12, d["check_rel"]

@@ -191,3 +191,49 @@ def test_gloo_colsplit_two_ranks_match_unsharded(tmp_path):
     want = restate.run_tasks_dense(A, None, 6)
     got = np.load(out)
     assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+
+
+def _engine_colsplit_worker(rank, world, port, out_path):
+    # ExpOptions(distributed=True), full mode, d > 512, 3 pairs on 2 ranks: the engine hands the
+    # native layer this rank's colsplit_plan tasks; LAPACK solves stand in for the GPU call
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2306_16778_b200 import ExpOptions, HermitianMatrix, _native, matexp_full, workloads
+    from paper_2306_16778_b200.sharding import colsplit_plan
+
+    seen = []
+
+    def fake_cols_host(a, theta2, coef2, col_ranges, shift_c=0.0, out=None, accumulate=False):
+        th = theta2[0::2] + 1j * theta2[1::2]
+        co = coef2[0::2] + 1j * coef2[1::2]
+        d = a.shape[0]
+        seen.append([tuple(r) for r in col_ranges])
+        acc = np.zeros((d, d), dtype=complex)
+        for k, (c0, c1) in enumerate(col_ranges):
+            P = np.zeros((d, d), dtype=complex)
+            P[:, c0:c1] = co[k] * np.linalg.solve(a + (th[k] - shift_c) * np.eye(d), np.eye(d)[:, c0:c1])
+            acc += P + P.conj().T
+        return acc
+
+    _native.expm_dense_cols_host = fake_cols_host
+    A, _, _ = workloads.random_complex_hermitian(576, -6.0, 0.0, seed=8)
+    res = matexp_full(HermitianMatrix(A), ExpOptions(n=6, distributed=True))
+    assert seen == [[(a, b) for _, a, b in colsplit_plan(3, 576, rank, world)]]
+    if rank == 0:
+        np.save(out_path, res.value)
+        assert len(res.per_term_times) == 3 and min(res.per_term_times) > 0
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_engine_distributed_colsplit_full_mode(tmp_path):
+    out = str(tmp_path / "engcs.npy")
+    mp.spawn(_engine_colsplit_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    from oracle import restate
+    from paper_2306_16778_b200 import workloads
+
+    A, _, _ = workloads.random_complex_hermitian(576, -6.0, 0.0, seed=8)
+    want = restate.run_tasks_dense(A, None, 6)
+    got = np.load(out)
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
