@@ -470,10 +470,11 @@ def main():
             return t
         if gloo:
             h = t.cpu()
-            dist.reduce(h, dst=0, op=dist.ReduceOp.SUM)
+            dist.reduce(torch.view_as_real(h) if h.is_complex() else h, dst=0, op=dist.ReduceOp.SUM)
             t.copy_(h)
         else:
-            dist.reduce(t, dst=0, op=dist.ReduceOp.SUM)
+            # complex partials go through the collective as their (re, im) float64 view (same memory)
+            dist.reduce(torch.view_as_real(t) if t.is_complex() else t, dst=0, op=dist.ReduceOp.SUM)
         return t
 
     def all_max(x: float) -> float:

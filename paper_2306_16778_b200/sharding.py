@@ -34,11 +34,12 @@ def _col_cost(u: float) -> float:
 def colsplit_plan(npairs: int, d: int, rank: int, world: int, align: int = 64):
     """Pole sharding with the leftover pairs split by columns (dense full mode).
 
-    Each rank takes npairs // world whole pairs (contiguous, ascending).  The npairs % world
-    leftover pairs are cut into `world` pieces of equal substitution cost along their inverse
-    columns (cut points rounded to `align`); a piece that crosses a pair boundary becomes two
-    ranges.  Returns this rank's [(pair, c0, c1), ...] in ascending pair order, whole pairs as
-    (k, 0, d).  Every pair's ranges over all ranks partition [0, d) exactly."""
+    Each rank takes npairs // world whole pairs (contiguous, ascending).  The ranks are then
+    dealt over the npairs % world leftover pairs (the first world % rem of them get one rank
+    more), and each leftover pair's inverse columns are cut into as many pieces of equal
+    substitution cost as it has ranks (cut points rounded to `align`), so a rank factors at most
+    one extra pair.  Returns this rank's [(pair, c0, c1), ...] in ascending pair order, whole
+    pairs as (k, 0, d).  Every pair's ranges over all ranks partition [0, d) exactly."""
     if world < 1 or not (0 <= rank < world):
         raise ValueError(f"bad rank/world {rank}/{world}")
     base, rem = divmod(npairs, world)
@@ -47,30 +48,35 @@ def colsplit_plan(npairs: int, d: int, rank: int, world: int, align: int = 64):
         return tasks
     total = _col_cost(1.0)
 
-    def cut(t: float) -> tuple[int, int]:
-        """Position t in [0, rem] of the cost line -> (leftover pair index, column)."""
-        t = min(max(t, 0.0), float(rem))
-        p = min(int(t), rem - 1)
-        target = (t - p) * total
+    def cut(frac: float) -> int:
+        """Column below which `frac` of one pair's substitution cost lies."""
+        if frac <= 0.0:
+            return 0
+        if frac >= 1.0:
+            return d
         lo, hi = 0.0, 1.0
         for _ in range(60):
             mid = 0.5 * (lo + hi)
-            if _col_cost(mid) < target:
+            if _col_cost(mid) < frac * total:
                 lo = mid
             else:
                 hi = mid
-        c = int(round(hi * d / align)) * align
-        return p, min(max(c, 0), d)
+        return min(max(int(round(hi * d / align)) * align, 0), d)
 
-    cuts = [cut(rem * r / world) for r in range(world + 1)]
-    cuts[0], cuts[-1] = (0, 0), (rem - 1, d)
-    (p0, c0), (p1, c1) = cuts[rank], cuts[rank + 1]
+    # ranks per leftover pair, then this rank's (pair, piece)
+    g, extra = divmod(world, rem)
     first = world * base
-    for p in range(p0, p1 + 1):
-        a = c0 if p == p0 else 0
-        b = c1 if p == p1 else d
-        if b > a:
-            tasks.append((first + p, a, b))
+    r = rank
+    for p in range(rem):
+        gp = g + (1 if p < extra else 0)
+        if r < gp:
+            c0, c1 = cut(r / gp), cut((r + 1) / gp)
+            if r == gp - 1:
+                c1 = d
+            if c1 > c0:
+                tasks.append((first + p, c0, c1))
+            break
+        r -= gp
     return tasks
 
 
@@ -82,7 +88,11 @@ def reduce_partials(local, group=None, dst: int = 0):
     import torch.distributed as dist
 
     if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.reduce(local, dst=dst, op=dist.ReduceOp.SUM, group=group)
+        import torch
+
+        # complex partials go through the collective as their (re, im) float64 view (same memory)
+        buf = torch.view_as_real(local) if local.is_complex() else local
+        dist.reduce(buf, dst=dst, op=dist.ReduceOp.SUM, group=group)
     return local
 
 

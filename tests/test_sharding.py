@@ -146,10 +146,10 @@ def test_colsplit_plan_partitions_every_pair():
                 iv.sort()
                 assert iv[0][0] == 0 and iv[-1][1] == d
                 assert all(x[1] == y[0] for x, y in zip(iv, iv[1:]))
-            # whole pairs are dealt evenly; nobody holds more than two partial ranges
-            whole = [sum(1 for _, a, b in t if (a, b) == (0, d)) for t in plans]
-            assert max(whole) - min(whole) <= (1 if npairs % world == 0 or world > npairs else 1)
-            assert all(sum(1 for _, a, b in t if (a, b) != (0, d)) <= 2 for t in plans)
+            # whole pairs are dealt evenly; a rank factors at most one pair beyond them
+            whole = [sum(1 for k, a, b in t if k < (npairs // world) * world) for t in plans]
+            assert max(whole) == min(whole) == npairs // world
+            assert all(len(t) <= npairs // world + 1 for t in plans)
     # 12 pairs on 8 ranks (C4): one whole pair + one cost-balanced part of a shared pair each
     p = [colsplit_plan(12, 4096, r, 8) for r in range(8)]
     assert p[0] == [(0, 0, 4096), (8, 0, 1664)] and p[1] == [(1, 0, 4096), (8, 1664, 4096)]
