@@ -513,7 +513,10 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
   const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, 64) * (int64_t)batch;
   static const bool ks32 = getenv("PFX_ZGEMM_KS16") == nullptr;
-  if (tiles64 < 2 * sms) {
+  // PFX_ZGEMM_SHORTK32=1 (A/B experiment): every K <= 64 launch on the 32 x 32 tiles (four CTAs
+  // per SM instead of two 64 x 64 ones: more prologue / epilogue overlap per unit of DMMA work)
+  static const bool shortk32 = getenv("PFX_ZGEMM_SHORTK32") != nullptr;
+  if (tiles64 < 2 * sms || (shortk32 && k <= 64)) {
     if (k <= 64 && ks32)  // short K: two 32-deep stages instead of four 16-deep ones
       return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)
                 : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);

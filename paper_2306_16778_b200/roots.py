@@ -10,9 +10,10 @@ Two sources, both pinned against the reference-generated golden fixtures
   * the native host routine `pfx_pole_table` (csrc/poles.cpp): Aberth starting
     points, double-double Newton, product-formula residues — bit-identical to
     the reference for every even n <= 58;
-  * `data/pole_tables_f8.txt`: the reference's numbers frozen as hex floats,
-    served by default_table() so the engine matches the reference bit-for-bit
-    at every n (see NATIVE_DIFFERS for the three orders where they differ).
+  * `data/pole_tables_f8.txt`: the reference's numbers frozen as hex floats.
+default_table() computes the table with the native routine and serves the frozen copy only for
+the three orders where the two differ (NATIVE_DIFFERS), so the engine matches the reference
+bit-for-bit at every n.
 """
 from __future__ import annotations
 
@@ -132,4 +133,13 @@ def default_table(n: int) -> PoleTable:
     """Process-wide table cache (reference roots.py:315-318), bit-identical to the
     reference's default_table(n).thetas_f8()/coeffs_f8() at even indices."""
     check_order(n)
+    # the product computes its own poles (native double-double routine, bit-identical to the
+    # reference for these orders: tests/test_poles.py); the three orders where the reference's
+    # own numbers differ in the last place, and a checkout without the built library, are
+    # served from the frozen copy of the reference's tables
+    if n not in NATIVE_DIFFERS:
+        from . import _native
+
+        if _native.available():
+            return native_table(n)
     return frozen_table(n)
