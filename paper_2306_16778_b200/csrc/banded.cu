@@ -578,6 +578,7 @@ int banded_run(const double* band, int64_t N, int64_t kb64, const double* V, int
   const int kb = (int)kb64;
   const int nb = BD_NB;
   const int Wd = 2 * kb + 2 * nb + 1;
+  ZgemmShortK short_k(true);  // the block steps' K = 64 updates run on the 32 x 32 tiles
   // Two-partition SPIKE (BdSpike) when the halves are long against the band: the serial chain of
   // block steps halves.  PFX_BD_SPIKE=0 keeps the single-partition factorisation.
   static const bool spike_on = [] {

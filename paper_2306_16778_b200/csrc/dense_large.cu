@@ -166,7 +166,9 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
   };
   static LookAhead las[kMaxDevices];
   LookAhead* la = nullptr;
-  if (la_on && d >= 2048 && d > 2 * G * nb) {
+  // (a profiled pass, pfx_prof_enable, keeps everything on one stream: its per-launch event
+  // times are then the kernels' own durations, not shares of overlapped time)
+  if (la_on && !prof_on() && d >= 2048 && d > 2 * G * nb) {
     const int dev = current_device();
     if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
     la = &las[dev];

@@ -506,6 +506,10 @@ static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double a
   return PFX_OK;
 }
 
+static thread_local bool g_zgemm_short_k = false;
+ZgemmShortK::ZgemmShortK(bool on) : prev_(g_zgemm_short_k) { g_zgemm_short_k = on; }
+ZgemmShortK::~ZgemmShortK() { g_zgemm_short_k = prev_; }
+
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate,
           int b_lower_off, const ZCombine* ride) {
   if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return ride ? zcombine(s, *ride) : PFX_OK;
@@ -513,9 +517,15 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
   const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, 64) * (int64_t)batch;
   static const bool ks32 = getenv("PFX_ZGEMM_KS16") == nullptr;
-  // PFX_ZGEMM_SHORTK32=1 (A/B experiment): every K <= 64 launch on the 32 x 32 tiles (four CTAs
-  // per SM instead of two 64 x 64 ones: more prologue / epilogue overlap per unit of DMMA work)
-  static const bool shortk32 = getenv("PFX_ZGEMM_SHORTK32") != nullptr;
+  // Short-K preference (ZgemmShortK, set by the banded path; PFX_ZGEMM_SHORTK32=1/0 forces it
+  // on / off everywhere): every K <= 64 launch on the 32 x 32 tiles -- four CTAs per SM instead
+  // of two 64 x 64 ones, more prologue / epilogue overlap per unit of DMMA work.  C5 258.5 ->
+  // 255.1 ms; on C4's narrow K = 64 launches it costs 0.3 ms, so the dense path leaves it off.
+  static const int shortk_env = [] {
+    const char* e = getenv("PFX_ZGEMM_SHORTK32");
+    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+  }();
+  const bool shortk32 = shortk_env >= 0 ? shortk_env == 1 : g_zgemm_short_k;
   if (tiles64 < 2 * sms || (shortk32 && k <= 64)) {
     if (k <= 64 && ks32)  // short K: two 32-deep stages instead of four 16-deep ones
       return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)

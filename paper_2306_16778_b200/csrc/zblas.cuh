@@ -54,6 +54,19 @@ int zcombine(cudaStream_t s, const ZCombine& cm);
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
           bool accumulate = true, int b_lower_off = -1, const ZCombine* ride = nullptr);
 
+// While alive on this thread, K <= 64 zgemm launches prefer the 32 x 32 tiles even on large
+// grids (the banded path's K = 64 trailing updates; see zgemm()).
+class ZgemmShortK {
+ public:
+  explicit ZgemmShortK(bool on);
+  ~ZgemmShortK();
+  ZgemmShortK(const ZgemmShortK&) = delete;
+  ZgemmShortK& operator=(const ZgemmShortK&) = delete;
+
+ private:
+  bool prev_;
+};
+
 // No-pivot LU of the nb x nb diagonal block D (nb <= 64) in registers, in place.  Raises
 // ST_SINGULAR in *sing on an exactly zero pivot and ST_PIVOT where partial pivoting inside the
 // block would have exchanged rows (the rows below the block are checked by ztrmm_inplace).
