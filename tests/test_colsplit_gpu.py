@@ -75,6 +75,17 @@ def test_accumulate_and_whole_ranges_match_unsplit_call():
     assert rel(out.cpu().numpy(), ref) <= 1e-13
 
 
+def test_host_mode_accumulate():
+    d, n = 640, 8
+    A, _, _ = workloads.random_complex_hermitian(d, -20.0, 0.0, seed=17)
+    t2, c2 = default_table(n).interleaved()
+    ref = _native.expm_dense_host(A, None, t2, c2, 0.0)
+    out = _native.expm_dense_cols_host(A, t2[:4], c2[:4], [(0, d)] * 2)
+    _native.expm_dense_cols_host(A, t2[4:], c2[4:], [(0, 192), (0, 192)], out=out, accumulate=True)
+    _native.expm_dense_cols_host(A, t2[4:], c2[4:], [(192, d), (192, d)], out=out, accumulate=True)
+    assert rel(out, ref) <= 1e-13, rel(out, ref)
+
+
 def test_shift_and_pivot_fallback():
     import torch
 
