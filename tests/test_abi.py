@@ -75,3 +75,29 @@ def test_structured_bad_arguments():
     assert lib.pfx_expm_banded(1, x.ctypes.data, 8, -1, x.ctypes.data, 1, 0.0, f64(t2), f64(c2), 8,
                                x.ctypes.data, None, None) == PFX_BADARG
     assert lib.pfx_pole_table(3, f64(x), f64(x)) == PFX_BADARG
+
+
+def test_dense_cols_bad_arguments():
+    lib = _native.lib()
+    t2, c2 = _poles(4)  # two pairs
+    A = np.zeros((8, 8))
+    out = np.zeros((8, 8))
+    f64 = _native._f64p
+    i64p = ctypes.POINTER(ctypes.c_int64)
+
+    def call(d, ranges, out_complex=0, a_complex=0, mem=1):
+        rg = np.ascontiguousarray(np.asarray(ranges, dtype=np.int64).reshape(-1))
+        return lib.pfx_expm_dense_cols(mem, A.ctypes.data, a_complex, d, 0.0, f64(t2), f64(c2), 2,
+                                       rg.ctypes.data_as(i64p), out.ctypes.data, out_complex, 0, None)
+
+    # the column split belongs to the blocked large path (d > 512)
+    assert call(256, [(0, 256), (0, 256)]) == PFX_BADARG
+    assert b"d > 512" in lib.pfx_last_error()
+    # ranges: start not a multiple of 64, empty, beyond d
+    assert call(1024, [(0, 1024), (32, 1024)]) == PFX_BADARG
+    assert call(1024, [(0, 1024), (128, 128)]) == PFX_BADARG
+    assert call(1024, [(0, 1024), (0, 1025)]) == PFX_BADARG
+    assert b"column ranges" in lib.pfx_last_error()
+    # out_complex must follow A
+    assert call(1024, [(0, 1024), (0, 1024)], out_complex=1) == PFX_BADARG
+    assert call(1024, [(0, 1024), (0, 1024)], mem=9) == PFX_BADARG
