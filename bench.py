@@ -691,7 +691,10 @@ def main():
                     "frac": achieved / peaks["fp64_tflops"], "traffic": ncu.get("dram_bytes_per_launch"),
                     "kernel": dom,
                     "kernel_ms": dom_ms / dom_cnt, "peak_source": peaks["fp64_source"],
-                    "share_of_step": (dom_ms / prof_steps) / ms_step,
+                    # the dominant kernel's share of all kernel time in the profiled pass (one
+                    # stream there, so the launches do not overlap) and that pass's kernel time per step
+                    "share_of_step": dom_ms / max(sum(v[1] for v in kern.values()), 1e-30),
+                    "kernel_ms_per_step_profiled": sum(v[1] for v in kern.values()) / prof_steps,
                     "path_frac": ALG_FLOPS[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e12
                     / peaks["fp64_tflops"] / world,
                     "hbm_gbs_alg": ALG_BYTES[args.workload] * wl.evals_per_step / (ms_step * 1e-3) / 1e9}
@@ -711,9 +714,10 @@ def main():
                                 "the trailing update); the profiled pass that times the kernels keeps one stream, "
                                 "so kernel_ms are the launches' own durations")
         if args.workload == "C5":
-            roofline["note"] = ("C5 runs its block steps as a graph on 5 concurrent streams: the per-launch "
-                                "durations overlap, so share_of_step counts overlapping time and path_frac is "
-                                "the step-level figure")
+            roofline["note"] = ("the timed steps replay the block steps as a CUDA graph on six streams; the "
+                                "profiled pass that times the kernels launches them one after another on one "
+                                "stream, so kernel_ms are the launches' own durations and their sum exceeds "
+                                "ms_per_step; path_frac is the step-level figure")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -430,6 +430,10 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
   BdStreams S;
   int rc;
   if ((rc = bd_streams(S))) return rc;
+  // a profiled pass (pfx_prof_enable; direct launches, no graph) keeps every launch on the one
+  // stream: its per-launch event times are then the kernels' own durations, not shares of
+  // overlapped time
+  if (prof_on()) S.s1 = S.s2 = S.s3 = S.s4 = S.s5 = stream;
   // PFX_BD_SKIP (timing experiments only, results are wrong): bit 0 back substitution,
   // bit 1 rhs chain, bit 2 trailing update, bit 3 diagonal LU + inverses, bit 4 panel products
   static const int skip = [] {
