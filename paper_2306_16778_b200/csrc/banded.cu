@@ -442,6 +442,15 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
   }();
   cudaEvent_t evT = S.ev[0], evU = S.ev[1], evL = S.ev[2], evR = S.ev[3], evP = S.ev[4], evB = S.ev[5];
   cudaEvent_t evS = S.ev[6], evA = S.ev[7], evT2 = S.ev[8];
+  // PFX_BD_LL=1 (opt-in): left-looking far update instead of t2 (see below).  Measured on C5:
+  // 278.7 ms against 255.8 -- the two long-K launches per step have few, long CTAs (at most
+  // 384 + 320 of 32 x 32, K up to 384) and the same one-step deadline as t2, so they hold the
+  // chain back more than their smaller traffic gains; with 64 x 64 tiles 304 ms.
+  static const bool ll_on = [] {
+    const char* e = getenv("PFX_BD_LL");
+    return e && atoi(e) != 0;
+  }();
+  const bool ll = ll_on && kb % nb == 0 && kb >= 4 * nb && N % nb == 0;
   bool pending_t2 = false;  // a t2 (far trailing update) is queued on s3
   bool pending_s = false;  // strips of the previous step queued on s4
   // s2 / s3 start after everything already queued on main (the build kernel)
@@ -512,8 +521,40 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
             return rc;
           PFX_CUDA_TRY(cudaEventRecord(evB, S.s5));
           pending_b = true;
-          // t2: the rest, two steps of slack (s3 keeps the steps' t2 in order)
-          if (r2 > rb) {
+          // Left-looking far update (PFX_BD_LL=1; kb and N multiples of 64): instead of t2 -- every block of
+          // the window taking panel j's K = 64 contribution now, eight read-modify-write passes
+          // per block -- the L-shaped panel of block c = j + 3 takes, in ONE product per arm, all
+          // the contributions still missing from it: those of the panels three or more steps
+          // back, c - 8 .. c - 3 = j - 5 .. j (the two nearest panels stay right-looking: the
+          // strips and t1).  K up to 384 instead of 64: a sixth of the traffic on the window
+          // blocks.  The operands' band edge is a trapezoid (U[i][s] = 0 for s - i > kb,
+          // L[r][i] = 0 for r - i > kb): zgemm skips the out-of-band K range per tile.
+          if (ll) {
+            const int64_t c0 = k0 + rb;  // first row / column of block j + 3
+            if (c0 < N) {
+              PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evA, 0));
+              const int64_t pend = j0 + jb;  // panels [p, pend) are final
+              // row arm: blocks (c, c .. c + 5)
+              const int64_t p0 = std::max<int64_t>(0, c0 - kb);
+              const int mr = (int)std::min<int64_t>(nb, N - c0);
+              const int ncr = (int)std::min<int64_t>(kb - 2 * nb, N - c0);
+              if ((rc = zgemm(S.s3, npairs, mr, ncr, (int)(pend - p0), -1.0, sub(M, c0, p0), sub(M, p0, c0),
+                              sub(M, c0, c0), true, (int)(kb - (c0 - p0)), nullptr, -2)))
+                return rc;
+              // column arm: blocks (c + 1 .. c + 5, c)
+              const int64_t r1 = c0 + nb;
+              if (r1 < N) {
+                const int64_t p1 = std::max<int64_t>(0, r1 - kb);
+                const int mc = (int)std::min<int64_t>(kb - 3 * nb, N - r1);
+                if (pend > p1 && (rc = zgemm(S.s3, npairs, mc, mr, (int)(pend - p1), -1.0, sub(M, r1, p1),
+                                             sub(M, p1, c0), sub(M, r1, c0), true, -1, nullptr,
+                                             (int)(kb - (r1 - p1)))))
+                  return rc;
+              }
+              PFX_CUDA_TRY(cudaEventRecord(evT2, S.s3));
+              pending_t2 = true;
+            }
+          } else if (r2 > rb) {
             PFX_CUDA_TRY(cudaStreamWaitEvent(S.s3, evA, 0));
             if ((rc = zgemm(S.s3, npairs, r2 - rb, r2 - rb, jb, -1.0, sub(M, k0 + rb, j0), sub(M, j0, k0 + rb),
                             sub(M, k0 + rb, k0 + rb))))

@@ -279,7 +279,8 @@ int zcombine(cudaStream_t s, const ZCombine& cm) {
 template <int TM, int TN, int NW, bool M3 = false, int GK = 16, bool TMA = false>
 __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 : 1)
     zgemm_kernel(int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, int accumulate, int b_lower_off,
-                 ZCombine ride, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+                 ZCombine ride, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 int a_upper_off) {
   constexpr int NT = NW * 32;
   if constexpr (TM == 64 && NW == 4) {  // only this layout carries a combine (register budget)
     // the carried residue combine is slice z = 0: dispatched first, it runs beside the tiles
@@ -316,8 +317,16 @@ __global__ void __launch_bounds__(NW * 32, (TM == 64 && NW == 4) || NW == 8 ? 2 
   // b_lower_off >= 0: B is lower triangular with offset (B[r][c] = 0 for r + off < c), so
   // this column tile's products start at row n0 - off of B; a tile entirely right of the
   // triangle adds nothing
-  const int kt0 = b_lower_off >= 0 ? max(0, n0 - b_lower_off) / GK : 0;
-  if (b_lower_off >= 0 && accumulate && kt0 >= ktiles) return;
+  // a_upper_off >= 0: A is upper trapezoidal with offset (A[r][c] = 0 for c + off < r: the band's
+  // edge in a left-looking update), so this row tile's products start at column m0 - off of A.
+  // a_upper_off != -1 (band storage, where out-of-band entries alias other rows beyond the 64
+  // padded diagonals): the start is rounded down to a 64-row block, never to a finer K stage.
+  int ks = 0;
+  if (b_lower_off >= 0) ks = max(ks, n0 - b_lower_off);
+  if (a_upper_off >= 0) ks = max(ks, m0 - a_upper_off);
+  if (a_upper_off != -1) ks &= ~63;
+  const int kt0 = ks / GK;
+  if ((b_lower_off >= 0 || a_upper_off >= 0) && accumulate && kt0 >= ktiles) return;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(GemmSmem<TM, TN, GK, NS>));
   if constexpr (TMA) {
     if (tid == 0) {
@@ -470,7 +479,7 @@ static bool zgemm_use_tma() {
 
 template <int TM, int TN, int NW, bool M3, int KS = 16>
 static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-                        bool accumulate, int b_lower_off, const ZCombine* ride) {
+                        bool accumulate, int b_lower_off, const ZCombine* ride, int a_upper_off) {
   constexpr int NS = gemm_stages<TM, NW>();
   CUtensorMap tmA, tmB;
   memset(&tmA, 0, sizeof(tmA));
@@ -499,19 +508,25 @@ static int zgemm_launch(cudaStream_t s, int batch, int m, int n, int k, double a
     for (int c = 0; c < n; ++c) nz += (double)std::max(0, k - std::max(0, c - b_lower_off));
     fl = 8.0 * (double)m * batch * nz;
   }
+  if (a_upper_off >= 0) {
+    double nz = 0.0;  // nonzero columns of A summed over its rows
+    for (int r = 0; r < m; ++r) nz += (double)std::max(0, k - std::max(0, r - a_upper_off));
+    fl = 8.0 * (double)n * batch * nz;
+  }
   PFX_LAUNCH_F("zgemm", s, fl,
                (kfn<<<grid, NW * 32, smem, s>>>(m, n, k, alpha, A, B, C, accumulate ? 1 : 0, b_lower_off, rd,
-                                                 tmA, tmB)));
+                                                 tmA, tmB, a_upper_off)));
   PFX_CUDA_TRY(cudaGetLastError());
   return PFX_OK;
 }
 
 static thread_local bool g_zgemm_short_k = false;
+
 ZgemmShortK::ZgemmShortK(bool on) : prev_(g_zgemm_short_k) { g_zgemm_short_k = on; }
 ZgemmShortK::~ZgemmShortK() { g_zgemm_short_k = prev_; }
 
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C, bool accumulate,
-          int b_lower_off, const ZCombine* ride) {
+          int b_lower_off, const ZCombine* ride, int a_upper_off) {
   if (m <= 0 || n <= 0 || k <= 0 || batch <= 0) return ride ? zcombine(s, *ride) : PFX_OK;
   const int sms = device_sms();
   static const bool m3 = getenv("PFX_ZGEMM_4M") == nullptr;  // 3M by default; 4M for A/B checks
@@ -528,19 +543,19 @@ int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, 
   const bool shortk32 = shortk_env >= 0 ? shortk_env == 1 : g_zgemm_short_k;
   if (tiles64 < 2 * sms || (shortk32 && k <= 64)) {
     if (k <= 64 && ks32)  // short K: two 32-deep stages instead of four 16-deep ones
-      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)
-                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
-    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)
-              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
+      return m3 ? zgemm_launch<32, 32, 4, true, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride, a_upper_off)
+                : zgemm_launch<32, 32, 4, false, 32>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride, a_upper_off);
+    return m3 ? zgemm_launch<32, 32, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride, a_upper_off)
+              : zgemm_launch<32, 32, 4, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride, a_upper_off);
   }
   // 64x64 tiles on 4 warps of 32x32 (248 registers, two CTAs per SM): per 4-deep K step a
   // warp issues 8 fragment loads and 8 operand sums for 48 DMMAs (3M), where the 8-warp
   // 32x16 layout issued 6 + 6 for 24; 5-8% faster on every C4 shape (tools/zgemm_probe.cu).
   // PFX_ZGEMM_W8=1 keeps the 8-warp layout for A/B checks.
   static const bool w8 = getenv("PFX_ZGEMM_W8") != nullptr;
-  if (m3 && !w8) return zgemm_launch<64, 64, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
-  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride)
-            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride);
+  if (m3 && !w8) return zgemm_launch<64, 64, 4, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride, a_upper_off);
+  return m3 ? zgemm_launch<64, 64, 8, true>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride, a_upper_off)
+            : zgemm_launch<64, 64, 8, false>(s, batch, m, n, k, alpha, A, B, C, accumulate, b_lower_off, ride, a_upper_off);
 }
 
 // ---------------------------------------------------------------------------

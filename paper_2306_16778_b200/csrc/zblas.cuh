@@ -52,7 +52,11 @@ int zcombine(cudaStream_t s, const ZCombine& cm);
 // identity right-hand side).  -1: B dense.
 // ride (optional): a residue combine carried by this launch (one extra z-slice of CTAs).
 int zgemm(cudaStream_t s, int batch, int m, int n, int k, double alpha, ZMat A, ZMat B, ZMat C,
-          bool accumulate = true, int b_lower_off = -1, const ZCombine* ride = nullptr);
+          bool accumulate = true, int b_lower_off = -1, const ZCombine* ride = nullptr, int a_upper_off = -1);
+// a_upper_off >= 0: A (m x k) is upper trapezoidal with that offset, A[r][c] = 0 for
+// c + a_upper_off < r; each row tile skips the zero columns (the band edge in a left-looking
+// update).  a_upper_off = -2: no structure in A, but -- like a_upper_off >= 0 -- the operands live
+// in band storage, so the skipped K range (also b_lower_off's) is rounded to whole 64-blocks.
 
 // While alive on this thread, K <= 64 zgemm launches prefer the 32 x 32 tiles even on large
 // grids (the banded path's K = 64 trailing updates; see zgemm()).

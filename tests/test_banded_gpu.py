@@ -91,3 +91,35 @@ def test_two_partition_spike_random_band():
     got = matexp_action(BandedHermitian(band), V, ExpOptions(n=20, mode="action")).value
     want = restate.banded_action(band, V, 20)
     assert rel(got, want) <= TOL, rel(got, want)
+
+
+@pytest.mark.parametrize("N,kb,spike", [(2560, 256, "0"), (3840, 320, "0"), (6400, 256, "1"), (4096, 512, "0"),
+                                        (1024, 448, "0")])
+def test_left_looking_far_update(N, kb, spike, monkeypatch):
+    # PFX_BD_LL=1 (opt-in), kb and N multiples of 64 with kb >= 256: the far trailing update runs left-looking (one
+    # K <= kb - 128 product per L-shaped panel, trapezoidal band edge skipped per tile), with
+    # and without the two-partition split; random bands, so every in-band entry is nonzero
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import restate
+from paper_2306_16778_b200 import BandedHermitian, ExpOptions, matexp_action
+N, kb = int(sys.argv[2]), int(sys.argv[3])
+rng = np.random.default_rng(N + kb)
+band = rng.uniform(-1, 1, (kb + 1, N)) * 0.5
+band[0] = -4.0 * (kb + 1) * rng.uniform(0.2, 1.0, N) / kb
+V = rng.standard_normal((N, 3))
+got = matexp_action(BandedHermitian(band), V, ExpOptions(n=12, mode="action")).value
+want = restate.banded_action(band, V, 12)
+print("REL", float(np.linalg.norm(got - want) / np.linalg.norm(want)))
+"""
+    import os
+    env = dict(os.environ, PFX_BD_SPIKE=spike, PFX_BD_LL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code, root, str(N), str(kb)], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    r = float([l for l in res.stdout.splitlines() if l.startswith("REL")][0].split()[1])
+    assert r <= TOL, r
