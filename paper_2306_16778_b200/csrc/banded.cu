@@ -571,6 +571,8 @@ static int bd_factor_solve(cudaStream_t stream, ZMat M, ZMat X, ZMat Li, ZMat Ui
   if (pending_t2) PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evT2, 0));
   PFX_CUDA_TRY(cudaEventRecord(evR, S.s2));
   PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evR, 0));
+  PFX_CUDA_TRY(cudaEventRecord(S.ev[9], S.s3));  // s3 joins even when nothing was queued on it
+  PFX_CUDA_TRY(cudaStreamWaitEvent(stream, S.ev[9], 0));
   if (sp && (rc = bd_spike_interface(stream, *sp, M, X, Li, Ui, N, nr, npairs / 2, sing))) return rc;
   const int64_t nblk = (N + nb - 1) / nb;
   for (int64_t pb = nblk - 1; pb >= 0 && !(skip & 1); --pb) {
