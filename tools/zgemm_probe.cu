@@ -19,6 +19,7 @@ int main() {
   auto sub = [](ZMat A, int64_t i, int64_t j) { ZMat r = A; r.p = A.p + i * A.ld + j; return r; };
   struct Shape { const char* name; int m, n, k, off; ZMat A, B, C; };
   std::vector<Shape> shapes = {
+      {"lu_trail_k256", 3840, 3840, 256, -1, sub(Mz, 256, 0), sub(Mz, 0, 256), sub(Mz, 256, 256)},
       {"lu_trail_k128", 3840, 3840, 128, -1, sub(Mz, 256, 128), sub(Mz, 128, 256), sub(Mz, 256, 256)},
       {"lu_trail_k128_small", 1024, 1024, 128, -1, sub(Mz, 3072, 2944), sub(Mz, 2944, 3072), sub(Mz, 3072, 3072)},
       {"bwd_outer", 512, 4096, 3584, -1, sub(Mz, 0, 512), sub(Xz, 512, 0), sub(Xz, 0, 0)},

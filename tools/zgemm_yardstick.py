@@ -4,7 +4,8 @@ import torch
 
 torch.backends.cuda.matmul.allow_tf32 = False
 dev = torch.device("cuda")
-for (m, n, k, b) in [(4096, 4096, 4096, 1), (3968, 3968, 128, 12), (512, 4096, 3584, 12), (64, 4096, 4032, 12)]:
+for (m, n, k, b) in [(4096, 4096, 4096, 1), (3840, 3840, 256, 12), (3840, 3840, 128, 12), (512, 4096, 3584, 12),
+                     (512, 4096, 1024, 12), (64, 4096, 448, 12), (512, 2048, 2048, 12)]:
     A = torch.randn(b, m, k, dtype=torch.complex128, device=dev)
     B = torch.randn(b, k, n, dtype=torch.complex128, device=dev)
     C = torch.empty(b, m, n, dtype=torch.complex128, device=dev)
