@@ -131,6 +131,8 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
     //   B: pivot row and displaced row are staged in prow/trow; then each thread eliminates
     //      its own rows (the interchange folded in) and tracks the next column's argmax.
     if (!PIV) {
+      const int tpr = m <= DB_THREADS / 4 ? 4 : (m <= DB_THREADS / 2 ? 2 : 1);  // threads per row
+      const int cq = tid % tpr;
       for (int jj = 0; jj < jb; ++jj) {
         __syncthreads();  // panel row jj is final
         const cplx pv = ld(&P[jj * PS + jj]);
@@ -141,16 +143,22 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
         }
         const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp_fast(pv);
         const double pabs = fabs(pv.re) + fabs(pv.im);
-        for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
-          double2* row = &P[r * PS];
+        // short panels: 2 or 4 threads share a row (interleaved groups of four columns), so the
+        // dependent load -> update -> store rounds per column step shrink with the panel
+        // (uniform trip count: every lane reaches the __syncwarp that orders the sharers' reads
+        // of the column entry before the multiplier overwrites it)
+        for (int rb = jj + 1; rb < m; rb += DB_THREADS / tpr) {
+          const int r = rb + tid / tpr;
+          const bool live = r < m;
+          double2* row = &P[(live ? r : jj) * PS];
           const cplx xj = ld(&row[jj]);
           // partial-pivoting check (izamax on the updated column): row r would displace jj
-          if (fabs(xj.re) + fabs(xj.im) > pabs) atomicOr(sing, ST_PIVOT);
+          if (live && cq == 0 && fabs(xj.re) + fabs(xj.im) > pabs) atomicOr(sing, ST_PIVOT);
           const cplx l = cmul(xj, rp);
           const double2* prow_j = &P[jj * PS];
           // four columns per round: all loads first (this row is never the pivot row, but
           // the compiler cannot prove it), then the updates and stores
-          for (int c = jj + 1; c < jb; c += 4) {
+          for (int c = jj + 1 + 4 * cq; live && c < jb; c += 4 * tpr) {
             cplx x[4], y[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -161,7 +169,8 @@ __device__ void lu_blocked(double2* __restrict__ W, int* __restrict__ ipiv, int 
             for (int u = 0; u < 4; ++u)
               if (c + u < jb) st(&row[c + u], cfms(x[u], l, y[u]));
           }
-          st(&row[jj], l);
+          if (tpr > 1) __syncwarp();
+          if (live && cq == 0) st(&row[jj], l);
         }
       }
     }
@@ -545,6 +554,8 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
     }
     __syncthreads();
     if (dbg && tid == 0) tph = clock64();
+    const int tpr = m <= DB_THREADS / 4 ? 4 : (m <= DB_THREADS / 2 ? 2 : 1);  // threads per row
+    const int cq = tid % tpr;
     for (int jj = 0; jj < jb; ++jj) {
       __syncthreads();  // panel row jj is final
       const cplx pv = ld(&P[jj * PS + jj]);
@@ -555,14 +566,18 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
       }
       const cplx rp = (pv.re == 0.0 && pv.im == 0.0) ? mk(0.0, 0.0) : crcp_fast(pv);
       const double pabs = fabs(pv.re) + fabs(pv.im);
-      for (int r = jj + 1 + tid; r < m; r += DB_THREADS) {
-        double2* row = &P[r * PS];
+      // short panels: 2 or 4 threads share a row (interleaved groups of four columns); uniform
+      // trip count, so every lane reaches the __syncwarp before the multiplier is stored
+      for (int rb = jj + 1; rb < m; rb += DB_THREADS / tpr) {
+        const int r = rb + tid / tpr;
+        const bool live = r < m;
+        double2* row = &P[(live ? r : jj) * PS];
         const cplx xj = ld(&row[jj]);
         // partial-pivoting check (izamax on the updated column): row r would displace jj
-        if (fabs(xj.re) + fabs(xj.im) > pabs) atomicOr(sing, ST_PIVOT);
+        if (live && cq == 0 && fabs(xj.re) + fabs(xj.im) > pabs) atomicOr(sing, ST_PIVOT);
         const cplx l = cmul(xj, rp);
         const double2* prow_j = &P[jj * PS];
-        for (int c = jj + 1; c < jb; c += 4) {
+        for (int c = jj + 1 + 4 * cq; live && c < jb; c += 4 * tpr) {
           cplx x[4], y[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -573,7 +588,8 @@ __device__ void lu_nopiv_dp(double2* __restrict__ W, int* __restrict__ ipiv, int
           for (int u = 0; u < 4; ++u)
             if (c + u < jb) st(&row[c + u], cfms(x[u], l, y[u]));
         }
-        st(&row[jj], l);
+        if (tpr > 1) __syncwarp();
+        if (live && cq == 0) st(&row[jj], l);
       }
     }
     __syncthreads();
