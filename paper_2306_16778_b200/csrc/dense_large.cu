@@ -21,6 +21,7 @@
 // Complex action (Yc = M^{-H} V) is obtained from the conjugate shifts theta_k^* as
 // extra batch members, since (A + theta I)^H = A + conj(theta) I for Hermitian A.
 #include <algorithm>
+#include <functional>
 #include <vector>
 
 #include "zblas.cuh"
@@ -96,6 +97,28 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
       if (scale != 1.0) acc = cscale(acc, scale);
       reinterpret_cast<double2*>(out)[e] = make_double2(acc.re, acc.im);
     }
+  }
+}
+
+// Complex full mode on the rectangle rows [r0, r1) x columns [c0, c1):
+// out = scale * sum_k (a_k X_k + (a_k X_k)^H), k ascending.  Entry (i, j) reads rows i and j of
+// every X_k, so a rectangle inside [J0, d)^2 is final as soon as the backward substitution has
+// finished the rows from J0 on: the host pipeline combines and copies back the L-shaped frontier
+// of every super-block while the substitution goes on above it.
+__global__ void dl_combine_rect(ZMat X, int d, int npairs, const double2* coef, double scale, double* out, int r0,
+                                int r1, int c0, int c1) {
+  const int w = c1 - c0;
+  const int64_t n = (int64_t)(r1 - r0) * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = r0 + e / w, j = c0 + e % w;
+    cplx acc = mk(0, 0);
+    for (int k = 0; k < npairs; ++k) {
+      const cplx a = ld(&coef[k]);
+      const cplx sk = cadd(cmul(a, ld(X.at(k, i, j))), cconj(cmul(a, ld(X.at(k, j, i)))));
+      acc = k == 0 ? sk : cadd(acc, sk);
+    }
+    if (scale != 1.0) acc = cscale(acc, scale);
+    reinterpret_cast<double2*>(out)[i * d + j] = make_double2(acc.re, acc.im);
   }
 }
 
@@ -251,7 +274,8 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
 // are zero, and the trailing block of L^{-1} is the inverse of L's trailing block, so the forward
 // substitution runs on rows >= c0 only; the backward substitution covers every row.
 int lu_subst_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int c0, int ncols,
-                   bool identity_rhs, bool sym_lower, const ZCombine* cmb) {
+                   bool identity_rhs, bool sym_lower, const ZCombine* cmb,
+                   const std::function<int(int, int)>* rows_final = nullptr) {
   const int nb = DL_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -332,15 +356,26 @@ int lu_subst_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
         pend.ncols = ncols;
       }
     }
+    // rows [J0, d) of every X are final
+    if (rows_final && (rc = (*rows_final)(J0, J1))) return rc;
   }
   if (pend.mode && (rc = zcombine(s, pend))) return rc;  // block row 0
   return PFX_OK;
 }
 
+// rows_final(J0, J1) (optional) is called when the backward substitution has finished the rows
+// from J0 on (super-block [J0, J1) last).
+static int lu_solve_nopiv_hook(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
+                               bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb,
+                               const std::function<int(int, int)>* rows_final) {
+  if (int rc = lu_factor_nopiv(s, nsys, d, 0, M, Li, Ui, sing, check_pivots)) return rc;
+  return lu_subst_nopiv(s, nsys, d, M, X, Li, Ui, 0, ncols, identity_rhs, sym_lower, cmb, rows_final);
+}
+
 int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
                    bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb) {
-  if (int rc = lu_factor_nopiv(s, nsys, d, 0, M, Li, Ui, sing, check_pivots)) return rc;
-  return lu_subst_nopiv(s, nsys, d, M, X, Li, Ui, 0, ncols, identity_rhs, sym_lower, cmb);
+  return lu_solve_nopiv_hook(s, nsys, d, M, X, Li, Ui, ncols, sing, identity_rhs, sym_lower, check_pivots, cmb,
+                             nullptr);
 }
 
 int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* ipiv, int* sing);
@@ -443,9 +478,40 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   // tiles and the step grew to 187-192 ms (profiles/r02_c4_combine_ab.txt), so it is opt-in.
   static const bool fuse = getenv("PFX_FUSED_COMBINE") != nullptr;
   const bool fused = fuse && !pivoted;
+  // Host mode, complex full mode: the result leaves by L-shaped frontiers.  When the backward
+  // substitution has finished the rows from J0 on, the entries (i, j) with min(i, j) in [J0, J1)
+  // are final (they read rows i, j >= J0 of every X_k): they are combined and copied back right
+  // then, so the 268 MB copy-out of C4 hides behind the substitution of the rows above.
+  // PFX_EARLY_OUT=0 keeps the row-chunk pipeline after the substitution.
+  static const bool early_on = [] {
+    const char* e = getenv("PFX_EARLY_OUT");
+    return !(e && atoi(e) == 0);
+  }();
+  bool early_out = early_on && out_host && full && !real_path && !pivoted && !fused;
+  std::function<int(int, int)> frontier = [&](int J0, int J1) -> int {
+    const size_t el = sizeof(double2);
+    // rows [J0, J1) x columns [J0, d), then rows [J1, d) x columns [J0, J1)
+    const int rect[2][4] = {{J0, J1, J0, d}, {J1, d, J0, J1}};
+    for (const auto& q : rect) {
+      if (q[1] <= q[0] || q[3] <= q[2]) continue;
+      PFX_LAUNCH("dl_combine", stream,
+                 dl_combine_rect<<<1184, 256, 0, stream>>>(X, d, npairs, coef_d, scale, out, q[0], q[1], q[2], q[3]));
+      PFX_CUDA_TRY(cudaGetLastError());
+    }
+    PFX_CUDA_TRY(cudaEventRecord(evs[NCH], stream));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(cin, evs[NCH], 0));
+    for (const auto& q : rect) {
+      if (q[1] <= q[0] || q[3] <= q[2]) continue;
+      const size_t off = ((size_t)q[0] * d + q[2]) * el;
+      PFX_CUDA_TRY(cudaMemcpy2DAsync(reinterpret_cast<char*>(out_host) + off, (size_t)d * el,
+                                     reinterpret_cast<char*>(out) + off, (size_t)d * el, (size_t)(q[3] - q[2]) * el,
+                                     (size_t)(q[1] - q[0]), cudaMemcpyDeviceToHost, cin));
+    }
+    return PFX_OK;
+  };
   if (!pivoted) {
-    rc = lu_solve_nopiv(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2,
-                        fused ? &cm : nullptr);
+    rc = lu_solve_nopiv_hook(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2,
+                             fused ? &cm : nullptr, early_out ? &frontier : nullptr);
     if (rc) return rc;
     if (pivot == 2) {
       PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -455,6 +521,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
         // factorisations with interchanges from the original matrices
         note_pivot_fallback();
         pivoted = true;
+        early_out = false;  // the frontiers already copied are overwritten by the pivoted result
         PFX_CUDA_TRY(cudaMemsetAsync(sing, 0, sizeof(int), stream));
         PFX_LAUNCH("dl_build", stream, dl_build<<<bg, 256, 0, stream>>>(A, a_complex, d, V, v_complex, ncols, full,
                                                                           shift_c, theta_d, npairs, nsys, M, X));
@@ -468,7 +535,11 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     if (rc) return rc;
   }
   const size_t orow = (size_t)ncols * sizeof(double) * (real_path ? 1 : 2);
-  if (!fused && out_host) {
+  if (early_out) {
+    // everything was combined and queued for the copy stream by the frontiers
+    PFX_CUDA_TRY(cudaEventRecord(evs[2 * NCH], cin));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(stream, evs[2 * NCH], 0));
+  } else if (!fused && out_host) {
     for (int c = 0; c < NCH; ++c) {
       const int r0 = (int)((int64_t)d * c / NCH), r1 = (int)((int64_t)d * (c + 1) / NCH);
       PFX_LAUNCH("dl_combine", stream,
