@@ -100,6 +100,36 @@ __global__ void dl_combine(ZMat X, int d, int ncols, int npairs, const double2* 
   }
 }
 
+// M_k = A - cI + theta_k I on the rectangle rows [r0, r1) x columns [c0, c1) (the host pipeline
+// builds the first panel group's column slab and then row chunks of the rest as they land)
+__global__ void dl_build_rect(const double* A, int a_complex, int d, double shift_c, const double2* theta, ZMat M,
+                              int r0, int r1, int c0, int c1) {
+  const int k = blockIdx.y;
+  const cplx th = ld(&theta[k]);
+  const int w = c1 - c0;
+  const int64_t n = (int64_t)(r1 - r0) * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = r0 + e / w, j = c0 + e % w;
+    double2 v = a_complex ? reinterpret_cast<const double2*>(A)[i * d + j] : make_double2(A[i * d + j], 0.0);
+    if (i == j) {
+      v.x = (v.x - shift_c) + th.re;
+      v.y = v.y + th.im;
+    }
+    *M.at(k, i, j) = v;
+  }
+}
+
+// Arrival of the matrices during a host call: `slab` = columns [0, 64 G) of every row are built,
+// chunk[c] = rows [.., r1[c]) of the remaining columns are built.  The LU waits for the slab and
+// the first rows before its first panel group and applies that group's trailing update chunk by
+// chunk, so the copy-in overlaps the first group instead of preceding it.
+struct LuArrive {
+  cudaEvent_t slab = nullptr;
+  cudaEvent_t chunk[8] = {};
+  int r1[8] = {};
+  int nch = 0;
+};
+
 // Complex full mode on the rectangle rows [r0, r1) x columns [c0, c1):
 // out = scale * sum_k (a_k X_k + (a_k X_k)^H), k ascending.  Entry (i, j) reads rows i and j of
 // every X_k, so a rectangle inside [J0, d)^2 is final as soon as the backward substitution has
@@ -126,8 +156,17 @@ __global__ void dl_combine_rect(ZMat X, int d, int npairs, const double2* coef, 
 // matrices M in place; naug extra columns right of each matrix (M is d x (d + naug), the
 // right-hand sides) take every row operation, so they leave as L^{-1} B.  Li / Ui receive the
 // diagonal blocks' triangular inverses.
-int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, ZMat Ui, int* sing,
-                    bool check_pivots) {
+static int lu_group() {
+  static const int G = [] {
+    const char* e = getenv("PFX_LU_GROUP");
+    const int g = e ? atoi(e) : DL_GROUP;
+    return g < 1 ? 1 : (g > 8 ? 8 : g);
+  }();
+  return G;
+}
+
+static int lu_factor_nopiv_arr(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, ZMat Ui, int* sing,
+                               bool check_pivots, const LuArrive* arrive) {
   const int nb = DL_NB;
   auto sub = [](ZMat A, int64_t i, int64_t j) {
     ZMat r = A;
@@ -168,11 +207,7 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
   // matrix (up to 12 x 268 MB, far beyond L2) is read and written once per 64 G columns
   // instead of once per 64, and every trailing tile does G times the DMMA work per epilogue.
   // PFX_LU_GROUP=<G> overrides the default group (A/B experiments).
-  static const int G = [] {
-    const char* e = getenv("PFX_LU_GROUP");
-    const int g = e ? atoi(e) : DL_GROUP;
-    return g < 1 ? 1 : (g > 8 ? 8 : g);
-  }();
+  const int G = lu_group();
   // Look-ahead (d >= 2048): the group's trailing update is split into the NEXT group's
   // L-shaped strip (its 64 G columns below and its 64 G rows to the right) and the remainder
   // beyond it.  The strip and the next group's panels (the latency-bound chain: diagonal LU,
@@ -208,6 +243,14 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
   }
   cudaStream_t const cs = la ? la->hp : s;  // the stream of the panel chain
   bool rest_pending = false;  // a remainder update on `s` the next strip update must wait for
+  if (arrive) {
+    // the first group's panels read the column slab (all rows) and the first 64 G rows
+    PFX_CUDA_TRY(cudaStreamWaitEvent(cs, arrive->slab, 0));
+    for (int c = 0; c < arrive->nch; ++c) {
+      PFX_CUDA_TRY(cudaStreamWaitEvent(cs, arrive->chunk[c], 0));
+      if (arrive->r1[c] >= std::min(d, G * nb)) break;
+    }
+  }
   for (int g0 = 0; g0 < d; g0 += G * nb) {
     const int gend = std::min(d, g0 + G * nb);
     for (int jp = g0; jp < gend; jp += nb) {
@@ -224,6 +267,18 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
     }
     if (gend >= d) break;
     const int K = gend - g0;
+    if (arrive && g0 == 0) {
+      // the first group's trailing update, by row chunks as they arrive (on the chain's stream:
+      // the next group's panels follow in order)
+      for (int c = 0; c < arrive->nch; ++c) {
+        const int ra = std::max(gend, c ? arrive->r1[c - 1] : 0), rb = std::min(d, arrive->r1[c]);
+        PFX_CUDA_TRY(cudaStreamWaitEvent(cs, arrive->chunk[c], 0));
+        if (rb > ra && (rc = zgemm(cs, nsys, rb - ra, d - gend + naug, K, -1.0, sub(M, ra, g0), sub(M, g0, gend),
+                                   sub(M, ra, gend))))
+          return rc;
+      }
+      continue;
+    }
     if (!la) {
       if ((rc = zgemm(s, nsys, d - gend, d - gend + naug, K, -1.0, sub(M, gend, g0), sub(M, g0, gend),
                       sub(M, gend, gend))))
@@ -254,6 +309,11 @@ int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, 
     PFX_CUDA_TRY(cudaStreamWaitEvent(s, la->done, 0));
   }
   return PFX_OK;
+}
+
+int lu_factor_nopiv(cudaStream_t s, int nsys, int d, int naug, ZMat M, ZMat Li, ZMat Ui, int* sing,
+                    bool check_pivots) {
+  return lu_factor_nopiv_arr(s, nsys, d, naug, M, Li, Ui, sing, check_pivots, nullptr);
 }
 
 // LU (no pivoting) of nsys d x d matrices M, then X = U^{-1} L^{-1} X.  identity_rhs: X
@@ -367,8 +427,8 @@ int lu_subst_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
 // from J0 on (super-block [J0, J1) last).
 static int lu_solve_nopiv_hook(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMat Ui, int ncols, int* sing,
                                bool identity_rhs, bool sym_lower, bool check_pivots, const ZCombine* cmb,
-                               const std::function<int(int, int)>* rows_final) {
-  if (int rc = lu_factor_nopiv(s, nsys, d, 0, M, Li, Ui, sing, check_pivots)) return rc;
+                               const std::function<int(int, int)>* rows_final, const LuArrive* arrive = nullptr) {
+  if (int rc = lu_factor_nopiv_arr(s, nsys, d, 0, M, Li, Ui, sing, check_pivots, arrive)) return rc;
   return lu_subst_nopiv(s, nsys, d, M, X, Li, Ui, 0, ncols, identity_rhs, sym_lower, cmb, rows_final);
 }
 
@@ -379,6 +439,7 @@ int lu_solve_nopiv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, ZMat Li, ZMa
 }
 
 int lu_solve_piv(cudaStream_t s, int nsys, int d, ZMat M, ZMat X, int ncols, int* ipiv, int* sing);
+__global__ void dl_ident_cols(ZMat X, int d, int c0, int nc);
 
 // pivot: 0 = interchange-free, 1 = partial pivoting (lu_solve_piv), 2 = checked: the
 // interchange-free LU verifies every column against partial pivoting and the call is redone
@@ -415,8 +476,9 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   // as they land; the result comes back by row chunks while the next ones are combined
   constexpr int NCH = 8;
   struct CopyIn {
-    cudaStream_t cs = nullptr;
+    cudaStream_t cs = nullptr, bs = nullptr;  // copy stream, build stream
     cudaEvent_t ev[2 * NCH + 1];
+    cudaEvent_t ev2[NCH + 2];  // early copy-in: slab copied, slab built, chunks built
   };
   static CopyIn cis[kMaxDevices];
   cudaStream_t cin = nullptr;
@@ -426,13 +488,65 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
     if (dev < 0 || dev >= kMaxDevices) return fail(PFX_CUDA, "device index out of range");
     if (!cis[dev].cs) {
       PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cis[dev].cs, cudaStreamNonBlocking));
+      PFX_CUDA_TRY(cudaStreamCreateWithFlags(&cis[dev].bs, cudaStreamNonBlocking));
       for (auto& e : cis[dev].ev) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      for (auto& e : cis[dev].ev2) PFX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     cin = cis[dev].cs;
     evs = cis[dev].ev;
   }
   const size_t arow = (size_t)d * sizeof(double) * (a_complex ? 2 : 1);
-  if (A_host) {
+  // Early copy-in (host calls, full mode, d >= 2048): the first panel group's column slab goes in
+  // first (a 2-D copy), then the remaining columns by row chunks; each piece is built on a build
+  // stream as it lands, and the LU starts on the slab + first rows and applies the first group's
+  // trailing update chunk by chunk (LuArrive), so the copy-in overlaps the first group instead of
+  // preceding the whole factorisation.  PFX_EARLY_IN=0 keeps the row-chunk pipeline.
+  static const bool early_in_on = [] {
+    const char* e = getenv("PFX_EARLY_IN");
+    return !(e && atoi(e) == 0);
+  }();
+  LuArrive arrive;
+  const int W0 = lu_group() * DL_NB;
+  const bool early_in = early_in_on && A_host && full && pivot != 1 && d >= 2048 && d > 2 * W0;
+  if (early_in) {
+    const int dev = current_device();
+    cudaStream_t bs = cis[dev].bs;
+    cudaEvent_t* ev2 = cis[dev].ev2;
+    const size_t el = sizeof(double) * (a_complex ? 2 : 1);
+    char* Ad = reinterpret_cast<char*>(const_cast<double*>(A));
+    const char* Ah = reinterpret_cast<const char*>(A_host);
+    // the staging buffers are idle on entry (host-mode calls end synchronised)
+    PFX_CUDA_TRY(cudaEventRecord(evs[2 * NCH], stream));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(cin, evs[2 * NCH], 0));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(bs, evs[2 * NCH], 0));
+    // X = I on the caller's stream (independent of A)
+    PFX_LAUNCH("dl_build", stream, dl_ident_cols<<<dim3(592, nsys), 256, 0, stream>>>(X, d, 0, d));
+    PFX_CUDA_TRY(cudaGetLastError());
+    // the slab: columns [0, W0) of every row
+    PFX_CUDA_TRY(cudaMemcpy2DAsync(Ad, arow, Ah, arow, (size_t)W0 * el, (size_t)d, cudaMemcpyHostToDevice, cin));
+    PFX_CUDA_TRY(cudaEventRecord(ev2[0], cin));
+    PFX_CUDA_TRY(cudaStreamWaitEvent(bs, ev2[0], 0));
+    PFX_LAUNCH("dl_build", bs,
+               dl_build_rect<<<dim3(296, nsys), 256, 0, bs>>>(A, a_complex, d, shift_c, theta_d, M, 0, d, 0, W0));
+    PFX_CUDA_TRY(cudaGetLastError());
+    PFX_CUDA_TRY(cudaEventRecord(ev2[1], bs));
+    arrive.slab = ev2[1];
+    arrive.nch = NCH;
+    for (int c = 0; c < NCH; ++c) {
+      const int r0 = (int)((int64_t)d * c / NCH), r1 = (int)((int64_t)d * (c + 1) / NCH);
+      const size_t off = (size_t)r0 * arow + (size_t)W0 * el;
+      PFX_CUDA_TRY(cudaMemcpy2DAsync(Ad + off, arow, Ah + off, arow, (size_t)(d - W0) * el, (size_t)(r1 - r0),
+                                     cudaMemcpyHostToDevice, cin));
+      PFX_CUDA_TRY(cudaEventRecord(evs[c], cin));
+      PFX_CUDA_TRY(cudaStreamWaitEvent(bs, evs[c], 0));
+      PFX_LAUNCH("dl_build", bs,
+                 dl_build_rect<<<dim3(1184, nsys), 256, 0, bs>>>(A, a_complex, d, shift_c, theta_d, M, r0, r1, W0, d));
+      PFX_CUDA_TRY(cudaGetLastError());
+      PFX_CUDA_TRY(cudaEventRecord(ev2[2 + c], bs));
+      arrive.chunk[c] = ev2[2 + c];
+      arrive.r1[c] = r1;
+    }
+  } else if (A_host) {
     // the staging buffers are idle on entry (host-mode calls end synchronised)
     PFX_CUDA_TRY(cudaEventRecord(evs[2 * NCH], stream));
     PFX_CUDA_TRY(cudaStreamWaitEvent(cin, evs[2 * NCH], 0));
@@ -511,7 +625,7 @@ int dense_large_run(const double* A, int a_complex, int d, const double* V, int 
   };
   if (!pivoted) {
     rc = lu_solve_nopiv_hook(stream, nsys, d, M, X, Li, Ui, ncols, sing, full != 0, sym_lower != 0, pivot == 2,
-                             fused ? &cm : nullptr, early_out ? &frontier : nullptr);
+                             fused ? &cm : nullptr, early_out ? &frontier : nullptr, early_in ? &arrive : nullptr);
     if (rc) return rc;
     if (pivot == 2) {
       PFX_CUDA_TRY(cudaMemcpyAsync(hsg, sing, sizeof(int), cudaMemcpyDeviceToHost, stream));
